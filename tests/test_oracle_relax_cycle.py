@@ -1,0 +1,188 @@
+"""Oracle pins: Vanka, BSR, coarse solve and cycle."""
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+import mg_inputs
+from oracle.mesh import Mesh
+from oracle.fem import Operator
+from oracle.relax import Vanka, BSR, vertex_patches
+from oracle.cycle import Hierarchy, CoarseSolver, lame
+from tests._golden import load
+
+
+def test_patch_sizes_and_natural_weights():
+    """Interior patch = 20 DoFs (tab:vanka22 caption; Fig. fig:patches); side 7, corners 4 / 1
+    (reading A8); natural weights 1 (P1), 1/2 (edges), 1/3 (P0)."""
+    n = 6
+    m = Mesh(n)
+    op = Operator(m, 1, 1, 1, 1, 1.0)
+    P = vertex_patches(m, "full")
+    sizes = {}
+    for vid, p in enumerate(P):
+        i, j = vid % (n + 1), vid // (n + 1)
+        sizes[(i, j)] = p.size
+    assert all(sizes[(i, j)] == 20 for i in range(1, n) for j in range(1, n))
+    assert all(sizes[(0, j)] == 7 and sizes[(n, j)] == 7 for j in range(1, n))
+    assert sizes[(n, 0)] == 4 and sizes[(0, n)] == 4 and sizes[(0, 0)] == 1 and sizes[(n, n)] == 1
+    V = Vanka(op)
+    kind = m.slot_kind(m.act_idx)
+    w = V.weight
+    assert np.allclose(w[kind <= 1], 1.0) and np.allclose(w[(kind >= 2) & (kind <= 7)], 0.5)
+    assert np.allclose(w[kind >= 8], 1.0 / 3.0)
+
+
+@pytest.mark.parametrize("invM", [1.0, 1e-2])
+def test_deflated_patch_solve_equals_plain(invM):
+    """The deflated solve (reading A9) is the plain patch inverse where the latter is well conditioned."""
+    rng = np.random.default_rng(1)
+    op = Operator(Mesh(8), lam=2.0, mu=1.0, tau=1.0, alpha=1.0, inv_M=invM, K=0.5)
+    V = Vanka(op)
+    for d in V.data:
+        R = rng.standard_normal(d["I"].shape)
+        Y = V.patch_solve(d, R)
+        Y0 = np.linalg.solve(d["K"], R[..., None])[..., 0]
+        assert np.abs(Y - Y0).max() <= 1e-11 * np.abs(Y0).max()
+
+
+def _dense_vanka_Minv(op):
+    """Brute force: M^{-1} = sum_l V_l^T D_l inv(V_l A V_l^T) V_l as a dense matrix."""
+    A = op.A.toarray()
+    N = A.shape[0]
+    patches = vertex_patches(op.mesh, "full")
+    cnt = np.zeros(N)
+    for p in patches:
+        cnt[p] += 1
+    Minv = np.zeros((N, N))
+    for p in patches:
+        if p.size:
+            Minv[np.ix_(p, p)] += np.diag(1.0 / cnt[p]) @ np.linalg.inv(A[np.ix_(p, p)])
+    return Minv
+
+
+@pytest.mark.parametrize("relax", ["vanka", "bsr"])
+def test_brute_force_two_grid(relax):
+    """Dense E_TG = E_s^nu2 (I - P A_H^{-1} R A) E_s^nu1 (eq. TG-Operator-Biot) built from explicit
+    inverses equals the oracle cycle applied to unit vectors (b = 0).  For BSR the dense smoother is
+    I - omega M^{-1} A with M = [[F, B^T], [B, -C_2]] of Appendix E, n_J = 1."""
+    n = 8
+    lam, mu, tau, alpha, invM, K = 3.0, 1.0, 1.0, 1.0, 1.0, 0.7
+    H = Hierarchy(n, 2, lam, mu, tau, alpha, invM, 1.0, K=K, relax=relax)
+    op, opc, tr = H.ops[0], H.ops[1], H.transfers[0]
+    A = op.A.toarray()
+    N = A.shape[0]
+    om, omJ = 0.8, 0.9
+    if relax == "vanka":
+        Es = np.eye(N) - om * _dense_vanka_Minv(op) @ A
+    else:
+        # F = diag(A_V,u, tau D_w): A_V,u^{-1} = sum_l V^T D inv(A_u,l) V over 8-DoF patches
+        iu, iw, ip = op.iu, op.iw, op.ip
+        Au = op.Au.toarray()
+        m = op.mesh
+        posu = np.full(m.nslots, -1)
+        posu[m.act_idx[iu]] = np.arange(iu.size)
+        pat = []
+        tris, edges = m.vertex_incidence()
+        for vid in range((n + 1) ** 2):
+            i, j = vid % (n + 1), vid // (n + 1)
+            s = [m.slot(0, i, j), m.slot(1, i, j)] + [m.slot(2 + k, a, b) for (k, a, b) in edges[vid]]
+            p = posu[np.array(s)]
+            p = p[p >= 0]
+            if p.size:
+                pat.append(p)
+        cnt = np.zeros(iu.size)
+        for p in pat:
+            cnt[p] += 1
+        AVinv = np.zeros((iu.size, iu.size))
+        for p in pat:
+            AVinv[np.ix_(p, p)] += np.diag(1.0 / cnt[p]) @ np.linalg.inv(Au[np.ix_(p, p)])
+        AV = np.linalg.inv(AVinv)
+        Dw = op.Mw.diagonal()
+        Bu, Bw = op.Bu.toarray(), op.Bw.toarray()
+        S = (invM + alpha ** 2 / (lam + mu)) * op.Mp.toarray() + tau * Bw @ np.diag(1 / Dw) @ Bw.T
+        C2 = (np.diag(np.diag(S)) / omJ - alpha ** 2 * Bu @ AVinv @ Bu.T - tau * Bw @ np.diag(1 / Dw) @ Bw.T)
+        Mm = np.zeros((N, N))
+        Mm[np.ix_(iu, iu)] = AV
+        Mm[np.ix_(iw, iw)] = tau * np.diag(Dw)
+        Mm[np.ix_(ip, iu)] = alpha * Bu
+        Mm[np.ix_(iu, ip)] = alpha * Bu.T
+        Mm[np.ix_(ip, iw)] = tau * Bw
+        Mm[np.ix_(iw, ip)] = tau * Bw.T
+        Mm[np.ix_(ip, ip)] = -C2
+        Es = np.eye(N) - om * np.linalg.solve(Mm, A)
+    P = tr.P.toarray()
+    AH = opc.A.toarray()
+    Ecgc = np.eye(N) - P @ np.linalg.solve(AH, P.T @ A)
+    E = Es @ Ecgc @ Es
+    opts = dict(nu1=1, nu2=1, omega=om, omega_J=omJ, jacobi_sweeps=1)
+    Ecyc = np.stack([H.cycle(e, np.zeros(N), opts) for e in np.eye(N)], axis=1)
+    assert np.abs(Ecyc - E).max() <= 1e-9 * np.abs(E).max()
+
+
+def test_cycle_affine_and_converges_to_lu():
+    """The cycle is affine in (x, b) and the stationary iteration converges to the sparse-LU solution."""
+    rng = np.random.default_rng(3)
+    H = Hierarchy(16, 3, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, K=1.0, relax="vanka")
+    N = H.ops[0].A.shape[0]
+    opts = dict(nu1=1, nu2=1, omega=0.7)
+    x1, x2, b1, b2 = (rng.standard_normal(N) for _ in range(4))
+    lhs = H.cycle(x1 + x2, b1 + b2, opts)
+    rhs = H.cycle(x1, b1, opts) + H.cycle(x2, b2, opts)
+    assert np.abs(lhs - rhs).max() <= 1e-10 * np.abs(lhs).max()
+    b = mg_inputs.uniform_rhs(16, 0)
+    bv = H.meshes[0].to_active(b)
+    x, hist = H.solve(np.zeros(N), bv, opts, rtol=1e-10, max_cycles=200)
+    xs = spla.spsolve(H.ops[0].A.tocsc(), bv)
+    assert hist[-1] <= 1e-10 * hist[0]
+    assert np.linalg.norm(x - xs) <= 1e-8 * np.linalg.norm(xs)
+
+
+def test_coarse_solver_deflated():
+    """Deflated dense coarsest solve (reading A9) agrees with sparse LU and leaves a tiny residual."""
+    rng = np.random.default_rng(4)
+    for invM in (1.0, 1e-6):
+        op = Operator(Mesh(4), 1.0, 1.0, 1.0, 1.0, invM)
+        cs = CoarseSolver(op)
+        b = rng.standard_normal(op.A.shape[0])
+        x = cs.solve(b)
+        assert np.linalg.norm(b - op.A @ x) <= 1e-12 * (np.linalg.norm(b) + abs(op.A).max() * np.linalg.norm(x))
+        if invM == 1.0:
+            xs = spla.spsolve(op.A.tocsc(), b)
+            assert np.linalg.norm(x - xs) <= 1e-12 * np.linalg.norm(xs)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cell", range(4))
+def test_tab_vanka22_rho(cell):
+    """Measured two-grid rho_N of additive Vanka(2,2), h = 1/64 (tab:vanka22).
+    Asymptotic factor after 60 cycles (reading A23); target +-0.03."""
+    c = load("paper_tables.json")["tab_vanka22"]["cells"][cell]
+    mu, lam = lame(3e4, c["nu"])
+    H = Hierarchy(64, 2, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], relax="vanka")
+    rho, rhos = H.measure_rho(dict(nu1=2, nu2=2, omega=c["omega"]), seed=0, min_cycles=60, max_cycles=60)
+    assert abs(np.mean(rhos[-2:]) - c["rho_N"]) <= 0.03, (rhos[-4:], c)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cell", range(3))
+def test_tab_bsr_vanka11_rho(cell):
+    """Measured two-grid rho_N of inexact BSR(1,1), one Jacobi sweep (tab:bsr_vanka11,
+    PAPER.md:862-907).  Asymptotic factor after 150 cycles (reading A23); target +-0.03."""
+    c = load("paper_tables.json")["tab_bsr_vanka11"]["cells"][cell]
+    mu, lam = lame(3e4, c["nu"])
+    H = Hierarchy(64, 2, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], relax="bsr")
+    opts = dict(nu1=1, nu2=1, omega=c["omega"], omega_J=c["omega_J"], jacobi_sweeps=1)
+    rho, rhos = H.measure_rho(opts, seed=0, min_cycles=150, max_cycles=150)
+    assert abs(rhos[-1] - c["rho_N"]) <= 0.03, (rhos[-4:], c)
+
+
+def test_manufactured_rates():
+    """FE convergence of the steady problem: |u-u_h|_1 = O(h),
+    ||p-p_h|| = O(h^2), for nu = 0.4 and 0.499, k = 1e-6."""
+    from oracle.manufactured import solve_direct, errors
+    for nu in (0.4, 0.499):
+        e = [errors(*solve_direct(n, nu=nu)) for n in (8, 16, 32)]
+        r1 = [np.log2(e[i][0] / e[i + 1][0]) for i in range(2)]
+        rp = [np.log2(e[i][1] / e[i + 1][1]) for i in range(2)]
+        assert all(0.95 < r < 1.1 for r in r1), r1
+        assert all(1.85 < r < 2.2 for r in rp), rp
