@@ -24,7 +24,7 @@ import scipy.sparse.linalg as spla
 from .mesh import Mesh
 from .fem import Operator
 from .transfer import Transfer, _parent
-from .relax import Vanka, BSR
+from .relax import Vanka, BSR, vertex_patches
 
 
 def coarsen_Kinv(fine: Mesh, coarse: Mesh, Kinv_f):
@@ -70,13 +70,29 @@ class CoarseSolver:
         return self.lu.solve(r)
 
 
+def reversed_rows(A):
+    """The same CSR matrix with every row stored in reverse column order, so that a matvec sums
+    each row in the opposite order (an equally legal fp64 evaluation; used by alt_order)."""
+    B = A.copy()
+    for i in range(B.shape[0]):
+        s, e = B.indptr[i], B.indptr[i + 1]
+        B.indices[s:e] = B.indices[s:e][::-1].copy()
+        B.data[s:e] = B.data[s:e][::-1].copy()
+    B.has_sorted_indices = False
+    return B
+
+
 class Hierarchy:
     """Per-level operators, transfers and smoothers.
 
-    relax: 'vanka' or 'bsr'.  levels = number of levels L (level 0 finest)."""
+    relax: 'vanka' or 'bsr'.  levels = number of levels L (level 0 finest).
+    alt_order=True builds the same method with every summation order reversed (CSR rows,
+    patch DoF order, hence the pivot order of the patch solves): the spread between the two
+    runs calibrates the fp64 rounding floor of the parity criterion (SURVEY.md 8(c) c-11,
+    DESIGN.md reading A22).  It changes no arithmetic of the method."""
 
     def __init__(self, n, levels, lam, mu, tau, alpha, inv_M, mu_f=1.0, K=1.0, Kinv_field=None,
-                 relax="vanka"):
+                 relax="vanka", alt_order=False):
         if levels < 1 or n % (2 ** (levels - 1)) != 0 or n // (2 ** (levels - 1)) < 2:
             raise ValueError("n must be divisible by 2^(levels-1) with coarsest n >= 2")
         self.levels = levels
@@ -93,8 +109,18 @@ class Hierarchy:
                 self.transfers.append(Transfer(self.meshes[l - 1], m))
         self.relax = relax
         for l in range(levels - 1):
-            self.smoothers.append(Vanka(self.ops[l]) if relax == "vanka" else BSR(self.ops[l]))
+            if relax == "vanka":
+                pat = [p[::-1] for p in vertex_patches(self.meshes[l], "full")] if alt_order else None
+                self.smoothers.append(Vanka(self.ops[l], pat))
+            else:
+                self.smoothers.append(BSR(self.ops[l], reverse=alt_order))
         self.coarse = CoarseSolver(self.ops[-1])
+        if alt_order:
+            for op in self.ops:
+                op.A = reversed_rows(op.A)
+            for tr in self.transfers:
+                tr.P = reversed_rows(tr.P)
+                tr.R = reversed_rows(tr.R)
 
     def smooth(self, l, x, b, opts):
         if self.relax == "vanka":

@@ -143,7 +143,7 @@ class DispVanka:
     """A_{V,u}^{-1}: additive Vanka with 8-DoF displacement patches on A_u^RQ
     (Fig. fig:patches left, eq. F-Vanka)."""
 
-    def __init__(self, op: Operator):
+    def __init__(self, op: Operator, reverse: bool = False):
         mesh = op.mesh
         Au = op.Au
         # positions in the displacement block: active slots of planes 0..4 in op.iu order
@@ -158,7 +158,7 @@ class DispVanka:
             pos = posu[np.array(slots)]
             pos = pos[pos >= 0]
             if pos.size:
-                patches.append(pos)
+                patches.append(pos[::-1] if reverse else pos)
         count = np.zeros(Au.shape[0])
         for p in patches:
             count[p] += 1
@@ -186,9 +186,9 @@ class DispVanka:
 class BSR:
     """Inexact Braess-Sarazin relaxation."""
 
-    def __init__(self, op: Operator, d: int = 2):
+    def __init__(self, op: Operator, d: int = 2, reverse: bool = False):
         self.op = op
-        self.Fu = DispVanka(op)
+        self.Fu = DispVanka(op, reverse)
         self.Dw = op.Mw.diagonal()                              # D_w = diag(M_w)
         s0 = op.inv_M + op.alpha ** 2 / (op.lam + 2.0 * op.mu / d)
         self.S = (s0 * op.Mp + op.tau * (op.Bw @ sp.diags(1.0 / self.Dw) @ op.Bw.T)).tocsr()
