@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 monolithic multigrid hot path (BASELINE.json metric).
+
+A step is one V(1,1) cycle of the whole hot path (residual, additive Vanka or
+inexact Braess-Sarazin relaxation, divergence-preserving restriction / prolongation, coarsest
+solve, fused residual norm) on the BASELINE workload, default config 5: 4096^2 cells, 11 levels,
+lambda = 100, mu = 1, K = 1e-2, tau = alpha = 1, 1/M = 1, b ~ U(-1,1) from seed 5, x0 = 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+* value: DoF-updates/s = active unknowns of level 0 x cycles (x ranks) / max-over-ranks device time
+  of the K timed cycles (CUDA events on the launching stream, inputs resident in HBM).
+* e2e: the same metric through the public C-ABI call with HOST buffers (mg_solve_host: pinned host
+  b and x copied in, K cycles, x copied back) timed by wall clock.
+* roofline: the dominant kernel (level-0 Vanka sweep, 2 launches per cycle) -- algorithmic bytes
+  (24 B per active DoF: read x, read b, write x) / its CUDA-event duration, against the measured
+  HBM copy bandwidth of MEASURED_PEAKS.json.
+* cpu_baseline / --impl reference: the CPU oracle (oracle/, test infrastructure) timed as it
+  stands on a bounded sample of the same workload (same parameters and RHS recipe on a smaller
+  grid, since the oracle cannot hold the 4096^2 operator).
+Multi-GPU (torchrun): every rank solves its own copy of the problem (independent problems, no
+data-path collective; weak scaling); barrier + max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import mg_inputs  # noqa: E402
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def workload(cfg_id: int):
+    c = dict(mg_inputs.CONFIGS[cfg_id])
+    relax = "bsr" if c["relax"] == "bsr" else "vanka"
+    c["relax_used"] = relax
+    return c
+
+
+def opts_for(c):
+    from paper_2107_04060_b200 import Opts
+    if c["relax_used"] == "vanka":
+        return Opts(1, 1, "vanka", c["omega"])
+    return Opts(1, 1, "bsr", c["bsr_omega"], c["omega_J"], 3)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for ln in self.lines:
+            try:
+                a, b, r = [p.strip() for p in ln.split(",")]
+                sm.append(float(a))
+                mx = max(mx, float(b))
+                bits = int(r, 16)
+                for k, v in REASONS.items():
+                    if bits & k and v != "gpu_idle":
+                        reasons.add(v)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def oracle_sample(c, cycles: int, warmup: int = 1, n_sample: int = 128):
+    """Time the oracle V(1,1) cycle on an n_sample^2 grid with the workload's parameters."""
+    from oracle.cycle import Hierarchy as OH
+    levels = max(2, int(np.log2(n_sample // 4)) + 1)
+    kinv = None if c["K_seed"] is None else 1.0 / mg_inputs.lognormal_K(n_sample, c["K_seed"])
+    H = OH(n_sample, levels, c["lam"], c["mu"], c["tau"], c["alpha"], c["inv_M"], c["mu_f"],
+           K=c["K"] if c["K"] is not None else 1.0, Kinv_field=kinv, relax=c["relax_used"])
+    b = H.meshes[0].to_active(mg_inputs.uniform_rhs(n_sample, c["b_seed"]))
+    o = opts_for(c)
+    od = dict(nu1=1, nu2=1, omega=o.omega, omega_J=o.omega_J, jacobi_sweeps=o.jacobi_sweeps)
+    x = np.zeros_like(b)
+    for _ in range(warmup):
+        x = H.cycle(x, b, od)
+    times = []
+    for _ in range(cycles):
+        t = time.perf_counter()
+        x = H.cycle(x, b, od)
+        times.append(time.perf_counter() - t)
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        cores = 1
+    nact = mg_inputs.n_active(n_sample)
+    return dict(value=nact * len(times) / sum(times), ms=1e3 * sum(times) / len(times), cores=cores,
+                sample=f"oracle V(1,1) on {n_sample}^2 ({levels} levels, {nact} active DoFs), same parameters and "
+                       f"RHS recipe, {len(times)} cycles after {warmup} warm-up; host has {os.cpu_count()} cores, "
+                       f"numpy/scipy (sparse matvec single-threaded, BLAS threads {cores})")
+
+
+def run_reference(args, c, rank, world):
+    if rank != 0:
+        return
+    s = oracle_sample(c, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": "DoF-updates/s per V(1,1) cycle (fp64)", "value": s["value"],
+            "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": s["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {args.config} (bounded sample, see cpu_baseline)"},
+            "cpu_baseline": {"value": s["value"], "unit": "DoF/s", "cores": s["cores"], "kind": "oracle",
+                             "sample": s["sample"]},
+            "e2e": {"value": s["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--trace-cycles", type=int, default=10)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    c = workload(args.config)
+    if args.impl == "reference":
+        return run_reference(args, c, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2107_04060_b200 import Hierarchy
+    n, L = c["n"], c["levels"]
+    kf = None if c["K_seed"] is None else mg_inputs.lognormal_K(n, c["K_seed"])
+    H = Hierarchy(n, L, c["lam"], c["mu"], K=c["K"] if c["K"] is not None else 1.0, tau=c["tau"],
+                  alpha=c["alpha"], inv_M=c["inv_M"], mu_f=c["mu_f"], K_field=kf)
+    o = opts_for(c)
+    b_host = mg_inputs.uniform_rhs(n, c["b_seed"])
+    b = H.to_device(b_host)
+    x = H.zeros()
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    nact = H.n_active(0)
+    for _ in range(args.warmup):
+        H.cycle_async(x, b, o, nrm)
+    torch.cuda.synchronize()
+    launches_per_cycle = H.cycle_kernels()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            H.cycle_async(x, b, o, nrm)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    res_norm = float(nrm.sqrt().item())
+
+    # kernel-class timing of the same cycle (event-traced graph, separate pass)
+    H.set_timing(True)
+    phases = np.zeros(5)
+    for _ in range(args.trace_cycles):
+        H.cycle_async(x, b, o, nrm)
+        phases += np.array(H.timing())
+    phases /= args.trace_cycles
+    H.set_timing(False)
+
+    # e2e through the public C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        bp = torch.from_numpy(b_host).pin_memory().numpy()
+        xp = torch.zeros(b_host.shape, dtype=torch.float64).pin_memory().numpy()
+        H.solve_host(xp, bp, o, rtol=0.0, max_cycles=2)              # warm the e2e buffers
+        xp[:] = 0.0
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        rc, hist = H.solve_host(xp, bp, o, rtol=0.0, max_cycles=args.steps)
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        cyc = len(hist) - 1
+        vbytes = 10 * (n + 1) * (n + 1) * 8
+        e2e = {"value": nact * cyc * world / el, "unit": "DoF/s", "h2d_bytes_per_step": 2 * vbytes / cyc,
+               "d2h_bytes_per_step": (vbytes + 8 * (cyc + 1)) / cyc,
+               "note": f"mg_solve_host of {cyc} cycles: pinned host b, x0 in; x, history out; bytes amortised per cycle"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = peaks()
+    relax_ms = (phases[0] + phases[4]) / 2.0
+    if o.relax == "vanka":
+        alg_bytes = 24.0 * nact                 # read x, read b, write x over the active DoFs
+        dom = "vanka_kernel (level 0, fused residual + 20-DoF patch solves + update)"
+    else:
+        alg_bytes = 8.0 * nact * 4.8 + 8.0 * 0.2 * nact   # 3 + 1.8 passes (+0.2 K field)
+        dom = "BSR relaxation (level 0: bsr_a + 2 jacobi + bsr_b)"
+    achieved = alg_bytes / (relax_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("config") == args.config:
+            traffic = tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    sum_levels = sum(mg_inputs.n_active(n >> l) for l in range(L))
+    passes = 10.5 if o.relax == "vanka" else 14.7 if c["K_seed"] is not None else 14.1
+    cycle_bytes = 8.0 * passes * sum_levels
+    ms_step = ms / args.steps
+    line = {
+        "metric": "DoF-updates/s per V(1,1) cycle (fp64) at 4096^2; ms per cycle; % of HBM roofline",
+        "value": nact * args.steps * world / (ms * 1e-3),
+        "unit": "DoF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE config {args.config}: {n}^2 cells, {L} levels, V(1,1) {o.relax}, "
+                               f"lambda={c['lam']}, mu={c['mu']}, K={'exp(N(0,4)) field' if kf is not None else c['K']}, "
+                               f"tau=alpha=1/M=1, b~U(-1,1) seed {c['b_seed']}, x0=0",
+                   "n": n, "levels": L, "relax": o.relax, "omega": o.omega,
+                   "omega_J": o.omega_J if o.relax == "bsr" else None,
+                   "active_dofs": nact, "l2": "inputs larger than L2 (one vector = %.2f GB)" % (10 * (n + 1) * H.pitch(0) * 8 / 1e9),
+                   "final_residual_norm": res_norm},
+        "gpu_launches": launches_per_cycle * args.steps,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": dom, "kernel_ms": relax_ms,
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+        "cycle_roofline": {"algorithmic_bytes": cycle_bytes, "achieved_gbs": cycle_bytes / (ms_step * 1e-3) / 1e9,
+                           "frac": cycle_bytes / (ms_step * 1e-3) / 1e9 / peak,
+                           "phase_ms": {"pre": phases[0], "restrict": phases[1], "coarse_levels": phases[2],
+                                        "prolong": phases[3], "post": phases[4]}},
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        s = oracle_sample(c, 20)
+        line["cpu_baseline"] = {"value": s["value"], "unit": "DoF/s", "cores": s["cores"], "kind": "oracle",
+                                "sample": s["sample"]}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

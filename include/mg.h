@@ -1,0 +1,210 @@
+/*
+ * mg.h -- C ABI of the B200 (sm_100a) monolithic multigrid hot path for the
+ * reduced-quadrature P1+bubble / RT0 / P0 three-field Biot discretisation of
+ * arXiv 2107.04060 ("Monolithic multigrid for a reduced-quadrature
+ * discretization of poroelasticity").  Citations "PAPER.md:N" are lines of the
+ * paper's LaTeX source; "SURVEY" is /root/repo/SURVEY.md; "reading Ak" is the
+ * numbered reading in DESIGN.md.
+ *
+ * PROBLEM (eq. block_form_rq).  One
+ * backward-Euler step of the three-field Biot model on the unit square, n x n
+ * cells each cut top-left -> bottom-right, u = 0 and w.n = 0 on
+ * the whole boundary:
+ *
+ *   A^RQ [u; w; p] = b,   A^RQ = [[A_u^RQ, 0, alpha B_u^T],
+ *                                 [0, tau M_w, tau B_w^T],
+ *                                 [alpha B_u, tau B_w, -(1/M) M_p]],
+ *   A_u^RQ = 2 mu A_eps + lambda B_u^T M_p^{-1} B_u,
+ *   M_w = (mu_f K^{-1} w, r),  K scalar or per triangle.
+ *
+ * VECTOR LAYOUT (every x, b, r, e below).  A level-l vector is 10 fp64 planes;
+ * plane k holds (n_l + 1) rows of mg_pitch(ctx, l) doubles; entry (k, j, i)
+ * is at k*(n_l+1)*pitch + j*pitch + i, 0 <= i, j <= n_l, x = i h, y = j h.
+ * Index (i, j) owns vertex (i,j), the edges H(i,j) = (i,j)-(i+1,j) [normal +y],
+ * V(i,j) = (i,j)-(i,j+1) [normal +x], D(i,j) = (i+1,j)-(i,j+1) [normal
+ * (1,1)/sqrt2] and the triangles LL = [(i,j),(i+1,j),(i,j+1)] and
+ * UR = [(i+1,j),(i+1,j+1),(i,j+1)] of cell (i,j)  (readings A1, A2):
+ *
+ *   plane 0/1  u_x / u_y (P1)          active iff 0<i<n, 0<j<n
+ *   plane 2    face bubble on H(i,j)   active iff i<n, 0<j<n
+ *   plane 3    face bubble on V(i,j)   active iff 0<i<n, j<n
+ *   plane 4    face bubble on D(i,j)   active iff i<n, j<n
+ *   plane 5-7  RT0 on H / V / D        as planes 2-4
+ *   plane 8/9  P0 on LL / UR           active iff i<n, j<n
+ *
+ * Bubbles are 4 lambda_a lambda_b n_e (normal trace 1 at the midpoint), RT0
+ * functions have normal trace 1 (reading A1).  Inactive and padding slots are
+ * 0 on input and are written as 0 on output.  The number of active unknowns is
+ * 10 n^2 - 8 n + 2 (the paper counts 10 n^2 + 8 n + 2 slots, tab:mgtime
+ * PAPER.md:1100-1104).
+ *
+ * HIERARCHY.  Level l has n_l = n / 2^l cells per side, l = 0 .. levels-1;
+ * operators are rediscretised on every level; level
+ * levels-1 is solved exactly.  A per-triangle K field is
+ * coarsened by averaging K^{-1} over the four children (reading A11).
+ *
+ * OWNERSHIP.  The caller owns every pointer passed in (x, b, r, e: DEVICE
+ * pointers to mg_vec_len(ctx, level) doubles, 8-byte aligned; *_host: host
+ * pointers) and every stream.  The context owns all per-level tables, the
+ * level >= 1 work vectors, one scratch vector per level, the K^{-1} pyramid
+ * and the coarsest inverse; they are allocated in mg_setup through the
+ * allocator installed with mg_set_allocator (default cudaMalloc) and released
+ * by mg_free.  A context must not be used from two host threads or two
+ * streams at the same time.
+ *
+ * ERRORS.  Every int function returns MG_OK (0) on success, a negative code on
+ * failure (message in mg_last_error(), thread local), or a positive status
+ * (MG_NOTCONV, MG_DIVERGED) from mg_solve.  Nothing aborts or throws across
+ * the ABI.  Device work is enqueued asynchronously on the given stream unless
+ * stated otherwise; functions returning host data synchronise that stream.
+ */
+#ifndef MG_H
+#define MG_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MG_OK        0
+#define MG_NOTCONV   1   /* mg_solve: max_cycles reached; history filled              */
+#define MG_DIVERGED  2   /* mg_solve: ||r_k|| > 1e8 ||r_0|| or non-finite  */
+#define MG_EINVAL   (-1) /* bad argument: see mg_last_error()                           */
+#define MG_ECUDA    (-2) /* CUDA runtime / driver error                                 */
+#define MG_ENOMEM   (-3) /* allocation failed                                           */
+
+#define MG_VANKA 0       /* additive Vanka, 20-DoF vertex patches    */
+#define MG_BSR   1       /* inexact Braess-Sarazin                   */
+
+typedef struct mg_ctx mg_ctx;
+
+typedef struct {
+    int32_t n;              /* finest cells per side; h = 1/n.  n divisible by 2^(levels-1)  */
+    const double* K_field;  /* NULL -> scalar K of mg_setup.  Else DEVICE pointer to 2 x n x n
+                               doubles [shape (0 = LL, 1 = UR)][j][i], the permeability of each
+                               triangle (> 0, finite); copied during mg_setup                     */
+    double inv_M;           /* 1/M >= 0 (Biot modulus); BASELINE configs use 1   */
+    double mu_f;            /* fluid viscosity > 0; 1                            */
+} mg_grid;
+
+typedef struct {
+    int32_t nu1, nu2;       /* pre / post relaxation sweeps (BASELINE: 1, 1)                 */
+    int32_t relax;          /* MG_VANKA or MG_BSR                                             */
+    double  omega;          /* outer damping                              */
+    double  omega_J;        /* BSR: weight of the Jacobi sweeps on S          */
+    int32_t jacobi_sweeps;  /* BSR: sweeps on S from dp = 0 (BASELINE: 3; paper: 1)          */
+} mg_cycle_opts;
+
+/* Device memory hooks: alloc(bytes, user) -> device pointer or NULL; free(ptr, user).
+ * Installed for the contexts created afterwards.  NULL, NULL restores cudaMalloc/cudaFree. */
+typedef void* (*mg_alloc_fn)(size_t bytes, void* user);
+typedef void  (*mg_free_fn)(void* ptr, void* user);
+void mg_set_allocator(mg_alloc_fn alloc, mg_free_fn free_, void* user);
+
+/* Build the hierarchy (host fp64 tables: stencils, deflated patch inverses, coarsest inverse;
+ * PAPER.md:477-484, 572-590, 945) and upload it to the current device.  Synchronous.
+ * lambda >= 0, mu > 0, K > 0 (ignored when grid->K_field != NULL), tau > 0, alpha finite,
+ * 1 <= levels, n_{levels-1} = n / 2^(levels-1) >= 2.  Errors: MG_EINVAL, MG_ECUDA, MG_ENOMEM. */
+int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau, double alpha,
+             int32_t levels, mg_ctx** out);
+void mg_free(mg_ctx* ctx);
+
+int32_t mg_levels (const mg_ctx* ctx);
+int32_t mg_level_n(const mg_ctx* ctx, int32_t level);  /* n_l, or -1 if level out of range   */
+int32_t mg_pitch  (const mg_ctx* ctx, int32_t level);  /* row pitch in doubles (multiple of 32) */
+int64_t mg_vec_len(const mg_ctx* ctx, int32_t level);  /* 10 (n_l+1) pitch                     */
+int64_t mg_n_active(const mg_ctx* ctx, int32_t level); /* 10 n_l^2 - 8 n_l + 2                 */
+
+/* r = b - A_l x on the active slots (eq. block_form_rq), r = 0 elsewhere.  r may be NULL (norm
+ * only).  norm2_dev: NULL or a DEVICE double receiving ||r||_2^2 over the active slots
+ * (deterministic order).  r must not alias x or b. */
+int mg_residual(mg_ctx* ctx, int32_t level, const double* x, const double* b, double* r,
+                double* norm2_dev, cudaStream_t s);
+
+/* `sweeps` additive Vanka sweeps on level l:
+ *   x <- x + omega sum_v V_v^T D_v (V_v A_l V_v^T)^{-1} V_v (b - A_l x),
+ * one patch per vertex, truncated to active DoFs (reading A8), natural weights D (1, 1/2, 1/3;
+ * PAPER.md:586-587), exactly deflated patch solves (reading A9).  In place on x; the context's
+ * level-l scratch vector is used for the out-of-place sweep.  Constant K only (reading A20). */
+int mg_relax_vanka(mg_ctx* ctx, int32_t level, double* x, const double* b, double omega,
+                   int32_t sweeps, cudaStream_t s);
+
+/* One inexact Braess-Sarazin relaxation on level l (App. D-E):
+ *   r = b - A x;  z_u = F_u^{-1} r_u (8-DoF displacement Vanka, weights 1, 1/2);
+ *   z_w = (tau D_w)^{-1} r_w;  g = alpha B_u z_u + tau B_w z_w - r_p;
+ *   dp = jacobi_sweeps weighted-Jacobi sweeps (weight omega_J) on
+ *        S dp = g,  S = (1/M + alpha^2/(lambda + mu)) M_p + tau B_w D_w^{-1} B_w^T, from dp = 0;
+ *   du = F_u^{-1}(r_u - alpha B_u^T dp);  dw = (tau D_w)^{-1}(r_w - tau B_w^T dp);
+ *   x += omega (du, dw, dp).   In place on x.  `sweeps` repetitions. */
+int mg_relax_bsr(mg_ctx* ctx, int32_t level, double* x, const double* b, double omega,
+                 double omega_J, int32_t jacobi_sweeps, int32_t sweeps, cudaStream_t s);
+
+/* b_coarse = P^T r_fine between levels fine_level and fine_level+1 (R = P^T, PAPER.md:484;
+ * P_u divergence preserving PAPER.md:510-566, P_w / P_p canonical).  Overwrites b_coarse. */
+int mg_restrict(mg_ctx* ctx, int32_t fine_level, const double* r_fine, double* b_coarse,
+                cudaStream_t s);
+/* x_fine += P e_coarse (same P).  In place on x_fine. */
+int mg_prolong(mg_ctx* ctx, int32_t fine_level, const double* e_coarse, double* x_fine,
+               cudaStream_t s);
+/* x = A_L^{-1} b on the coarsest level L = levels-1 (dense deflated inverse, reading A9). */
+int mg_coarse_solve(mg_ctx* ctx, const double* b, double* x, cudaStream_t s);
+
+/* One V(nu1, nu2) cycle on level 0 (recursed), in place on x.
+ * res_norm_host: NULL or receives ||b - A_0 x||_2 after the cycle (then the stream is
+ * synchronised).  The level sequence is captured once into a CUDA graph per (x, b, opts) and
+ * replayed. */
+int mg_cycle(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts,
+             double* res_norm_host, cudaStream_t s);
+
+/* One V-cycle without any host synchronisation (the building block of mg_solve and of the
+ * benchmark).  in_norm2_dev: NULL or a DEVICE double receiving ||b - A_0 x_in||_2^2 for the INPUT
+ * x, fused into the level-0 pre-relaxation (no extra pass; deterministic order).  Graph-cached
+ * like mg_cycle. */
+int mg_cycle_async(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts,
+                   double* in_norm2_dev, cudaStream_t s);
+
+/* Kernel-class tracing.  enable != 0: cycles captured afterwards record CUDA events between the
+ * level-0 phases; mg_timing (synchronises the stream of the last cycle) returns the elapsed ms of
+ * the most recent cycle per phase: [0] level-0 pre-relaxation, [1] level-0 residual+restriction,
+ * [2] all coarser levels including the coarsest solve, [3] level-0 prolongation, [4] level-0
+ * post-relaxation.  Returns MG_EINVAL if no traced cycle ran. */
+int mg_set_timing(mg_ctx* ctx, int32_t enable);
+/* Number of kernel nodes of the most recently captured cycle graph (all of them libmg kernels). */
+int32_t mg_cycle_kernels(const mg_ctx* ctx);
+int mg_timing(mg_ctx* ctx, float* ms5);
+
+/* Stationary iteration of V-cycles from the given x until ||r_k|| <= rtol ||r_0|| or
+ * max_cycles.  history_host: NULL or max_cycles+1 doubles, history[k] = ||b - A x_k||_2
+ * (history[0] for the input x).  *n_cycles = cycles done.  Returns MG_OK, MG_NOTCONV or
+ * MG_DIVERGED (or an error).  Synchronous. */
+int mg_solve(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts, double rtol,
+             int32_t max_cycles, double* history_host, int32_t* n_cycles, cudaStream_t s);
+
+/* mg_solve with HOST vectors in the unpadded layout [10][n+1][n+1] (the end-to-end path):
+ * b_host is copied to the device, x starts at x_host, the solution is copied back to x_host.
+ * Host buffers should be pinned for full copy bandwidth.  Synchronous. */
+int mg_solve_host(mg_ctx* ctx, double* x_host, const double* b_host, const mg_cycle_opts* opts,
+                  double rtol, int32_t max_cycles, double* history_host, int32_t* n_cycles,
+                  cudaStream_t s);
+
+const char* mg_last_error(void);
+
+/* ---- host-only diagnostics (no GPU needed; used by the CPU test-suite) -------------------
+ * Fill the level tables mg_setup would upload, for a level of n cells, scalar K:
+ *   stencil_coef[141]  merged stencil coefficients of A^RQ without M_w (mg_tables.h order)
+ *   ww[18]             tau mu_f K^{-1} h^2 (M_w1)_{shape,e,e'}
+ *   vanka[9*400]       per vertex class c = cx + 3 cy (cx: 0 interior, 1 at i=0, 2 at i=n),
+ *                      the weighted deflated patch inverse D_v K_v^{-1} (20x20, slot order of
+ *                      DESIGN.md section 4), rows/cols of inactive slots 0
+ *   disp[9*64]         same for the 8-DoF displacement patches of BSR: D_v (A_u^RQ)_v^{-1}
+ * Returns MG_OK or MG_EINVAL. */
+int mg_host_level_tables(int32_t n, double lambda, double mu, double K, double tau, double alpha,
+                         double inv_M, double mu_f, double* stencil_coef, double* ww,
+                         double* vanka, double* disp);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MG_H */

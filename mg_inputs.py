@@ -86,16 +86,19 @@ def lognormal_K(n: int, seed: int, sigma: float = 2.0) -> np.ndarray:
 
 # BASELINE.json configs.  1/M = 1 and mu_f = 1 (readings A5, A6 of DESIGN.md;
 # with 1/M = 1e-6 the rediscretised V-cycle diverges like 1/gamma at these parameters, see E0).
-# omega / omega_J: experiment E0 (tools/e0_omega_scan.py) -- filled in below.
+# omega / omega_J: the minimisers of experiment E0 (tools/e0_omega_scan.py,
+# tests/golden/e0_omega_scan.json; V(1,1) on 64^2, 5 levels): Vanka 0.74 (configs 1/2),
+# 0.70 (configs 3, 5); BSR (omega_J, omega) = (1.0, 0.75) (config 2) and (0.7, 0.3) for the
+# heterogeneous config 4, where every scanned pair diverges (reading A24).
 CONFIGS = {
     1: dict(n=16, levels=3, lam=1.0, mu=1.0, K=1.0, tau=1.0, alpha=1.0, inv_M=1.0, mu_f=1.0,
-            b_seed=0, K_seed=None, relax="vanka", cycles=10),
+            b_seed=0, K_seed=None, relax="vanka", cycles=10, omega=0.74),
     2: dict(n=256, levels=7, lam=1.0, mu=1.0, K=1.0, tau=1.0, alpha=1.0, inv_M=1.0, mu_f=1.0,
-            b_seed=1, K_seed=None, relax="vanka+bsr", cycles=20),
+            b_seed=1, K_seed=None, relax="vanka+bsr", cycles=20, omega=0.74, bsr_omega=0.75, omega_J=1.0),
     3: dict(n=1024, levels=9, lam=1e6, mu=1.0, K=1e-6, tau=1.0, alpha=1.0, inv_M=1.0, mu_f=1.0,
-            b_seed=2, K_seed=None, relax="vanka", rtol=1e-8),
+            b_seed=2, K_seed=None, relax="vanka", rtol=1e-8, omega=0.70),
     4: dict(n=2048, levels=10, lam=1.0, mu=1.0, K=None, tau=1.0, alpha=1.0, inv_M=1.0, mu_f=1.0,
-            b_seed=4, K_seed=3, relax="bsr", cycles=20),
+            b_seed=4, K_seed=3, relax="bsr", cycles=20, bsr_omega=0.3, omega_J=0.7),
     5: dict(n=4096, levels=11, lam=100.0, mu=1.0, K=1e-2, tau=1.0, alpha=1.0, inv_M=1.0, mu_f=1.0,
-            b_seed=5, K_seed=None, relax="vanka", rtol=1e-8),
+            b_seed=5, K_seed=None, relax="vanka", rtol=1e-8, omega=0.70),
 }

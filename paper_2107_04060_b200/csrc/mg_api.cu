@@ -1,0 +1,650 @@
+// C ABI of the B200 monolithic multigrid hot path (include/mg.h): context and hierarchy setup,
+// the per-operation entry points and the V-cycle driver (captured once into a CUDA graph per
+// (x, b, options) and replayed).  mg_solve keeps the iteration on the device: the level-0
+// pre-smoothing kernel of each cycle fuses the residual norm of its input, the block that
+// completes that norm appends it to the history and raises a stop flag that every later kernel
+// polls at entry, so cycles can be launched ahead without host round trips.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "mg_internal.h"
+#include "mg_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+mg_alloc_fn g_alloc = nullptr;
+mg_free_fn g_free = nullptr;
+void* g_user = nullptr;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) return fail(MG_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct Level {
+    int n = 0, pitch = 0;
+    int64_t plane = 0, len = 0;
+    double* x = nullptr;     // level >= 1 iterate
+    double* b = nullptr;     // level >= 1 right-hand side
+    double* t = nullptr;     // scratch for out-of-place sweeps
+    double* g = nullptr;     // BSR: 2 planes
+    double* dpa = nullptr;   // BSR: 2 planes
+    double* dpb = nullptr;
+    double* kinv = nullptr;  // 2 planes, heterogeneous K only
+    double* gbnd = nullptr;  // 9 x 400
+    double* ubnd = nullptr;  // 9 x 64
+    VankaParams vp;
+    DispParams up;
+};
+
+struct GraphEntry {
+    const double* x;
+    const double* b;
+    mg_cycle_opts o;
+    int solve;            // 0 plain, 1 solve state, 2 fused input norm into `nout`
+    const double* nout;
+    bool timed;
+    cudaGraphExec_t exec;
+};
+
+}  // namespace
+
+struct mg_ctx {
+    int levels = 0;
+    Material m{};
+    bool het = false;
+    std::vector<Level> L;
+    int Nc = 0;
+    double* Ginv = nullptr;
+    int64_t* slots = nullptr;
+    // norms
+    double* partials = nullptr;
+    unsigned* counter = nullptr;
+    double* norm = nullptr;
+    int* stop = nullptr;
+    SolveState* state = nullptr;  // device struct
+    double* hist = nullptr;
+    int hist_cap = 0;
+    double* pinned = nullptr;     // host: 4 doubles
+    // e2e buffers
+    double* hx = nullptr;
+    double* hb = nullptr;
+    std::vector<void*> allocs;
+    std::vector<GraphEntry> graphs;
+    cudaStream_t cap = nullptr;   // capture stream
+    bool timing = false;
+    bool timed_ran = false;
+    int launches = 0;             // kernel launches enqueued by the last captured cycle
+    cudaEvent_t ev[6] = {};
+};
+
+namespace {
+
+void* dalloc(mg_ctx* c, size_t bytes) {
+    void* p = nullptr;
+    if (g_alloc) p = g_alloc(bytes, g_user);
+    else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+    if (p) c->allocs.push_back(p);
+    return p;
+}
+
+void dfree_all(mg_ctx* c) {
+    for (void* p : c->allocs) {
+        if (g_free) g_free(p, g_user);
+        else cudaFree(p);
+    }
+    c->allocs.clear();
+}
+
+int pitch_of(int n) { return ((n + 1 + 31) / 32) * 32; }
+
+bool aligned(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) % 8 == 0); }
+
+int check_level(const mg_ctx* c, int level, int maxl) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (level < 0 || level > maxl) return fail(MG_EINVAL, "level %d out of range [0, %d]", level, maxl);
+    return MG_OK;
+}
+
+NormSink no_norm() { return NormSink{nullptr, nullptr, nullptr, nullptr}; }
+
+// one relaxation sweep on level l: xin -> xout (out of place)
+int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xout, bool xzero,
+               const mg_cycle_opts& o, NormSink S, cudaStream_t s) {
+    Level& Lv = c->L[l];
+    if (o.relax == MG_VANKA) {
+        VankaParams P = Lv.vp;
+        P.omega = o.omega;
+        CK(launch_vanka(P, xin, b, xout, xzero, S, s));
+        return MG_OK;
+    }
+    const double omJ = o.jacobi_sweeps >= 1 ? o.omega_J : 0.0;
+    CK(launch_bsr_a(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s));
+    double* cur = Lv.dpa;
+    double* nxt = Lv.dpb;
+    for (int k = 1; k < o.jacobi_sweeps; ++k) {
+        CK(launch_bsr_jacobi(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
+        std::swap(cur, nxt);
+    }
+    CK(launch_bsr_b(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
+    return MG_OK;
+}
+
+// enqueue one V(nu1, nu2) cycle (PAPER.md:471-476 recursed).  solve != 0: the
+// first level-0 operation appends ||b - A x||^2 to the solve state.
+int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& o, int solve, double* nout,
+                  bool timed, cudaStream_t s) {
+    const int Lc = c->levels - 1;
+    std::vector<double*> cur(c->levels, nullptr);
+    NormSink S = no_norm();
+    if (solve == 1) S = NormSink{nullptr, c->partials, c->counter, c->state};
+    if (solve == 2) S = NormSink{nout, c->partials, c->counter, nullptr};
+    auto mark = [&](int i) -> int {
+        if (timed) CK(cudaEventRecordWithFlags(c->ev[i], s, cudaEventRecordExternal));
+        return MG_OK;
+    };
+    if (int rc = mark(0)) return rc;
+    if (solve && o.nu1 == 0) {
+        CK(launch_residual(c->L[0].vp.L, x0, b0, nullptr, S, s));
+        S = no_norm();
+    }
+    for (int l = 0; l < Lc; ++l) {
+        Level& Lv = c->L[l];
+        double* xl = l == 0 ? x0 : Lv.x;
+        const double* bl = l == 0 ? b0 : Lv.b;
+        const bool zero = l > 0;
+        double* a = xl;
+        double* t = Lv.t;
+        for (int k = 0; k < o.nu1; ++k) {
+            int rc = relax_once(c, l, a, bl, t, zero && k == 0, o, l == 0 && k == 0 ? S : no_norm(), s);
+            if (rc) return rc;
+            std::swap(a, t);
+        }
+        if (l == 0)
+            if (int rc = mark(1)) return rc;
+        if (zero && o.nu1 == 0) CK(cudaMemsetAsync(xl, 0, sizeof(double) * Lv.len, s));
+        const int mode = (zero && o.nu1 == 0) ? 2 : 1;
+        CK(launch_restrict(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, mode, a, bl, c->L[l + 1].b, s));
+        if (l == 0)
+            if (int rc = mark(2)) return rc;
+        cur[l] = a;
+    }
+    CK(launch_coarse(c->Nc, c->Ginv, c->slots, c->L[Lc].b, c->L[Lc].x, c->stop, s));
+    cur[Lc] = c->L[Lc].x;
+    for (int l = Lc - 1; l >= 0; --l) {
+        Level& Lv = c->L[l];
+        if (l == 0)
+            if (int rc = mark(3)) return rc;
+        CK(launch_prolong(Lv.n, Lv.pitch, c->L[l + 1].n, c->L[l + 1].pitch, cur[l + 1], cur[l], c->stop, s));
+        if (l == 0)
+            if (int rc = mark(4)) return rc;
+        const double* bl = l == 0 ? b0 : Lv.b;
+        double* xl = l == 0 ? x0 : Lv.x;
+        double* a = cur[l];
+        double* t = (a == xl) ? Lv.t : xl;
+        for (int k = 0; k < o.nu2; ++k) {
+            int rc = relax_once(c, l, a, bl, t, false, o, no_norm(), s);
+            if (rc) return rc;
+            std::swap(a, t);
+        }
+        if (l == 0 && a != x0) CK(cudaMemcpyAsync(x0, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+        cur[l] = a;
+    }
+    return mark(5);
+}
+
+bool same_opts(const mg_cycle_opts& a, const mg_cycle_opts& b) {
+    return a.nu1 == b.nu1 && a.nu2 == b.nu2 && a.relax == b.relax && a.omega == b.omega &&
+           a.omega_J == b.omega_J && a.jacobi_sweeps == b.jacobi_sweeps;
+}
+
+int get_graph(mg_ctx* c, double* x, const double* b, const mg_cycle_opts& o, int solve, double* nout,
+              cudaGraphExec_t* out) {
+    for (auto& g : c->graphs)
+        if (g.x == x && g.b == b && g.solve == solve && g.nout == nout && g.timed == c->timing && same_opts(g.o, o)) {
+            *out = g.exec;
+            return MG_OK;
+        }
+    if (c->graphs.size() >= 16) {
+        cudaGraphExecDestroy(c->graphs.front().exec);
+        c->graphs.erase(c->graphs.begin());
+    }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_cycle(c, x, b, o, solve, nout, c->timing, c->cap);
+    cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(MG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    {
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(graph, nodes.data(), &nn);
+        int k = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(nd, &t);
+            if (t == cudaGraphNodeTypeKernel) ++k;
+        }
+        c->launches = k;
+    }
+    cudaGraphExec_t exec;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(MG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    c->graphs.push_back(GraphEntry{x, b, o, solve, nout, c->timing, exec});
+    *out = exec;
+    return MG_OK;
+}
+
+int check_opts(const mg_cycle_opts* o) {
+    if (!o) return fail(MG_EINVAL, "null options");
+    if (o->nu1 < 0 || o->nu2 < 0 || o->nu1 + o->nu2 < 0) return fail(MG_EINVAL, "nu1, nu2 must be >= 0");
+    if (o->relax != MG_VANKA && o->relax != MG_BSR) return fail(MG_EINVAL, "relax must be MG_VANKA or MG_BSR");
+    if (!std::isfinite(o->omega) || !std::isfinite(o->omega_J)) return fail(MG_EINVAL, "omega not finite");
+    if (o->relax == MG_BSR && o->jacobi_sweeps < 0) return fail(MG_EINVAL, "jacobi_sweeps < 0");
+    return MG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void mg_set_allocator(mg_alloc_fn a, mg_free_fn f, void* user) {
+    g_alloc = a;
+    g_free = f;
+    g_user = user;
+}
+
+const char* mg_last_error(void) { return g_err.c_str(); }
+
+int32_t mg_levels(const mg_ctx* c) { return c ? c->levels : -1; }
+int32_t mg_level_n(const mg_ctx* c, int32_t l) { return (c && l >= 0 && l < c->levels) ? c->L[l].n : -1; }
+int32_t mg_pitch(const mg_ctx* c, int32_t l) { return (c && l >= 0 && l < c->levels) ? c->L[l].pitch : -1; }
+int64_t mg_vec_len(const mg_ctx* c, int32_t l) { return (c && l >= 0 && l < c->levels) ? c->L[l].len : -1; }
+int64_t mg_n_active(const mg_ctx* c, int32_t l) {
+    return (c && l >= 0 && l < c->levels) ? n_active_of(c->L[l].n) : -1;
+}
+
+int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau, double alpha, int32_t levels,
+             mg_ctx** out) {
+    if (!out) return fail(MG_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!grid) return fail(MG_EINVAL, "grid is NULL");
+    const int n = grid->n;
+    if (levels < 1) return fail(MG_EINVAL, "levels = %d < 1", levels);
+    if (levels > 24 || n < 2 || n % (1 << (levels - 1)) != 0 || (n >> (levels - 1)) < 2)
+        return fail(MG_EINVAL, "n = %d must be divisible by 2^(levels-1) with coarsest n >= 2 (levels = %d)", n, levels);
+    if (!(mu > 0) || !(lambda >= 0) || !(tau > 0) || !std::isfinite(alpha) || !std::isfinite(lambda) ||
+        !std::isfinite(mu) || !std::isfinite(tau))
+        return fail(MG_EINVAL, "need lambda >= 0, mu > 0, tau > 0, finite alpha");
+    if (!grid->K_field && !(K > 0 && std::isfinite(K))) return fail(MG_EINVAL, "K must be > 0 and finite");
+    if (!(grid->inv_M > 0) || !std::isfinite(grid->inv_M))
+        return fail(MG_EINVAL, "inv_M must be > 0 (the deflated solves need the -(1/M) M_p block)");
+    if (!(grid->mu_f > 0)) return fail(MG_EINVAL, "mu_f must be > 0");
+    if (grid->K_field && !aligned(grid->K_field)) return fail(MG_EINVAL, "K_field not 8-byte aligned");
+    const int nc = n >> (levels - 1);
+    // the dense coarsest solve needs n_c <= 20; a single-level context (levels == 1) may be larger
+    // and then offers the per-level operations only (no coarse solve, no cycle)
+    const bool dense_ok = 10LL * nc * nc - 8LL * nc + 2 <= 4096;
+    if (!dense_ok && levels > 1)
+        return fail(MG_EINVAL, "coarsest level n = %d too large for the dense solve (n_c <= 20)", nc);
+
+    mg_ctx* c = new mg_ctx;
+    c->levels = levels;
+    c->het = grid->K_field != nullptr;
+    c->m = Material{lambda, mu, grid->K_field ? 1.0 : K, tau, alpha, grid->inv_M, grid->mu_f};
+    c->L.resize(levels);
+    kernels_init();
+    auto bail = [&](int rc) {
+        mg_free(c);
+        return rc;
+    };
+    char err[256];
+    if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(MG_ECUDA, "stream create failed"));
+    int max_blocks = 1;
+    for (int l = 0; l < levels; ++l) {
+        Level& Lv = c->L[l];
+        Lv.n = n >> l;
+        Lv.pitch = pitch_of(Lv.n);
+        Lv.plane = (int64_t)(Lv.n + 1) * Lv.pitch;
+        Lv.len = 10 * Lv.plane;
+        max_blocks = std::max(max_blocks, std::max(blocks_vanka(Lv.n), std::max(blocks_residual(Lv.n), blocks_bsr(Lv.n))));
+        HostLevelTables* t = new HostLevelTables;
+        if (host_level_tables(Lv.n, c->m, t, err, sizeof(err))) {
+            delete t;
+            return bail(fail(MG_EINVAL, "level %d: %s", l, err));
+        }
+        Lv.vp.L = t->L;
+        Lv.vp.L.pitch = Lv.pitch;
+        Lv.vp.L.plane = Lv.plane;
+        memcpy(Lv.vp.gp, t->gp, sizeof(t->gp));
+        memcpy(Lv.vp.gm, t->gm, sizeof(t->gm));
+        memcpy(Lv.up.up, t->up, sizeof(t->up));
+        memcpy(Lv.up.um, t->um, sizeof(t->um));
+        if (!c->het) {
+            for (int s = 0; s < 2; ++s)
+                for (int e = 0; e < 3; ++e)
+                    for (int e2 = 0; e2 < 3; ++e2) Lv.vp.L.ww[s][e][e2] *= Lv.vp.L.kinv;
+        }
+        size_t vb = sizeof(double) * Lv.len, pb = sizeof(double) * 2 * Lv.plane;
+        Lv.t = (double*)dalloc(c, vb);
+        Lv.g = (double*)dalloc(c, pb);
+        Lv.dpa = (double*)dalloc(c, pb);
+        Lv.dpb = (double*)dalloc(c, pb);
+        Lv.gbnd = (double*)dalloc(c, sizeof(t->vanka));
+        Lv.ubnd = (double*)dalloc(c, sizeof(t->disp));
+        if (l > 0) {
+            Lv.x = (double*)dalloc(c, vb);
+            Lv.b = (double*)dalloc(c, vb);
+        }
+        if (c->het) Lv.kinv = (double*)dalloc(c, pb);
+        if (!Lv.t || !Lv.g || !Lv.dpa || !Lv.dpb || !Lv.gbnd || !Lv.ubnd || (l > 0 && (!Lv.x || !Lv.b)) ||
+            (c->het && !Lv.kinv)) {
+            delete t;
+            return bail(fail(MG_ENOMEM, "device allocation failed at level %d", l));
+        }
+        if (cudaMemcpy(Lv.gbnd, t->vanka, sizeof(t->vanka), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(Lv.ubnd, t->disp, sizeof(t->disp), cudaMemcpyHostToDevice) != cudaSuccess) {
+            delete t;
+            return bail(fail(MG_ECUDA, "table upload failed"));
+        }
+        delete t;
+        Lv.vp.gbnd = Lv.gbnd;
+        Lv.up.ubnd = Lv.ubnd;
+        Lv.vp.L.kinv_field = Lv.kinv;
+        cudaMemset(Lv.t, 0, vb);
+        cudaMemset(Lv.g, 0, pb);
+        cudaMemset(Lv.dpa, 0, pb);
+        cudaMemset(Lv.dpb, 0, pb);
+        if (l > 0) {
+            cudaMemset(Lv.x, 0, vb);
+            cudaMemset(Lv.b, 0, vb);
+        }
+    }
+    // K^{-1} pyramid (reading A11)
+    if (c->het) {
+        for (int l = 0; l < levels; ++l) cudaMemset(c->L[l].kinv, 0, sizeof(double) * 2 * c->L[l].plane);
+        if (launch_kinv_from_K(n, c->L[0].pitch, grid->K_field, c->L[0].kinv, 0) != cudaSuccess)
+            return bail(fail(MG_ECUDA, "kinv launch: %s", cudaGetErrorString(cudaGetLastError())));
+        for (int l = 1; l < levels; ++l)
+            if (launch_kinv_coarsen(c->L[l - 1].n, c->L[l - 1].pitch, c->L[l - 1].kinv, c->L[l].pitch, c->L[l].kinv, 0) !=
+                cudaSuccess)
+                return bail(fail(MG_ECUDA, "kinv coarsen launch failed"));
+    }
+    // norms and solve state
+    c->partials = (double*)dalloc(c, sizeof(double) * max_blocks);
+    c->counter = (unsigned*)dalloc(c, 64);
+    c->norm = (double*)dalloc(c, 64);
+    c->stop = (int*)dalloc(c, 64);
+    c->state = (SolveState*)dalloc(c, sizeof(SolveState) + 64);
+    if (!c->partials || !c->counter || !c->norm || !c->stop || !c->state)
+        return bail(fail(MG_ENOMEM, "device allocation failed (norm buffers)"));
+    cudaMemset(c->counter, 0, 64);
+    cudaMemset(c->stop, 0, 64);
+    for (int l = 0; l < levels; ++l) c->L[l].vp.L.stop = c->stop;
+    if (cudaMallocHost(&c->pinned, 4 * sizeof(double)) != cudaSuccess) return bail(fail(MG_ENOMEM, "pinned alloc failed"));
+    // coarsest dense deflated inverse (reading A9)
+    if (dense_ok) {
+        Level& Lc = c->L[levels - 1];
+        int N = 0;
+        host_coarse_inverse(Lc.n, Lc.pitch, c->m, nullptr, nullptr, nullptr, &N, err, sizeof(err));
+        std::vector<double> G((size_t)N * N);
+        std::vector<int64_t> sl(N);
+        std::vector<double> kc;
+        const double* kcp = nullptr;
+        if (c->het) {
+            std::vector<double> tmp(2 * Lc.plane);
+            if (cudaDeviceSynchronize() != cudaSuccess ||
+                cudaMemcpy(tmp.data(), Lc.kinv, sizeof(double) * 2 * Lc.plane, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return bail(fail(MG_ECUDA, "K^-1 download: %s", cudaGetErrorString(cudaGetLastError())));
+            kc.resize(2 * (size_t)Lc.n * Lc.n);
+            for (int sh = 0; sh < 2; ++sh)
+                for (int j = 0; j < Lc.n; ++j)
+                    for (int i = 0; i < Lc.n; ++i)
+                        kc[((size_t)sh * Lc.n + j) * Lc.n + i] = tmp[sh * Lc.plane + (size_t)j * Lc.pitch + i];
+            kcp = kc.data();
+        }
+        if (host_coarse_inverse(Lc.n, Lc.pitch, c->m, kcp, G.data(), sl.data(), &N, err, sizeof(err)))
+            return bail(fail(MG_EINVAL, "coarsest level: %s", err));
+        c->Nc = N;
+        c->Ginv = (double*)dalloc(c, sizeof(double) * G.size());
+        c->slots = (int64_t*)dalloc(c, sizeof(int64_t) * N);
+        if (!c->Ginv || !c->slots) return bail(fail(MG_ENOMEM, "coarse allocation failed"));
+        if (cudaMemcpy(c->Ginv, G.data(), sizeof(double) * G.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->slots, sl.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(MG_ECUDA, "coarse upload failed"));
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return bail(fail(MG_ECUDA, "setup: %s", cudaGetErrorString(e)));
+    *out = c;
+    return MG_OK;
+}
+
+void mg_free(mg_ctx* c) {
+    if (!c) return;
+    cudaDeviceSynchronize();
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    for (int i = 0; i < 6; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    dfree_all(c);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->cap) cudaStreamDestroy(c->cap);
+    delete c;
+}
+
+int mg_residual(mg_ctx* c, int32_t level, const double* x, const double* b, double* r, double* norm2_dev,
+                cudaStream_t s) {
+    if (int rc = check_level(c, level, c ? c->levels - 1 : 0)) return rc;
+    if (!aligned(x) || !aligned(b) || (r && !aligned(r)) || (norm2_dev && !aligned(norm2_dev)))
+        return fail(MG_EINVAL, "null or misaligned pointer");
+    if (r && (r == x || r == b)) return fail(MG_EINVAL, "r must not alias x or b");
+    NormSink S = norm2_dev ? NormSink{norm2_dev, c->partials, c->counter, nullptr} : no_norm();
+    CK(launch_residual(c->L[level].vp.L, x, b, r, S, s));
+    return MG_OK;
+}
+
+int mg_relax_vanka(mg_ctx* c, int32_t level, double* x, const double* b, double omega, int32_t sweeps,
+                   cudaStream_t s) {
+    if (int rc = check_level(c, level, c ? c->levels - 1 : 0)) return rc;
+    if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (c->het) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
+    if (sweeps < 0) return fail(MG_EINVAL, "sweeps < 0");
+    mg_cycle_opts o{1, 1, MG_VANKA, omega, 0.0, 0};
+    Level& Lv = c->L[level];
+    double* a = x;
+    double* t = Lv.t;
+    for (int k = 0; k < sweeps; ++k) {
+        if (int rc = relax_once(c, level, a, b, t, false, o, no_norm(), s)) return rc;
+        std::swap(a, t);
+    }
+    if (a != x) CK(cudaMemcpyAsync(x, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+    return MG_OK;
+}
+
+int mg_relax_bsr(mg_ctx* c, int32_t level, double* x, const double* b, double omega, double omega_J,
+                 int32_t jacobi_sweeps, int32_t sweeps, cudaStream_t s) {
+    if (int rc = check_level(c, level, c ? c->levels - 1 : 0)) return rc;
+    if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (sweeps < 0 || jacobi_sweeps < 0) return fail(MG_EINVAL, "sweeps < 0");
+    mg_cycle_opts o{1, 1, MG_BSR, omega, omega_J, jacobi_sweeps};
+    Level& Lv = c->L[level];
+    double* a = x;
+    double* t = Lv.t;
+    for (int k = 0; k < sweeps; ++k) {
+        if (int rc = relax_once(c, level, a, b, t, false, o, no_norm(), s)) return rc;
+        std::swap(a, t);
+    }
+    if (a != x) CK(cudaMemcpyAsync(x, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+    return MG_OK;
+}
+
+int mg_restrict(mg_ctx* c, int32_t fl, const double* r, double* bc, cudaStream_t s) {
+    if (int rc = check_level(c, fl, c ? c->levels - 2 : 0)) return rc;
+    if (!aligned(r) || !aligned(bc)) return fail(MG_EINVAL, "null or misaligned pointer");
+    CK(launch_restrict(c->L[fl].vp.L, c->L[fl + 1].n, c->L[fl + 1].pitch, 0, nullptr, r, bc, s));
+    return MG_OK;
+}
+
+int mg_prolong(mg_ctx* c, int32_t fl, const double* e, double* xf, cudaStream_t s) {
+    if (int rc = check_level(c, fl, c ? c->levels - 2 : 0)) return rc;
+    if (!aligned(e) || !aligned(xf)) return fail(MG_EINVAL, "null or misaligned pointer");
+    CK(launch_prolong(c->L[fl].n, c->L[fl].pitch, c->L[fl + 1].n, c->L[fl + 1].pitch, e, xf, c->stop, s));
+    return MG_OK;
+}
+
+int mg_coarse_solve(mg_ctx* c, const double* b, double* x, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (!c->Ginv) return fail(MG_EINVAL, "no dense coarsest solve on this context (n_c > 20)");
+    if (!aligned(b) || !aligned(x)) return fail(MG_EINVAL, "null or misaligned pointer");
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * c->L[c->levels - 1].len, s));
+    CK(launch_coarse(c->Nc, c->Ginv, c->slots, b, x, c->stop, s));
+    return MG_OK;
+}
+
+int mg_cycle(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double* res_norm_host, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (int rc = check_opts(o)) return rc;
+    if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
+    if (!c->Ginv) return fail(MG_EINVAL, "no dense coarsest solve on this context (n_c > 20)");
+    if (c->levels == 1) {
+        CK(launch_coarse(c->Nc, c->Ginv, c->slots, b, x, c->stop, s));
+    } else {
+        cudaGraphExec_t g;
+        if (int rc = get_graph(c, x, b, *o, 0, nullptr, &g)) return rc;
+        CK(cudaGraphLaunch(g, s));
+        if (c->timing) c->timed_ran = true;
+    }
+    if (res_norm_host) {
+        CK(launch_residual(c->L[0].vp.L, x, b, nullptr, NormSink{c->norm, c->partials, c->counter, nullptr}, s));
+        CK(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *res_norm_host = std::sqrt(c->pinned[0]);
+    }
+    return MG_OK;
+}
+
+int mg_cycle_async(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double* in_norm2_dev,
+                   cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (int rc = check_opts(o)) return rc;
+    if (!aligned(x) || !aligned(b) || (in_norm2_dev && !aligned(in_norm2_dev)))
+        return fail(MG_EINVAL, "null or misaligned pointer");
+    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
+    if (!c->Ginv || c->levels < 2) return fail(MG_EINVAL, "mg_cycle_async needs levels >= 2 and a coarsest solve");
+    cudaGraphExec_t g;
+    if (int rc = get_graph(c, x, b, *o, in_norm2_dev ? 2 : 0, in_norm2_dev, &g)) return rc;
+    CK(cudaGraphLaunch(g, s));
+    if (c->timing) c->timed_ran = true;
+    return MG_OK;
+}
+
+int32_t mg_cycle_kernels(const mg_ctx* c) { return c ? c->launches : -1; }
+
+int mg_set_timing(mg_ctx* c, int32_t enable) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (enable && !c->ev[0])
+        for (int i = 0; i < 6; ++i) CK(cudaEventCreate(&c->ev[i]));
+    c->timing = enable != 0;
+    c->timed_ran = false;
+    return MG_OK;
+}
+
+int mg_timing(mg_ctx* c, float* ms) {
+    if (!c || !ms) return fail(MG_EINVAL, "null argument");
+    if (!c->timed_ran || !c->ev[0]) return fail(MG_EINVAL, "no traced cycle ran");
+    CK(cudaEventSynchronize(c->ev[5]));
+    for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
+    return MG_OK;
+}
+
+int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_cycles,
+             double* history_host, int32_t* n_cycles, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (int rc = check_opts(o)) return rc;
+    if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (max_cycles < 0) return fail(MG_EINVAL, "max_cycles < 0");
+    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
+    if (c->levels == 1) return fail(MG_EINVAL, "mg_solve needs levels >= 2");
+    if (max_cycles + 1 > c->hist_cap) {
+        int cap = std::max(256, max_cycles + 1);
+        double* h = (double*)dalloc(c, sizeof(double) * cap);
+        if (!h) return fail(MG_ENOMEM, "history allocation failed");
+        c->hist = h;
+        c->hist_cap = cap;
+    }
+    SolveState st{0, max_cycles, rtol * rtol, c->hist, c->stop};
+    CK(cudaMemcpyAsync(c->state, &st, sizeof(st), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(c->stop, 0, sizeof(int), s));
+    cudaGraphExec_t g;
+    if (int rc = get_graph(c, x, b, *o, 1, nullptr, &g)) return rc;
+    int launched = 0, stop = 0, k = 0;
+    const int batch = 4;
+    while (launched < max_cycles + 1) {
+        int nb = std::min(batch, max_cycles + 1 - launched);
+        for (int i = 0; i < nb; ++i) CK(cudaGraphLaunch(g, s));
+        launched += nb;
+        CK(cudaMemcpyAsync(c->pinned, c->stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->pinned + 1, c->state, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        memcpy(&stop, c->pinned, sizeof(int));
+        memcpy(&k, c->pinned + 1, sizeof(int));
+        if (stop) break;
+    }
+    if (!stop) return fail(MG_ECUDA, "solve state inconsistent (no stop after %d launches)", launched);
+    std::vector<double> h(k);
+    CK(cudaMemcpy(h.data(), c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    CK(cudaMemsetAsync(c->stop, 0, sizeof(int), s));
+    CK(cudaStreamSynchronize(s));
+    if (history_host)
+        for (int i = 0; i < k; ++i) history_host[i] = std::sqrt(h[i]);
+    if (n_cycles) *n_cycles = k - 1;
+    if (stop == 1) return MG_OK;
+    if (stop == 2) return MG_DIVERGED;
+    return MG_NOTCONV;
+}
+
+int mg_solve_host(mg_ctx* c, double* x_host, const double* b_host, const mg_cycle_opts* o, double rtol,
+                  int32_t max_cycles, double* history_host, int32_t* n_cycles, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (!x_host || !b_host) return fail(MG_EINVAL, "null host pointer");
+    Level& L0 = c->L[0];
+    if (!c->hx) {
+        c->hx = (double*)dalloc(c, sizeof(double) * L0.len);
+        c->hb = (double*)dalloc(c, sizeof(double) * L0.len);
+        if (!c->hx || !c->hb) return fail(MG_ENOMEM, "device allocation failed (e2e buffers)");
+        CK(cudaMemset(c->hx, 0, sizeof(double) * L0.len));
+        CK(cudaMemset(c->hb, 0, sizeof(double) * L0.len));
+    }
+    const size_t w = sizeof(double) * (L0.n + 1), dp = sizeof(double) * L0.pitch;
+    const size_t rows = 10 * (size_t)(L0.n + 1);
+    CK(cudaMemcpy2DAsync(c->hb, dp, b_host, w, w, rows, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpy2DAsync(c->hx, dp, x_host, w, w, rows, cudaMemcpyHostToDevice, s));
+    int rc = mg_solve(c, c->hx, c->hb, o, rtol, max_cycles, history_host, n_cycles, s);
+    if (rc < 0) return rc;
+    CK(cudaMemcpy2DAsync(x_host, w, c->hx, dp, w, rows, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Internal definitions shared by the host setup (mg_setup.cpp), the kernels (mg_kernels.cu) and
+// the C ABI (mg_api.cu).  Not part of the public ABI (include/mg.h).
+#pragma once
+#include <stdint.h>
+
+#define MG_NCOEF 141      // merged stencil coefficients (mg_tables.h MG_STENCIL_NCOEF)
+#define MG_PSLOTS 20      // Vanka patch slots
+#define MG_USLOTS 8       // displacement patch slots (BSR)
+#define MG_NCLASS 9       // vertex classes: cx + 3 cy, cx = 0 interior, 1 at i = 0, 2 at i = n
+
+// Patch slot s of the vertex (a, b) sits at (a + dx, b + dy) in plane p:  VSLOT[s] = {dx, dy, p}.
+// Order: u_x, u_y, bubbles on the spokes E, W, N, S, NW, SE, RT0 on the same spokes, P0 of the
+// triangles LL(a,b), UR(a-1,b-1), LL(a-1,b), UR(a,b-1), UR(a-1,b), LL(a,b-1) (Fig. fig:patches,
+// PAPER.md:592-652).  Consecutive pairs (2,3) ... (18,19) are images of each other under the 180
+// degree rotation about the vertex.
+#define MG_VSLOT_TABLE {                                                           \
+    {0, 0, 0}, {0, 0, 1},                                                          \
+    {0, 0, 2}, {-1, 0, 2}, {0, 0, 3}, {0, -1, 3}, {-1, 0, 4}, {0, -1, 4},          \
+    {0, 0, 5}, {-1, 0, 5}, {0, 0, 6}, {0, -1, 6}, {-1, 0, 7}, {0, -1, 7},          \
+    {0, 0, 8}, {-1, -1, 9}, {-1, 0, 8}, {0, -1, 9}, {-1, 0, 9}, {0, -1, 8} }
+
+// Geometry + coefficients of one level, passed by value to every kernel (constant bank).
+struct LevelParams {
+    int32_t n, pitch;
+    int64_t plane;               // (n+1) * pitch
+    double coef[MG_NCOEF];       // merged stencil of A^RQ without M_w (mg_tables.h order)
+    double ww[2][3][3];          // tau mu_f h^2 (M_w1)_{shape,e,e'}; multiplied by K^{-1}_T
+    double kinv;                 // scalar K^{-1} (used when kinv_field == nullptr)
+    const double* kinv_field;    // 2 planes [shape][j][i] with row pitch `pitch`, or nullptr
+    // BSR data: S = s0 M_p + tau B_w D_w^{-1} B_w^T
+    double s0h2;                 // s0 |T| = (1/M + alpha^2/(lambda+mu)) h^2/2
+    double tau, alpha;
+    double bw[2][3];             // h (B_w1)_{shape,e}
+    double bu[2][9];             // h (B_u1)_{shape,q}
+    double mw1d[2][3];           // mu_f h^2 (M_w1)_{shape,e,e}   (diagonal, times K^{-1}_T)
+    const int* stop;             // device flag of mg_solve: every kernel returns at entry if *stop != 0
+};
+
+// Device state of mg_solve, updated by the block that finishes a fused residual norm:
+// hist[k] = ||b - A x_k||^2, then *stop = 1 (converged: hist[k] <= rtol2 hist[0], k > 0),
+// 2 (diverged: non-finite or > 1e16 hist[0]) or 3 (k == maxk).
+struct SolveState {
+    int k;                       // next history slot
+    int maxk;                    // max_cycles
+    double rtol2;                // rtol^2
+    double* hist;                // maxk + 1 doubles
+    int* stop;                   // the flag every kernel polls (LevelParams::stop)
+};
+
+// Interior (symmetric) patch inverse in the +/- basis of the 180-degree rotation:
+// + block (9): bubble diffs (3), RT0 diffs (3), P0 sums (3)
+// - block (11): u_x, u_y, bubble sums (3), RT0 sums (3), P0 diffs (3)
+// with 1/2 folded into the rows of pair components.
+struct VankaParams {
+    LevelParams L;
+    double gp[9][9];
+    double gm[11][11];
+    const double* gbnd;          // device: MG_NCLASS x 20 x 20 (weighted, deflated), row major
+    double omega;
+};
+
+struct DispParams {               // 8-DoF displacement Vanka (F_u^{-1} of BSR)
+    double up[3][3];              // + block: bubble diffs
+    double um[5][5];              // - block: u_x, u_y, bubble sums
+    const double* ubnd;           // device: MG_NCLASS x 8 x 8
+};
+
+// host tables of one level (mg_setup.cpp)
+struct HostLevelTables {
+    int n;
+    double h;
+    LevelParams L;                // device pointers left null
+    double vanka[MG_NCLASS][MG_PSLOTS * MG_PSLOTS];
+    double gp[9][9], gm[11][11];
+    double disp[MG_NCLASS][MG_USLOTS * MG_USLOTS];
+    double up[3][3], um[5][5];
+};
+
+struct Material {
+    double lambda, mu, K, tau, alpha, inv_M, mu_f;
+};
+
+// mg_setup.cpp
+int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, int errlen);
+// dense coarsest operator: Ginv (N x N, column major: G[col*N + row]) of the deflated inverse and
+// the slot offsets (k*(n+1)*pitch + j*pitch + i) of the N active unknowns.  kinv: nullptr (scalar)
+// or 2 x n x n [shape][j][i].
+int host_coarse_inverse(int n, int pitch, const Material& m, const double* kinv, double* Ginv,
+                        int64_t* slots, int* N, char* err, int errlen);
+int64_t n_active_of(int n);

@@ -1,0 +1,951 @@
+// fp64 sm_100a kernels of the monolithic multigrid V-cycle for the RQ Biot operator
+// (arXiv 2107.04060).  Every kernel is matrix free: the operator stencil and the prolongation
+// weights come from mg_tables.h (generated geometry) and the per-level coefficients from the
+// LevelParams passed by value (constant bank).  Layout: include/mg.h.
+//
+//   residual_kernel     r = b - A^RQ x                      (eq. block_form_rq)
+//   vanka_kernel        fused additive Vanka sweep
+//   restrict_kernel     b_H = P^T (b - A x), fused
+//   prolong_kernel      x += P e_H
+//   coarse_kernel       dense deflated coarsest solve       (reading A9)
+//   bsr_a/jacobi/b      inexact Braess-Sarazin stages
+//
+// Tiles: a CTA owns TX x TY grid indices (each index owns 10 DoFs) and recomputes the residual
+// on a halo ring instead of exchanging it, so every sweep reads x and b once and writes x once
+// (owner computes; no atomics; deterministic).  The Vanka sweep is out of place (x -> xout):
+// neighbouring CTAs read x in their halos.
+#include <cstdint>
+
+#include "mg_kernels.cuh"
+#include "mg_tables.h"
+
+namespace {
+
+__device__ __forceinline__ bool is_active(int p, int i, int j, int n) {
+    if (i < 0 || j < 0 || i > n || j > n) return false;
+    switch (p) {
+        case 0: case 1: return i > 0 && i < n && j > 0 && j < n;
+        case 2: case 5: return i < n && j > 0 && j < n;
+        case 3: case 6: return i > 0 && i < n && j < n;
+        default: return i < n && j < n;
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double ws[NT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < NT / 32; ++k) t += ws[k];
+    return t;  // valid in thread 0
+}
+
+// one partial per block; the last block to arrive sums the partials in block order
+template <int NT>
+__device__ void norm_finish(const NormSink& S, double v) {
+    const int nb = gridDim.x * gridDim.y;
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    double t = block_sum<NT>(v);
+    __shared__ unsigned last;
+    if (threadIdx.x == 0) {
+        S.partials[bid] = t;
+        __threadfence();
+        unsigned prev = atomicAdd(S.counter, 1u);
+        last = (prev == (unsigned)nb - 1u);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double acc = 0.0;
+        for (int k = threadIdx.x; k < nb; k += NT) acc += __ldcg(S.partials + k);
+        double tot = block_sum<NT>(acc);
+        if (threadIdx.x == 0) {
+            if (S.state) {
+                SolveState* st = S.state;
+                const int k = st->k;
+                st->hist[k] = tot;
+                const double h0 = k == 0 ? tot : st->hist[0];
+                int stop = 0;
+                if (!isfinite(tot)) stop = 2;
+                else if (k > 0 && tot <= st->rtol2 * h0) stop = 1;
+                else if (k > 0 && tot > 1e16 * h0) stop = 2;
+                else if (k >= st->maxk) stop = 3;
+                st->k = k + 1;
+                if (stop) *st->stop = stop;
+            } else {
+                *S.out = tot;
+            }
+            *S.counter = 0u;
+        }
+    }
+}
+
+// zero-padded tile load: dst[p][ly][lx] = src(p, j0+ly, i0+lx) for 0 <= i, j <= n, else 0
+template <int W, int HT, int NP>
+__device__ __forceinline__ void load_tile(double* __restrict__ dst, const double* __restrict__ src, int i0,
+                                          int j0, int n, int pitch, int64_t plane, int p0 = 0) {
+    for (int t = threadIdx.x; t < NP * W * HT; t += blockDim.x) {
+        int p = t / (W * HT);
+        int rem = t - p * (W * HT);
+        int ly = rem / W;
+        int lx = rem - ly * W;
+        int i = i0 + lx, j = j0 + ly;
+        dst[t] = (i >= 0 && i <= n && j >= 0 && j <= n) ? __ldg(src + (p0 + p) * plane + (int64_t)j * pitch + i)
+                                                         : 0.0;
+    }
+}
+
+// K^{-1} of triangle `sh` of cell (ci, cj); 0 outside the mesh
+template <bool HET>
+__device__ __forceinline__ double kinv_at(const LevelParams& L, int ci, int cj, int sh) {
+    if (!HET) return L.kinv;
+    if (ci < 0 || cj < 0 || ci >= L.n || cj >= L.n) return 0.0;
+    return __ldg(L.kinv_field + sh * L.plane + (int64_t)cj * L.pitch + ci);
+}
+
+// scale of the per-triangle M_w entries in the residual: L.ww already holds K^{-1} when K is scalar
+template <bool HET>
+__device__ __forceinline__ double kinv_ww(const LevelParams& L, int ci, int cj, int sh) {
+    if (!HET) return 1.0;
+    return kinv_at<true>(L, ci, cj, sh);
+}
+
+// r = b - A x for the 10 DoFs of index (i, j); xs is a W x HT x 10 tile holding (i, j) at
+// (lx, ly) with a ring of at least 1.  Inactive rows give 0.
+template <int W, int HT, bool HET>
+__device__ __forceinline__ void residual_at(const LevelParams& L, const double* __restrict__ xs, int lx, int ly,
+                                            int i, int j, const double* __restrict__ b, double r[10]) {
+    const double* x0 = xs + ly * W + lx;
+#define XS(dx, dy, pl) x0[(pl) * (W * HT) + (dy) * W + (dx)]
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0, a8 = 0, a9 = 0;
+#define MG_X(row, dx, dy, pl, ci) a##row = fma(L.coef[ci], XS(dx, dy, pl), a##row);
+    MG_STENCIL_ROW_0(MG_X)
+    MG_STENCIL_ROW_1(MG_X)
+    MG_STENCIL_ROW_2(MG_X)
+    MG_STENCIL_ROW_3(MG_X)
+    MG_STENCIL_ROW_4(MG_X)
+    MG_STENCIL_ROW_5(MG_X)
+    MG_STENCIL_ROW_6(MG_X)
+    MG_STENCIL_ROW_7(MG_X)
+    MG_STENCIL_ROW_8(MG_X)
+    MG_STENCIL_ROW_9(MG_X)
+#undef MG_X
+#define MG_W(row, cdx, cdy, sh, dx, dy, pl, e, e2) \
+    a##row = fma(L.ww[sh][e][e2] * kinv_ww<HET>(L, i + (cdx), j + (cdy), sh), XS(dx, dy, pl), a##row);
+    MG_STENCIL_WW_5(MG_W)
+    MG_STENCIL_WW_6(MG_W)
+    MG_STENCIL_WW_7(MG_W)
+#undef MG_W
+#undef XS
+    const int n = L.n;
+    const int64_t o = (int64_t)j * L.pitch + i;
+    const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
+    double av[10] = {a0, a1, a2, a3, a4, a5, a6, a7, a8, a9};
+#pragma unroll
+    for (int k = 0; k < 10; ++k) r[k] = is_active(k, i, j, n) ? (__ldg(b + k * L.plane + (in ? o : 0)) - av[k]) : 0.0;
+}
+
+// ------------------------------------------------------------------------------------------
+// residual
+constexpr int RTX = 32, RTY = 8, RNT = 256;
+
+template <bool HET>
+__global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, const double* __restrict__ x,
+                                                       const double* __restrict__ b, double* __restrict__ r,
+                                                       NormSink S) {
+    constexpr int XW = RTX + 2, XH = RTY + 2;
+    __shared__ double xs[10 * XW * XH];
+    if (*L.stop) return;
+    const int i0 = blockIdx.x * RTX, j0 = blockIdx.y * RTY;
+    load_tile<XW, XH, 10>(xs, x, i0 - 1, j0 - 1, L.n, L.pitch, L.plane);
+    __syncthreads();
+    const int lx = threadIdx.x % RTX, ly = threadIdx.x / RTX;
+    const int i = i0 + lx, j = j0 + ly;
+    double nrm = 0.0;
+    if (i <= L.n && j <= L.n) {
+        double rv[10];
+        residual_at<XW, XH, HET>(L, xs, lx + 1, ly + 1, i, j, b, rv);
+        const int64_t o = (int64_t)j * L.pitch + i;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+            if (r) r[k * L.plane + o] = rv[k];
+            nrm = fma(rv[k], rv[k], nrm);
+        }
+    }
+    if (S.out || S.state) norm_finish<RNT>(S, nrm);
+}
+
+// ------------------------------------------------------------------------------------------
+// additive Vanka sweep: xout = x + omega sum_v V^T D K_v^{-1} V (b - A x)
+constexpr int VTX = 32, VTY = 8, VNT = 256;
+constexpr int V_XW = VTX + 4, V_XH = VTY + 4, V_RW = VTX + 2, V_RH = VTY + 2, V_PW = VTX + 1, V_PH = VTY + 1;
+constexpr int V_XSZ = 10 * V_XW * V_XH, V_CSZ = 20 * V_PW * V_PH;
+constexpr int V_USZ = V_XSZ > V_CSZ ? V_XSZ : V_CSZ;
+constexpr int V_SMEM = (V_USZ + 10 * V_RW * V_RH) * 8;
+
+// gather the 20 patch residuals of the vertex at r-tile position r00 (MG_VSLOT_TABLE order)
+template <int RW, int RH>
+__device__ __forceinline__ void gather20(const double* r00, double rr[20]) {
+#define RR(dx, dy, pl) r00[(pl) * (RW * RH) + (dy) * RW + (dx)]
+    rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+    rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+    rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+    rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+    rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+    rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+    rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+}
+
+__device__ __forceinline__ int vertex_class(int a, int b, int n) {
+    return (a == 0 ? 1 : (a == n ? 2 : 0)) + 3 * (b == 0 ? 1 : (b == n ? 2 : 0));
+}
+
+// out[s * os] = (D K^{-1} r)_s for one 20-DoF patch (interior: +/- blocks; boundary class: dense
+// table), written straight to shared memory
+__device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, const double rr[20], double* out, int os) {
+    if (cls == 0) {
+        double hp[9], hm[11];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            hp[q] = rr[2 + 2 * q] - rr[3 + 2 * q];
+            hm[2 + q] = rr[2 + 2 * q] + rr[3 + 2 * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            hp[6 + q] = rr[14 + 2 * q] + rr[15 + 2 * q];
+            hm[8 + q] = rr[14 + 2 * q] - rr[15 + 2 * q];
+        }
+        hm[0] = rr[0];
+        hm[1] = rr[1];
+        double yp[9], ym[11];
+#pragma unroll
+        for (int a = 0; a < 9; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 9; ++c) s = fma(P.gp[a][c], hp[c], s);
+            yp[a] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < 11; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 11; ++c) s = fma(P.gm[a][c], hm[c], s);
+            ym[a] = s;
+        }
+        out[0] = ym[0];
+        out[os] = ym[1];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            out[(2 + 2 * q) * os] = ym[2 + q] + yp[q];
+            out[(3 + 2 * q) * os] = ym[2 + q] - yp[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            out[(14 + 2 * q) * os] = yp[6 + q] + ym[8 + q];
+            out[(15 + 2 * q) * os] = yp[6 + q] - ym[8 + q];
+        }
+    } else {
+        const double* G = P.gbnd + cls * 400;
+#pragma unroll 1
+        for (int a = 0; a < 20; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 20; ++c) s = fma(__ldg(G + a * 20 + c), rr[c], s);
+            out[a * os] = s;
+        }
+    }
+}
+
+template <bool XZERO>
+__global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
+                                                       const double* __restrict__ b, double* __restrict__ xo,
+                                                       NormSink S) {
+    extern __shared__ double sm[];
+    double* xs = sm;          // x tile (phase 1)
+    double* cs = sm;          // patch corrections (phase 2-3), overlays xs
+    double* rs = sm + V_USZ;  // residual tile
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n, pitch = L.pitch;
+    const int64_t plane = L.plane;
+    const int i0 = blockIdx.x * VTX, j0 = blockIdx.y * VTY;
+    if (!XZERO) {
+        load_tile<V_XW, V_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        __syncthreads();
+#pragma unroll 1
+        for (int t = threadIdx.x; t < V_RW * V_RH; t += VNT) {
+            const int ly = t / V_RW, lx = t - ly * V_RW;
+            double rv[10];
+            residual_at<V_XW, V_XH, false>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rs[k * V_RW * V_RH + t] = rv[k];
+        }
+    } else {
+        load_tile<V_RW, V_RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);  // r = b (x = 0)
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int t = threadIdx.x; t < V_PW * V_PH; t += VNT) {
+        const int py = t / V_PW, px = t - py * V_PW;
+        const int a = i0 + px, bb = j0 + py;
+        if (a <= n && bb <= n) {
+            double rr[20];
+            gather20<V_RW, V_RH>(rs + (py + 1) * V_RW + (px + 1), rr);
+            patch_apply20(P, vertex_class(a, bb, n), rr, cs + t, V_PW * V_PH);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 20; ++s) cs[s * V_PW * V_PH + t] = 0.0;
+        }
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    {
+        const int lx = threadIdx.x % VTX, ly = threadIdx.x / VTX;
+        const int i = i0 + lx, j = j0 + ly;
+        if (i <= n && j <= n) {
+            const double* c00 = cs + ly * V_PW + lx;
+#define CC(s, dx, dy) c00[(s) * (V_PW * V_PH) + (dy) * V_PW + (dx)]
+            double d[10];
+            d[0] = CC(0, 0, 0);
+            d[1] = CC(1, 0, 0);
+            d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+            d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+            d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+            d[5] = CC(8, 0, 0) + CC(9, 1, 0);
+            d[6] = CC(10, 0, 0) + CC(11, 0, 1);
+            d[7] = CC(12, 1, 0) + CC(13, 0, 1);
+            d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
+            d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
+#undef CC
+            const int64_t o = (int64_t)j * pitch + i;
+            const double* r00 = rs + (ly + 1) * V_RW + (lx + 1);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                const double xv = XZERO ? 0.0 : __ldg(x + k * plane + o);
+                xo[k * plane + o] = is_active(k, i, j, n) ? fma(P.omega, d[k], xv) : 0.0;
+                const double rv = r00[k * V_RW * V_RH];
+                nrm = fma(rv, rv, nrm);
+            }
+        }
+    }
+    if (S.out || S.state) norm_finish<VNT>(S, nrm);
+}
+
+// ------------------------------------------------------------------------------------------
+// restriction b_H = P^T r (R = P^T), optionally fused with r = b - A x
+constexpr int CX = 16, CY = 8, CNT = 256;
+constexpr int C_RW = 2 * CX + 2, C_RH = 2 * CY + 2, C_XW = C_RW + 2, C_XH = C_RH + 2;
+constexpr int C_SMEM_FUSED = (10 * C_RW * C_RH + 10 * C_XW * C_XH) * 8;
+constexpr int C_SMEM_PLAIN = 10 * C_RW * C_RH * 8;
+
+template <int MODE, bool HET>
+__global__ void __launch_bounds__(CNT, 2) restrict_kernel(const LevelParams L, int nc, int pitchc,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ br,
+                                                          double* __restrict__ bc) {
+    extern __shared__ double sm[];
+    double* rs = sm;
+    double* xs = sm + 10 * C_RW * C_RH;
+    if (*L.stop) return;
+    const int I0 = blockIdx.x * CX, J0 = blockIdx.y * CY;
+    const int fi0 = 2 * I0 - 2, fj0 = 2 * J0 - 2;
+    if (MODE == 1) {
+        load_tile<C_XW, C_XH, 10>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane);
+        __syncthreads();
+#pragma unroll 1
+        for (int t = threadIdx.x; t < C_RW * C_RH; t += CNT) {
+            const int ly = t / C_RW, lx = t - ly * C_RW;
+            double rv[10];
+            residual_at<C_XW, C_XH, HET>(L, xs, lx + 1, ly + 1, fi0 + lx, fj0 + ly, br, rv);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rs[k * C_RW * C_RH + t] = rv[k];
+        }
+    } else {
+        load_tile<C_RW, C_RH, 10>(rs, br, fi0, fj0, L.n, L.pitch, L.plane);
+    }
+    __syncthreads();
+    const int c = threadIdx.x & (CX * CY - 1), half = threadIdx.x / (CX * CY);
+    const int cy = c / CX, cx = c - cy * CX;
+    const int I = I0 + cx, J = J0 + cy;
+    if (I > nc || J > nc) return;
+    const double* r00 = rs + (2 * cy + 2) * C_RW + (2 * cx + 2);
+    const int64_t planec = (int64_t)(nc + 1) * pitchc;
+    const int64_t o = (int64_t)J * pitchc + I;
+#define RF(cdI, cdJ, di, dj, kf) r00[(kf) * (C_RW * C_RH) + (-2 * (cdJ) + (dj)) * C_RW + (-2 * (cdI) + (di))]
+#define MG_T(cdI, cdJ, di, dj, kf, w) acc = fma(w, RF(cdI, cdJ, di, dj, kf), acc);
+#define OUT(k)                                                       \
+    {                                                                \
+        double acc = 0.0;                                            \
+        MG_RESTRICT_##k(MG_T) bc[k * planec + o] = is_active(k, I, J, nc) ? acc : 0.0; \
+    }
+    if (half == 0) {
+        OUT(0) OUT(1) OUT(2) OUT(3)
+    } else {
+        OUT(4) OUT(5) OUT(6) OUT(7) OUT(8) OUT(9)
+    }
+#undef OUT
+#undef MG_T
+#undef RF
+}
+
+// ------------------------------------------------------------------------------------------
+// prolongation x_f += P e_c: one thread per coarse cell writes its 4 fine indices
+__global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc, int pitchc,
+                                                      const double* __restrict__ e, double* __restrict__ x,
+                                                      const int* __restrict__ stop) {
+    if (*stop) return;
+    const int I = blockIdx.x * 32 + (threadIdx.x & 31), J = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (I >= nc || J >= nc) return;
+    const int64_t planec = (int64_t)(nc + 1) * pitchc, planef = (int64_t)(nf + 1) * pitchf;
+    const double* e0 = e + (int64_t)J * pitchc + I;
+#define EC(dI, dJ, pl) __ldg(e0 + (pl) * planec + (dJ) * pitchc + (dI))
+#define MG_Q(dI, dJ, pl, w) v = fma(w, EC(dI, dJ, pl), v);
+    const int fi = 2 * I, fj = 2 * J;
+    double* x0 = x + (int64_t)fj * pitchf + fi;
+#define PROL(di, dj, kf)                                                            \
+    {                                                                               \
+        double v = 0.0;                                                             \
+        MG_PROLONG_##di##_##dj##_##kf(MG_Q) if (is_active(kf, fi + di, fj + dj, nf)) \
+            x0[kf * planef + dj * pitchf + di] += v;                                \
+    }
+#define PROL4(kf) PROL(0, 0, kf) PROL(1, 0, kf) PROL(0, 1, kf) PROL(1, 1, kf)
+    PROL4(0) PROL4(1) PROL4(2) PROL4(3) PROL4(4) PROL4(5) PROL4(6) PROL4(7) PROL4(8) PROL4(9)
+#undef PROL4
+#undef PROL
+#undef MG_Q
+#undef EC
+}
+
+// ------------------------------------------------------------------------------------------
+// coarsest solve: x[slots] = Ginv b[slots] (Ginv column major, deflation folded in)
+__global__ void __launch_bounds__(256) coarse_kernel(int N, const double* __restrict__ G,
+                                                     const int64_t* __restrict__ slots,
+                                                     const double* __restrict__ b, double* __restrict__ x,
+                                                     const int* __restrict__ stop) {
+    extern __shared__ double rb[];
+    if (*stop) return;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) rb[k] = __ldg(b + slots[k]);
+    __syncthreads();
+    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < N; row += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int k = 0; k < N; ++k) acc = fma(__ldg(G + (int64_t)k * N + row), rb[k], acc);
+        x[slots[row]] = acc;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// inexact Braess-Sarazin
+constexpr int BTX = 32, BTY = 8, BNT = 256;
+
+__device__ __forceinline__ void patch_apply8(const DispParams& U, int cls, const double rr[8], double* out, int os) {
+    if (cls == 0) {
+        double hp[3], hm[5];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            hp[q] = rr[2 + 2 * q] - rr[3 + 2 * q];
+            hm[2 + q] = rr[2 + 2 * q] + rr[3 + 2 * q];
+        }
+        hm[0] = rr[0];
+        hm[1] = rr[1];
+        double yp[3], ym[5];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) s = fma(U.up[a][c], hp[c], s);
+            yp[a] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) s = fma(U.um[a][c], hm[c], s);
+            ym[a] = s;
+        }
+        out[0] = ym[0];
+        out[os] = ym[1];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            out[(2 + 2 * q) * os] = ym[2 + q] + yp[q];
+            out[(3 + 2 * q) * os] = ym[2 + q] - yp[q];
+        }
+    } else {
+        const double* G = U.ubnd + cls * 64;
+#pragma unroll 1
+        for (int a = 0; a < 8; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) s = fma(__ldg(G + a * 8 + c), rr[c], s);
+            out[a * os] = s;
+        }
+    }
+}
+
+template <int RW, int RH>
+__device__ __forceinline__ void gather8(const double* r00, double rr[8]) {
+#define RR(dx, dy, pl) r00[(pl) * (RW * RH) + (dy) * RW + (dx)]
+    rr[0] = RR(0, 0, 0);  rr[1] = RR(0, 0, 1);
+    rr[2] = RR(0, 0, 2);  rr[3] = RR(-1, 0, 2); rr[4] = RR(0, 0, 3); rr[5] = RR(0, -1, 3);
+    rr[6] = RR(-1, 0, 4); rr[7] = RR(0, -1, 4);
+#undef RR
+}
+
+// D_w(e) = mu_f h^2 sum_{T ni e} K_T^{-1} (M_w1)_T[e][e] for the RT0 DoF of plane k at index (i, j)
+template <bool HET>
+__device__ __forceinline__ double Dw_at(const LevelParams& L, int k, int i, int j) {
+    double d = 0.0;
+#define MG_I(kk, cdx, cdy, sh, q) d = fma(L.mw1d[sh][(q) - 9], kinv_at<HET>(L, i + (cdx), j + (cdy), sh), d);
+    if (k == 5) { MG_INCIDENT_5(MG_I) }
+    else if (k == 6) { MG_INCIDENT_6(MG_I) }
+    else { MG_INCIDENT_7(MG_I) }
+#undef MG_I
+    return d;
+}
+
+// active-edge flags of the local edges of triangle sh in cell (i, j)
+__device__ __forceinline__ void tri_edges_active(int sh, int i, int j, int n, bool act[3]) {
+    if (sh == 0) {
+        act[0] = is_active(5, i, j, n);
+        act[1] = is_active(6, i, j, n);
+        act[2] = true;
+    } else {
+        act[0] = is_active(5, i, j + 1, n);
+        act[1] = is_active(6, i + 1, j, n);
+        act[2] = true;
+    }
+}
+
+// D_w of the local edges of triangle sh in cell (i, j)
+template <bool HET>
+__device__ __forceinline__ void tri_Dw(const LevelParams& L, int sh, int i, int j, double dw[3]) {
+    if (sh == 0) {
+        dw[0] = Dw_at<HET>(L, 5, i, j);
+        dw[1] = Dw_at<HET>(L, 6, i, j);
+    } else {
+        dw[0] = Dw_at<HET>(L, 5, i, j + 1);
+        dw[1] = Dw_at<HET>(L, 6, i + 1, j);
+    }
+    dw[2] = Dw_at<HET>(L, 7, i, j);
+}
+
+// diag(S)_T = s0 |T| + tau sum_{e in T active} Bw_T[e]^2 / D_w(e)
+template <bool HET>
+__device__ __forceinline__ double diagS(const LevelParams& L, int sh, int i, int j) {
+    double dw[3];
+    bool act[3];
+    tri_Dw<HET>(L, sh, i, j, dw);
+    tri_edges_active(sh, i, j, L.n, act);
+    double s = L.s0h2;
+#pragma unroll
+    for (int e = 0; e < 3; ++e)
+        if (act[e]) s += L.tau * L.bw[sh][e] * L.bw[sh][e] / dw[e];
+    return s;
+}
+
+// stage A: r, z_u = F_u^{-1} r_u, z_w = (tau D_w)^{-1} r_w, g = alpha B_u z_u + tau B_w z_w - r_p,
+// first Jacobi sweep dp = omega_J g / diag(S)
+constexpr int BA_XW = BTX + 5, BA_XH = BTY + 5, BA_RW = BTX + 3, BA_RH = BTY + 3;
+constexpr int BA_ZW = BTX + 2, BA_ZH = BTY + 2, BA_UW = BTX + 1, BA_UH = BTY + 1;
+constexpr int BA_XSZ = 10 * BA_XW * BA_XH, BA_ZSZ = 8 * BA_ZW * BA_ZH + 5 * BA_UW * BA_UH;
+constexpr int BA_USZ = BA_XSZ > BA_ZSZ ? BA_XSZ : BA_ZSZ;
+constexpr int BA_SMEM = (BA_USZ + 10 * BA_RW * BA_RH) * 8;
+
+template <bool HET, bool XZERO>
+__global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, const DispParams U, double omJ,
+                                                       const double* __restrict__ x, const double* __restrict__ b,
+                                                       double* __restrict__ g, double* __restrict__ dp, NormSink S) {
+    extern __shared__ double sm[];
+    double* xs = sm;
+    double* zs = sm;                              // disp patch outputs, overlays xs
+    double* zu = sm + 8 * BA_ZW * BA_ZH;          // z_u on owned + high ring
+    double* rs = sm + BA_USZ;
+    if (*L.stop) return;
+    const int n = L.n, pitch = L.pitch;
+    const int64_t plane = L.plane;
+    const int i0 = blockIdx.x * BTX, j0 = blockIdx.y * BTY;
+    if (!XZERO) {
+        load_tile<BA_XW, BA_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        __syncthreads();
+#pragma unroll 1
+        for (int t = threadIdx.x; t < BA_RW * BA_RH; t += BNT) {
+            const int ly = t / BA_RW, lx = t - ly * BA_RW;
+            double rv[10];
+            residual_at<BA_XW, BA_XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rs[k * BA_RW * BA_RH + t] = rv[k];
+        }
+    } else {
+        load_tile<BA_RW, BA_RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);
+    }
+    __syncthreads();
+    // displacement patches at vertices [i0, i0+BTX+1] x [j0, j0+BTY+1]
+#pragma unroll 1
+    for (int t = threadIdx.x; t < BA_ZW * BA_ZH; t += BNT) {
+        const int py = t / BA_ZW, px = t - py * BA_ZW;
+        const int a = i0 + px, bb = j0 + py;
+        if (a <= n && bb <= n) {
+            double rr[8];
+            gather8<BA_RW, BA_RH>(rs + (py + 1) * BA_RW + (px + 1), rr);
+            patch_apply8(U, vertex_class(a, bb, n), rr, zs + t, BA_ZW * BA_ZH);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) zs[s * BA_ZW * BA_ZH + t] = 0.0;
+        }
+    }
+    __syncthreads();
+    // z_u on indices [i0, i0+BTX] x [j0, j0+BTY]
+#pragma unroll 1
+    for (int t = threadIdx.x; t < BA_UW * BA_UH; t += BNT) {
+        const int ly = t / BA_UW, lx = t - ly * BA_UW;
+        const double* c00 = zs + ly * BA_ZW + lx;
+#define CC(s, dx, dy) c00[(s) * (BA_ZW * BA_ZH) + (dy) * BA_ZW + (dx)]
+        zu[0 * BA_UW * BA_UH + t] = CC(0, 0, 0);
+        zu[1 * BA_UW * BA_UH + t] = CC(1, 0, 0);
+        zu[2 * BA_UW * BA_UH + t] = CC(2, 0, 0) + CC(3, 1, 0);
+        zu[3 * BA_UW * BA_UH + t] = CC(4, 0, 0) + CC(5, 0, 1);
+        zu[4 * BA_UW * BA_UH + t] = CC(6, 1, 0) + CC(7, 0, 1);
+#undef CC
+    }
+    __syncthreads();
+    const int lx = threadIdx.x % BTX, ly = threadIdx.x / BTX;
+    const int i = i0 + lx, j = j0 + ly;
+    double nrm = 0.0;
+    if (i <= n && j <= n) {
+        const double* r00 = rs + (ly + 1) * BA_RW + (lx + 1);
+        if (S.out || S.state) {
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                const double rv = r00[k * BA_RW * BA_RH];
+                nrm = fma(rv, rv, nrm);
+            }
+        }
+        const int64_t o = (int64_t)j * pitch + i;
+        if (i < n && j < n) {
+            const double* u00 = zu + ly * BA_UW + lx;
+#pragma unroll
+            for (int sh = 0; sh < 2; ++sh) {
+                double dw[3];
+                bool act[3];
+                tri_Dw<HET>(L, sh, i, j, dw);
+                tri_edges_active(sh, i, j, n, act);
+                double gu = 0.0, gw = 0.0, ds = L.s0h2;
+#define MG_L(s, q, dx, dy, pl)                                                              \
+    if ((s) == sh) {                                                                        \
+        if ((q) < 9) gu = fma(L.bu[s][(q) < 9 ? (q) : 0], u00[(pl) * (BA_UW * BA_UH) + (dy) * BA_UW + (dx)], gu); \
+        else if ((q) < 12) {                                                                \
+            const int e = (q) < 12 ? (q) - 9 : 0;                                           \
+            if (act[e]) {                                                                   \
+                const double rw = r00[(pl) * (BA_RW * BA_RH) + (dy) * BA_RW + (dx)];        \
+                gw = fma(L.bw[s][e], rw / (L.tau * dw[e]), gw);                             \
+                ds += L.tau * L.bw[s][e] * L.bw[s][e] / dw[e];                              \
+            }                                                                               \
+        }                                                                                   \
+    }
+                MG_LOCAL_0(MG_L)
+                MG_LOCAL_1(MG_L)
+#undef MG_L
+                const double rp = r00[(8 + sh) * (BA_RW * BA_RH)];
+                const double gv = L.alpha * gu + L.tau * gw - rp;
+                g[sh * plane + o] = gv;
+                dp[sh * plane + o] = omJ * gv / ds;
+            }
+        } else {
+            g[o] = 0.0;
+            g[plane + o] = 0.0;
+            dp[o] = 0.0;
+            dp[plane + o] = 0.0;
+        }
+    }
+    if (S.out || S.state) norm_finish<BNT>(S, nrm);
+}
+
+// Jacobi sweep on S dp = g: dp' = dp + omega_J (g - S dp) / diag(S)
+template <bool HET>
+__global__ void __launch_bounds__(256) bsr_jacobi_kernel(const LevelParams L, double omJ,
+                                                         const double* __restrict__ g,
+                                                         const double* __restrict__ dpi, double* __restrict__ dpo) {
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int n = L.n;
+    if (i > n || j > n || *L.stop) return;
+    const int64_t plane = L.plane, pitch = L.pitch;
+    const int64_t o = (int64_t)j * pitch + i;
+    if (i == n || j == n) {
+        dpo[o] = 0.0;
+        dpo[plane + o] = 0.0;
+        return;
+    }
+    // neighbours: LL(i,j) -- e0 H(i,j): UR(i,j-1); e1 V(i,j): UR(i-1,j); e2 D: UR(i,j)
+    //             UR(i,j) -- e0 H(i,j+1): LL(i,j+1); e1 V(i+1,j): LL(i+1,j); e2 D: LL(i,j)
+#pragma unroll
+    for (int sh = 0; sh < 2; ++sh) {
+        double dw[3];
+        bool act[3];
+        tri_Dw<HET>(L, sh, i, j, dw);
+        tri_edges_active(sh, i, j, n, act);
+        const double dself = __ldg(dpi + sh * plane + o);
+        double ds = L.s0h2, off = 0.0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            if (!act[e]) continue;
+            const double c = L.tau * L.bw[sh][e] / dw[e];
+            ds += c * L.bw[sh][e];
+            int ni, nj;
+            if (sh == 0) { ni = e == 1 ? i - 1 : i; nj = e == 0 ? j - 1 : j; }
+            else         { ni = e == 1 ? i + 1 : i; nj = e == 0 ? j + 1 : j; }
+            const double dn = __ldg(dpi + (1 - sh) * plane + (int64_t)nj * pitch + ni);
+            off = fma(c * L.bw[1 - sh][e], dn, off);
+        }
+        const double sd = fma(ds, dself, off);
+        dpo[sh * plane + o] = dself + omJ * (__ldg(g + sh * plane + o) - sd) / ds;
+    }
+}
+
+// stage B: du = F_u^{-1}(r_u - alpha B_u^T dp), dw = (r_w - tau B_w^T dp)/(tau D_w),
+// xout = x + omega (du, dw, dp)
+constexpr int BB_XW = BTX + 4, BB_XH = BTY + 4, BB_RW = BTX + 2, BB_RH = BTY + 2;
+constexpr int BB_PW = BTX + 1, BB_PH = BTY + 1, BB_DW = BTX + 3, BB_DH = BTY + 3;
+constexpr int BB_XSZ = 10 * BB_XW * BB_XH, BB_ZSZ = 8 * BB_PW * BB_PH;
+constexpr int BB_USZ = BB_XSZ > BB_ZSZ ? BB_XSZ : BB_ZSZ;
+constexpr int BB_SMEM = (BB_USZ + 10 * BB_RW * BB_RH + 2 * BB_DW * BB_DH) * 8;
+
+template <bool HET, bool XZERO>
+__global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
+                                                       const double* __restrict__ x, const double* __restrict__ b,
+                                                       const double* __restrict__ dp, double* __restrict__ xo) {
+    extern __shared__ double sm[];
+    double* xs = sm;
+    double* zs = sm;
+    double* rs = sm + BB_USZ;
+    double* ps = rs + 10 * BB_RW * BB_RH;   // dp on cells [i0-2, i0+BTX] x [j0-2, j0+BTY]
+    if (*L.stop) return;
+    const int n = L.n, pitch = L.pitch;
+    const int64_t plane = L.plane;
+    const int i0 = blockIdx.x * BTX, j0 = blockIdx.y * BTY;
+    for (int t = threadIdx.x; t < 2 * BB_DW * BB_DH; t += BNT) {
+        const int sh = t / (BB_DW * BB_DH), rem = t - sh * (BB_DW * BB_DH);
+        const int ly = rem / BB_DW, lx = rem - ly * BB_DW;
+        const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
+        ps[t] = (ci >= 0 && cj >= 0 && ci < n && cj < n) ? __ldg(dp + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+    }
+    if (!XZERO) {
+        load_tile<BB_XW, BB_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        __syncthreads();
+#pragma unroll 1
+        for (int t = threadIdx.x; t < BB_RW * BB_RH; t += BNT) {
+            const int ly = t / BB_RW, lx = t - ly * BB_RW;
+            double rv[10];
+            residual_at<BB_XW, BB_XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) rs[k * BB_RW * BB_RH + t] = rv[k];
+        }
+    } else {
+        load_tile<BB_RW, BB_RH, 8>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);
+    }
+    __syncthreads();
+    // y_u = r_u - alpha B_u^T dp on the r tile (u planes, active DoFs)
+#pragma unroll 1
+    for (int t = threadIdx.x; t < BB_RW * BB_RH; t += BNT) {
+        const int ly = t / BB_RW, lx = t - ly * BB_RW;
+        const int c = i0 - 1 + lx, d = j0 - 1 + ly;
+        const double* p00 = ps + (ly + 1) * BB_DW + (lx + 1);   // cell (c, d)
+        double bt[5] = {0, 0, 0, 0, 0};
+#define MG_I(k, cdx, cdy, sh, q) bt[k] = fma(L.bu[sh][q], p00[(sh) * (BB_DW * BB_DH) + (cdy) * BB_DW + (cdx)], bt[k]);
+        MG_INCIDENT_0(MG_I) MG_INCIDENT_1(MG_I) MG_INCIDENT_2(MG_I) MG_INCIDENT_3(MG_I) MG_INCIDENT_4(MG_I)
+#undef MG_I
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+            if (is_active(k, c, d, n)) rs[k * BB_RW * BB_RH + t] -= L.alpha * bt[k];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int t = threadIdx.x; t < BB_PW * BB_PH; t += BNT) {
+        const int py = t / BB_PW, px = t - py * BB_PW;
+        const int a = i0 + px, bb = j0 + py;
+        if (a <= n && bb <= n) {
+            double rr[8];
+            gather8<BB_RW, BB_RH>(rs + (py + 1) * BB_RW + (px + 1), rr);
+            patch_apply8(U, vertex_class(a, bb, n), rr, zs + t, BB_PW * BB_PH);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) zs[s * BB_PW * BB_PH + t] = 0.0;
+        }
+    }
+    __syncthreads();
+    const int lx = threadIdx.x % BTX, ly = threadIdx.x / BTX;
+    const int i = i0 + lx, j = j0 + ly;
+    if (i > n || j > n) return;
+    const double* c00 = zs + ly * BB_PW + lx;
+#define CC(s, dx, dy) c00[(s) * (BB_PW * BB_PH) + (dy) * BB_PW + (dx)]
+    double d[10];
+    d[0] = CC(0, 0, 0);
+    d[1] = CC(1, 0, 0);
+    d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+    d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+    d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+#undef CC
+    const double* p00 = ps + (ly + 2) * BB_DW + (lx + 2);   // cell (i, j)
+    const double* r00 = rs + (ly + 1) * BB_RW + (lx + 1);
+    double bw[3] = {0, 0, 0};
+#define MG_I(k, cdx, cdy, sh, q) bw[(k) - 5] = fma(L.bw[sh][(q) - 9], p00[(sh) * (BB_DW * BB_DH) + (cdy) * BB_DW + (cdx)], bw[(k) - 5]);
+    MG_INCIDENT_5(MG_I) MG_INCIDENT_6(MG_I) MG_INCIDENT_7(MG_I)
+#undef MG_I
+#pragma unroll
+    for (int k = 5; k < 8; ++k) {
+        const double dwk = Dw_at<HET>(L, k, i, j);
+        d[k] = is_active(k, i, j, n) ? (r00[k * BB_RW * BB_RH] - L.tau * bw[k - 5]) / (L.tau * dwk) : 0.0;
+    }
+    d[8] = p00[0];
+    d[9] = p00[BB_DW * BB_DH];
+    const int64_t o = (int64_t)j * pitch + i;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+        const double xv = XZERO ? 0.0 : __ldg(x + k * plane + o);
+        xo[k * plane + o] = is_active(k, i, j, n) ? fma(omega, d[k], xv) : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K^{-1} pyramid (reading A11): level 0 from the user's K [shape][j][i] (n x n), then averages
+__global__ void kinv_from_K_kernel(int n, int pitch, const double* __restrict__ K, double* __restrict__ kinv) {
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (i >= n || j >= n) return;
+    const int64_t plane = (int64_t)(n + 1) * pitch;
+    for (int sh = 0; sh < 2; ++sh)
+        kinv[sh * plane + (int64_t)j * pitch + i] = 1.0 / K[((int64_t)sh * n + j) * n + i];
+}
+
+__global__ void kinv_coarsen_kernel(int nf, int pitchf, const double* __restrict__ kf, int pitchc,
+                                    double* __restrict__ kc) {
+    const int I = blockIdx.x * 32 + (threadIdx.x & 31), J = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int nc = nf / 2;
+    if (I >= nc || J >= nc) return;
+    const int64_t pf = (int64_t)(nf + 1) * pitchf, pc = (int64_t)(nc + 1) * pitchc;
+#define KF(sh, di, dj) kf[(sh) * pf + (int64_t)(2 * J + (dj)) * pitchf + 2 * I + (di)]
+    // children in the oracle's accumulation order (shape-major, then j, then i)
+    const double ll = ((KF(0, 0, 0) + KF(0, 1, 0)) + KF(0, 0, 1)) + KF(1, 0, 0);
+    const double ur = ((KF(0, 1, 1) + KF(1, 1, 0)) + KF(1, 0, 1)) + KF(1, 1, 1);
+#undef KF
+    kc[(int64_t)J * pitchc + I] = ll / 4.0;
+    kc[pc + (int64_t)J * pitchc + I] = ur / 4.0;
+}
+
+template <typename F>
+void set_smem(F* f, int bytes) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace
+
+void kernels_init() {
+    set_smem(vanka_kernel<false>, V_SMEM);
+    set_smem(vanka_kernel<true>, V_SMEM);
+    set_smem(restrict_kernel<0, false>, C_SMEM_PLAIN);
+    set_smem(restrict_kernel<2, false>, C_SMEM_PLAIN);
+    set_smem(restrict_kernel<1, false>, C_SMEM_FUSED);
+    set_smem(restrict_kernel<1, true>, C_SMEM_FUSED);
+    set_smem(coarse_kernel, 4096 * 8);
+    set_smem(bsr_a_kernel<false, false>, BA_SMEM);
+    set_smem(bsr_a_kernel<false, true>, BA_SMEM);
+    set_smem(bsr_a_kernel<true, false>, BA_SMEM);
+    set_smem(bsr_a_kernel<true, true>, BA_SMEM);
+    set_smem(bsr_b_kernel<false, false>, BB_SMEM);
+    set_smem(bsr_b_kernel<false, true>, BB_SMEM);
+    set_smem(bsr_b_kernel<true, false>, BB_SMEM);
+    set_smem(bsr_b_kernel<true, true>, BB_SMEM);
+}
+
+int blocks_residual(int n) { return ((n + RTX) / RTX) * ((n + RTY) / RTY); }
+int blocks_vanka(int n) { return ((n + VTX) / VTX) * ((n + VTY) / VTY); }
+int blocks_bsr(int n) { return ((n + BTX) / BTX) * ((n + BTY) / BTY); }
+
+cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
+                            cudaStream_t s) {
+    dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
+    if (L.kinv_field) residual_kernel<true><<<grid, RNT, 0, s>>>(L, x, b, r, S);
+    else residual_kernel<false><<<grid, RNT, 0, s>>>(L, x, b, r, S);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
+                         NormSink S, cudaStream_t s) {
+    dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
+    if (x_zero) vanka_kernel<true><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
+    else vanka_kernel<false><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode, const double* x,
+                            const double* br, double* bc, cudaStream_t s) {
+    dim3 grid((nc + CX) / CX, (nc + CY) / CY);
+    if (mode == 1) {
+        if (Lf.kinv_field) restrict_kernel<1, true><<<grid, CNT, C_SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
+        else restrict_kernel<1, false><<<grid, CNT, C_SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
+    } else if (mode == 0) {
+        restrict_kernel<0, false><<<grid, CNT, C_SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+    } else {
+        restrict_kernel<2, false><<<grid, CNT, C_SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double* e, double* x, const int* stop,
+                           cudaStream_t s) {
+    dim3 grid((nc + 31) / 32, (nc + 7) / 8);
+    prolong_kernel<<<grid, 256, 0, s>>>(nf, pitchf, nc, pitchc, e, x, stop);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coarse(int N, const double* G, const int64_t* slots, const double* b, double* x,
+                          const int* stop, cudaStream_t s) {
+    int blocks = N <= 1024 ? 1 : (N + 255) / 256;
+    coarse_kernel<<<blocks, 256, N * 8, s>>>(N, G, slots, b, x, stop);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_a(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
+                         double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s) {
+    dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
+    const bool het = L.kinv_field != nullptr;
+    if (het && x_zero) bsr_a_kernel<true, true><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    else if (het) bsr_a_kernel<true, false><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    else if (x_zero) bsr_a_kernel<false, true><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    else bsr_a_kernel<false, false><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_jacobi(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
+                              cudaStream_t s) {
+    dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
+    if (L.kinv_field) bsr_jacobi_kernel<true><<<grid, 256, 0, s>>>(L, omJ, g, dpi, dpo);
+    else bsr_jacobi_kernel<false><<<grid, 256, 0, s>>>(L, omJ, g, dpi, dpo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega, const double* x, const double* b,
+                         const double* dp, double* xo, bool x_zero, cudaStream_t s) {
+    dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
+    const bool het = L.kinv_field != nullptr;
+    if (het && x_zero) bsr_b_kernel<true, true><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    else if (het) bsr_b_kernel<true, false><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    else if (x_zero) bsr_b_kernel<false, true><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    else bsr_b_kernel<false, false><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kinv_from_K(int n, int pitch, const double* K, double* kinv, cudaStream_t s) {
+    dim3 grid((n + 31) / 32, (n + 7) / 8);
+    kinv_from_K_kernel<<<grid, 256, 0, s>>>(n, pitch, K, kinv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kinv_coarsen(int nf, int pitchf, const double* kf, int pitchc, double* kc, cudaStream_t s) {
+    dim3 grid((nf / 2 + 31) / 32, (nf / 2 + 7) / 8);
+    kinv_coarsen_kernel<<<grid, 256, 0, s>>>(nf, pitchf, kf, pitchc, kc);
+    return cudaGetLastError();
+}

@@ -1,0 +1,41 @@
+// Kernel declarations and launch helpers (sm_100a, fp64).  See mg_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include "mg_internal.h"
+
+// Deterministic norm accumulation: one partial per block, the last block sums them in index order.
+struct NormSink {
+    double* out;          // device double receiving sum of squares (nullptr: no norm)
+    double* partials;     // >= number of blocks of the launch
+    unsigned* counter;    // zero-initialised; reset by the last block
+    SolveState* state;    // non-null: append the norm to state->hist and decide state->stop
+};
+void kernels_init();
+
+// All launchers return cudaGetLastError() of the launch.
+cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r,
+                            NormSink norm, cudaStream_t s);
+cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
+                         bool x_zero, NormSink norm, cudaStream_t s);
+// mode 0: r_fine given (x_fine, b_fine unused); 1: r = b - A x fused; 2: x == 0 (r = b)
+cudaError_t launch_restrict(const LevelParams& Lf, int n_coarse, int pitch_coarse, int mode,
+                            const double* x_fine, const double* b_or_r_fine, double* b_coarse,
+                            cudaStream_t s);
+cudaError_t launch_prolong(int n_fine, int pitch_fine, int n_coarse, int pitch_coarse,
+                           const double* e_coarse, double* x_fine, const int* stop, cudaStream_t s);
+cudaError_t launch_coarse(int N, const double* Ginv, const int64_t* slots, const double* b, double* x,
+                          const int* stop, cudaStream_t s);
+// BSR
+cudaError_t launch_bsr_a(const LevelParams& L, const DispParams& U, double omega_J, const double* x,
+                         const double* b, double* g, double* dp, NormSink norm, bool x_zero,
+                         cudaStream_t s);
+cudaError_t launch_bsr_jacobi(const LevelParams& L, double omega_J, const double* g, const double* dp_in,
+                              double* dp_out, cudaStream_t s);
+cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega, const double* x,
+                         const double* b, const double* dp, double* xout, bool x_zero, cudaStream_t s);
+cudaError_t launch_kinv_coarsen(int n_fine, int pitch_fine, const double* kf, int pitch_coarse, double* kc,
+                                cudaStream_t s);
+cudaError_t launch_kinv_from_K(int n, int pitch, const double* K, double* kinv, cudaStream_t s);
+int blocks_residual(int n);
+int blocks_vanka(int n);
+int blocks_bsr(int n);

@@ -1,0 +1,368 @@
+// Host-side setup of the B200 multigrid path: per-level stencil coefficients, deflated Vanka
+// patch inverses, displacement-patch inverses (BSR) and the dense deflated coarsest inverse.
+// Pure host fp64 / long double math; no CUDA calls, so the CPU test-suite can call it through
+// mg_host_level_tables().  Geometry comes from the generated mg_tables.h (gen_tables.py).
+//
+//  * element entries of A^RQ: eq. block_form_rq
+//  * Vanka patch matrices K_v = V_v A V_v^T and natural weights D_v: PAPER.md:575-590
+//  * exact deflation of the constant-pressure eigenvector (reading A9)
+//  * displacement patches A^RQ_{u,v} for the inexact BSR smoother: PAPER.md:686, 1682-1688
+//  * coarsest direct solve: PAPER.md:945
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "mg_internal.h"
+#include "mg_tables.h"
+
+namespace {
+
+const int VSLOT[MG_PSLOTS][3] = MG_VSLOT_TABLE;
+
+int blk(int q) { return q < 9 ? 0 : (q < 12 ? 1 : 2); }   // 0 = u, 1 = w, 2 = p
+
+// Entry (q, q2) of the element matrix of A^RQ on a triangle of shape s at mesh size h.
+double elem_entry(int s, int q, int q2, const Material& m, double h, double kinv) {
+    int a = blk(q), b = blk(q2);
+    if (a == 0 && b == 0) return 2.0 * m.mu * REF_AEPS[s][q][q2] + 2.0 * m.lambda * REF_BU[s][q] * REF_BU[s][q2];
+    if (a == 0 && b == 2) return m.alpha * h * REF_BU[s][q];
+    if (a == 2 && b == 0) return m.alpha * h * REF_BU[s][q2];
+    if (a == 1 && b == 1) return m.tau * m.mu_f * kinv * h * h * REF_MW1[s][q - 9][q2 - 9];
+    if (a == 1 && b == 2) return m.tau * h * REF_BW[s][q - 9];
+    if (a == 2 && b == 1) return m.tau * h * REF_BW[s][q2 - 9];
+    if (a == 2 && b == 2) return -m.inv_M * h * h * REF_MP[s];
+    return 0.0;
+}
+
+bool active(int p, int i, int j, int n) {
+    if (i < 0 || j < 0 || i > n || j > n) return false;
+    switch (p) {
+        case 0: case 1: return i > 0 && i < n && j > 0 && j < n;
+        case 2: case 5: return i < n && j > 0 && j < n;
+        case 3: case 6: return i > 0 && i < n && j < n;
+        default: return i < n && j < n;
+    }
+}
+
+// In-place inverse of the m x m matrix A (row major) by Gauss-Jordan elimination with partial
+// pivoting in long double.  Returns false if singular.
+bool invert(std::vector<long double>& A, int m) {
+    std::vector<long double> I(m * (size_t)m, 0.0L);
+    for (int i = 0; i < m; ++i) I[i * (size_t)m + i] = 1.0L;
+    for (int c = 0; c < m; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < m; ++r)
+            if (fabsl(A[r * (size_t)m + c]) > fabsl(A[piv * (size_t)m + c])) piv = r;
+        if (A[piv * (size_t)m + c] == 0.0L) return false;
+        if (piv != c)
+            for (int k = 0; k < m; ++k) {
+                std::swap(A[c * (size_t)m + k], A[piv * (size_t)m + k]);
+                std::swap(I[c * (size_t)m + k], I[piv * (size_t)m + k]);
+            }
+        long double d = 1.0L / A[c * (size_t)m + c];
+        for (int k = 0; k < m; ++k) { A[c * (size_t)m + k] *= d; I[c * (size_t)m + k] *= d; }
+        for (int r = 0; r < m; ++r) {
+            if (r == c) continue;
+            long double f = A[r * (size_t)m + c];
+            if (f == 0.0L) continue;
+            for (int k = 0; k < m; ++k) {
+                A[r * (size_t)m + k] -= f * A[c * (size_t)m + k];
+                I[r * (size_t)m + k] -= f * I[c * (size_t)m + k];
+            }
+        }
+    }
+    A.swap(I);
+    return true;
+}
+
+// Deflated inverse of a symmetric saddle-point block K (m x m, row major) whose pressure
+// indicator vector (ispress) spans an exact eigenvector v = 1_p / sqrt(mp) with eigenvalue
+// -gamma (reading A9):  K^{-1} r = (v.r / -gamma) v + (K - sigma v v^T)^{-1} (r - v v.r).
+// Returns the matrix of that map.  Without pressure DoFs it is the plain inverse.
+bool deflated_inverse(const std::vector<double>& K, const std::vector<int>& ispress, int m,
+                      std::vector<double>& G, char* err, int errlen) {
+    int mp = 0;
+    for (int i = 0; i < m; ++i) mp += ispress[i];
+    std::vector<long double> Kd(m * (size_t)m);
+    for (size_t i = 0; i < Kd.size(); ++i) Kd[i] = K[i];
+    G.assign(m * (size_t)m, 0.0);
+    if (mp == 0) {
+        if (!invert(Kd, m)) { snprintf(err, errlen, "singular displacement patch"); return false; }
+        for (size_t i = 0; i < G.size(); ++i) G[i] = (double)Kd[i];
+        return true;
+    }
+    std::vector<long double> v(m, 0.0L);
+    for (int i = 0; i < m; ++i) v[i] = ispress[i] ? 1.0L / sqrtl((long double)mp) : 0.0L;
+    // gamma = -v^T K v and the eigen-residual check
+    std::vector<long double> Kv(m, 0.0L);
+    long double kmax = 0.0L;
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) {
+            Kv[i] += (long double)K[i * (size_t)m + k] * v[k];
+            kmax = fmaxl(kmax, fabsl((long double)K[i * (size_t)m + k]));
+        }
+    long double gamma = 0.0L;
+    for (int i = 0; i < m; ++i) gamma -= v[i] * Kv[i];
+    long double res = 0.0L;
+    for (int i = 0; i < m; ++i) res = fmaxl(res, fabsl(Kv[i] + gamma * v[i]));
+    if (res > 1e-12L * fmaxl(kmax, 1.0L)) {
+        snprintf(err, errlen, "constant pressure is not an exact eigenvector (res %.3Le)", res);
+        return false;
+    }
+    if (gamma <= 0.0L) {
+        snprintf(err, errlen, "inv_M must be > 0 for the deflated solve (gamma = %.3Le)", gamma);
+        return false;
+    }
+    // sigma: mean diagonal of the pressure Schur complement in the diagonal approximation
+    long double sig = 0.0L;
+    for (int p = 0; p < m; ++p) {
+        if (!ispress[p]) continue;
+        for (int y = 0; y < m; ++y)
+            if (!ispress[y] && K[y * (size_t)m + y] != 0.0)
+                sig += (long double)K[p * (size_t)m + y] * K[p * (size_t)m + y] / K[y * (size_t)m + y];
+    }
+    sig /= mp;
+    if (sig == 0.0L) sig = gamma;
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) Kd[i * (size_t)m + k] -= sig * v[i] * v[k];
+    if (!invert(Kd, m)) { snprintf(err, errlen, "singular deflated patch"); return false; }
+    // G = Kd^{-1} (I - v v^T) + (-1/gamma) v v^T
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) {
+            long double s = 0.0L;
+            for (int t = 0; t < m; ++t) s += Kd[i * (size_t)m + t] * ((t == k ? 1.0L : 0.0L) - v[t] * v[k]);
+            s += -v[i] * v[k] / gamma;
+            G[i * (size_t)m + k] = (double)s;
+        }
+    return true;
+}
+
+// Patch matrix K (ns x ns, row major over the first ns VSLOT entries) of vertex (a, b) at mesh
+// size n: sum over the star triangles of the element matrices restricted to active patch DoFs.
+// ww_scale multiplies the M_w part (0 for the displacement patches, which use A_u^RQ only).
+void patch_matrix(int a, int b, int n, int ns, const Material& m, double h, std::vector<double>& K,
+                  std::vector<int>& act) {
+    K.assign(ns * (size_t)ns, 0.0);
+    act.assign(ns, 0);
+    for (int s = 0; s < ns; ++s) act[s] = active(VSLOT[s][2], a + VSLOT[s][0], b + VSLOT[s][1], n);
+    for (int cx = -1; cx <= 0; ++cx)
+        for (int cy = -1; cy <= 0; ++cy) {
+            int ci = a + cx, cj = b + cy;
+            if (ci < 0 || cj < 0 || ci >= n || cj >= n) continue;
+            for (int sh = 0; sh < 2; ++sh) {
+                int loc[13];
+                for (int q = 0; q < 13; ++q) {
+                    loc[q] = -1;
+                    int dx = cx + LOCAL_DOF[sh][q][0], dy = cy + LOCAL_DOF[sh][q][1], p = LOCAL_DOF[sh][q][2];
+                    for (int s = 0; s < ns; ++s)
+                        if (VSLOT[s][0] == dx && VSLOT[s][1] == dy && VSLOT[s][2] == p && act[s]) loc[q] = s;
+                }
+                for (int q = 0; q < 13; ++q)
+                    for (int q2 = 0; q2 < 13; ++q2) {
+                        if (loc[q] < 0 || loc[q2] < 0) continue;
+                        K[loc[q] * (size_t)ns + loc[q2]] += elem_entry(sh, q, q2, m, h, 1.0 / m.K);
+                    }
+            }
+        }
+}
+
+// weighted, deflated inverse over the active slots, embedded in ns x ns
+bool patch_inverse(int a, int b, int n, int ns, const Material& m, double h, double* out, char* err,
+                   int errlen) {
+    std::vector<double> K;
+    std::vector<int> act;
+    patch_matrix(a, b, n, ns, m, h, K, act);
+    std::vector<int> idx;
+    for (int s = 0; s < ns; ++s)
+        if (act[s]) idx.push_back(s);
+    int mm = (int)idx.size();
+    memset(out, 0, sizeof(double) * ns * ns);
+    if (mm == 0) return true;
+    std::vector<double> Ks(mm * (size_t)mm), G;
+    std::vector<int> isp(mm);
+    for (int r = 0; r < mm; ++r) {
+        isp[r] = idx[r] >= 14;
+        for (int c = 0; c < mm; ++c) Ks[r * (size_t)mm + c] = K[idx[r] * (size_t)ns + idx[c]];
+    }
+    if (!deflated_inverse(Ks, isp, mm, G, err, errlen)) return false;
+    for (int r = 0; r < mm; ++r) {
+        int s = idx[r];
+        double w = s < 2 ? 1.0 : (s < 14 ? 0.5 : 1.0 / 3.0);   // natural weights
+        for (int c = 0; c < mm; ++c) out[s * ns + idx[c]] = w * G[r * (size_t)mm + c];
+    }
+    return true;
+}
+
+int class_coord(int c, int n) { return c == 0 ? 1 : (c == 1 ? 0 : n); }
+
+// +/- basis of the 180-degree rotation for ns = 20 (Vanka) or 8 (displacement).  comp[t] lists
+// hat component t as (slot a, slot b, sign): hat_t = r_a + sign r_b (b < 0: single).
+struct HatComp { int a, b, sg; };
+void hat_basis(int ns, std::vector<HatComp>& plus, std::vector<HatComp>& minus) {
+    plus.clear(); minus.clear();
+    minus.push_back({0, -1, 0});
+    minus.push_back({1, -1, 0});
+    int npair_edge = ns == 20 ? 6 : 3;
+    for (int q = 0; q < npair_edge; ++q) {          // bubble / RT0 pairs: diff in +, sum in -
+        plus.push_back({2 + 2 * q, 3 + 2 * q, -1});
+        minus.push_back({2 + 2 * q, 3 + 2 * q, +1});
+    }
+    if (ns == 20)
+        for (int q = 0; q < 3; ++q) {               // P0 pairs: sum in +, diff in -
+            plus.push_back({14 + 2 * q, 15 + 2 * q, +1});
+            minus.push_back({14 + 2 * q, 15 + 2 * q, -1});
+        }
+}
+
+// Split the interior weighted inverse G (ns x ns) into the +/- blocks (with 1/2 folded into pair
+// rows).  Checks block diagonality.
+bool split_pm(const double* G, int ns, double* gp, double* gm, char* err, int errlen) {
+    std::vector<HatComp> P, M;
+    hat_basis(ns, P, M);
+    std::vector<HatComp> all(P);
+    all.insert(all.end(), M.begin(), M.end());
+    int np = (int)P.size();
+    // T (ns x ns): hat = T r ; Tinv: r = Tinv hat
+    std::vector<double> T(ns * ns, 0.0), Ti(ns * ns, 0.0);
+    for (int t = 0; t < ns; ++t) {
+        T[t * ns + all[t].a] = 1.0;
+        if (all[t].b >= 0) T[t * ns + all[t].b] = all[t].sg;
+    }
+    for (int t = 0; t < ns; ++t) {                    // columns of Tinv
+        if (all[t].b < 0) { Ti[all[t].a * ns + t] = 1.0; continue; }
+        Ti[all[t].a * ns + t] = 0.5;
+        Ti[all[t].b * ns + t] = 0.5 * all[t].sg;
+    }
+    std::vector<double> TG(ns * ns, 0.0), Gh(ns * ns, 0.0);
+    for (int i = 0; i < ns; ++i)
+        for (int k = 0; k < ns; ++k) {
+            double s = 0;
+            for (int t = 0; t < ns; ++t) s += T[i * ns + t] * G[t * ns + k];
+            TG[i * ns + k] = s;
+        }
+    double gmax = 0;
+    for (int i = 0; i < ns; ++i)
+        for (int k = 0; k < ns; ++k) {
+            double s = 0;
+            for (int t = 0; t < ns; ++t) s += TG[i * ns + t] * Ti[t * ns + k];
+            Gh[i * ns + k] = s;
+            gmax = fmax(gmax, fabs(s));
+        }
+    for (int i = 0; i < ns; ++i)
+        for (int k = 0; k < ns; ++k)
+            if ((i < np) != (k < np) && fabs(Gh[i * ns + k]) > 1e-11 * gmax) {
+                snprintf(err, errlen, "interior patch inverse is not block diagonal in the +/- basis (%d,%d: %g)",
+                         i, k, Gh[i * ns + k]);
+                return false;
+            }
+    int nm = ns - np;
+    for (int i = 0; i < np; ++i)
+        for (int k = 0; k < np; ++k) gp[i * np + k] = Gh[i * ns + k] * (P[i].b >= 0 ? 0.5 : 1.0);
+    for (int i = 0; i < nm; ++i)
+        for (int k = 0; k < nm; ++k) gm[i * nm + k] = Gh[(np + i) * ns + np + k] * (M[i].b >= 0 ? 0.5 : 1.0);
+    return true;
+}
+
+}  // namespace
+
+int64_t n_active_of(int n) { return 10LL * n * n - 8LL * n + 2; }
+
+int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, int errlen) {
+    if (n < 2) { snprintf(err, errlen, "level n = %d < 2", n); return -1; }
+    memset(t, 0, sizeof(*t));
+    double h = 1.0 / n;
+    t->n = n;
+    t->h = h;
+    LevelParams& L = t->L;
+    L.n = n;
+    double kinv = 1.0 / m.K;
+#define Y(ci, s, q, q2) L.coef[ci] += elem_entry(s, q, q2, m, h, kinv);
+    MG_STENCIL_CONTRIB(Y)
+#undef Y
+    for (int s = 0; s < 2; ++s)
+        for (int e = 0; e < 3; ++e) {
+            for (int e2 = 0; e2 < 3; ++e2) L.ww[s][e][e2] = m.tau * m.mu_f * h * h * REF_MW1[s][e][e2];
+            L.bw[s][e] = h * REF_BW[s][e];
+            L.mw1d[s][e] = m.mu_f * h * h * REF_MW1[s][e][e];
+        }
+    for (int s = 0; s < 2; ++s)
+        for (int q = 0; q < 9; ++q) L.bu[s][q] = h * REF_BU[s][q];
+    L.kinv = kinv;
+    L.tau = m.tau;
+    L.alpha = m.alpha;
+    L.s0h2 = (m.inv_M + m.alpha * m.alpha / (m.lambda + m.mu)) * h * h * 0.5;   // d = 2 (reading A19)
+    // Vanka and displacement patch inverses per vertex class
+    Material mu_only = m;
+    for (int cy = 0; cy < 3; ++cy)
+        for (int cx = 0; cx < 3; ++cx) {
+            int c = cx + 3 * cy, a = class_coord(cx, n), b = class_coord(cy, n);
+            if (!patch_inverse(a, b, n, MG_PSLOTS, m, h, t->vanka[c], err, errlen)) return -1;
+            if (!patch_inverse(a, b, n, MG_USLOTS, mu_only, h, t->disp[c], err, errlen)) return -1;
+        }
+    if (!split_pm(t->vanka[0], MG_PSLOTS, &t->gp[0][0], &t->gm[0][0], err, errlen)) return -1;
+    if (!split_pm(t->disp[0], MG_USLOTS, &t->up[0][0], &t->um[0][0], err, errlen)) return -1;
+    return 0;
+}
+
+int host_coarse_inverse(int n, int pitch, const Material& m, const double* kinvf, double* Ginv,
+                        int64_t* slots, int* Nout, char* err, int errlen) {
+    double h = 1.0 / n;
+    // active numbering in plane-major slot order
+    std::vector<int> num(10 * (size_t)(n + 1) * (n + 1), -1);
+    int N = 0;
+    for (int p = 0; p < 10; ++p)
+        for (int j = 0; j <= n; ++j)
+            for (int i = 0; i <= n; ++i)
+                if (active(p, i, j, n)) {
+                    num[(p * (size_t)(n + 1) + j) * (n + 1) + i] = N;
+                    if (slots) slots[N] = (int64_t)p * (n + 1) * pitch + (int64_t)j * pitch + i;
+                    ++N;
+                }
+    *Nout = N;
+    if (!Ginv) return 0;
+    std::vector<double> A(N * (size_t)N, 0.0);
+    for (int cj = 0; cj < n; ++cj)
+        for (int ci = 0; ci < n; ++ci)
+            for (int sh = 0; sh < 2; ++sh) {
+                double kinv = kinvf ? kinvf[(sh * (size_t)n + cj) * n + ci] : 1.0 / m.K;
+                int g[13];
+                for (int q = 0; q < 13; ++q) {
+                    int i = ci + LOCAL_DOF[sh][q][0], j = cj + LOCAL_DOF[sh][q][1], p = LOCAL_DOF[sh][q][2];
+                    g[q] = num[(p * (size_t)(n + 1) + j) * (n + 1) + i];
+                }
+                for (int q = 0; q < 13; ++q)
+                    for (int q2 = 0; q2 < 13; ++q2)
+                        if (g[q] >= 0 && g[q2] >= 0)
+                            A[g[q] * (size_t)N + g[q2]] += elem_entry(sh, q, q2, m, h, kinv);
+            }
+    std::vector<int> isp(N, 0);
+    for (int p = 8; p < 10; ++p)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) isp[num[(p * (size_t)(n + 1) + j) * (n + 1) + i]] = 1;
+    std::vector<double> G;
+    if (!deflated_inverse(A, isp, N, G, err, errlen)) return -1;
+    for (int r = 0; r < N; ++r)
+        for (int c = 0; c < N; ++c) Ginv[c * (size_t)N + r] = G[r * (size_t)N + c];   // column major
+    return 0;
+}
+
+extern "C" int mg_host_level_tables(int32_t n, double lambda, double mu, double K, double tau, double alpha,
+                                    double inv_M, double mu_f, double* stencil_coef, double* ww,
+                                    double* vanka, double* disp) {
+    Material m{lambda, mu, K, tau, alpha, inv_M, mu_f};
+    static thread_local char err[256];
+    HostLevelTables* t = new HostLevelTables;
+    int rc = host_level_tables(n, m, t, err, sizeof(err));
+    if (rc == 0) {
+        if (stencil_coef) memcpy(stencil_coef, t->L.coef, sizeof(t->L.coef));
+        if (ww)
+            for (int s = 0; s < 2; ++s)
+                for (int e = 0; e < 3; ++e)
+                    for (int e2 = 0; e2 < 3; ++e2) ww[(s * 3 + e) * 3 + e2] = t->L.ww[s][e][e2] * t->L.kinv;
+        if (vanka) memcpy(vanka, t->vanka, sizeof(t->vanka));
+        if (disp) memcpy(disp, t->disp, sizeof(t->disp));
+    }
+    delete t;
+    return rc == 0 ? 0 : -1;
+}

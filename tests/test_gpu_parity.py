@@ -1,0 +1,244 @@
+"""GPU parity: every C-ABI operation of libmg.so against the CPU oracle on the same seeded inputs.
+
+Tolerances:
+* residual: componentwise |r_G - r_O| <= 32 u (|b| + |A||x|), u = 2^-53 (rounding of one residual
+  evaluation in two summation orders);
+* one relaxation sweep / transfer / coarse solve: the result is a linear map of rounded inputs;
+  compared in the max norm relative to the result, bounds derived from the operator's conditioning
+  and stated per case;
+* cycles: per-cycle residual norms within 1e-10 relative while the norm is above the rounding floor
+  (SURVEY 8c-11), convergence factors within 1e-3.
+"""
+import numpy as np
+import pytest
+
+import mg_inputs
+from tests import _cases as C
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _inactive_zero(H, v, level=0):
+    """Inactive and padding slots of a device vector are exactly 0."""
+    nl = H.level_n(level)
+    a = v.cpu().numpy()
+    mask = np.zeros(a.shape, dtype=bool)
+    mask[:, :, : nl + 1] = mg_inputs.active_mask(nl)
+    assert np.all(a[~mask] == 0.0)
+
+
+@pytest.mark.parametrize("n,pname,het", [(4, "unit", None), (8, "mixed", None), (16, "stiff", None),
+                                         (40, "cfg5", None), (66, "mixed", None), (24, "unit", 3),
+                                         (34, "mixed", 7)])
+def test_residual(n, pname, het):
+    torch = _torch()
+    H = C.gpu_hierarchy(n, 1, pname, het)
+    op = C.operator(n, pname, het)
+    m = C.mesh(n)
+    x = mg_inputs.uniform_vector(n, 11)
+    b = mg_inputs.uniform_rhs(n, 12)
+    xd, bd = H.to_device(x), H.to_device(b)
+    rd = H.zeros()
+    nrm = H.residual(0, xd, bd, rd, norm=True)
+    torch.cuda.synchronize()
+    rG = m.to_active(H.to_host(rd))
+    xa, ba = m.to_active(x), m.to_active(b)
+    rO = ba - op.A @ xa
+    scale = np.abs(ba) + C.abs_matvec(op, xa)
+    err = np.abs(rG - rO)
+    assert np.all(err <= 32 * U * scale), (err / scale).max() / U
+    assert abs(nrm - np.linalg.norm(rO)) <= 1e-13 * np.linalg.norm(rO) + 32 * U * np.linalg.norm(scale)
+    _inactive_zero(H, rd)
+
+
+@pytest.mark.parametrize("n,pname,omega", [(4, "unit", 0.74), (8, "mixed", 0.9), (16, "stiff", 0.7),
+                                           (40, "cfg5", 0.7), (66, "unit", 0.74)])
+def test_vanka_sweep(n, pname, omega):
+    torch = _torch()
+    H = C.gpu_hierarchy(n, 1, pname)
+    from oracle.relax import Vanka
+    op = C.operator(n, pname)
+    V = Vanka(op)
+    m = C.mesh(n)
+    x = mg_inputs.uniform_vector(n, 21)
+    b = mg_inputs.uniform_rhs(n, 22)
+    xd, bd = H.to_device(x), H.to_device(b)
+    H.relax_vanka(0, xd, bd, omega, sweeps=1)
+    torch.cuda.synchronize()
+    xG = H.to_host(xd)
+    xO = m.from_active(V.sweep(m.to_active(x), m.to_active(b), omega))
+    err = np.abs(xG - xO).max() / np.abs(xO).max()
+    tol = 1e-12 if pname != "stiff" else 1e-9
+    assert err <= tol, err
+    _inactive_zero(H, xd)
+
+
+@pytest.mark.parametrize("n,pname", [(8, "unit"), (16, "mixed"), (40, "stiff"), (66, "cfg5")])
+def test_restrict_prolong(n, pname):
+    torch = _torch()
+    from oracle.transfer import Transfer
+    H = C.gpu_hierarchy(n, 2, pname)
+    mf, mc = C.mesh(n), C.mesh(n // 2)
+    T = Transfer(mf, mc)
+    r = mg_inputs.uniform_vector(n, 31)
+    e = mg_inputs.uniform_vector(n // 2, 32)
+    x = mg_inputs.uniform_vector(n, 33)
+    rd, bc = H.to_device(r), H.zeros(1)
+    H.restrict(0, rd, bc)
+    ed, xd = H.to_device(e, 1), H.to_device(x)
+    H.prolong(0, ed, xd)
+    torch.cuda.synchronize()
+    bO = T.R @ mf.to_active(r)
+    bG = mc.to_active(H.to_host(bc, 1))
+    assert np.abs(bG - bO).max() <= 1e-14 * np.abs(bO).max()
+    xO = mf.to_active(x) + T.P @ mc.to_active(e)
+    xG = mf.to_active(H.to_host(xd))
+    assert np.abs(xG - xO).max() <= 1e-14 * np.abs(xO).max()
+    _inactive_zero(H, bc, 1)
+    _inactive_zero(H, xd)
+
+
+@pytest.mark.parametrize("nc,pname,het", [(4, "unit", None), (4, "stiff", None), (8, "mixed", None), (4, "unit", 5)])
+def test_coarse_solve(nc, pname, het):
+    torch = _torch()
+    from oracle.cycle import CoarseSolver
+    n = nc * 4
+    H = C.gpu_hierarchy(n, 3, pname, het)
+    Oh = C.hierarchy(n, 3, pname, "bsr" if het else "vanka", het)
+    opc = Oh.ops[-1]
+    mc = Oh.meshes[-1]
+    b = mg_inputs.uniform_vector(nc, 41)
+    bd, xd = H.to_device(b, 2), H.zeros(2)
+    H.coarse_solve(bd, xd)
+    torch.cuda.synchronize()
+    xG = mc.to_active(H.to_host(xd, 2))
+    xO = Oh.coarse.solve(mc.to_active(b))
+    err = np.abs(xG - xO).max() / np.abs(xO).max()
+    assert err <= 1e-11, err
+    # and it is a solve: residual at the rounding level of A_c
+    res = mc.to_active(b) - opc.A @ xG
+    assert np.linalg.norm(res) <= 1e-12 * (np.linalg.norm(mc.to_active(b)) + np.linalg.norm(C.abs_matvec(opc, xG)))
+
+
+@pytest.mark.parametrize("n,pname,het,nJ", [(8, "unit", None, 1), (16, "mixed", None, 3), (40, "unit", None, 3),
+                                            (16, "unit", 3, 3), (34, "mixed", 9, 2)])
+def test_bsr_sweep(n, pname, het, nJ):
+    torch = _torch()
+    from oracle.relax import BSR
+    H = C.gpu_hierarchy(n, 1, pname, het)
+    op = C.operator(n, pname, het)
+    S = BSR(op)
+    m = C.mesh(n)
+    x = mg_inputs.uniform_vector(n, 51)
+    b = mg_inputs.uniform_rhs(n, 52)
+    xd, bd = H.to_device(x), H.to_device(b)
+    om, omJ = 0.7, 0.9
+    H.relax_bsr(0, xd, bd, om, omJ, nJ, sweeps=1)
+    torch.cuda.synchronize()
+    xG = H.to_host(xd)
+    xO = m.from_active(S.sweep(m.to_active(x), m.to_active(b), om, omJ, nJ))
+    err = np.abs(xG - xO).max() / np.abs(xO).max()
+    assert err <= 1e-11, err
+    _inactive_zero(H, xd)
+
+
+def _oracle_history(Oh, b, opts, cycles):
+    N = Oh.ops[0].A.shape[0]
+    x = np.zeros(N)
+    hist = [Oh.residual_norm(x, b)]
+    xs = [x]
+    for _ in range(cycles):
+        x = Oh.cycle(x, b, opts)
+        hist.append(Oh.residual_norm(x, b))
+        xs.append(x)
+    return xs, np.array(hist)
+
+
+def floor_parity(Oh, Oalt, b, xs_O, xs_alt, hO, hAlt):
+    """Per-cycle rounding floor F_k = max(8 u || |b| + |A||x_k| ||, 4 |h_k - h'_k|) where h' is the
+    oracle run with every summation order reversed (reading A22)."""
+    op = Oh.ops[0]
+    F = np.array([max(8 * U * np.linalg.norm(np.abs(b) + C.abs_matvec(op, x)), 4 * abs(h - ha))
+                  for x, h, ha in zip(xs_O, hO, hAlt)])
+    return F
+
+
+@pytest.mark.parametrize("n,levels,pname,relax,het,cycles", [
+    (16, 3, "unit", "vanka", None, 10),      # BASELINE config 1
+    (32, 4, "stiff", "vanka", None, 8),      # config 3 regime
+    (32, 4, "cfg5", "vanka", None, 8),       # config 5 regime
+    (32, 4, "unit", "bsr", None, 8),         # config 2 (BSR) regime
+    (32, 4, "unit", "bsr", 3, 6),            # config 4 regime (heterogeneous K)
+])
+def test_cycle_history(n, levels, pname, relax, het, cycles):
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    from oracle.cycle import Hierarchy as OH
+    H = C.gpu_hierarchy(n, levels, pname, het)
+    Oh = C.hierarchy(n, levels, pname, relax, het)
+    lam, mu, K, tau, alpha, invM = C.PARAMS[pname]
+    kinv = None if het is None else 1.0 / mg_inputs.lognormal_K(n, het)
+    Oalt = OH(n, levels, lam, mu, tau, alpha, invM, 1.0, K=K, Kinv_field=kinv, relax=relax, alt_order=True)
+    m = Oh.meshes[0]
+    b = mg_inputs.uniform_rhs(n, 0)
+    ba = m.to_active(b)
+    if relax == "vanka":
+        od = dict(nu1=1, nu2=1, omega=0.72)
+        go = Opts(1, 1, "vanka", 0.72)
+    else:
+        od = dict(nu1=1, nu2=1, omega=0.5 if het else 0.75, omega_J=0.7 if het else 1.0, jacobi_sweeps=3)
+        go = Opts(1, 1, "bsr", od["omega"], od["omega_J"], 3)
+    xsO, hO = _oracle_history(Oh, ba, od, cycles)
+    xsA, hA = _oracle_history(Oalt, ba, od, cycles)
+    F = floor_parity(Oh, Oalt, ba, xsO, xsA, hO, hA)
+    xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+    hG = [H.residual(0, xd, bd, norm=True)]
+    for _ in range(cycles):
+        hG.append(H.cycle(xd, bd, go))
+    hG = np.array(hG)
+    dev = np.abs(hG - hO)
+    print("rel dev", dev / hO, "floor/h", F / hO, "oracle spread/h", np.abs(hA - hO) / hO)
+    assert np.all(dev <= 1e-10 * hO + F), (dev / hO, F / hO)
+    # final iterate per block, floor = 4x the oracle self-spread
+    xG = H.to_host(xd)
+    e_go = C.block_rel_err(m, xG, m.from_active(xsO[-1]))
+    e_oo = C.block_rel_err(m, m.from_active(xsA[-1]), m.from_active(xsO[-1]))
+    for k in e_go:
+        assert e_go[k] <= 1e-9 + 4 * e_oo[k], (e_go, e_oo)
+    rG, rO = hG[1:] / hG[:-1], hO[1:] / hO[:-1]
+    ok = hO[1:] >= 1e3 * F[1:]
+    assert np.all(np.abs(rG - rO)[ok] <= 1e-3)
+
+
+def test_solve_matches_cycles():
+    """mg_solve (device-side stop flag, fused norms) reproduces the cycle-by-cycle history and stops at rtol."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    n, levels = 16, 3
+    H = C.gpu_hierarchy(n, levels, "unit")
+    Oh = C.hierarchy(n, levels, "unit", "vanka")
+    m = Oh.meshes[0]
+    b = mg_inputs.uniform_rhs(n, 0)
+    od = dict(nu1=1, nu2=1, omega=0.74)
+    _, hO = _oracle_history(Oh, m.to_active(b), od, 40)
+    xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+    rc, hist = H.solve(xd, bd, Opts(1, 1, "vanka", 0.74), rtol=1e-8, max_cycles=40)
+    k = len(hist) - 1
+    assert rc == 0
+    assert hist[-1] <= 1e-8 * hist[0] and hist[-2] > 1e-8 * hist[0]
+    floor = 64 * U * np.linalg.norm(m.to_active(b))
+    assert np.all(np.abs(hist - hO[: k + 1]) <= 1e-10 * hO[: k + 1] + floor)
+    # not converged within 3 cycles -> MG_NOTCONV with 4 history entries
+    xd.zero_()
+    rc, hist = H.solve(xd, bd, Opts(1, 1, "vanka", 0.74), rtol=1e-14, max_cycles=3)
+    assert rc == 1 and len(hist) == 4
+    assert np.all(np.abs(hist - hO[:4]) <= 1e-10 * hO[:4])
