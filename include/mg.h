@@ -106,7 +106,10 @@ void mg_set_allocator(mg_alloc_fn alloc, mg_free_fn free_, void* user);
 /* Build the hierarchy (host fp64 tables: stencils, deflated patch inverses, coarsest inverse;
  * PAPER.md:477-484, 572-590, 945) and upload it to the current device.  Synchronous.
  * lambda >= 0, mu > 0, K > 0 (ignored when grid->K_field != NULL), tau > 0, alpha finite,
- * 1 <= levels, n_{levels-1} = n / 2^(levels-1) >= 2.  Errors: MG_EINVAL, MG_ECUDA, MG_ENOMEM. */
+ * 1 <= levels, n_{levels-1} = n / 2^(levels-1) >= 2.  The dense coarsest solve needs
+ * n_{levels-1} <= 20; a context with a larger coarsest level supports the per-level operations
+ * only (mg_coarse_solve / mg_cycle / mg_solve then return MG_EINVAL).
+ * Errors: MG_EINVAL, MG_ECUDA, MG_ENOMEM. */
 int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau, double alpha,
              int32_t levels, mg_ctx** out);
 void mg_free(mg_ctx* ctx);

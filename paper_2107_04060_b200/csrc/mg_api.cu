@@ -301,11 +301,9 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (!(grid->mu_f > 0)) return fail(MG_EINVAL, "mu_f must be > 0");
     if (grid->K_field && !aligned(grid->K_field)) return fail(MG_EINVAL, "K_field not 8-byte aligned");
     const int nc = n >> (levels - 1);
-    // the dense coarsest solve needs n_c <= 20; a single-level context (levels == 1) may be larger
-    // and then offers the per-level operations only (no coarse solve, no cycle)
+    // the dense coarsest solve needs n_c <= 20; a context with a larger coarsest level offers the
+    // per-level operations only (mg_coarse_solve, mg_cycle and mg_solve return MG_EINVAL)
     const bool dense_ok = 10LL * nc * nc - 8LL * nc + 2 <= 4096;
-    if (!dense_ok && levels > 1)
-        return fail(MG_EINVAL, "coarsest level n = %d too large for the dense solve (n_c <= 20)", nc);
 
     mg_ctx* c = new mg_ctx;
     c->levels = levels;
@@ -586,6 +584,7 @@ int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, doub
     if (max_cycles < 0) return fail(MG_EINVAL, "max_cycles < 0");
     if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (c->levels == 1) return fail(MG_EINVAL, "mg_solve needs levels >= 2");
+    if (!c->Ginv) return fail(MG_EINVAL, "no dense coarsest solve on this context (n_c > 20)");
     if (max_cycles + 1 > c->hist_cap) {
         int cap = std::max(256, max_cycles + 1);
         double* h = (double*)dalloc(c, sizeof(double) * cap);

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, cons
 
 // ------------------------------------------------------------------------------------------
 // additive Vanka sweep: xout = x + omega sum_v V^T D K_v^{-1} V (b - A x)
-constexpr int VTX = 32, VTY = 8, VNT = 256;
+constexpr int VTX = 32, VTY = 8, VNT = 352;   // (VTX+2)(VTY+2) = 340 residual positions, one per thread
 constexpr int V_XW = VTX + 4, V_XH = VTY + 4, V_RW = VTX + 2, V_RH = VTY + 2, V_PW = VTX + 1, V_PH = VTY + 1;
 constexpr int V_XSZ = 10 * V_XW * V_XH, V_CSZ = 20 * V_PW * V_PH;
 constexpr int V_USZ = V_XSZ > V_CSZ ? V_XSZ : V_CSZ;
@@ -275,11 +275,13 @@ __global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, cons
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
     const int i0 = blockIdx.x * VTX, j0 = blockIdx.y * VTY;
+    const int t = threadIdx.x;
+    // phase 1: r = b - A x on the tile + 1 ring (one index per thread; straight-line code keeps
+    // the stencil coefficients as constant-bank operands instead of hoisted registers)
     if (!XZERO) {
         load_tile<V_XW, V_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
-#pragma unroll 1
-        for (int t = threadIdx.x; t < V_RW * V_RH; t += VNT) {
+        if (t < V_RW * V_RH) {
             const int ly = t / V_RW, lx = t - ly * V_RW;
             double rv[10];
             residual_at<V_XW, V_XH, false>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
@@ -290,8 +292,8 @@ __global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, cons
         load_tile<V_RW, V_RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);  // r = b (x = 0)
     }
     __syncthreads();
-#pragma unroll 1
-    for (int t = threadIdx.x; t < V_PW * V_PH; t += VNT) {
+    // phase 2: patch solves at the vertices of the tile + high ring
+    if (t < V_PW * V_PH) {
         const int py = t / V_PW, px = t - py * V_PW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
@@ -300,13 +302,14 @@ __global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, cons
             patch_apply20(P, vertex_class(a, bb, n), rr, cs + t, V_PW * V_PH);
         } else {
 #pragma unroll
-            for (int s = 0; s < 20; ++s) cs[s * V_PW * V_PH + t] = 0.0;
+            for (int q = 0; q < 20; ++q) cs[q * V_PW * V_PH + t] = 0.0;
         }
     }
     __syncthreads();
+    // phase 3: owners sum the corrections of the (up to) 4 patches touching their DoFs
     double nrm = 0.0;
-    {
-        const int lx = threadIdx.x % VTX, ly = threadIdx.x / VTX;
+    if (t < VTX * VTY) {
+        const int lx = t % VTX, ly = t / VTX;
         const int i = i0 + lx, j = j0 + ly;
         if (i <= n && j <= n) {
             const double* c00 = cs + ly * V_PW + lx;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, cons
 
 // ------------------------------------------------------------------------------------------
 // restriction b_H = P^T r (R = P^T), optionally fused with r = b - A x
-constexpr int CX = 16, CY = 8, CNT = 256;
+constexpr int CX = 16, CY = 4, CNT = 352;   // fine residual region 34 x 10 = 340 positions
 constexpr int C_RW = 2 * CX + 2, C_RH = 2 * CY + 2, C_XW = C_RW + 2, C_XH = C_RH + 2;
 constexpr int C_SMEM_FUSED = (10 * C_RW * C_RH + 10 * C_XW * C_XH) * 8;
 constexpr int C_SMEM_PLAIN = 10 * C_RW * C_RH * 8;
@@ -355,11 +358,11 @@ __global__ void __launch_bounds__(CNT, 2) restrict_kernel(const LevelParams L, i
     if (*L.stop) return;
     const int I0 = blockIdx.x * CX, J0 = blockIdx.y * CY;
     const int fi0 = 2 * I0 - 2, fj0 = 2 * J0 - 2;
+    const int t = threadIdx.x;
     if (MODE == 1) {
         load_tile<C_XW, C_XH, 10>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane);
         __syncthreads();
-#pragma unroll 1
-        for (int t = threadIdx.x; t < C_RW * C_RH; t += CNT) {
+        if (t < C_RW * C_RH) {
             const int ly = t / C_RW, lx = t - ly * C_RW;
             double rv[10];
             residual_at<C_XW, C_XH, HET>(L, xs, lx + 1, ly + 1, fi0 + lx, fj0 + ly, br, rv);
@@ -370,7 +373,9 @@ __global__ void __launch_bounds__(CNT, 2) restrict_kernel(const LevelParams L, i
         load_tile<C_RW, C_RH, 10>(rs, br, fi0, fj0, L.n, L.pitch, L.plane);
     }
     __syncthreads();
-    const int c = threadIdx.x & (CX * CY - 1), half = threadIdx.x / (CX * CY);
+    // coarse outputs: (coarse index, pair of planes) per thread; the plane pair is warp uniform
+    if (t >= 5 * CX * CY) return;
+    const int c = t % (CX * CY), grp = t / (CX * CY);
     const int cy = c / CX, cx = c - cy * CX;
     const int I = I0 + cx, J = J0 + cy;
     if (I > nc || J > nc) return;
@@ -384,10 +389,12 @@ __global__ void __launch_bounds__(CNT, 2) restrict_kernel(const LevelParams L, i
         double acc = 0.0;                                            \
         MG_RESTRICT_##k(MG_T) bc[k * planec + o] = is_active(k, I, J, nc) ? acc : 0.0; \
     }
-    if (half == 0) {
-        OUT(0) OUT(1) OUT(2) OUT(3)
-    } else {
-        OUT(4) OUT(5) OUT(6) OUT(7) OUT(8) OUT(9)
+    switch (grp) {
+        case 0: OUT(0) OUT(1) break;
+        case 1: OUT(2) OUT(3) break;
+        case 2: OUT(4) OUT(5) break;
+        case 3: OUT(6) OUT(7) break;
+        default: OUT(8) OUT(9) break;
     }
 #undef OUT
 #undef MG_T
@@ -441,7 +448,7 @@ __global__ void __launch_bounds__(256) coarse_kernel(int N, const double* __rest
 
 // ------------------------------------------------------------------------------------------
 // inexact Braess-Sarazin
-constexpr int BTX = 32, BTY = 8, BNT = 256;
+constexpr int BTX = 32, BTY = 8, BANT = 416, BBNT = 352;   // one position per thread in every phase
 
 __device__ __forceinline__ void patch_apply8(const DispParams& U, int cls, const double rr[8], double* out, int os) {
     if (cls == 0) {
@@ -557,7 +564,7 @@ constexpr int BA_USZ = BA_XSZ > BA_ZSZ ? BA_XSZ : BA_ZSZ;
 constexpr int BA_SMEM = (BA_USZ + 10 * BA_RW * BA_RH) * 8;
 
 template <bool HET, bool XZERO>
-__global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, const DispParams U, double omJ,
+__global__ void __launch_bounds__(BANT, 2) bsr_a_kernel(const LevelParams L, const DispParams U, double omJ,
                                                        const double* __restrict__ x, const double* __restrict__ b,
                                                        double* __restrict__ g, double* __restrict__ dp, NormSink S) {
     extern __shared__ double sm[];
@@ -572,8 +579,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, cons
     if (!XZERO) {
         load_tile<BA_XW, BA_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
-#pragma unroll 1
-        for (int t = threadIdx.x; t < BA_RW * BA_RH; t += BNT) {
+        if (const int t = threadIdx.x; t < BA_RW * BA_RH) {
             const int ly = t / BA_RW, lx = t - ly * BA_RW;
             double rv[10];
             residual_at<BA_XW, BA_XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
@@ -585,8 +591,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, cons
     }
     __syncthreads();
     // displacement patches at vertices [i0, i0+BTX+1] x [j0, j0+BTY+1]
-#pragma unroll 1
-    for (int t = threadIdx.x; t < BA_ZW * BA_ZH; t += BNT) {
+    if (const int t = threadIdx.x; t < BA_ZW * BA_ZH) {
         const int py = t / BA_ZW, px = t - py * BA_ZW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
@@ -600,8 +605,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, cons
     }
     __syncthreads();
     // z_u on indices [i0, i0+BTX] x [j0, j0+BTY]
-#pragma unroll 1
-    for (int t = threadIdx.x; t < BA_UW * BA_UH; t += BNT) {
+    if (const int t = threadIdx.x; t < BA_UW * BA_UH) {
         const int ly = t / BA_UW, lx = t - ly * BA_UW;
         const double* c00 = zs + ly * BA_ZW + lx;
 #define CC(s, dx, dy) c00[(s) * (BA_ZW * BA_ZH) + (dy) * BA_ZW + (dx)]
@@ -616,7 +620,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, cons
     const int lx = threadIdx.x % BTX, ly = threadIdx.x / BTX;
     const int i = i0 + lx, j = j0 + ly;
     double nrm = 0.0;
-    if (i <= n && j <= n) {
+    if (threadIdx.x < BTX * BTY && i <= n && j <= n) {
         const double* r00 = rs + (ly + 1) * BA_RW + (lx + 1);
         if (S.out || S.state) {
 #pragma unroll
@@ -662,7 +666,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_a_kernel(const LevelParams L, cons
             dp[plane + o] = 0.0;
         }
     }
-    if (S.out || S.state) norm_finish<BNT>(S, nrm);
+    if (S.out || S.state) norm_finish<BANT>(S, nrm);
 }
 
 // Jacobi sweep on S dp = g: dp' = dp + omega_J (g - S dp) / diag(S)
@@ -715,7 +719,7 @@ constexpr int BB_USZ = BB_XSZ > BB_ZSZ ? BB_XSZ : BB_ZSZ;
 constexpr int BB_SMEM = (BB_USZ + 10 * BB_RW * BB_RH + 2 * BB_DW * BB_DH) * 8;
 
 template <bool HET, bool XZERO>
-__global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
+__global__ void __launch_bounds__(BBNT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
                                                        const double* __restrict__ x, const double* __restrict__ b,
                                                        const double* __restrict__ dp, double* __restrict__ xo) {
     extern __shared__ double sm[];
@@ -727,7 +731,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, cons
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
     const int i0 = blockIdx.x * BTX, j0 = blockIdx.y * BTY;
-    for (int t = threadIdx.x; t < 2 * BB_DW * BB_DH; t += BNT) {
+    for (int t = threadIdx.x; t < 2 * BB_DW * BB_DH; t += BBNT) {
         const int sh = t / (BB_DW * BB_DH), rem = t - sh * (BB_DW * BB_DH);
         const int ly = rem / BB_DW, lx = rem - ly * BB_DW;
         const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
@@ -736,8 +740,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, cons
     if (!XZERO) {
         load_tile<BB_XW, BB_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
-#pragma unroll 1
-        for (int t = threadIdx.x; t < BB_RW * BB_RH; t += BNT) {
+        if (const int t = threadIdx.x; t < BB_RW * BB_RH) {
             const int ly = t / BB_RW, lx = t - ly * BB_RW;
             double rv[10];
             residual_at<BB_XW, BB_XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
@@ -749,8 +752,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, cons
     }
     __syncthreads();
     // y_u = r_u - alpha B_u^T dp on the r tile (u planes, active DoFs)
-#pragma unroll 1
-    for (int t = threadIdx.x; t < BB_RW * BB_RH; t += BNT) {
+    if (const int t = threadIdx.x; t < BB_RW * BB_RH) {
         const int ly = t / BB_RW, lx = t - ly * BB_RW;
         const int c = i0 - 1 + lx, d = j0 - 1 + ly;
         const double* p00 = ps + (ly + 1) * BB_DW + (lx + 1);   // cell (c, d)
@@ -763,8 +765,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, cons
             if (is_active(k, c, d, n)) rs[k * BB_RW * BB_RH + t] -= L.alpha * bt[k];
     }
     __syncthreads();
-#pragma unroll 1
-    for (int t = threadIdx.x; t < BB_PW * BB_PH; t += BNT) {
+    if (const int t = threadIdx.x; t < BB_PW * BB_PH) {
         const int py = t / BB_PW, px = t - py * BB_PW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
@@ -779,7 +780,7 @@ __global__ void __launch_bounds__(BNT, 2) bsr_b_kernel(const LevelParams L, cons
     __syncthreads();
     const int lx = threadIdx.x % BTX, ly = threadIdx.x / BTX;
     const int i = i0 + lx, j = j0 + ly;
-    if (i > n || j > n) return;
+    if (threadIdx.x >= BTX * BTY || i > n || j > n) return;
     const double* c00 = zs + ly * BB_PW + lx;
 #define CC(s, dx, dy) c00[(s) * (BB_PW * BB_PH) + (dy) * BB_PW + (dx)]
     double d[10];
@@ -860,6 +861,11 @@ void kernels_init() {
     set_smem(bsr_b_kernel<true, true>, BB_SMEM);
 }
 
+static_assert(VNT >= V_RW * V_RH && VNT % 32 == 0, "one residual position per thread");
+static_assert(CNT >= C_RW * C_RH && CNT >= 5 * CX * CY && CNT % 32 == 0, "restrict thread mapping");
+static_assert(BANT >= BA_RW * BA_RH && BANT % 32 == 0, "bsr_a thread mapping");
+static_assert(BBNT >= BB_RW * BB_RH && BBNT % 32 == 0, "bsr_b thread mapping");
+
 int blocks_residual(int n) { return ((n + RTX) / RTX) * ((n + RTY) / RTY); }
 int blocks_vanka(int n) { return ((n + VTX) / VTX) * ((n + VTY) / VTY); }
 int blocks_bsr(int n) { return ((n + BTX) / BTX) * ((n + BTY) / BTY); }
@@ -912,10 +918,10 @@ cudaError_t launch_bsr_a(const LevelParams& L, const DispParams& U, double omJ, 
                          double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s) {
     dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     const bool het = L.kinv_field != nullptr;
-    if (het && x_zero) bsr_a_kernel<true, true><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
-    else if (het) bsr_a_kernel<true, false><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
-    else if (x_zero) bsr_a_kernel<false, true><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
-    else bsr_a_kernel<false, false><<<grid, BNT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    if (het && x_zero) bsr_a_kernel<true, true><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    else if (het) bsr_a_kernel<true, false><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    else if (x_zero) bsr_a_kernel<false, true><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    else bsr_a_kernel<false, false><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
     return cudaGetLastError();
 }
 
@@ -931,10 +937,10 @@ cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega
                          const double* dp, double* xo, bool x_zero, cudaStream_t s) {
     dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     const bool het = L.kinv_field != nullptr;
-    if (het && x_zero) bsr_b_kernel<true, true><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
-    else if (het) bsr_b_kernel<true, false><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
-    else if (x_zero) bsr_b_kernel<false, true><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
-    else bsr_b_kernel<false, false><<<grid, BNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    if (het && x_zero) bsr_b_kernel<true, true><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    else if (het) bsr_b_kernel<true, false><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    else if (x_zero) bsr_b_kernel<false, true><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    else bsr_b_kernel<false, false><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
     return cudaGetLastError();
 }
 
