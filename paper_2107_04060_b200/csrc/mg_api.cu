@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -92,6 +93,8 @@ struct mg_ctx {
     bool timing = false;
     bool timed_ran = false;
     int launches = 0;             // kernel launches enqueued by the last captured cycle
+    int vanka_impl = 1;           // 1: row-marching TMA kernel (default), 0: 2-D tile kernel
+    int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     cudaEvent_t ev[6] = {};
 };
 
@@ -132,7 +135,8 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     if (o.relax == MG_VANKA) {
         VankaParams P = Lv.vp;
         P.omega = o.omega;
-        CK(launch_vanka(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 1) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
+        else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
     }
     const double omJ = o.jacobi_sweeps >= 1 ? o.omega_J : 0.0;
@@ -181,7 +185,10 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
             if (int rc = mark(1)) return rc;
         if (zero && o.nu1 == 0) CK(cudaMemsetAsync(xl, 0, sizeof(double) * Lv.len, s));
         const int mode = (zero && o.nu1 == 0) ? 2 : 1;
-        CK(launch_restrict(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, mode, a, bl, c->L[l + 1].b, s));
+        if (mode == 1 && c->restrict_impl == 1)
+            CK(launch_restrict_march(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, a, bl, c->L[l + 1].b, s));
+        else
+            CK(launch_restrict(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, mode, a, bl, c->L[l + 1].b, s));
         if (l == 0)
             if (int rc = mark(2)) return rc;
         cur[l] = a;
@@ -311,6 +318,8 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     c->m = Material{lambda, mu, grid->K_field ? 1.0 : K, tau, alpha, grid->inv_M, grid->mu_f};
     c->L.resize(levels);
     kernels_init();
+    if (const char* v = getenv("MG_VANKA_IMPL")) c->vanka_impl = atoi(v);
+    if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
     auto bail = [&](int rc) {
         mg_free(c);
         return rc;
@@ -326,6 +335,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         Lv.plane = (int64_t)(Lv.n + 1) * Lv.pitch;
         Lv.len = 10 * Lv.plane;
         max_blocks = std::max(max_blocks, std::max(blocks_vanka(Lv.n), std::max(blocks_residual(Lv.n), blocks_bsr(Lv.n))));
+        max_blocks = std::max(max_blocks, blocks_vanka_march(Lv.n));
         HostLevelTables* t = new HostLevelTables;
         if (host_level_tables(Lv.n, c->m, t, err, sizeof(err))) {
             delete t;

@@ -15,6 +15,7 @@
 // (owner computes; no atomics; deterministic).  The Vanka sweep is out of place (x -> xout):
 // neighbouring CTAs read x in their halos.
 #include <cstdint>
+#include <cuda.h>
 
 #include "mg_kernels.cuh"
 #include "mg_tables.h"
@@ -115,13 +116,13 @@ __device__ __forceinline__ double kinv_ww(const LevelParams& L, int ci, int cj, 
     return kinv_at<true>(L, ci, cj, sh);
 }
 
-// r = b - A x for the 10 DoFs of index (i, j); xs is a W x HT x 10 tile holding (i, j) at
-// (lx, ly) with a ring of at least 1.  Inactive rows give 0.
-template <int W, int HT, bool HET>
-__device__ __forceinline__ void residual_at(const LevelParams& L, const double* __restrict__ xs, int lx, int ly,
-                                            int i, int j, const double* __restrict__ b, double r[10]) {
-    const double* x0 = xs + ly * W + lx;
-#define XS(dx, dy, pl) x0[(pl) * (W * HT) + (dy) * W + (dx)]
+// A x for the 10 DoFs of index (i, j) (eq. block_form_rq): xm, x0, xp point at (i, j-1), (i, j),
+// (i, j+1) in plane 0 of a shared-memory tile whose planes are PS doubles apart and whose rows
+// hold the column neighbours contiguously (all offsets compile-time constants).
+template <int PS, bool HET>
+__device__ __forceinline__ void apply_rows(const LevelParams& L, const double* xm, const double* x0, const double* xp,
+                                           int i, int j, double av[10]) {
+#define XS(dx, dy, pl) ((dy) < 0 ? xm : ((dy) > 0 ? xp : x0))[(pl) * PS + (dx)]
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0, a8 = 0, a9 = 0;
 #define MG_X(row, dx, dy, pl, ci) a##row = fma(L.coef[ci], XS(dx, dy, pl), a##row);
     MG_STENCIL_ROW_0(MG_X)
@@ -142,10 +143,21 @@ __device__ __forceinline__ void residual_at(const LevelParams& L, const double* 
     MG_STENCIL_WW_7(MG_W)
 #undef MG_W
 #undef XS
+    av[0] = a0; av[1] = a1; av[2] = a2; av[3] = a3; av[4] = a4;
+    av[5] = a5; av[6] = a6; av[7] = a7; av[8] = a8; av[9] = a9;
+}
+
+// r = b - A x for the 10 DoFs of index (i, j); xs is a W x HT x 10 tile holding (i, j) at
+// (lx, ly) with a ring of at least 1.  Inactive rows give 0.
+template <int W, int HT, bool HET>
+__device__ __forceinline__ void residual_at(const LevelParams& L, const double* __restrict__ xs, int lx, int ly,
+                                            int i, int j, const double* __restrict__ b, double r[10]) {
+    const double* x0 = xs + ly * W + lx;
+    double av[10];
+    apply_rows<W * HT, HET>(L, x0 - W, x0, x0 + W, i, j, av);
     const int n = L.n;
     const int64_t o = (int64_t)j * L.pitch + i;
     const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
-    double av[10] = {a0, a1, a2, a3, a4, a5, a6, a7, a8, a9};
 #pragma unroll
     for (int k = 0; k < 10; ++k) r[k] = is_active(k, i, j, n) ? (__ldg(b + k * L.plane + (in ? o : 0)) - av[k]) : 0.0;
 }
@@ -836,6 +848,198 @@ __global__ void kinv_coarsen_kernel(int nf, int pitchf, const double* __restrict
     kc[pc + (int64_t)J * pitchc + I] = ur / 4.0;
 }
 
+// ------------------------------------------------------------------------------------------
+// Row-marching additive Vanka sweep with TMA-prefetched row chunks (the level-0 hot kernel).
+//
+// A CTA owns a strip of MT columns [i0, i0+MT) and MH rows [j0, j0+MH) and marches up in
+// steps of MR rows.  Step s computes the residual rows j0+s*MR+1 .. j0+(s+1)*MR (one index per
+// thread), the patch solves at the same vertex rows, and updates the owner rows
+// j0+s*MR .. j0+(s+1)*MR-1 (the lowest patch row and residual row are carried from step s-1;
+// step -1 is the prologue).  So the y halo is never recomputed (only the x halo: (MT+2)/MT).
+// x and b arrive as TMA boxes of MR rows x 10 planes (zero fill outside the mesh) in 3-slot ring
+// buffers guarded by mbarriers and are prefetched two steps ahead, so the loads of later rows
+// overlap the fp64 work of the current ones.  r overwrites b in place.
+constexpr int MT = 30, MR = 4, MNT = (MT + 2) * MR;   // 128 threads: one residual position each
+constexpr int M_XW = MT + 4, M_BW = MT + 4, M_CW = MT + 1;   // b box as wide as x: box origins must be 16-B aligned
+static_assert(MT % 2 == 0, "strip origin i0 - 2 must be an even column (16-byte aligned TMA box)");
+constexpr int M_XCH = 10 * MR * M_XW, M_BCH = 10 * MR * M_BW, M_CCH = 20 * MR * M_CW;   // doubles per chunk
+constexpr int M_SMEM = (3 * M_XCH + 3 * M_BCH + 2 * M_CCH) * 8 + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 3-D TMA box load (dims: column, row, plane) completing on `bar`
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <bool XZERO>
+__global__ void __launch_bounds__(MNT, 2) vanka_march_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                             const __grid_constant__ CUtensorMap tmb,
+                                                             const VankaParams P, double* __restrict__ xo,
+                                                             NormSink S, int MH) {
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;                    // [3][10][MR][M_XW]
+    double* br = xr + 3 * M_XCH;        // [3][10][MR][M_BW]  (b, overwritten by r)
+    double* cr = br + 3 * M_BCH;        // [2][20][MR][M_CW]  patch corrections
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + 2 * M_CCH);   // bars[0..2] x, bars[3..5] b
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n;
+    const int i0 = blockIdx.x * MT, j0 = blockIdx.y * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int nsteps = (rows + MR - 1) / MR;
+    const int t = threadIdx.x;
+    // chunk c of x holds rows [j0 + (c-1) MR, j0 + c MR); chunk d of b holds rows [j0 + (d-1) MR + 1, j0 + d MR]
+    const int nxc = nsteps + 2, nbc = nsteps + 1;
+    auto issue_x = [&](int c) {
+        if (!XZERO && c < nxc) {
+            mbar_expect_tx(&bars[c % 3], M_XCH * 8);
+            tma_load3(xr + (c % 3) * M_XCH, &tmx, i0 - 2, j0 + (c - 1) * MR, 0, &bars[c % 3]);
+        }
+    };
+    auto issue_b = [&](int d) {
+        if (d < nbc) {
+            mbar_expect_tx(&bars[3 + d % 3], M_BCH * 8);
+            tma_load3(br + (d % 3) * M_BCH, &tmb, i0 - 2, j0 + (d - 1) * MR + 1, 0, &bars[3 + d % 3]);
+        }
+    };
+    if (t == 0) {
+        for (int k = 0; k < 6; ++k) mbar_init(&bars[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue_x(0);
+        issue_x(1);
+        issue_x(2);
+        issue_b(0);
+        issue_b(1);
+    }
+    double nrm = 0.0;
+    for (int s = -1; s < nsteps; ++s) {
+        // ---- residual rows y = j0 + s MR + 1 + q (b chunk s+1, row q), x rows y-1 .. y+1
+        const int bslot = (s + 1) % 3;
+        if (!XZERO) {
+            mbar_wait(&bars[(s + 1) % 3], ((s + 1) / 3) & 1);
+            mbar_wait(&bars[(s + 2) % 3], ((s + 2) / 3) & 1);
+        }
+        mbar_wait(&bars[3 + bslot], ((s + 1) / 3) & 1);
+        {
+            const int q = t / (MT + 2), lx = t - q * (MT + 2);
+            const int y = j0 + s * MR + 1 + q, i = i0 - 1 + lx;
+            double* bp = br + bslot * M_BCH + q * M_BW + (lx + 1);
+            double rv[10];
+            if (!XZERO) {
+                // x row y lives in chunk s+1 (rows q+1 < MR) or s+2; rows y-1 and y+1 likewise
+                const int ym = q, y0 = q + 1, yp = q + 2;   // offsets from the first row of chunk s+1
+                const double* base1 = xr + ((s + 1) % 3) * M_XCH + (lx + 1);
+                const double* base2 = xr + ((s + 2) % 3) * M_XCH + (lx + 1);
+                const double* xm = (ym < MR ? base1 + ym * M_XW : base2 + (ym - MR) * M_XW);
+                const double* x0 = (y0 < MR ? base1 + y0 * M_XW : base2 + (y0 - MR) * M_XW);
+                const double* xp = (yp < MR ? base1 + yp * M_XW : base2 + (yp - MR) * M_XW);
+                double av[10];
+                apply_rows<MR * M_XW, false>(L, xm, x0, xp, i, y, av);
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, y, n) ? bp[k * MR * M_BW] - av[k] : 0.0;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) bp[k * MR * M_BW] = rv[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rv[k] = bp[k * MR * M_BW];   // r = b (b inactive slots are 0)
+            }
+            if (lx >= 1 && lx <= MT && i <= n && y >= j0 && y < j0 + rows) {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+            }
+        }
+        __syncthreads();
+        // ---- patch solves at vertex rows bb = j0 + s MR + 1 + q: r rows bb-1 (carry for q = 0) and bb
+        const int cslot = (s + 1) & 1;
+        if (t < MR * M_CW) {
+            const int q = t / M_CW, px = t - q * M_CW;
+            const int a = i0 + px, bb = j0 + s * MR + 1 + q;
+            double* out = cr + cslot * M_CCH + q * M_CW + px;
+            if (a <= n && bb >= 0 && bb <= n) {
+                const double* r0 = br + bslot * M_BCH + q * M_BW + (px + 2);
+                const double* rm = (q > 0) ? r0 - M_BW : br + (s % 3 + (s < 0 ? 3 : 0)) % 3 * M_BCH + (MR - 1) * M_BW + (px + 2);
+                double rr[20];
+#define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * (MR * M_BW) + (dx)]
+                rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+                rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+                rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+                rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+                rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+                rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+                rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+                patch_apply20(P, vertex_class(a, bb, n), rr, out, MR * M_CW);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 20; ++k) out[k * MR * M_CW] = 0.0;
+            }
+        }
+        __syncthreads();
+        // ---- owners y = j0 + s MR + q: patch rows y (carry for q = 0) and y + 1
+        if (s >= 0 && t < MR * MT) {
+            const int q = t / MT, lx = t - q * MT;
+            const int y = j0 + s * MR + q, i = i0 + lx;
+            if (i <= n && y < j0 + rows) {
+                const double* c1 = cr + cslot * M_CCH + q * M_CW + lx;                         // row y + 1
+                const double* c0 = (q > 0) ? c1 - M_CW : cr + (cslot ^ 1) * M_CCH + (MR - 1) * M_CW + lx;   // row y
+#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * (MR * M_CW) + (dx)]
+                double d[10];
+                d[0] = CC(0, 0, 0);
+                d[1] = CC(1, 0, 0);
+                d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+                d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+                d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+                d[5] = CC(8, 0, 0) + CC(9, 1, 0);
+                d[6] = CC(10, 0, 0) + CC(11, 0, 1);
+                d[7] = CC(12, 1, 0) + CC(13, 0, 1);
+                d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
+                d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
+#undef CC
+                // x at row y = chunk s+1, row q
+                const double* xv = xr + ((s + 1) % 3) * M_XCH + q * M_XW + (lx + 2);
+                const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) {
+                    const double xk = XZERO ? 0.0 : xv[k * MR * M_XW];
+                    xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(P.omega, d[k], xk) : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- prefetch: x chunk s+4 into the slot of chunk s+1 (last used now), b chunk s+3 into the slot
+        //      of chunk s (the carry of this step)
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_x(s + 4);
+            issue_b(s + 3);
+        }
+    }
+    if (S.out || S.state) norm_finish<MNT>(S, nrm);
+}
+
 template <typename F>
 void set_smem(F* f, int bytes) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -843,7 +1047,159 @@ void set_smem(F* f, int bytes) {
 
 }  // namespace
 
+// ------------------------------------------------------------------------------------------
+// Row-marching fused residual + restriction b_H = P^T (b - A x) with TMA row chunks.
+// A CTA owns coarse columns [I0, I0+QT) and coarse rows [J0, J0+MH); step s produces coarse rows
+// J0 + s QR .. J0 + (s+1) QR - 1 from the fine residual rows 2(J0 + s QR) - 2 .. 2(J0 + s QR) + 2QR - 1,
+// of which the lowest two are carried from step s-1 (no recompute in y).
+constexpr int QT = 15, QR = 2, QF = 2 * QR;                 // coarse cols, coarse rows per step, fine rows per step
+constexpr int Q_RW = 2 * QT + 2, Q_XW = 2 * QT + 6;          // fine r columns, x box width (origin 2 I0 - 4)
+constexpr int QNT = Q_RW * QF;                               // 128 threads
+constexpr int Q_XCH = 10 * QF * Q_XW, Q_BCH = 10 * QF * Q_RW;
+constexpr int Q_SMEM = (3 * Q_XCH + 3 * Q_BCH) * 8 + 64;
+
+template <bool HET>
+__global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                                const __grid_constant__ CUtensorMap tmb,
+                                                                const LevelParams L, int nc, int pitchc,
+                                                                double* __restrict__ bc, int MH) {
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;                    // [3][10][QF][Q_XW]
+    double* br = xr + 3 * Q_XCH;        // [3][10][QF][Q_RW]  (b, overwritten by r)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(br + 3 * Q_BCH);
+    if (*L.stop) return;
+    const int n = L.n;
+    const int I0 = blockIdx.x * QT, J0 = blockIdx.y * MH;
+    const int crow = min(MH, nc + 1 - J0);
+    const int nsteps = (crow + QR - 1) / QR;
+    const int F0 = 2 * J0;
+    const int t = threadIdx.x;
+    const int nxc = nsteps + 2, nbc = nsteps + 1;
+    // x chunk c: fine rows [F0 + (c-1) QF - 1, F0 + c QF - 1); b chunk d: fine rows [F0 + (d-1) QF, F0 + d QF)
+    auto issue_x = [&](int c) {
+        if (c < nxc) {
+            mbar_expect_tx(&bars[c % 3], Q_XCH * 8);
+            tma_load3(xr + (c % 3) * Q_XCH, &tmx, 2 * I0 - 4, F0 + (c - 1) * QF - 1, 0, &bars[c % 3]);
+        }
+    };
+    auto issue_b = [&](int d) {
+        if (d < nbc) {
+            mbar_expect_tx(&bars[3 + d % 3], Q_BCH * 8);
+            tma_load3(br + (d % 3) * Q_BCH, &tmb, 2 * I0 - 2, F0 + (d - 1) * QF, 0, &bars[3 + d % 3]);
+        }
+    };
+    if (t == 0) {
+        for (int k = 0; k < 6; ++k) mbar_init(&bars[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue_x(0);
+        issue_x(1);
+        issue_x(2);
+        issue_b(0);
+        issue_b(1);
+    }
+    const int64_t planec = (int64_t)(nc + 1) * pitchc;
+    for (int s = -1; s < nsteps; ++s) {
+        const int bslot = (s + 1) % 3;
+        mbar_wait(&bars[(s + 1) % 3], ((s + 1) / 3) & 1);
+        mbar_wait(&bars[(s + 2) % 3], ((s + 2) / 3) & 1);
+        mbar_wait(&bars[3 + bslot], ((s + 1) / 3) & 1);
+        {
+            // fine residual row y = F0 + s QF + q, column i = 2 I0 - 2 + lx
+            const int q = t / Q_RW, lx = t - q * Q_RW;
+            const int y = F0 + s * QF + q, i = 2 * I0 - 2 + lx;
+            const int ym = q, y0 = q + 1, yp = q + 2;   // offsets from the first row of x chunk s+1
+            const double* base1 = xr + ((s + 1) % 3) * Q_XCH + (lx + 2);
+            const double* base2 = xr + ((s + 2) % 3) * Q_XCH + (lx + 2);
+            const double* xm = (ym < QF ? base1 + ym * Q_XW : base2 + (ym - QF) * Q_XW);
+            const double* x0 = (y0 < QF ? base1 + y0 * Q_XW : base2 + (y0 - QF) * Q_XW);
+            const double* xp = (yp < QF ? base1 + yp * Q_XW : base2 + (yp - QF) * Q_XW);
+            double av[10];
+            apply_rows<QF * Q_XW, HET>(L, xm, x0, xp, i, y, av);
+            double* bp = br + bslot * Q_BCH + q * Q_RW + lx;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) bp[k * QF * Q_RW] = is_active(k, i, y, n) ? bp[k * QF * Q_RW] - av[k] : 0.0;
+        }
+        __syncthreads();
+        // coarse rows J = J0 + s QR + q: fine rows 2J - 2 .. 2J + 1 = rows 2q - 2 .. 2q + 1 of this step
+        // (negative: the carried rows of b/r chunk s).  Warps: (q, plane half) uniform.
+        if (s >= 0) {
+            const int q = (t >> 5) & 1, half = t >> 6, cx = t & 31;
+            const int I = I0 + cx, J = J0 + s * QR + q;
+            if (cx < QT && I <= nc && J < J0 + crow) {
+                const double* cur = br + bslot * Q_BCH + (2 * cx + 2);
+                const double* car = br + ((s % 3) * Q_BCH) + (2 * cx + 2);
+                const int64_t o = (int64_t)J * pitchc + I;
+                // row pointer for fine-row offset f = 2q - 2cdJ + dj in [-2, 3]
+#define ROWP(f) ((f) < 0 ? car + (QF + (f)) * Q_RW : cur + (f) * Q_RW)
+#define RF(cdI, cdJ, di, dj, kf) ROWP(2 * q - 2 * (cdJ) + (dj))[(kf) * (QF * Q_RW) - 2 * (cdI) + (di)]
+#define MG_T(cdI, cdJ, di, dj, kf, w) acc = fma(w, RF(cdI, cdJ, di, dj, kf), acc);
+#define OUT(k)                                                                          \
+    {                                                                                   \
+        double acc = 0.0;                                                               \
+        MG_RESTRICT_##k(MG_T) bc[k * planec + o] = is_active(k, I, J, nc) ? acc : 0.0; \
+    }
+                if (half == 0) {
+                    OUT(0) OUT(1) OUT(2) OUT(3) OUT(4)
+                } else {
+                    OUT(5) OUT(6) OUT(7) OUT(8) OUT(9)
+                }
+#undef OUT
+#undef MG_T
+#undef RF
+#undef ROWP
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_x(s + 4);
+            issue_b(s + 3);
+        }
+    }
+}
+
+// Rows marched by one CTA: as many as possible (the prologue step is overhead) while keeping
+// >= ~4 CTAs per SM of work (148 SMs) so that small levels still fill the GPU.
+static int march_height(int n, int tcols, int rstep) {
+    const long strips = (n + tcols) / tcols;
+    int mh = 128;
+    while (mh > 4 * rstep && strips * ((n + mh) / mh) < 4L * 148) mh /= 2;
+    return mh;
+}
+
+// ---- TMA descriptors (driver entry point fetched once through the runtime)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn g_encode = nullptr;
+
+static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int pitch, int64_t plane, int boxw,
+                                  int boxh) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)(n + 1), (cuuint64_t)(n + 1), 10};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)plane * 8};
+    cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, 10};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 void kernels_init() {
+    set_smem(restrict_march_kernel<false>, Q_SMEM);
+    set_smem(restrict_march_kernel<true>, Q_SMEM);
+    set_smem(vanka_march_kernel<false>, M_SMEM);
+    set_smem(vanka_march_kernel<true>, M_SMEM);
     set_smem(vanka_kernel<false>, V_SMEM);
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(restrict_kernel<0, false>, C_SMEM_PLAIN);
@@ -883,6 +1239,39 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
     dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
     if (x_zero) vanka_kernel<true><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
     else vanka_kernel<false><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
+                               NormSink S, cudaStream_t s) {
+    const LevelParams& L = P.L;
+    CUtensorMap mx, mb;
+    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, M_XW, MR);
+    if (e != cudaSuccess) return e;
+    e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, M_BW, MR);   // both boxes start at column i0 - 2
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(L.n, MT, MR);
+    dim3 grid((L.n + MT) / MT, (L.n + MH) / MH);
+    if (x_zero) vanka_march_kernel<true><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
+    else vanka_march_kernel<false><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
+    return cudaGetLastError();
+}
+int blocks_vanka_march(int n) {
+    const int MH = march_height(n, MT, MR);
+    return ((n + MT) / MT) * ((n + MH) / MH);
+}
+
+cudaError_t launch_restrict_march(const LevelParams& Lf, int nc, int pitchc, const double* x, const double* b,
+                                  double* bc, cudaStream_t s) {
+    CUtensorMap mx, mb;
+    cudaError_t e = encode_vec_map(&mx, x, Lf.n, Lf.pitch, Lf.plane, Q_XW, QF);
+    if (e != cudaSuccess) return e;
+    e = encode_vec_map(&mb, b, Lf.n, Lf.pitch, Lf.plane, Q_RW, QF);
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(nc, QT, QR);
+    dim3 grid((nc + QT) / QT, (nc + MH) / MH);
+    if (Lf.kinv_field) restrict_march_kernel<true><<<grid, QNT, Q_SMEM, s>>>(mx, mb, Lf, nc, pitchc, bc, MH);
+    else restrict_march_kernel<false><<<grid, QNT, Q_SMEM, s>>>(mx, mb, Lf, nc, pitchc, bc, MH);
     return cudaGetLastError();
 }
 

@@ -17,6 +17,13 @@ cudaError_t launch_residual(const LevelParams& L, const double* x, const double*
                             NormSink norm, cudaStream_t s);
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
                          bool x_zero, NormSink norm, cudaStream_t s);
+// row-marching TMA variant of the same sweep (identical arithmetic); the production kernel
+cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const double* b, double* xout,
+                               bool x_zero, NormSink norm, cudaStream_t s);
+int blocks_vanka_march(int n);
+// row-marching TMA variant of the fused residual + restriction (mode 1)
+cudaError_t launch_restrict_march(const LevelParams& Lf, int n_coarse, int pitch_coarse, const double* x_fine,
+                                  const double* b_fine, double* b_coarse, cudaStream_t s);
 // mode 0: r_fine given (x_fine, b_fine unused); 1: r = b - A x fused; 2: x == 0 (r = b)
 cudaError_t launch_restrict(const LevelParams& Lf, int n_coarse, int pitch_coarse, int mode,
                             const double* x_fine, const double* b_or_r_fine, double* b_coarse,
