@@ -25,6 +25,8 @@ solved for the bubble beta_{e*} of the interior edge e* of t.
 """
 from __future__ import annotations
 
+import copy
+
 import numpy as np
 import scipy.sparse as sp
 
@@ -94,8 +96,16 @@ def _first(keys):
 
 def build_P(fine: Mesh, coarse: Mesh):
     """Full-slot prolongation matrices P_u (with divergence fix), P_w, P_p and the
-    standard interpolation Phat_u.  Shapes (fine.nslots, coarse.nslots)."""
+    standard interpolation Phat_u.  Shapes (fine.nslots, coarse.nslots).
+
+    Every weight is invariant under a uniform scaling of the mesh (point values, normal
+    traces and the zero-flux condition of PAPER.md:532-537 are all homogeneous), so the
+    geometry is evaluated on integer grid coordinates (fine spacing 1, coarse spacing 2),
+    which are exact in floating point: the weights then carry only the round-off of the
+    formulas, not an O(n u) error from the coordinates i/n."""
     assert fine.n == 2 * coarse.n
+    fine, coarse = copy.copy(fine), copy.copy(coarse)
+    fine.h, coarse.h = 1.0, 2.0
     Nf, Nc = fine.nslots, coarse.nslots
     h = fine.h
     nt = fine.ntri
