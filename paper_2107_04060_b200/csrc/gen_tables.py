@@ -331,6 +331,20 @@ def emit(path):
         counts.append(len(items))
         w("#define MG_STENCIL_ROW_%d(X) " % k + " ".join(items))
     w("#define MG_STENCIL_NCOEF %d" % cidx)
+    # the same entries interleaved round-robin over the 10 rows (each row keeps its own summation
+    # order): consecutive FMAs then belong to independent accumulator chains
+    per_row = [[] for _ in range(10)]
+    ci = 0
+    for k, r in enumerate(rows):
+        for (col, lst) in r["entries"]:
+            per_row[k].append("X(%d,%d,%d,%d,%d)" % (k, col[0], col[1], col[2], ci))
+            ci += 1
+    il = []
+    for e in range(max(len(x) for x in per_row)):
+        for k in range(10):
+            if e < len(per_row[k]):
+                il.append(per_row[k][e])
+    w("#define MG_STENCIL_INTERLEAVED(X) " + " ".join(il))
     w("// coefficient contributions: Y(coef_index, shape, q, q') -- coef = sum of element entries")
     w("#define MG_STENCIL_CONTRIB(Y) " + " ".join("Y(%d,%d,%d,%d)" % c for c in contribs))
     w("// M_w part of the RT0 rows, per triangle: W(row, cell_dx, cell_dy, shape, dx, dy, plane, e, e')")
@@ -356,6 +370,24 @@ def emit(path):
     for (di, dj, kf), ent in sorted(P.items()):
         items = " ".join("Q(%d,%d,%d,%s)" % (COARSE_DOFS[c] + (_f(v),)) for c, v in sorted(ent.items()))
         w("#define MG_PROLONG_%d_%d_%d(Q) %s" % (di, dj, kf, items))
+    # restriction entries of planes 0-4 and 5-9, interleaved round-robin over the planes:
+    # U(kc, cell_dI, cell_dJ, di, dj, kf, weight)
+    for name, planes in (("LO", range(0, 5)), ("HI", range(5, 10))):
+        lists = []
+        for kc in planes:
+            lst = []
+            for (di, dj, kf), ent in sorted(P.items()):
+                for c, v in sorted(ent.items()):
+                    dI, dJ, pc = COARSE_DOFS[c]
+                    if pc == kc:
+                        lst.append("U(%d,%d,%d,%d,%d,%d,%s)" % (kc, dI, dJ, di, dj, kf, _f(v)))
+            lists.append(lst)
+        il = []
+        for e in range(max(len(x) for x in lists)):
+            for lst in lists:
+                if e < len(lst):
+                    il.append(lst[e])
+        w("#define MG_RESTRICT_IL_%s(U) " % name + " ".join(il))
     w("// restriction R = P^T for coarse plane kc: T(cell_dI, cell_dJ, di, dj, kf, weight); the fine index is")
     w("// (2(I-cell_dI)+di, 2(J-cell_dJ)+dj) for coarse index (I, J)")
     for kc in range(10):

@@ -125,16 +125,8 @@ __device__ __forceinline__ void apply_rows(const LevelParams& L, const double* x
 #define XS(dx, dy, pl) ((dy) < 0 ? xm : ((dy) > 0 ? xp : x0))[(pl) * PS + (dx)]
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0, a8 = 0, a9 = 0;
 #define MG_X(row, dx, dy, pl, ci) a##row = fma(L.coef[ci], XS(dx, dy, pl), a##row);
-    MG_STENCIL_ROW_0(MG_X)
-    MG_STENCIL_ROW_1(MG_X)
-    MG_STENCIL_ROW_2(MG_X)
-    MG_STENCIL_ROW_3(MG_X)
-    MG_STENCIL_ROW_4(MG_X)
-    MG_STENCIL_ROW_5(MG_X)
-    MG_STENCIL_ROW_6(MG_X)
-    MG_STENCIL_ROW_7(MG_X)
-    MG_STENCIL_ROW_8(MG_X)
-    MG_STENCIL_ROW_9(MG_X)
+    // rows interleaved round-robin (each row keeps its summation order): 10 independent FMA chains
+    MG_STENCIL_INTERLEAVED(MG_X)
 #undef MG_X
 #define MG_W(row, cdx, cdy, sh, dx, dy, pl, e, e2) \
     a##row = fma(L.ww[sh][e][e2] * kinv_ww<HET>(L, i + (cdx), j + (cdy), sh), XS(dx, dy, pl), a##row);
@@ -235,20 +227,20 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
         }
         hm[0] = rr[0];
         hm[1] = rr[1];
+        // column-outer loops: the 20 output chains advance together (same per-output summation order)
         double yp[9], ym[11];
 #pragma unroll
-        for (int a = 0; a < 9; ++a) {
-            double s = 0.0;
+        for (int a = 0; a < 9; ++a) yp[a] = 0.0;
 #pragma unroll
-            for (int c = 0; c < 9; ++c) s = fma(P.gp[a][c], hp[c], s);
-            yp[a] = s;
-        }
+        for (int a = 0; a < 11; ++a) ym[a] = 0.0;
 #pragma unroll
-        for (int a = 0; a < 11; ++a) {
-            double s = 0.0;
+        for (int c = 0; c < 11; ++c) {
 #pragma unroll
-            for (int c = 0; c < 11; ++c) s = fma(P.gm[a][c], hm[c], s);
-            ym[a] = s;
+            for (int a = 0; a < 11; ++a) ym[a] = fma(P.gm[a][c], hm[c], ym[a]);
+            if (c < 9) {
+#pragma unroll
+                for (int a = 0; a < 9; ++a) yp[a] = fma(P.gp[a][c], hp[c], yp[a]);
+            }
         }
         out[0] = ym[0];
         out[os] = ym[1];
@@ -472,20 +464,15 @@ __device__ __forceinline__ void patch_apply8(const DispParams& U, int cls, const
         }
         hm[0] = rr[0];
         hm[1] = rr[1];
-        double yp[3], ym[5];
+        double yp[3] = {0, 0, 0}, ym[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            double s = 0.0;
+        for (int c = 0; c < 5; ++c) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) s = fma(U.up[a][c], hp[c], s);
-            yp[a] = s;
-        }
+            for (int a = 0; a < 5; ++a) ym[a] = fma(U.um[a][c], hm[c], ym[a]);
+            if (c < 3) {
 #pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            double s = 0.0;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) s = fma(U.um[a][c], hm[c], s);
-            ym[a] = s;
+                for (int a = 0; a < 3; ++a) yp[a] = fma(U.up[a][c], hp[c], yp[a]);
+            }
         }
         out[0] = ym[0];
         out[os] = ym[1];
@@ -1136,17 +1123,22 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
 #define ROWP(f) ((f) < 0 ? car + (QF + (f)) * Q_RW : cur + (f) * Q_RW)
 #define RF(cdI, cdJ, di, dj, kf) ROWP(2 * q - 2 * (cdJ) + (dj))[(kf) * (QF * Q_RW) - 2 * (cdI) + (di)]
 #define MG_T(cdI, cdJ, di, dj, kf, w) acc = fma(w, RF(cdI, cdJ, di, dj, kf), acc);
-#define OUT(k)                                                                          \
-    {                                                                                   \
-        double acc = 0.0;                                                               \
-        MG_RESTRICT_##k(MG_T) bc[k * planec + o] = is_active(k, I, J, nc) ? acc : 0.0; \
-    }
+                // planes 0-4 or 5-9, their entries interleaved (5 independent chains)
+                double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#define MG_U0(kc, cdI, cdJ, di, dj, kf, w) acc[kc] = fma(w, RF(cdI, cdJ, di, dj, kf), acc[kc]);
+#define MG_U5(kc, cdI, cdJ, di, dj, kf, w) acc[(kc) - 5] = fma(w, RF(cdI, cdJ, di, dj, kf), acc[(kc) - 5]);
                 if (half == 0) {
-                    OUT(0) OUT(1) OUT(2) OUT(3) OUT(4)
+                    MG_RESTRICT_IL_LO(MG_U0)
                 } else {
-                    OUT(5) OUT(6) OUT(7) OUT(8) OUT(9)
+                    MG_RESTRICT_IL_HI(MG_U5)
                 }
-#undef OUT
+#undef MG_U0
+#undef MG_U5
+#pragma unroll
+                for (int kk = 0; kk < 5; ++kk) {
+                    const int k = 5 * half + kk;
+                    bc[k * planec + o] = is_active(k, I, J, nc) ? acc[kk] : 0.0;
+                }
 #undef MG_T
 #undef RF
 #undef ROWP

@@ -99,12 +99,13 @@ def test_restrict_prolong(n, pname):
     torch.cuda.synchronize()
     # componentwise rounding bound of a sparse matvec in two summation orders: 32 u |R| |r|
     absR, absP = abs(T.R), abs(T.P)
+    ra, ea = np.abs(mf.to_active(r)), np.abs(mc.to_active(e))
     bO = T.R @ mf.to_active(r)
     bG = mc.to_active(H.to_host(bc, 1))
-    assert np.all(np.abs(bG - bO) <= 32 * U * (absR @ np.abs(mf.to_active(r))))
+    assert np.all(np.abs(bG - bO) <= 32 * U * (absR @ ra))
     xO = mf.to_active(x) + T.P @ mc.to_active(e)
     xG = mf.to_active(H.to_host(xd))
-    assert np.all(np.abs(xG - xO) <= 32 * U * (np.abs(mf.to_active(x)) + absP @ np.abs(mc.to_active(e))))
+    assert np.all(np.abs(xG - xO) <= 32 * U * (np.abs(mf.to_active(x)) + absP @ ea))
     _inactive_zero(H, bc, 1)
     _inactive_zero(H, xd)
 
