@@ -226,10 +226,18 @@ def main():
     # kernel-class timing of the same cycle (event-traced graph, separate pass)
     H.set_timing(True)
     phases = np.zeros(5)
+    per_level = None
     for _ in range(args.trace_cycles):
         H.cycle_async(x, b, o, nrm)
         phases += np.array(H.timing())
+        tl = H.timing_levels()
+        if per_level is None:
+            per_level = {k: np.array(v, dtype=float) for k, v in tl.items()}
+        else:
+            for k, v in tl.items():
+                per_level[k] = per_level[k] + np.array(v, dtype=float)
     phases /= args.trace_cycles
+    per_level = {k: (v / args.trace_cycles).round(4).tolist() for k, v in per_level.items()}
     H.set_timing(False)
 
     # e2e through the public C ABI with host buffers
@@ -303,7 +311,8 @@ def main():
         "cycle_roofline": {"algorithmic_bytes": cycle_bytes, "achieved_gbs": cycle_bytes / (ms_step * 1e-3) / 1e9,
                            "frac": cycle_bytes / (ms_step * 1e-3) / 1e9 / peak,
                            "phase_ms": {"pre": phases[0], "restrict": phases[1], "coarse_levels": phases[2],
-                                        "prolong": phases[3], "post": phases[4]}},
+                                        "prolong": phases[3], "post": phases[4]},
+                           "per_level_ms": per_level},
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:

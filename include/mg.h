@@ -177,6 +177,11 @@ int mg_set_timing(mg_ctx* ctx, int32_t enable);
 /* Number of kernel nodes of the most recently captured cycle graph (all of them libmg kernels). */
 int32_t mg_cycle_kernels(const mg_ctx* ctx);
 int mg_timing(mg_ctx* ctx, float* ms5);
+/* Per-level intervals of the most recent traced cycle, in execution order: for l = 0 .. L-2
+ * [pre-relaxation(l), residual+restriction(l)], then the coarsest solve, then for l = L-2 .. 0
+ * [prolongation(l), post-relaxation(l)] -- 4 (L-1) + 1 values.  Returns the count (>= 0) or a
+ * negative error (cap too small, no traced cycle). */
+int mg_timing_levels(mg_ctx* ctx, float* ms, int32_t cap);
 
 /* Stationary iteration of V-cycles from the given x until ||r_k|| <= rtol ||r_0|| or
  * max_cycles.  history_host: NULL or max_cycles+1 doubles, history[k] = ||b - A x_k||_2

@@ -92,6 +92,7 @@ struct mg_ctx {
     cudaStream_t cap = nullptr;   // capture stream
     bool timing = false;
     bool timed_ran = false;
+    std::vector<cudaEvent_t> lev;  // per-level phase events of the traced cycle (4 (L-1) + 2)
     int launches = 0;             // kernel launches enqueued by the last captured cycle
     int vanka_impl = 1;           // 1: row-marching TMA kernel (default), 0: 2-D tile kernel
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
@@ -164,6 +165,13 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         if (timed) CK(cudaEventRecordWithFlags(c->ev[i], s, cudaEventRecordExternal));
         return MG_OK;
     };
+    int nlev = 0;   // per-level boundaries: pre(0) restrict(0) ... pre(L-2) restrict(L-2) coarse prolong(L-2) post(L-2) ...
+    auto lmark = [&]() -> int {
+        if (timed) CK(cudaEventRecordWithFlags(c->lev[nlev], s, cudaEventRecordExternal));
+        ++nlev;
+        return MG_OK;
+    };
+    if (int rc = lmark()) return rc;
     if (int rc = mark(0)) return rc;
     if (solve && o.nu1 == 0) {
         CK(launch_residual(c->L[0].vp.L, x0, b0, nullptr, S, s));
@@ -183,6 +191,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         }
         if (l == 0)
             if (int rc = mark(1)) return rc;
+        if (int rc = lmark()) return rc;
         if (zero && o.nu1 == 0) CK(cudaMemsetAsync(xl, 0, sizeof(double) * Lv.len, s));
         const int mode = (zero && o.nu1 == 0) ? 2 : 1;
         if (mode == 1 && c->restrict_impl == 1)
@@ -191,9 +200,11 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
             CK(launch_restrict(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, mode, a, bl, c->L[l + 1].b, s));
         if (l == 0)
             if (int rc = mark(2)) return rc;
+        if (int rc = lmark()) return rc;
         cur[l] = a;
     }
     CK(launch_coarse(c->Nc, c->Ginv, c->slots, c->L[Lc].b, c->L[Lc].x, c->stop, s));
+    if (int rc = lmark()) return rc;
     cur[Lc] = c->L[Lc].x;
     for (int l = Lc - 1; l >= 0; --l) {
         Level& Lv = c->L[l];
@@ -202,6 +213,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         CK(launch_prolong(Lv.n, Lv.pitch, c->L[l + 1].n, c->L[l + 1].pitch, cur[l + 1], cur[l], c->stop, s));
         if (l == 0)
             if (int rc = mark(4)) return rc;
+        if (int rc = lmark()) return rc;
         const double* bl = l == 0 ? b0 : Lv.b;
         double* xl = l == 0 ? x0 : Lv.x;
         double* a = cur[l];
@@ -212,6 +224,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
             std::swap(a, t);
         }
         if (l == 0 && a != x0) CK(cudaMemcpyAsync(x0, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+        if (int rc = lmark()) return rc;
         cur[l] = a;
     }
     return mark(5);
@@ -454,6 +467,7 @@ void mg_free(mg_ctx* c) {
     c->graphs.clear();
     for (int i = 0; i < 6; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    for (auto e : c->lev) cudaEventDestroy(e);
     dfree_all(c);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->cap) cudaStreamDestroy(c->cap);
@@ -571,8 +585,11 @@ int32_t mg_cycle_kernels(const mg_ctx* c) { return c ? c->launches : -1; }
 
 int mg_set_timing(mg_ctx* c, int32_t enable) {
     if (!c) return fail(MG_EINVAL, "null context");
-    if (enable && !c->ev[0])
+    if (enable && !c->ev[0]) {
         for (int i = 0; i < 6; ++i) CK(cudaEventCreate(&c->ev[i]));
+        c->lev.resize(4 * (c->levels - 1) + 2);
+        for (auto& e : c->lev) CK(cudaEventCreate(&e));
+    }
     c->timing = enable != 0;
     c->timed_ran = false;
     return MG_OK;
@@ -584,6 +601,16 @@ int mg_timing(mg_ctx* c, float* ms) {
     CK(cudaEventSynchronize(c->ev[5]));
     for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
     return MG_OK;
+}
+
+int mg_timing_levels(mg_ctx* c, float* ms, int32_t cap) {
+    if (!c || !ms) return fail(MG_EINVAL, "null argument");
+    if (!c->timed_ran || c->lev.empty()) return fail(MG_EINVAL, "no traced cycle ran");
+    const int m = (int)c->lev.size() - 1;
+    if (cap < m) return fail(MG_EINVAL, "cap %d < %d intervals", cap, m);
+    CK(cudaEventSynchronize(c->lev.back()));
+    for (int i = 0; i < m; ++i) CK(cudaEventElapsedTime(&ms[i], c->lev[i], c->lev[i + 1]));
+    return m;
 }
 
 int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_cycles,

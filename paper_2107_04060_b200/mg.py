@@ -67,6 +67,7 @@ SIGNATURES = {
     "mg_set_timing": (ctypes.c_int, [_VP, ctypes.c_int32]),
     "mg_cycle_kernels": (ctypes.c_int32, [_VP]),
     "mg_timing": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_float)]),
+    "mg_timing_levels": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_float), ctypes.c_int32]),
     "mg_last_error": (ctypes.c_char_p, []),
     "mg_host_level_tables": (ctypes.c_int, [ctypes.c_int32] + [ctypes.c_double] * 7 + [_D] * 4),
 }
@@ -259,6 +260,24 @@ class Hierarchy:
         out = (ctypes.c_float * 5)()
         _check(self.lib.mg_timing(self.ctx, out), "mg_timing")
         return list(out)
+
+    def timing_levels(self):
+        """Per-level ms of the latest traced cycle: dict(pre=[...], restrict=[...], coarse=..,
+        prolong=[...], post=[...]) indexed by level."""
+        cap = 4 * self.levels
+        out = (ctypes.c_float * cap)()
+        m = _check(self.lib.mg_timing_levels(self.ctx, out, cap), "mg_timing_levels")
+        v = list(out)[:m]
+        L1 = self.levels - 1
+        pre = [v[2 * l] for l in range(L1)]
+        res = [v[2 * l + 1] for l in range(L1)]
+        coarse = v[2 * L1]
+        tail = v[2 * L1 + 1:]
+        pro = [0.0] * L1
+        post = [0.0] * L1
+        for k, l in enumerate(range(L1 - 1, -1, -1)):
+            pro[l], post[l] = tail[2 * k], tail[2 * k + 1]
+        return dict(pre=pre, restrict=res, coarse=coarse, prolong=pro, post=post)
 
     def solve(self, x, b, opts: Opts, rtol=1e-8, max_cycles=100, stream=None):
         hist = np.zeros(max_cycles + 1)
