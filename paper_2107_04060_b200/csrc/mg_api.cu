@@ -96,6 +96,7 @@ struct mg_ctx {
     int launches = 0;             // kernel launches enqueued by the last captured cycle
     int vanka_impl = 1;           // 1: row-marching TMA kernel (default), 0: 2-D tile kernel
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
+    int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     cudaEvent_t ev[6] = {};
 };
 
@@ -136,7 +137,7 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     if (o.relax == MG_VANKA) {
         VankaParams P = Lv.vp;
         P.omega = o.omega;
-        if (c->vanka_impl == 1) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 1 && Lv.n >= c->march_min_n) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
     }
@@ -194,7 +195,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         if (int rc = lmark()) return rc;
         if (zero && o.nu1 == 0) CK(cudaMemsetAsync(xl, 0, sizeof(double) * Lv.len, s));
         const int mode = (zero && o.nu1 == 0) ? 2 : 1;
-        if (mode == 1 && c->restrict_impl == 1)
+        if (mode == 1 && c->restrict_impl == 1 && Lv.n >= c->march_min_n)
             CK(launch_restrict_march(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, a, bl, c->L[l + 1].b, s));
         else
             CK(launch_restrict(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, mode, a, bl, c->L[l + 1].b, s));
@@ -333,6 +334,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     kernels_init();
     if (const char* v = getenv("MG_VANKA_IMPL")) c->vanka_impl = atoi(v);
     if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
+    if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
     auto bail = [&](int rc) {
         mg_free(c);
         return rc;
