@@ -94,7 +94,7 @@ struct mg_ctx {
     bool timed_ran = false;
     std::vector<cudaEvent_t> lev;  // per-level phase events of the traced cycle (4 (L-1) + 2)
     int launches = 0;             // kernel launches enqueued by the last captured cycle
-    int vanka_impl = 1;           // 1: row-marching TMA kernel (default), 0: 2-D tile kernel
+    int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     cudaEvent_t ev[6] = {};
@@ -137,7 +137,8 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     if (o.relax == MG_VANKA) {
         VankaParams P = Lv.vp;
         P.omega = o.omega;
-        if (c->vanka_impl == 1 && Lv.n >= c->march_min_n) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
+        else if (c->vanka_impl == 1 && Lv.n >= c->march_min_n) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
     }
@@ -350,7 +351,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         Lv.plane = (int64_t)(Lv.n + 1) * Lv.pitch;
         Lv.len = 10 * Lv.plane;
         max_blocks = std::max(max_blocks, std::max(blocks_vanka(Lv.n), std::max(blocks_residual(Lv.n), blocks_bsr(Lv.n))));
-        max_blocks = std::max(max_blocks, blocks_vanka_march(Lv.n));
+        max_blocks = std::max(max_blocks, std::max(blocks_vanka_march(Lv.n), blocks_vanka_march2(Lv.n)));
         HostLevelTables* t = new HostLevelTables;
         if (host_level_tables(Lv.n, c->m, t, err, sizeof(err))) {
             delete t;

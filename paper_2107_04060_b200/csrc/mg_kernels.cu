@@ -1035,6 +1035,154 @@ void set_smem(F* f, int bytes) {
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
+// Row-marching Vanka, row-granular rings (3 CTAs / SM).  Same arithmetic as vanka_march_kernel;
+// x, b and the patch outputs live in modular rings of single rows (x: 10, b/r: 9, patches: 5
+// rows), filled by one 3-D TMA box per row (32 columns x 1 row x 10 planes) and prefetched one
+// step ahead, which cuts shared memory to 72 KB per CTA.
+constexpr int M2T = 28, M2R = 4, M2W = M2T + 4, M2C = M2T + 1, M2NT = 128;
+constexpr int M2XR = 10, M2BR = 9, M2CR = 5;
+constexpr int M2ROW = 10 * M2W;                                  // doubles per x / b ring row
+constexpr int M2SMEM = (M2XR * M2ROW + M2BR * M2ROW + M2CR * 20 * M2C) * 8 + 64;
+static_assert((M2T + 2) * M2R <= M2NT, "one residual position per thread");
+static_assert(M2T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
+
+template <bool XZERO>
+__global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const __grid_constant__ CUtensorMap tmb,
+                                                               const VankaParams P, double* __restrict__ xo,
+                                                               NormSink S, int MH) {
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;                        // [M2XR][10][M2W]
+    double* br = xr + M2XR * M2ROW;         // [M2BR][10][M2W]   b, overwritten by r
+    double* cr = br + M2BR * M2ROW;         // [M2CR][20][M2C]   patch corrections
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M2CR * 20 * M2C);
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n;
+    const int i0 = blockIdx.x * M2T, j0 = blockIdx.y * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int nsteps = (rows + M2R - 1) / M2R;
+    const int t = threadIdx.x;
+    // ring slot of global row y (the offset keeps the argument non-negative down to j0 - 2 M2R)
+    auto sx = [&](int y) { return (y - j0 + 2 * M2R) % M2XR; };
+    auto sb = [&](int y) { return (y - j0 + 2 * M2R) % M2BR; };
+    auto sc = [&](int y) { return (y - j0 + 2 * M2R) % M2CR; };
+    // group g brings the rows first used by step g: x rows j0+gR+2 .. j0+gR+R+1 (g = -1: j0-R .. j0+1)
+    // and b rows j0+gR+1 .. j0+gR+R
+    auto issue = [&](int g) {
+        if (g >= nsteps) return;
+        uint64_t* bar = &bars[(g + 1) & 1];
+        const int nx = XZERO ? 0 : (g < 0 ? M2R + 2 : M2R);
+        mbar_expect_tx(bar, (nx + M2R) * M2ROW * 8);
+        const int xfirst = g < 0 ? j0 - M2R : j0 + g * M2R + 2;
+        for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * M2ROW, &tmx, i0 - 2, xfirst + k, 0, bar);
+        const int bfirst = j0 + g * M2R + 1;
+        for (int k = 0; k < M2R; ++k) tma_load3(br + sb(bfirst + k) * M2ROW, &tmb, i0 - 2, bfirst + k, 0, bar);
+    };
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue(-1);
+        issue(0);
+    }
+    double nrm = 0.0;
+    for (int s = -1; s < nsteps; ++s) {
+        mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
+        // ---- residual rows y = j0 + s R + 1 + q
+        if (t < (M2T + 2) * M2R) {
+            const int q = t / (M2T + 2), lx = t - q * (M2T + 2);
+            const int y = j0 + s * M2R + 1 + q, i = i0 - 1 + lx;
+            double* bp = br + sb(y) * M2ROW + (lx + 1);
+            const bool own = lx >= 1 && lx <= M2T && i <= n && y >= j0 && y < j0 + rows;
+            double rv[10];
+            if (!XZERO) {
+                const double* xm = xr + sx(y - 1) * M2ROW + (lx + 1);
+                const double* x0 = xr + sx(y) * M2ROW + (lx + 1);
+                const double* xp = xr + sx(y + 1) * M2ROW + (lx + 1);
+                double av[10];
+                apply_rows<M2W, false>(L, xm, x0, xp, i, y, av);
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, y, n) ? bp[k * M2W] - av[k] : 0.0;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) bp[k * M2W] = rv[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rv[k] = bp[k * M2W];
+            }
+            if (own) {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+            }
+        }
+        __syncthreads();
+        // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
+        if (t < M2R * M2C) {
+            const int q = t / M2C, px = t - q * M2C;
+            const int a = i0 + px, bb = j0 + s * M2R + 1 + q;
+            double* out = cr + sc(bb) * (20 * M2C) + px;
+            if (a <= n && bb >= 0 && bb <= n) {
+                const double* r0 = br + sb(bb) * M2ROW + (px + 2);
+                const double* rm = br + sb(bb - 1) * M2ROW + (px + 2);
+                double rr[20];
+#define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * M2W + (dx)]
+                rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+                rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+                rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+                rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+                rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+                rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+                rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+                patch_apply20(P, vertex_class(a, bb, n), rr, out, M2C);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 20; ++k) out[k * M2C] = 0.0;
+            }
+        }
+        __syncthreads();
+        // ---- owners y = j0 + s R + q: patch rows y and y + 1
+        if (s >= 0 && t < M2R * M2T) {
+            const int q = t / M2T, lx = t - q * M2T;
+            const int y = j0 + s * M2R + q, i = i0 + lx;
+            if (i <= n && y < j0 + rows) {
+                const double* c0 = cr + sc(y) * (20 * M2C) + lx;
+                const double* c1 = cr + sc(y + 1) * (20 * M2C) + lx;
+#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * M2C + (dx)]
+                double d[10];
+                d[0] = CC(0, 0, 0);
+                d[1] = CC(1, 0, 0);
+                d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+                d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+                d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+                d[5] = CC(8, 0, 0) + CC(9, 1, 0);
+                d[6] = CC(10, 0, 0) + CC(11, 0, 1);
+                d[7] = CC(12, 1, 0) + CC(13, 0, 1);
+                d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
+                d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
+#undef CC
+                const double* xv = xr + sx(y) * M2ROW + (lx + 2);
+                const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) {
+                    const double xk = XZERO ? 0.0 : xv[k * M2W];
+                    xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(P.omega, d[k], xk) : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s + 2);
+        }
+    }
+    if (S.out || S.state) norm_finish<M2NT>(S, nrm);
+}
+
+// ------------------------------------------------------------------------------------------
 // Row-marching fused residual + restriction b_H = P^T (b - A x) with TMA row chunks.
 // A CTA owns coarse columns [I0, I0+QT) and coarse rows [J0, J0+MH); step s produces coarse rows
 // J0 + s QR .. J0 + (s+1) QR - 1 from the fine residual rows 2(J0 + s QR) - 2 .. 2(J0 + s QR) + 2QR - 1,
@@ -1188,6 +1336,8 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
 }
 
 void kernels_init() {
+    set_smem(vanka_march2_kernel<false>, M2SMEM);
+    set_smem(vanka_march2_kernel<true>, M2SMEM);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
     set_smem(restrict_march_kernel<true>, Q_SMEM);
     set_smem(vanka_march_kernel<false>, M_SMEM);
@@ -1248,6 +1398,25 @@ cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const doub
     else vanka_march_kernel<false><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
     return cudaGetLastError();
 }
+cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
+                                NormSink S, cudaStream_t s) {
+    const LevelParams& L = P.L;
+    CUtensorMap mx, mb;
+    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, M2W, 1);
+    if (e != cudaSuccess) return e;
+    e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, M2W, 1);
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(L.n, M2T, M2R);
+    dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
+    if (x_zero) vanka_march2_kernel<true><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH);
+    else vanka_march2_kernel<false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH);
+    return cudaGetLastError();
+}
+int blocks_vanka_march2(int n) {
+    const int MH = march_height(n, M2T, M2R);
+    return ((n + M2T) / M2T) * ((n + MH) / MH);
+}
+
 int blocks_vanka_march(int n) {
     const int MH = march_height(n, MT, MR);
     return ((n + MT) / MT) * ((n + MH) / MH);
