@@ -360,10 +360,14 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         Lv.vp.L = t->L;
         Lv.vp.L.pitch = Lv.pitch;
         Lv.vp.L.plane = Lv.plane;
-        memcpy(Lv.vp.gp, t->gp, sizeof(t->gp));
-        memcpy(Lv.vp.gm, t->gm, sizeof(t->gm));
-        memcpy(Lv.up.up, t->up, sizeof(t->up));
-        memcpy(Lv.up.um, t->um, sizeof(t->um));
+        for (int a = 0; a < 9; ++a)
+            for (int cc = 0; cc < 9; ++cc) Lv.vp.gpT[cc][a] = t->gp[a][cc];
+        for (int a = 0; a < 11; ++a)
+            for (int cc = 0; cc < 11; ++cc) Lv.vp.gmT[cc][a] = t->gm[a][cc];
+        for (int a = 0; a < 3; ++a)
+            for (int cc = 0; cc < 3; ++cc) Lv.up.upT[cc][a] = t->up[a][cc];
+        for (int a = 0; a < 5; ++a)
+            for (int cc = 0; cc < 5; ++cc) Lv.up.umT[cc][a] = t->um[a][cc];
         if (!c->het) {
             for (int s = 0; s < 2; ++s)
                 for (int e = 0; e < 3; ++e)

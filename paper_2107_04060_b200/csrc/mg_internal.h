@@ -53,15 +53,15 @@ struct SolveState {
 // with 1/2 folded into the rows of pair components.
 struct VankaParams {
     LevelParams L;
-    double gp[9][9];
-    double gm[11][11];
+    double gpT[9][9];            // transposed: gpT[c][a] = G+[a][c] (column-outer FMA loops read pairs)
+    double gmT[11][11];
     const double* gbnd;          // device: MG_NCLASS x 20 x 20 (weighted, deflated), row major
     double omega;
 };
 
 struct DispParams {               // 8-DoF displacement Vanka (F_u^{-1} of BSR)
-    double up[3][3];              // + block: bubble diffs
-    double um[5][5];              // - block: u_x, u_y, bubble sums
+    double upT[3][3];             // + block: bubble diffs (transposed, [c][a])
+    double umT[5][5];             // - block: u_x, u_y, bubble sums (transposed)
     const double* ubnd;           // device: MG_NCLASS x 8 x 8
 };
 

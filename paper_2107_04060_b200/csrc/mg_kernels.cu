@@ -236,10 +236,10 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
 #pragma unroll
         for (int c = 0; c < 11; ++c) {
 #pragma unroll
-            for (int a = 0; a < 11; ++a) ym[a] = fma(P.gm[a][c], hm[c], ym[a]);
+            for (int a = 0; a < 11; ++a) ym[a] = fma(P.gmT[c][a], hm[c], ym[a]);
             if (c < 9) {
 #pragma unroll
-                for (int a = 0; a < 9; ++a) yp[a] = fma(P.gp[a][c], hp[c], yp[a]);
+                for (int a = 0; a < 9; ++a) yp[a] = fma(P.gpT[c][a], hp[c], yp[a]);
             }
         }
         out[0] = ym[0];
@@ -468,10 +468,10 @@ __device__ __forceinline__ void patch_apply8(const DispParams& U, int cls, const
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
 #pragma unroll
-            for (int a = 0; a < 5; ++a) ym[a] = fma(U.um[a][c], hm[c], ym[a]);
+            for (int a = 0; a < 5; ++a) ym[a] = fma(U.umT[c][a], hm[c], ym[a]);
             if (c < 3) {
 #pragma unroll
-                for (int a = 0; a < 3; ++a) yp[a] = fma(U.up[a][c], hp[c], yp[a]);
+                for (int a = 0; a < 3; ++a) yp[a] = fma(U.upT[c][a], hp[c], yp[a]);
             }
         }
         out[0] = ym[0];
@@ -1043,7 +1043,7 @@ constexpr int M2T = 28, M2R = 4, M2W = M2T + 4, M2C = M2T + 1, M2NT = 128;
 constexpr int M2XR = 10, M2BR = 9, M2CR = 5;
 constexpr int M2ROW = 10 * M2W;                                  // doubles per x / b ring row
 constexpr int M2SMEM = (M2XR * M2ROW + M2BR * M2ROW + M2CR * 20 * M2C) * 8 + 64;
-static_assert((M2T + 2) * M2R <= M2NT, "one residual position per thread");
+static_assert(M2T + 2 <= 32 && M2R * 32 == M2NT, "one warp per row, one residual position per thread");
 static_assert(M2T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
 
 template <bool XZERO>
@@ -1093,8 +1093,9 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
     for (int s = -1; s < nsteps; ++s) {
         mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
         // ---- residual rows y = j0 + s R + 1 + q
-        if (t < (M2T + 2) * M2R) {
-            const int q = t / (M2T + 2), lx = t - q * (M2T + 2);
+        // one warp per row (lanes beyond the row idle): no bank conflicts from rows wrapping in a warp
+        if ((t & 31) < M2T + 2) {
+            const int q = t >> 5, lx = t & 31;
             const int y = j0 + s * M2R + 1 + q, i = i0 - 1 + lx;
             double* bp = br + sb(y) * M2ROW + (lx + 1);
             const bool own = lx >= 1 && lx <= M2T && i <= n && y >= j0 && y < j0 + rows;
@@ -1120,8 +1121,8 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
         }
         __syncthreads();
         // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
-        if (t < M2R * M2C) {
-            const int q = t / M2C, px = t - q * M2C;
+        if ((t & 31) < M2C) {
+            const int q = t >> 5, px = t & 31;
             const int a = i0 + px, bb = j0 + s * M2R + 1 + q;
             double* out = cr + sc(bb) * (20 * M2C) + px;
             if (a <= n && bb >= 0 && bb <= n) {
@@ -1145,8 +1146,8 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
         }
         __syncthreads();
         // ---- owners y = j0 + s R + q: patch rows y and y + 1
-        if (s >= 0 && t < M2R * M2T) {
-            const int q = t / M2T, lx = t - q * M2T;
+        if (s >= 0 && (t & 31) < M2T) {
+            const int q = t >> 5, lx = t & 31;
             const int y = j0 + s * M2R + q, i = i0 + lx;
             if (i <= n && y < j0 + rows) {
                 const double* c0 = cr + sc(y) * (20 * M2C) + lx;
