@@ -1,0 +1,189 @@
+"""GPU parity at BASELINE's full sizes (4096^2 config 5 parameters, 1024^2 config 3 parameters) on
+SAMPLED outputs, in the launch configuration bench.py times (the 11- / 9-level production
+contexts, row-marching TMA kernels on level 0).
+
+The oracle cannot assemble a 4096^2 operator, but every sampled output depends only on a small
+window of its inputs, and the discretisation is translation invariant away from the boundary.  So
+each sample is recomputed by the UNCHANGED oracle on a 12 x 12 mesh whose spacing is overridden to
+h = 1/n: the input window around the sample (x, b within 2 indices, enough for r, the patches and
+the owners) is copied into the small mesh at a position with the same distance to the boundary, and
+the oracle's residual / Vanka sweep / transfer is read back at the mapped DoF.  Tolerances as in
+test_gpu_parity.py.  Properties that hold at any size (adjointness R = P^T, norm consistency) are
+checked on the full vectors.
+"""
+import numpy as np
+import pytest
+
+import mg_inputs
+from tests import _cases as C
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+NS = 12           # small oracle mesh
+W = 3             # window half-width copied around a sample
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _map(i, n):
+    """Index of the big mesh -> index of the small mesh with the same boundary neighbourhood."""
+    if i <= W + 1:
+        return i
+    if i >= n - W - 1:
+        return NS - (n - i)
+    return NS // 2
+
+
+def _window_to_small(arr, i, j, n, m_small):
+    """Copy arr (10, n+1, n+1) in [i-W, i+W] x [j-W, j+W] into a small (10, NS+1, NS+1) array,
+    aligned so that (i, j) lands at (_map(i), _map(j)); inactive slots of the small mesh zeroed."""
+    out = np.zeros((10, NS + 1, NS + 1))
+    si, sj = _map(i, n), _map(j, n)
+    for dj in range(-W, W + 1):
+        for di in range(-W, W + 1):
+            I, J, a, b = i + di, j + dj, si + di, sj + dj
+            if 0 <= I <= n and 0 <= J <= n and 0 <= a <= NS and 0 <= b <= NS:
+                out[:, b, a] = arr[:, J, I]
+    out[~mg_inputs.active_mask(NS)] = 0.0
+    return out, si, sj
+
+
+def _small_operator(n, pname):
+    from oracle.fem import Operator
+    from oracle.mesh import Mesh
+    lam, mu, K, tau, alpha, invM = C.PARAMS[pname]
+    m = Mesh(NS)
+    m.h = 1.0 / n                       # same spacing as the big mesh: same element integrals
+    return m, Operator(m, lam, mu, tau, alpha, invM, 1.0, K=K)
+
+
+def _samples(n, rng, count):
+    pts = {(0, 0), (n, n), (0, n), (n, 0), (1, 1), (n - 1, n - 1), (1, n - 1), (n // 2, 0), (0, n // 2),
+           (n - 1, n // 3), (n // 3, n - 1), (2, 3)}
+    while len(pts) < count:
+        pts.add((int(rng.integers(0, n + 1)), int(rng.integers(0, n + 1))))
+    return sorted(pts)
+
+
+@pytest.fixture(scope="module", params=[(4096, 11, "cfg5"), (1024, 9, "stiff")])
+def big(request):
+    torch = _torch()
+    n, levels, pname = request.param
+    H = C.gpu_hierarchy(n, levels, pname)
+    x = mg_inputs.uniform_vector(n, 101)
+    b = mg_inputs.uniform_rhs(n, 102)
+    xd, bd = H.to_device(x), H.to_device(b)
+    rd = H.zeros()
+    H.residual(0, xd, bd, rd)
+    x1 = xd.clone()
+    H.relax_vanka(0, x1, bd, 0.7, sweeps=1)
+    torch.cuda.synchronize()
+    out = dict(n=n, pname=pname, H=H, x=x, b=b, r=H.to_host(rd), x1=H.to_host(x1))
+    del x1, rd
+    yield out
+    H.close()
+    torch.cuda.empty_cache()
+
+
+def test_fullsize_residual_and_vanka_samples(big):
+    """Residual rows and one production Vanka sweep at sampled DoFs vs the oracle on a window."""
+    from oracle.relax import Vanka
+    n = big["n"]
+    m, op = _small_operator(n, big["pname"])
+    V = Vanka(op)
+    absA = op.A.copy()
+    absA.data = np.abs(absA.data)
+    rng = np.random.default_rng(7)
+    worst_r, worst_v = 0.0, 0.0
+    for (i, j) in _samples(n, rng, 48):
+        xs, si, sj = _window_to_small(big["x"], i, j, n, m)
+        bs, _, _ = _window_to_small(big["b"], i, j, n, m)
+        xa, ba = m.to_active(xs), m.to_active(bs)
+        rO = m.from_active(ba - op.A @ xa)
+        scale = m.from_active(np.abs(ba) + absA @ np.abs(xa))
+        x1O = m.from_active(V.sweep(xa, ba, 0.7))
+        act = mg_inputs.active_mask(n)[:, j, i]
+        for k in range(10):
+            if not act[k]:
+                assert big["r"][k, j, i] == 0.0 and big["x1"][k, j, i] == 0.0
+                continue
+            dr = abs(big["r"][k, j, i] - rO[k, sj, si])
+            assert dr <= 32 * U * scale[k, sj, si], (i, j, k, dr, scale[k, sj, si])
+            worst_r = max(worst_r, dr / scale[k, sj, si] / U)
+            dv = abs(big["x1"][k, j, i] - x1O[k, sj, si])
+            ref = max(abs(x1O[k, sj, si]), np.abs(x1O).max() * 1e-3)
+            assert dv <= 1e-9 * ref, (i, j, k, big["x1"][k, j, i], x1O[k, sj, si])
+            worst_v = max(worst_v, dv / ref)
+    print(f"n={n}: worst residual deviation {worst_r:.2f} u x scale, worst sweep deviation {worst_v:.2e}")
+
+
+def test_fullsize_transfer_adjoint_and_samples(big):
+    """<P e, r> = <e, R r> on the full vectors (R = P^T), and sampled restriction values vs the
+    oracle's P on a window (P is scale and translation invariant)."""
+    torch = _torch()
+    from oracle.mesh import Mesh
+    from oracle.transfer import Transfer
+    H, n = big["H"], big["n"]
+    nc = n // 2
+    r = mg_inputs.uniform_vector(n, 201)
+    e = mg_inputs.uniform_vector(nc, 202)
+    rd, ed = H.to_device(r), H.to_device(e, 1)
+    bc = H.zeros(1)
+    H.restrict(0, rd, bc)
+    pe = H.zeros()
+    H.prolong(0, ed, pe)
+    lhs = torch.sum(pe.double() * rd).item()
+    rhs = torch.sum(ed * bc).item()
+    scale = torch.sum(torch.abs(pe) * torch.abs(rd)).item()
+    assert abs(lhs - rhs) <= 1e-13 * scale
+    bcH = H.to_host(bc, 1)
+    # sampled restriction against the oracle on a 2 NS -> NS window
+    mf, mc = Mesh(2 * NS), Mesh(NS)
+    T = Transfer(mf, mc)
+    rng = np.random.default_rng(9)
+    for (I, J) in _samples(nc, rng, 24):
+        si, sj = _map(I, nc), _map(J, nc)
+        rs = np.zeros((10, 2 * NS + 1, 2 * NS + 1))
+        for dj in range(-2 * W, 2 * W + 1):
+            for di in range(-2 * W, 2 * W + 1):
+                fi, fj, a, b2 = 2 * I + di, 2 * J + dj, 2 * si + di, 2 * sj + dj
+                if 0 <= fi <= n and 0 <= fj <= n and 0 <= a <= 2 * NS and 0 <= b2 <= 2 * NS:
+                    rs[:, b2, a] = r[:, fj, fi]
+        rs[~mg_inputs.active_mask(2 * NS)] = 0.0
+        bO = mc.from_active(T.R @ mf.to_active(rs))
+        absR = abs(T.R)
+        bnd = mc.from_active(32 * U * (absR @ np.abs(mf.to_active(rs))))
+        act = mg_inputs.active_mask(nc)[:, J, I]
+        for k in range(10):
+            if act[k]:
+                assert abs(bcH[k, J, I] - bO[k, sj, si]) <= bnd[k, sj, si], (I, J, k)
+            else:
+                assert bcH[k, J, I] == 0.0
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_fullsize_solve(cfg):
+    """BASELINE configs 3 and 5: mg_solve to 1e-8 relative residual reduction (V(1,1) Vanka,
+    omega from E0); the device history is consistent with an independent residual evaluation and
+    every convergence factor is < 1."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Hierarchy, Opts
+    c = mg_inputs.CONFIGS[cfg]
+    H = Hierarchy(c["n"], c["levels"], c["lam"], c["mu"], K=c["K"], tau=c["tau"], alpha=c["alpha"],
+                  inv_M=c["inv_M"])
+    b = H.to_device(mg_inputs.uniform_rhs(c["n"], c["b_seed"]))
+    x = H.zeros()
+    rc, hist = H.solve(x, b, Opts(1, 1, "vanka", c["omega"]), rtol=1e-8, max_cycles=200)
+    rho = hist[1:] / hist[:-1]
+    print(f"config {cfg}: {len(hist) - 1} cycles, rho mean {np.exp(np.mean(np.log(rho))):.3f}, max {rho.max():.3f}")
+    assert rc == 0 and hist[-1] <= 1e-8 * hist[0]
+    assert rho[1:].max() < 1.0
+    rn = H.residual(0, x, b, norm=True)
+    assert abs(rn - hist[-1]) <= 1e-6 * hist[-1] + 1e-13 * hist[0]
+    H.close()
+    torch.cuda.empty_cache()
