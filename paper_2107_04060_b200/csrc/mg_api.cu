@@ -87,6 +87,13 @@ struct mg_ctx {
     // e2e buffers
     double* hx = nullptr;
     double* hb = nullptr;
+    // FGMRES work space (allocated on first use, grown with the restart length)
+    std::vector<double*> kv, kz;
+    double* kw = nullptr;
+    double* kdots = nullptr;      // device: 2 x 72 dot results + 8 coefficients
+    double* kpart = nullptr;
+    unsigned* kcnt = nullptr;
+    int kcap = 0;
     std::vector<void*> allocs;
     std::vector<GraphEntry> graphs;
     cudaStream_t cap = nullptr;   // capture stream
@@ -175,7 +182,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
     };
     if (int rc = lmark()) return rc;
     if (int rc = mark(0)) return rc;
-    if (solve && o.nu1 == 0) {
+    if ((solve == 1 || solve == 2) && o.nu1 == 0) {
         CK(launch_residual(c->L[0].vp.L, x0, b0, nullptr, S, s));
         S = no_norm();
     }
@@ -183,7 +190,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         Level& Lv = c->L[l];
         double* xl = l == 0 ? x0 : Lv.x;
         const double* bl = l == 0 ? b0 : Lv.b;
-        const bool zero = l > 0;
+        const bool zero = l > 0 || solve == 3;   // solve == 3: x0 is zero (FGMRES preconditioner)
         double* a = xl;
         double* t = Lv.t;
         for (int k = 0; k < o.nu1; ++k) {
@@ -244,7 +251,7 @@ int get_graph(mg_ctx* c, double* x, const double* b, const mg_cycle_opts& o, int
             *out = g.exec;
             return MG_OK;
         }
-    if (c->graphs.size() >= 16) {
+    if (c->graphs.size() >= 96) {
         cudaGraphExecDestroy(c->graphs.front().exec);
         c->graphs.erase(c->graphs.begin());
     }
@@ -618,6 +625,152 @@ int mg_timing_levels(mg_ctx* c, float* ms, int32_t cap) {
     CK(cudaEventSynchronize(c->lev.back()));
     for (int i = 0; i < m; ++i) CK(cudaEventElapsedTime(&ms[i], c->lev[i], c->lev[i + 1]));
     return m;
+}
+
+int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_iters,
+              int32_t restart, double* history_host, int32_t* n_iters, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (int rc = check_opts(o)) return rc;
+    if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (max_iters < 0 || restart < 1 || restart > 64) return fail(MG_EINVAL, "need max_iters >= 0, 1 <= restart <= 64");
+    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
+    if (!c->Ginv || c->levels < 2) return fail(MG_EINVAL, "mg_fgmres needs levels >= 2 and a coarsest solve");
+    Level& L0 = c->L[0];
+    const int64_t len = L0.len;
+    const size_t vb = sizeof(double) * len;
+    if (restart > c->kcap) {
+        // zero-filled once: the kernels never write the padding / inactive slots, and the FGMRES dot
+        // products run over whole padded vectors
+        while ((int)c->kv.size() < restart + 1) {
+            double* p = (double*)dalloc(c, vb);
+            if (!p) return fail(MG_ENOMEM, "FGMRES basis allocation failed (restart %d)", restart);
+            CK(cudaMemsetAsync(p, 0, vb, s));
+            c->kv.push_back(p);
+        }
+        while ((int)c->kz.size() < restart) {
+            double* p = (double*)dalloc(c, vb);
+            if (!p) return fail(MG_ENOMEM, "FGMRES basis allocation failed (restart %d)", restart);
+            CK(cudaMemsetAsync(p, 0, vb, s));
+            c->kz.push_back(p);
+        }
+        c->kcap = restart;
+    }
+    if (!c->kw) {
+        c->kw = (double*)dalloc(c, vb);
+        c->kdots = (double*)dalloc(c, sizeof(double) * 160);
+        c->kpart = (double*)dalloc(c, sizeof(double) * dot_partials_needed());
+        c->kcnt = (unsigned*)dalloc(c, 64);
+        if (!c->kw || !c->kdots || !c->kpart || !c->kcnt) return fail(MG_ENOMEM, "FGMRES work allocation failed");
+        CK(cudaMemsetAsync(c->kcnt, 0, 64, s));
+        CK(cudaMemsetAsync(c->kw, 0, vb, s));
+    }
+    const LevelParams& LP = L0.vp.L;
+    auto dots = [&](const double* w, const std::vector<double*>& vs, int first, int k, double* out) -> int {
+        for (int q0 = 0; q0 < k; q0 += 8) {
+            VecPtrs P{};
+            const int kk = std::min(8, k - q0);
+            for (int q = 0; q < kk; ++q) P.p[q] = vs[first + q0 + q];
+            CK(launch_dots(w, P, kk, len, c->kpart, c->kcnt, out + q0, s));
+        }
+        return MG_OK;
+    };
+    auto update = [&](double* w, const std::vector<double*>& vs, int first, int k, const double* coef) -> int {
+        for (int q0 = 0; q0 < k; q0 += 8) {
+            VecPtrs P{};
+            const int kk = std::min(8, k - q0);
+            for (int q = 0; q < kk; ++q) P.p[q] = vs[first + q0 + q];
+            CK(launch_update(w, P, kk, coef + q0, len, s));
+        }
+        return MG_OK;
+    };
+    double* hd = c->kdots;           // [0..63] first CGS pass, [64..127] second, [128] norm^2
+    std::vector<double> hist;
+    int iters = 0;
+    double beta0 = -1.0, target = 0.0;
+    bool done = false;
+    std::vector<double> H, cs, sn, g, hcol(130);
+    while (!done) {
+        // r = b - A x -> v_0, beta = ||r||
+        CK(launch_residual(LP, x, b, c->kv[0], no_norm(), s));
+        if (int rc = dots(c->kv[0], c->kv, 0, 1, hd + 128)) return rc;
+        CK(cudaMemcpyAsync(hcol.data() + 128, hd + 128, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const double beta = std::sqrt(hcol[128]);
+        if (beta0 < 0.0) {
+            beta0 = beta;
+            target = rtol * beta0;
+            hist.push_back(beta);
+        }
+        if (!std::isfinite(beta)) return fail(MG_ECUDA, "non-finite residual in FGMRES");
+        if (beta <= target || beta == 0.0 || iters >= max_iters) break;
+        CK(launch_scale(c->kv[0], c->kv[0], 1.0 / beta, len, s));
+        const int m = std::min(restart, max_iters - iters);
+        H.assign((m + 1) * m, 0.0);
+        cs.assign(m, 0.0);
+        sn.assign(m, 0.0);
+        g.assign(m + 1, 0.0);
+        g[0] = beta;
+        int k = 0;
+        for (int j = 0; j < m; ++j) {
+            // z_j = one V-cycle from zero on v_j; w = A z_j
+            cudaGraphExec_t ge;
+            if (int rc = get_graph(c, c->kz[j], c->kv[j], *o, 3, nullptr, &ge)) return rc;
+            CK(cudaGraphLaunch(ge, s));
+            CK(launch_apply(LP, c->kz[j], c->kw, no_norm(), s));
+            // classical Gram-Schmidt, twice
+            if (int rc = dots(c->kw, c->kv, 0, j + 1, hd)) return rc;
+            if (int rc = update(c->kw, c->kv, 0, j + 1, hd)) return rc;
+            if (int rc = dots(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
+            if (int rc = update(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
+            std::vector<double*> wv{c->kw};
+            if (int rc = dots(c->kw, wv, 0, 1, hd + 128)) return rc;
+            CK(cudaMemcpyAsync(hcol.data(), hd, sizeof(double) * 129, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const double hn = std::sqrt(hcol[128]);
+            for (int i = 0; i <= j; ++i) H[i * m + j] = hcol[i] + hcol[64 + i];
+            H[(j + 1) * m + j] = hn;
+            if (hn > 0.0) CK(launch_scale(c->kv[j + 1], c->kw, 1.0 / hn, len, s));
+            for (int i = 0; i < j; ++i) {   // previous Givens rotations
+                const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
+                H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
+                H[i * m + j] = t;
+            }
+            const double d = std::hypot(H[j * m + j], H[(j + 1) * m + j]);
+            cs[j] = H[j * m + j] / d;
+            sn[j] = H[(j + 1) * m + j] / d;
+            H[j * m + j] = d;
+            H[(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            k = j + 1;
+            ++iters;
+            hist.push_back(std::fabs(g[j + 1]));
+            if (!std::isfinite(hist.back())) return fail(MG_ECUDA, "non-finite FGMRES residual estimate");
+            if (hist.back() <= target) break;
+        }
+        // y = H^{-1} g (upper triangular), x += Z y
+        std::vector<double> y(k);
+        for (int i = k - 1; i >= 0; --i) {
+            double t = g[i];
+            for (int l = i + 1; l < k; ++l) t -= H[i * m + l] * y[l];
+            y[i] = t / H[i * m + i];
+        }
+        for (int i = 0; i < k; ++i) y[i] = -y[i];   // the update kernel subtracts
+        CK(cudaMemcpyAsync(hd + 130, y.data(), sizeof(double) * std::min(k, 8), cudaMemcpyHostToDevice, s));
+        for (int q0 = 0; q0 < k; q0 += 8) {
+            const int kk = std::min(8, k - q0);
+            CK(cudaMemcpyAsync(hd + 130, y.data() + q0, sizeof(double) * kk, cudaMemcpyHostToDevice, s));
+            if (int rc = update(x, c->kz, q0, kk, hd + 130)) return rc;
+            CK(cudaStreamSynchronize(s));   // hd + 130 is reused by the next chunk
+        }
+        if (hist.back() <= target || iters >= max_iters) done = true;
+    }
+    CK(cudaStreamSynchronize(s));
+    const int nh = (int)hist.size();
+    if (history_host)
+        for (int i = 0; i < nh; ++i) history_host[i] = hist[i];
+    if (n_iters) *n_iters = nh - 1;
+    return hist.back() <= target ? MG_OK : MG_NOTCONV;
 }
 
 int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_cycles,

@@ -158,7 +158,7 @@ __device__ __forceinline__ void residual_at(const LevelParams& L, const double* 
 // residual
 constexpr int RTX = 32, RTY = 8, RNT = 256;
 
-template <bool HET>
+template <bool HET, bool APPLY>
 __global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, const double* __restrict__ x,
                                                        const double* __restrict__ b, double* __restrict__ r,
                                                        NormSink S) {
@@ -173,7 +173,15 @@ __global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, cons
     double nrm = 0.0;
     if (i <= L.n && j <= L.n) {
         double rv[10];
-        residual_at<XW, XH, HET>(L, xs, lx + 1, ly + 1, i, j, b, rv);
+        if (APPLY) {
+            // out = A x (masked): the operator application of FGMRES (b unused)
+            const double* x0 = xs + (ly + 1) * XW + (lx + 1);
+            apply_rows<XW * XH, HET>(L, x0 - XW, x0, x0 + XW, i, j, rv);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, j, L.n) ? rv[k] : 0.0;
+        } else {
+            residual_at<XW, XH, HET>(L, xs, lx + 1, ly + 1, i, j, b, rv);
+        }
         const int64_t o = (int64_t)j * L.pitch + i;
 #pragma unroll
         for (int k = 0; k < 10; ++k) {
@@ -1372,10 +1380,120 @@ int blocks_bsr(int n) { return ((n + BTX) / BTX) * ((n + BTY) / BTY); }
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
                             cudaStream_t s) {
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
-    if (L.kinv_field) residual_kernel<true><<<grid, RNT, 0, s>>>(L, x, b, r, S);
-    else residual_kernel<false><<<grid, RNT, 0, s>>>(L, x, b, r, S);
+    if (L.kinv_field) residual_kernel<true, false><<<grid, RNT, 0, s>>>(L, x, b, r, S);
+    else residual_kernel<false, false><<<grid, RNT, 0, s>>>(L, x, b, r, S);
     return cudaGetLastError();
 }
+
+cudaError_t launch_apply(const LevelParams& L, const double* x, double* y, NormSink S, cudaStream_t s) {
+    dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
+    if (L.kinv_field) residual_kernel<true, true><<<grid, RNT, 0, s>>>(L, x, nullptr, y, S);
+    else residual_kernel<false, true><<<grid, RNT, 0, s>>>(L, x, nullptr, y, S);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Vector kernels of FGMRES over whole padded level vectors (inactive / padding slots are 0).
+// Deterministic: fixed grid, per-block partials, summed in block order by the last block.
+constexpr int DOT_BLOCKS = 296, DOT_NT = 256, VK = 8;
+
+__global__ void __launch_bounds__(DOT_NT) vec_dots_kernel(const double* __restrict__ w, VecPtrs V, int k,
+                                                          int64_t len, double* __restrict__ partials,
+                                                          unsigned* __restrict__ counter, double* __restrict__ out) {
+    double acc[VK];
+#pragma unroll
+    for (int q = 0; q < VK; ++q) acc[q] = 0.0;
+    const int64_t n2 = len / 2;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    for (int64_t e = (int64_t)blockIdx.x * DOT_NT + threadIdx.x; e < n2; e += (int64_t)DOT_BLOCKS * DOT_NT) {
+        const double2 a = __ldg(w2 + e);
+#pragma unroll
+        for (int q = 0; q < VK; ++q) {
+            if (q < k) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(V.p[q]) + e);
+                acc[q] = fma(a.x, v.x, acc[q]);
+                acc[q] = fma(a.y, v.y, acc[q]);
+            }
+        }
+    }
+    __shared__ double red[VK][DOT_NT / 32];
+    __shared__ unsigned last;
+#pragma unroll
+    for (int q = 0; q < VK; ++q) {
+        double v = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {
+        double t = 0.0;
+        for (int u = 0; u < DOT_NT / 32; ++u) t += red[threadIdx.x][u];
+        partials[threadIdx.x * DOT_BLOCKS + blockIdx.x] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == DOT_BLOCKS - 1);
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        if (threadIdx.x < k) {
+            double t = 0.0;
+            for (int u = 0; u < DOT_BLOCKS; ++u) t += __ldcg(partials + threadIdx.x * DOT_BLOCKS + u);
+            out[threadIdx.x] = t;
+        }
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+// w = w - sum_q c[q] v_q   (c in device memory)
+__global__ void __launch_bounds__(DOT_NT) vec_update_kernel(double* __restrict__ w, VecPtrs V, int k,
+                                                            const double* __restrict__ c, int64_t len) {
+    const int64_t n2 = len / 2;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    double cq[VK];
+#pragma unroll
+    for (int q = 0; q < VK; ++q) cq[q] = q < k ? c[q] : 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * DOT_NT + threadIdx.x; e < n2; e += (int64_t)gridDim.x * DOT_NT) {
+        double2 a = w2[e];
+#pragma unroll
+        for (int q = 0; q < VK; ++q) {
+            if (q < k) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(V.p[q]) + e);
+                a.x = fma(-cq[q], v.x, a.x);
+                a.y = fma(-cq[q], v.y, a.y);
+            }
+        }
+        w2[e] = a;
+    }
+}
+
+// y = s * x
+__global__ void __launch_bounds__(DOT_NT) vec_scale_kernel(double* __restrict__ y, const double* __restrict__ x,
+                                                           double s, int64_t len) {
+    const int64_t n2 = len / 2;
+    for (int64_t e = (int64_t)blockIdx.x * DOT_NT + threadIdx.x; e < n2; e += (int64_t)gridDim.x * DOT_NT) {
+        double2 a = __ldg(reinterpret_cast<const double2*>(x) + e);
+        a.x *= s;
+        a.y *= s;
+        reinterpret_cast<double2*>(y)[e] = a;
+    }
+}
+
+cudaError_t launch_dots(const double* w, const VecPtrs& V, int k, int64_t len, double* partials, unsigned* counter,
+                        double* out, cudaStream_t s) {
+    vec_dots_kernel<<<DOT_BLOCKS, DOT_NT, 0, s>>>(w, V, k, len, partials, counter, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_update(double* w, const VecPtrs& V, int k, const double* c, int64_t len, cudaStream_t s) {
+    vec_update_kernel<<<2 * DOT_BLOCKS, DOT_NT, 0, s>>>(w, V, k, c, len);
+    return cudaGetLastError();
+}
+cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cudaStream_t s) {
+    vec_scale_kernel<<<2 * DOT_BLOCKS, DOT_NT, 0, s>>>(y, x, sc, len);
+    return cudaGetLastError();
+}
+int dot_partials_needed() { return VK * DOT_BLOCKS; }
 
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
                          NormSink S, cudaStream_t s) {

@@ -12,9 +12,22 @@ struct NormSink {
 };
 void kernels_init();
 
+// up to 8 vector pointers for the FGMRES multi-vector kernels
+struct VecPtrs {
+    const double* p[8];
+};
+
 // All launchers return cudaGetLastError() of the launch.
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r,
                             NormSink norm, cudaStream_t s);
+// y = A x (masked), the FGMRES operator application
+cudaError_t launch_apply(const LevelParams& L, const double* x, double* y, NormSink norm, cudaStream_t s);
+// FGMRES vector kernels (deterministic): out[q] = <w, V.p[q]>, q < k <= 8;  w -= sum c[q] V.p[q];  y = sc x
+cudaError_t launch_dots(const double* w, const VecPtrs& V, int k, int64_t len, double* partials, unsigned* counter,
+                        double* out, cudaStream_t s);
+cudaError_t launch_update(double* w, const VecPtrs& V, int k, const double* c, int64_t len, cudaStream_t s);
+cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cudaStream_t s);
+int dot_partials_needed();
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
                          bool x_zero, NormSink norm, cudaStream_t s);
 // row-marching TMA variant of the same sweep (identical arithmetic); the production kernel

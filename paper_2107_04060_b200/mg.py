@@ -61,6 +61,8 @@ SIGNATURES = {
     "mg_cycle": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), _D, _VP]),
     "mg_solve": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
                                 _D, ctypes.POINTER(ctypes.c_int32), _VP]),
+    "mg_fgmres": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
+                                 ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_solve_host": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
                                      _D, ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_cycle_async": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), _VP, _VP]),
@@ -113,8 +115,11 @@ def _install_torch_allocator(lib):
             return None
 
     def _f(ptr, _user):
-        if ptr:
-            torch.cuda.caching_allocator_delete(ptr)
+        try:
+            if ptr:
+                torch.cuda.caching_allocator_delete(ptr)
+        except Exception:      # interpreter shutdown: torch already torn down, memory goes with the process
+            pass
 
     _alloc_cbs = (ALLOC(_a), FREE(_f))
     lib.mg_set_allocator(ctypes.cast(_alloc_cbs[0], _VP), ctypes.cast(_alloc_cbs[1], _VP), None)
@@ -285,6 +290,16 @@ class Hierarchy:
         o = opts.c()
         rc = _check(self.lib.mg_solve(self.ctx, _ptr(x), _ptr(b), ctypes.byref(o), float(rtol), int(max_cycles),
                                       hist.ctypes.data_as(_D), ctypes.byref(nc), _stream(stream)), "mg_solve")
+        return rc, hist[: nc.value + 1]
+
+    def fgmres(self, x, b, opts: Opts, rtol=1e-6, max_iters=100, restart=20, stream=None):
+        """FGMRES preconditioned by one V-cycle per iteration; returns (rc, history)."""
+        hist = np.zeros(max_iters + 1)
+        nc = ctypes.c_int32(0)
+        o = opts.c()
+        rc = _check(self.lib.mg_fgmres(self.ctx, _ptr(x), _ptr(b), ctypes.byref(o), float(rtol), int(max_iters),
+                                       int(restart), hist.ctypes.data_as(_D), ctypes.byref(nc), _stream(stream)),
+                    "mg_fgmres")
         return rc, hist[: nc.value + 1]
 
     def solve_host(self, x_host: np.ndarray, b_host: np.ndarray, opts: Opts, rtol=1e-8, max_cycles=100,

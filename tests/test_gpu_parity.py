@@ -245,3 +245,43 @@ def test_solve_matches_cycles():
     rc, hist = H.solve(xd, bd, Opts(1, 1, "vanka", 0.74), rtol=1e-14, max_cycles=3)
     assert rc == 1 and len(hist) == 4
     assert np.all(np.abs(hist - hO[:4]) <= 1e-10 * hO[:4])
+
+
+@pytest.mark.parametrize("n,levels,pname,relax", [(16, 3, "unit", "vanka"), (32, 4, "cfg5", "vanka"),
+                                                 (32, 4, "unit", "bsr")])
+def test_fgmres_history(n, levels, pname, relax):
+    """FGMRES + one V-cycle per iteration: the GPU history equals the oracle's
+    (oracle: modified Gram-Schmidt; GPU: classical Gram-Schmidt twice) to 1e-9 relative while
+    above 1e3 x the rounding floor, and the final iterates agree."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    from oracle.krylov import fgmres_mg
+    H = C.gpu_hierarchy(n, levels, pname)
+    Oh = C.hierarchy(n, levels, pname, relax)
+    m = Oh.meshes[0]
+    b = mg_inputs.uniform_rhs(n, 3)
+    ba = m.to_active(b)
+    if relax == "vanka":
+        od, go = dict(nu1=1, nu2=1, omega=0.72), Opts(1, 1, "vanka", 0.72)
+    else:
+        od, go = dict(nu1=1, nu2=1, omega=0.75, omega_J=1.0, jacobi_sweeps=3), Opts(1, 1, "bsr", 0.75, 1.0, 3)
+    from oracle.cycle import Hierarchy as OH
+    lam, mu, K, tau, alpha, invM = C.PARAMS[pname]
+    Oalt = OH(n, levels, lam, mu, tau, alpha, invM, 1.0, K=K, relax=relax, alt_order=True)
+    xO, hO = fgmres_mg(Oh, ba, od, rtol=1e-9, max_iters=40, restart=30)
+    xA, hA = fgmres_mg(Oalt, ba, od, rtol=1e-9, max_iters=40, restart=30)
+    xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+    rc, hG = H.fgmres(xd, bd, go, rtol=1e-9, max_iters=40, restart=30)
+    k = min(len(hG), len(hO), len(hA))
+    # floor: 4 x the spread between two legal summation orders of the oracle (SURVEY 8c-11); Krylov
+    # iterations amplify rounding, so late iterations are compared at that level
+    F = 4 * np.abs(hA[:k] - hO[:k]) + 64 * U * np.linalg.norm(ba)
+    dev = np.abs(hG[:k] - hO[:k])
+    print("fgmres its GPU/oracle/alt", len(hG) - 1, len(hO) - 1, len(hA) - 1,
+          "max rel dev", (dev / hO[:k]).max(), "max rel spread", (np.abs(hA[:k] - hO[:k]) / hO[:k]).max())
+    assert abs(len(hG) - len(hO)) <= 1
+    assert np.all(dev <= 1e-9 * hO[:k] + F)
+    errs = C.block_rel_err(m, H.to_host(xd), m.from_active(xO))
+    e_oo = C.block_rel_err(m, m.from_active(xA), m.from_active(xO))
+    for key in errs:
+        assert errs[key] <= 1e-7 + 4 * e_oo[key], (errs, e_oo)
