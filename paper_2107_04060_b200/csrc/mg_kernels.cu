@@ -14,6 +14,7 @@
 // on a halo ring instead of exchanging it, so every sweep reads x and b once and writes x once
 // (owner computes; no atomics; deterministic).  The Vanka sweep is out of place (x -> xout):
 // neighbouring CTAs read x in their halos.
+#include <algorithm>
 #include <cstdint>
 #include <cuda.h>
 
@@ -1310,13 +1311,29 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
     }
 }
 
-// Rows marched by one CTA: as many as possible (the prologue step is overhead) while keeping
-// >= ~4 CTAs per SM of work (148 SMs) so that small levels still fill the GPU.
-static int march_height(int n, int tcols, int rstep) {
+// Rows marched by one CTA.  All CTAs of a marching launch carry equal work, so the number of row
+// segments per strip is chosen to make the launch an (almost) whole number of waves of resident
+// CTAs (SMs x CTAs per SM), with segments of about `target` rows: a fractional last wave left ~35% of
+// the SM time idle at level 1 (profiles/r01_ncu_level1.txt); a single lock-step wave (all CTAs
+// loading, then all computing) halved the throughput at level 0, so several waves are kept.
+static int g_sms = 0;
+static int sm_count() {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+static int march_height(int n, int tcols, int rstep, int ctas_per_sm, int target = 128) {
     const long strips = (n + tcols) / tcols;
-    int mh = 128;
-    while (mh > 4 * rstep && strips * ((n + mh) / mh) < 4L * 148) mh /= 2;
-    return mh;
+    const long slots = (long)sm_count() * ctas_per_sm;
+    const long base = (n + target) / target;                            // segments of ~target rows
+    const long waves = std::max(2L, (strips * base + slots / 2) / slots);
+    const long segs = std::max(1L, waves * slots / strips);
+    int mh = (int)((n + segs) / segs);                                   // ceil((n + 1) / segs)
+    mh = ((mh + rstep - 1) / rstep) * rstep;
+    return std::max(mh, rstep);
 }
 
 // ---- TMA descriptors (driver entry point fetched once through the runtime)
@@ -1511,7 +1528,7 @@ cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const doub
     if (e != cudaSuccess) return e;
     e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, M_BW, MR);   // both boxes start at column i0 - 2
     if (e != cudaSuccess) return e;
-    const int MH = march_height(L.n, MT, MR);
+    const int MH = march_height(L.n, MT, MR, 2);
     dim3 grid((L.n + MT) / MT, (L.n + MH) / MH);
     if (x_zero) vanka_march_kernel<true><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
     else vanka_march_kernel<false><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
@@ -1525,19 +1542,19 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     if (e != cudaSuccess) return e;
     e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, M2W, 1);
     if (e != cudaSuccess) return e;
-    const int MH = march_height(L.n, M2T, M2R);
+    const int MH = march_height(L.n, M2T, M2R, 3);
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     if (x_zero) vanka_march2_kernel<true><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH);
     else vanka_march2_kernel<false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH);
     return cudaGetLastError();
 }
 int blocks_vanka_march2(int n) {
-    const int MH = march_height(n, M2T, M2R);
+    const int MH = march_height(n, M2T, M2R, 3);
     return ((n + M2T) / M2T) * ((n + MH) / MH);
 }
 
 int blocks_vanka_march(int n) {
-    const int MH = march_height(n, MT, MR);
+    const int MH = march_height(n, MT, MR, 2);
     return ((n + MT) / MT) * ((n + MH) / MH);
 }
 
@@ -1548,7 +1565,7 @@ cudaError_t launch_restrict_march(const LevelParams& Lf, int nc, int pitchc, con
     if (e != cudaSuccess) return e;
     e = encode_vec_map(&mb, b, Lf.n, Lf.pitch, Lf.plane, Q_RW, QF);
     if (e != cudaSuccess) return e;
-    const int MH = march_height(nc, QT, QR);
+    const int MH = march_height(nc, QT, QR, 3, 128);
     dim3 grid((nc + QT) / QT, (nc + MH) / MH);
     if (Lf.kinv_field) restrict_march_kernel<true><<<grid, QNT, Q_SMEM, s>>>(mx, mb, Lf, nc, pitchc, bc, MH);
     else restrict_march_kernel<false><<<grid, QNT, Q_SMEM, s>>>(mx, mb, Lf, nc, pitchc, bc, MH);
