@@ -144,7 +144,8 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     if (o.relax == MG_VANKA) {
         VankaParams P = Lv.vp;
         P.omega = o.omega;
-        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 3 && Lv.n >= c->march_min_n) CK(launch_vanka_march3(P, xin, b, xout, xzero, S, s));
+        else if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
         else if (c->vanka_impl == 1 && Lv.n >= c->march_min_n) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
@@ -359,6 +360,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         Lv.len = 10 * Lv.plane;
         max_blocks = std::max(max_blocks, std::max(blocks_vanka(Lv.n), std::max(blocks_residual(Lv.n), blocks_bsr(Lv.n))));
         max_blocks = std::max(max_blocks, std::max(blocks_vanka_march(Lv.n), blocks_vanka_march2(Lv.n)));
+        max_blocks = std::max(max_blocks, blocks_vanka_march3(Lv.n));
         HostLevelTables* t = new HostLevelTables;
         if (host_level_tables(Lv.n, c->m, t, err, sizeof(err))) {
             delete t;

@@ -1193,6 +1193,155 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
 }
 
 // ------------------------------------------------------------------------------------------
+// Row-marching Vanka, 4 CTAs / SM.  As vanka_march2_kernel, but b is read straight from global
+// memory into registers at the start of each step (it is used once, by one thread, so staging it in
+// shared memory buys nothing) and only r is kept in a 5-row ring: 54 KB of shared memory per CTA.
+constexpr int M3T = 24, M3R = 4, M3W = M3T + 4, M3RW = M3T + 2, M3C = M3T + 1, M3NT = 128;
+constexpr int M3XR = 10, M3RR = 5, M3CR = 5;
+constexpr int M3XROW = ((10 * M3W * 8 + 127) / 128) * 16, M3RROW = 10 * M3RW;   // x slots 128-byte aligned (TMA)
+constexpr int M3SMEM = (M3XR * M3XROW + M3RR * M3RROW + M3CR * 20 * M3C) * 8 + 64;
+static_assert(M3T + 2 <= 32 && M3R * 32 == M3NT, "one warp per row, one residual position per thread");
+static_assert(M3T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
+
+template <bool XZERO>
+__global__ void __launch_bounds__(M3NT, 4) vanka_march3_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const VankaParams P, const double* __restrict__ b,
+                                                               double* __restrict__ xo, NormSink S, int MH) {
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;                        // [M3XR][10][M3W]
+    double* rr_ = xr + M3XR * M3XROW;       // [M3RR][10][M3RW]   residual rows
+    double* cr = rr_ + M3RR * M3RROW;       // [M3CR][20][M3C]    patch corrections
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M3CR * 20 * M3C);
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n;
+    const int i0 = blockIdx.x * M3T, j0 = blockIdx.y * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int nsteps = (rows + M3R - 1) / M3R;
+    const int t = threadIdx.x;
+    auto sx = [&](int y) { return (y - j0 + 2 * M3R) % M3XR; };
+    auto sr = [&](int y) { return (y - j0 + 2 * M3R) % M3RR; };
+    auto sc = [&](int y) { return (y - j0 + 2 * M3R) % M3CR; };
+    // group g: x rows first used by step g (g = -1: j0-R .. j0+1; else j0+gR+2 .. j0+gR+R+1)
+    auto issue = [&](int g) {
+        if (XZERO || g >= nsteps) return;
+        uint64_t* bar = &bars[(g + 1) & 1];
+        const int nx = g < 0 ? M3R + 2 : M3R;
+        mbar_expect_tx(bar, nx * 10 * M3W * 8);
+        const int xfirst = g < 0 ? j0 - M3R : j0 + g * M3R + 2;
+        for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * M3XROW, &tmx, i0 - 2, xfirst + k, 0, bar);
+    };
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue(-1);
+        issue(0);
+    }
+    const int lane = t & 31, q = t >> 5;
+    double nrm = 0.0;
+    for (int s = -1; s < nsteps; ++s) {
+        // ---- residual rows y = j0 + s R + 1 + q, column i = i0 - 1 + lane; b straight from HBM
+        {
+            const int y = j0 + s * M3R + 1 + q, i = i0 - 1 + lane;
+            const bool inrow = lane < M3RW;
+            const bool in = inrow && i >= 0 && i <= n && y >= 0 && y <= n;
+            double bv[10];
+            const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) bv[k] = (in && is_active(k, i, y, n)) ? __ldg(b + k * L.plane + o) : 0.0;
+            if (!XZERO) mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
+            if (inrow) {
+                double* rp = rr_ + sr(y) * M3RROW + lane;
+                const bool own = lane >= 1 && lane <= M3T && i <= n && y >= j0 && y < j0 + rows;
+                double rv[10];
+                if (!XZERO) {
+                    const double* xm = xr + sx(y - 1) * M3XROW + (lane + 1);
+                    const double* x0 = xr + sx(y) * M3XROW + (lane + 1);
+                    const double* xp = xr + sx(y + 1) * M3XROW + (lane + 1);
+                    double av[10];
+                    apply_rows<M3W, false>(L, xm, x0, xp, i, y, av);
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, y, n) ? bv[k] - av[k] : 0.0;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) rv[k] = bv[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rp[k * M3RW] = rv[k];
+                if (own) {
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
+        if (lane < M3C) {
+            const int px = lane;
+            const int a = i0 + px, bb = j0 + s * M3R + 1 + q;
+            double* out = cr + sc(bb) * (20 * M3C) + px;
+            if (a <= n && bb >= 0 && bb <= n) {
+                const double* r0 = rr_ + sr(bb) * M3RROW + (px + 1);
+                const double* rm = rr_ + sr(bb - 1) * M3RROW + (px + 1);
+                double rr[20];
+#define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * M3RW + (dx)]
+                rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+                rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+                rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+                rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+                rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+                rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+                rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+                patch_apply20(P, vertex_class(a, bb, n), rr, out, M3C);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 20; ++k) out[k * M3C] = 0.0;
+            }
+        }
+        __syncthreads();
+        // ---- owners y = j0 + s R + q: patch rows y and y + 1
+        if (s >= 0 && lane < M3T) {
+            const int y = j0 + s * M3R + q, i = i0 + lane;
+            if (i <= n && y < j0 + rows) {
+                const double* c0 = cr + sc(y) * (20 * M3C) + lane;
+                const double* c1 = cr + sc(y + 1) * (20 * M3C) + lane;
+#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * M3C + (dx)]
+                double d[10];
+                d[0] = CC(0, 0, 0);
+                d[1] = CC(1, 0, 0);
+                d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+                d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+                d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+                d[5] = CC(8, 0, 0) + CC(9, 1, 0);
+                d[6] = CC(10, 0, 0) + CC(11, 0, 1);
+                d[7] = CC(12, 1, 0) + CC(13, 0, 1);
+                d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
+                d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
+#undef CC
+                const double* xv = xr + sx(y) * M3XROW + (lane + 2);
+                const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) {
+                    const double xk = XZERO ? 0.0 : xv[k * M3W];
+                    xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(P.omega, d[k], xk) : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s + 2);
+        }
+    }
+    if (S.out || S.state) norm_finish<M3NT>(S, nrm);
+}
+
+// ------------------------------------------------------------------------------------------
 // Row-marching fused residual + restriction b_H = P^T (b - A x) with TMA row chunks.
 // A CTA owns coarse columns [I0, I0+QT) and coarse rows [J0, J0+MH); step s produces coarse rows
 // J0 + s QR .. J0 + (s+1) QR - 1 from the fine residual rows 2(J0 + s QR) - 2 .. 2(J0 + s QR) + 2QR - 1,
@@ -1362,6 +1511,8 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
 }
 
 void kernels_init() {
+    set_smem(vanka_march3_kernel<false>, M3SMEM);
+    set_smem(vanka_march3_kernel<true>, M3SMEM);
     set_smem(vanka_march2_kernel<false>, M2SMEM);
     set_smem(vanka_march2_kernel<true>, M2SMEM);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
@@ -1551,6 +1702,23 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
 int blocks_vanka_march2(int n) {
     const int MH = march_height(n, M2T, M2R, 3);
     return ((n + M2T) / M2T) * ((n + MH) / MH);
+}
+
+cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
+                                NormSink S, cudaStream_t s) {
+    const LevelParams& L = P.L;
+    CUtensorMap mx;
+    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, M3W, 1);
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(L.n, M3T, M3R, 4);
+    dim3 grid((L.n + M3T) / M3T, (L.n + MH) / MH);
+    if (x_zero) vanka_march3_kernel<true><<<grid, M3NT, M3SMEM, s>>>(mx, P, b, xo, S, MH);
+    else vanka_march3_kernel<false><<<grid, M3NT, M3SMEM, s>>>(mx, P, b, xo, S, MH);
+    return cudaGetLastError();
+}
+int blocks_vanka_march3(int n) {
+    const int MH = march_height(n, M3T, M3R, 4);
+    return ((n + M3T) / M3T) * ((n + MH) / MH);
 }
 
 int blocks_vanka_march(int n) {

@@ -37,6 +37,9 @@ int blocks_vanka_march(int n);
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march2(int n);
+cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
+                                bool x_zero, NormSink norm, cudaStream_t s);
+int blocks_vanka_march3(int n);
 // row-marching TMA variant of the fused residual + restriction (mode 1)
 cudaError_t launch_restrict_march(const LevelParams& Lf, int n_coarse, int pitch_coarse, const double* x_fine,
                                   const double* b_fine, double* b_coarse, cudaStream_t s);

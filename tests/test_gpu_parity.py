@@ -60,11 +60,16 @@ def test_residual(n, pname, het):
     _inactive_zero(H, rd)
 
 
-@pytest.mark.parametrize("n,pname,omega", [(4, "unit", 0.74), (8, "mixed", 0.9), (16, "stiff", 0.7),
-                                           (40, "cfg5", 0.7), (66, "unit", 0.74)])
-def test_vanka_sweep(n, pname, omega):
+@pytest.mark.parametrize("n,pname,omega,march", [(4, "unit", 0.74, False), (8, "mixed", 0.9, False),
+                                                 (16, "stiff", 0.7, False), (40, "cfg5", 0.7, False),
+                                                 (66, "unit", 0.74, False), (4, "unit", 0.74, True),
+                                                 (30, "mixed", 0.9, True), (57 * 2, "stiff", 0.7, True),
+                                                 (130, "cfg5", 0.7, True)])
+def test_vanka_sweep(n, pname, omega, march):
+    """One Vanka sweep; march=True runs the production row-marching TMA kernel on small grids
+    (ragged strips: n + 1 not a multiple of the strip width, several row segments)."""
     torch = _torch()
-    H = C.gpu_hierarchy(n, 1, pname)
+    H = C.gpu_hierarchy(n, 1, pname, march=march)
     from oracle.relax import Vanka
     op = C.operator(n, pname)
     V = Vanka(op)
@@ -175,18 +180,21 @@ def floor_parity(Oh, Oalt, b, xs_O, xs_alt, hO, hAlt):
     return F
 
 
-@pytest.mark.parametrize("n,levels,pname,relax,het,cycles", [
-    (16, 3, "unit", "vanka", None, 10),      # BASELINE config 1
-    (32, 4, "stiff", "vanka", None, 8),      # config 3 regime
-    (32, 4, "cfg5", "vanka", None, 8),       # config 5 regime
-    (32, 4, "unit", "bsr", None, 8),         # config 2 (BSR) regime
-    (32, 4, "unit", "bsr", 3, 6),            # config 4 regime (heterogeneous K)
+@pytest.mark.parametrize("n,levels,pname,relax,het,cycles,march", [
+    (16, 3, "unit", "vanka", None, 10, False),      # BASELINE config 1
+    (64, 5, "cfg5", "vanka", None, 6, True),        # config 5 regime, marching kernels on every level
+    (64, 5, "unit", "bsr", None, 4, True),          # marching restriction under BSR
+    (32, 4, "stiff", "vanka", None, 8, False),      # config 3 regime
+    (32, 4, "cfg5", "vanka", None, 8, False),       # config 5 regime
+    (32, 4, "unit", "bsr", None, 8, False),         # config 2 (BSR) regime
+    (32, 4, "unit", "bsr", 3, 6, False),            # config 4 regime (heterogeneous K)
+    (32, 4, "unit", "bsr", 3, 4, True),             # config 4 regime, marching restriction (K field)
 ])
-def test_cycle_history(n, levels, pname, relax, het, cycles):
+def test_cycle_history(n, levels, pname, relax, het, cycles, march):
     torch = _torch()
     from paper_2107_04060_b200 import Opts
     from oracle.cycle import Hierarchy as OH
-    H = C.gpu_hierarchy(n, levels, pname, het)
+    H = C.gpu_hierarchy(n, levels, pname, het, march=march)
     Oh = C.hierarchy(n, levels, pname, relax, het)
     lam, mu, K, tau, alpha, invM = C.PARAMS[pname]
     kinv = None if het is None else 1.0 / mg_inputs.lognormal_K(n, het)
