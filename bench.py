@@ -44,6 +44,23 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
+def max_over_ranks(value: float, dist=None) -> float:
+    """Max of a per-rank timing over all ranks (all_reduce MAX; CUDA tensor under NCCL, CPU under gloo)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(units_per_rank: float, steps: int, world: int, ms_max: float) -> float:
+    """Whole-job throughput: the units all ranks processed (independent replicas: weak scaling)
+    divided by the slowest rank's time."""
+    return units_per_rank * steps * world / (ms_max * 1e-3)
+
+
 def workload(cfg_id: int):
     c = dict(mg_inputs.CONFIGS[cfg_id])
     relax = "bsr" if c["relax"] == "bsr" else "vanka"
@@ -119,8 +136,10 @@ def peaks():
 
 
 def oracle_sample(c, cycles: int, warmup: int = 1, n_sample: int = 128):
-    """Time the oracle V(1,1) cycle on an n_sample^2 grid with the workload's parameters."""
+    """Time the oracle V(1,1) cycle on an n_sample^2 grid (the workload itself when smaller) with the
+    workload's parameters."""
     from oracle.cycle import Hierarchy as OH
+    n_sample = min(n_sample, c["n"])
     levels = max(2, int(np.log2(n_sample // 4)) + 1)
     kinv = None if c["K_seed"] is None else 1.0 / mg_inputs.lognormal_K(n_sample, c["K_seed"])
     H = OH(n_sample, levels, c["lam"], c["mu"], c["tau"], c["alpha"], c["inv_M"], c["mu_f"],
@@ -217,11 +236,7 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dist)
     res_norm = float(nrm.sqrt().item())
 
     # kernel-class timing of the same cycle (event-traced graph, separate pass)
@@ -270,14 +285,10 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         rc, hist = H.solve_host(xp, bp, o, rtol=0.0, max_cycles=args.steps)
-        el = time.perf_counter() - t0
-        if dist:
-            t = torch.tensor([el], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = max_over_ranks(time.perf_counter() - t0, dist)
         cyc = len(hist) - 1
         vbytes = 10 * (n + 1) * (n + 1) * 8
-        e2e = {"value": nact * cyc * world / el, "unit": "DoF/s", "h2d_bytes_per_step": 2 * vbytes / cyc,
+        e2e = {"value": aggregate_rate(nact, cyc, world, el * 1e3), "unit": "DoF/s", "h2d_bytes_per_step": 2 * vbytes / cyc,
                "d2h_bytes_per_step": (vbytes + 8 * (cyc + 1)) / cyc,
                "note": f"mg_solve_host of {cyc} cycles: pinned host b, x0 in; x, history out; bytes amortised per cycle"}
 
@@ -308,7 +319,7 @@ def main():
     ms_step = ms / args.steps
     line = {
         "metric": "DoF-updates/s per V(1,1) cycle (fp64) at 4096^2; ms per cycle; % of HBM roofline",
-        "value": nact * args.steps * world / (ms * 1e-3),
+        "value": aggregate_rate(nact, args.steps, world, ms),
         "unit": "DoF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step,
