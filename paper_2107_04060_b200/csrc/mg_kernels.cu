@@ -427,17 +427,25 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
 #define EC(dI, dJ, pl) __ldg(e0 + (pl) * planec + (dJ) * pitchc + (dI))
 #define MG_Q(dI, dJ, pl, w) v = fma(w, EC(dI, dJ, pl), v);
     const int fi = 2 * I, fj = 2 * J;
-    double* x0 = x + (int64_t)fj * pitchf + fi;
-#define PROL(di, dj, kf)                                                            \
-    {                                                                               \
-        double v = 0.0;                                                             \
-        MG_PROLONG_##di##_##dj##_##kf(MG_Q) if (is_active(kf, fi + di, fj + dj, nf)) \
-            x0[kf * planef + dj * pitchf + di] += v;                                \
+    double* x0 = x + (int64_t)fj * pitchf + fi;   // fi even, rows 256-B aligned: 16-B aligned pairs
+    // the two fine columns 2I, 2I+1 of a fine row move as one 16-byte load / store (a warp covers
+    // 512 contiguous bytes per instruction)
+#define PROL2(dj, kf)                                                                   \
+    {                                                                                   \
+        double v = 0.0;                                                                 \
+        MG_PROLONG_0_##dj##_##kf(MG_Q) const double v0 = v;                             \
+        v = 0.0;                                                                        \
+        MG_PROLONG_1_##dj##_##kf(MG_Q) const double v1 = v;                             \
+        double2* p2 = reinterpret_cast<double2*>(x0 + kf * planef + dj * pitchf);       \
+        double2 xv = *p2;                                                               \
+        if (is_active(kf, fi, fj + dj, nf)) xv.x += v0;                                 \
+        if (is_active(kf, fi + 1, fj + dj, nf)) xv.y += v1;                             \
+        *p2 = xv;                                                                       \
     }
-#define PROL4(kf) PROL(0, 0, kf) PROL(1, 0, kf) PROL(0, 1, kf) PROL(1, 1, kf)
+#define PROL4(kf) PROL2(0, kf) PROL2(1, kf)
     PROL4(0) PROL4(1) PROL4(2) PROL4(3) PROL4(4) PROL4(5) PROL4(6) PROL4(7) PROL4(8) PROL4(9)
 #undef PROL4
-#undef PROL
+#undef PROL2
 #undef MG_Q
 #undef EC
 }
