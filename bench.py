@@ -193,11 +193,14 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace-cycles", type=int, default=10)
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--n", type=int, default=0, help="experiment: override the grid size (levels keep n_c = 4)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     c = workload(args.config)
+    if args.n:
+        c["n"], c["levels"] = args.n, int(np.log2(args.n // 4)) + 1
     if args.impl == "reference":
         return run_reference(args, c, rank, world)
 
