@@ -104,6 +104,7 @@ struct mg_ctx {
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
+    int cgs_passes = 2;           // FGMRES Gram-Schmidt passes (MG_CGS_PASSES)
     cudaEvent_t ev[6] = {};
 };
 
@@ -344,6 +345,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_VANKA_IMPL")) c->vanka_impl = atoi(v);
     if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
     if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
+    if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
     auto bail = [&](int rc) {
         mg_free(c);
         return rc;
@@ -719,11 +721,15 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
             if (int rc = get_graph(c, c->kz[j], c->kv[j], *o, 3, nullptr, &ge)) return rc;
             CK(cudaGraphLaunch(ge, s));
             CK(launch_apply(LP, c->kz[j], c->kw, no_norm(), s));
-            // classical Gram-Schmidt, twice
+            // classical Gram-Schmidt, twice (the second pass only if c->cgs_passes == 2)
             if (int rc = dots(c->kw, c->kv, 0, j + 1, hd)) return rc;
             if (int rc = update(c->kw, c->kv, 0, j + 1, hd)) return rc;
-            if (int rc = dots(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
-            if (int rc = update(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
+            if (c->cgs_passes == 2) {
+                if (int rc = dots(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
+                if (int rc = update(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
+            } else {
+                CK(cudaMemsetAsync(hd + 64, 0, sizeof(double) * 64, s));
+            }
             std::vector<double*> wv{c->kw};
             if (int rc = dots(c->kw, wv, 0, 1, hd + 128)) return rc;
             CK(cudaMemcpyAsync(hcol.data(), hd, sizeof(double) * 129, cudaMemcpyDeviceToHost, s));
