@@ -301,9 +301,18 @@ def main():
         return
     peak, peak_src = peaks()
     relax_ms = (phases[0] + phases[4]) / 2.0
+    # levels whose first post-sweep absorbs the prolongation (marching Vanka levels, mg_api.cu
+    # fused_prolong): that sweep also reads the coarse iterate, 1/4 of a fine pass
+    march_min = int(os.environ.get("MG_MARCH_MIN_N", "512"))
+    fused = o.relax == "vanka" and os.environ.get("MG_FUSE_PROLONG", "1") != "0" and \
+        os.environ.get("MG_VANKA_IMPL", "2") == "2"
     if o.relax == "vanka":
-        alg_bytes = 24.0 * nact                 # read x, read b, write x over the active DoFs
-        dom = "vanka_kernel (level 0, fused residual + 20-DoF patch solves + update)"
+        # read x, read b, write x over the active DoFs; averaged over the pre-sweep and the post-sweep
+        # (which with the fused prolongation also reads e_H: + 8 B x N_1 ~ 2 B per fine DoF)
+        alg_bytes = (24.0 * nact + (24.0 * nact + 8.0 * mg_inputs.n_active(n >> 1) if fused and n >= march_min
+                                    else 24.0 * nact)) / 2.0
+        dom = ("vanka_march2_kernel (level 0: fused residual + 20-DoF patch solves + update; "
+               "mean of the pre-sweep and the post-sweep" + (" with the prolongation fused in)" if fused else ")"))
     else:
         alg_bytes = 8.0 * nact * 4.8 + 8.0 * 0.2 * nact   # 3 + 1.8 passes (+0.2 K field)
         dom = "BSR relaxation (level 0: bsr_a + 2 jacobi + bsr_b)"
@@ -316,9 +325,15 @@ def main():
             traffic = tj.get("dram_bytes_per_launch")
     except Exception:
         pass
-    sum_levels = sum(mg_inputs.n_active(n >> l) for l in range(L))
-    passes = 10.5 if o.relax == "vanka" else 14.7 if c["K_seed"] is not None else 14.1
-    cycle_bytes = 8.0 * passes * sum_levels
+    # algorithmic passes per level per V(1,1): Vanka 3 + 3 sweeps, 2.25 restriction,
+    # 2.25 prolongation (fused into the post-sweep: 0.25, the read of e_H); BSR 14.1 (14.7 with K field)
+    def level_passes(l):
+        if o.relax != "vanka":
+            return 14.7 if c["K_seed"] is not None else 14.1
+        if l == L - 1:
+            return 0.0 if L > 1 else 6.0
+        return 8.5 if fused and (n >> l) >= march_min else 10.5
+    cycle_bytes = 8.0 * sum(level_passes(l) * mg_inputs.n_active(n >> l) for l in range(L))
     ms_step = ms / args.steps
     line = {
         "metric": "DoF-updates/s per V(1,1) cycle (fp64) at 4096^2; ms per cycle; % of HBM roofline",

@@ -27,7 +27,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     deps.append(os.path.join(HERE, "..", "include", "mg.h"))
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
-    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB, *srcs, "-lcudart"]
+    extra = os.environ.get("MG_NVCC_EXTRA", "").split()   # diagnostics only (e.g. -DMG_PROL_NOOP)
+    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", LIB, *srcs, "-lcudart"]
     out = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if verbose or out.returncode != 0:
         sys.stderr.write(out.stdout + out.stderr)

@@ -104,6 +104,7 @@ struct mg_ctx {
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
+    int fuse_prolong = 1;         // 1: prolongation fused into the first post-sweep of marching Vanka levels
     int cgs_passes = 2;           // FGMRES Gram-Schmidt passes (MG_CGS_PASSES)
     cudaEvent_t ev[6] = {};
 };
@@ -138,13 +139,26 @@ int check_level(const mg_ctx* c, int level, int maxl) {
 
 NormSink no_norm() { return NormSink{nullptr, nullptr, nullptr, nullptr}; }
 
-// one relaxation sweep on level l: xin -> xout (out of place)
+// does the first post-sweep on level l absorb the prolongation (relax_once with e_coarse)?
+bool fused_prolong(const mg_ctx* c, int l, const mg_cycle_opts& o) {
+    return c->fuse_prolong && o.relax == MG_VANKA && o.nu2 >= 1 && c->vanka_impl == 2 &&
+           c->L[l].n >= c->march_min_n;
+}
+
+// one relaxation sweep on level l: xin -> xout (out of place).  e_coarse != nullptr (only where
+// fused_prolong): the sweep relaxes xin + P e_coarse, e_coarse being level l + 1's iterate.
 int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xout, bool xzero,
-               const mg_cycle_opts& o, NormSink S, cudaStream_t s) {
+               const mg_cycle_opts& o, NormSink S, cudaStream_t s, const double* e_coarse = nullptr) {
     Level& Lv = c->L[l];
     if (o.relax == MG_VANKA) {
         VankaParams P = Lv.vp;
         P.omega = o.omega;
+        if (e_coarse) {
+            const Level& Lc = c->L[l + 1];
+            const ProlSrc E{e_coarse, Lc.n, Lc.pitch, (int64_t)(Lc.n + 1) * Lc.pitch};
+            CK(launch_vanka_march2(P, xin, b, xout, false, S, s, &E));
+            return MG_OK;
+        }
         if (c->vanka_impl == 3 && Lv.n >= c->march_min_n) CK(launch_vanka_march3(P, xin, b, xout, xzero, S, s));
         else if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
         else if (c->vanka_impl == 1 && Lv.n >= c->march_min_n) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
@@ -221,7 +235,8 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         Level& Lv = c->L[l];
         if (l == 0)
             if (int rc = mark(3)) return rc;
-        CK(launch_prolong(Lv.n, Lv.pitch, c->L[l + 1].n, c->L[l + 1].pitch, cur[l + 1], cur[l], c->stop, s));
+        const bool fuse = fused_prolong(c, l, o);
+        if (!fuse) CK(launch_prolong(Lv.n, Lv.pitch, c->L[l + 1].n, c->L[l + 1].pitch, cur[l + 1], cur[l], c->stop, s));
         if (l == 0)
             if (int rc = mark(4)) return rc;
         if (int rc = lmark()) return rc;
@@ -230,7 +245,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         double* a = cur[l];
         double* t = (a == xl) ? Lv.t : xl;
         for (int k = 0; k < o.nu2; ++k) {
-            int rc = relax_once(c, l, a, bl, t, false, o, no_norm(), s);
+            int rc = relax_once(c, l, a, bl, t, false, o, no_norm(), s, fuse && k == 0 ? cur[l + 1] : nullptr);
             if (rc) return rc;
             std::swap(a, t);
         }
@@ -345,6 +360,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_VANKA_IMPL")) c->vanka_impl = atoi(v);
     if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
     if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
+    if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
     auto bail = [&](int rc) {
         mg_free(c);

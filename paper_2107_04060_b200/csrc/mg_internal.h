@@ -51,6 +51,12 @@ struct SolveState {
 // + block (9): bubble diffs (3), RT0 diffs (3), P0 sums (3)
 // - block (11): u_x, u_y, bubble sums (3), RT0 sums (3), P0 diffs (3)
 // with 1/2 folded into the rows of pair components.
+struct ProlSrc {                  // coarse iterate e_H for a sweep with fused prolongation
+    const double* e;
+    int nc, pitchc;
+    int64_t planec;
+};
+
 struct VankaParams {
     LevelParams L;
     double gpT[9][9];            // transposed: gpT[c][a] = G+[a][c] (column-outer FMA loops read pairs)

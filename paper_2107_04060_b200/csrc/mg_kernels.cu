@@ -34,6 +34,14 @@ __device__ __forceinline__ bool is_active(int p, int i, int j, int n) {
     }
 }
 
+// bit p set <=> is_active(p, i, j, n), for all ten planes at once
+__device__ __forceinline__ unsigned active_mask(int i, int j, int n) {
+    if (i < 0 || j < 0 || i > n || j > n) return 0u;
+    const bool ii = i > 0 && i < n, ij = j > 0 && j < n, li = i < n, lj = j < n;
+    return (ii && ij ? 0x003u : 0u) | (li && ij ? 0x024u : 0u) | (ii && lj ? 0x048u : 0u) |
+           (li && lj ? 0x390u : 0u);
+}
+
 template <int NT>
 __device__ __forceinline__ double block_sum(double v) {
     __shared__ double ws[NT / 32];
@@ -265,13 +273,25 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
             out[(15 + 2 * q) * os] = yp[6 + q] - ym[8 + q];
         }
     } else {
-        const double* G = P.gbnd + cls * 400;
+        // boundary class: dense 20 x 20 (row major in gbnd), four output rows per pass so four
+        // independent chains hide the load and fp64 latency (each output sums c = 0 .. 19 in order)
+        const double2* G = reinterpret_cast<const double2*>(P.gbnd + cls * 400);
 #pragma unroll 1
-        for (int a = 0; a < 20; ++a) {
-            double s = 0.0;
+        for (int a = 0; a < 20; a += 4) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-            for (int c = 0; c < 20; ++c) s = fma(__ldg(G + a * 20 + c), rr[c], s);
-            out[a * os] = s;
+            for (int c2 = 0; c2 < 10; ++c2) {
+                const double2 g0 = __ldg(G + (a + 0) * 10 + c2), g1 = __ldg(G + (a + 1) * 10 + c2);
+                const double2 g2 = __ldg(G + (a + 2) * 10 + c2), g3 = __ldg(G + (a + 3) * 10 + c2);
+                s0 = fma(g0.x, rr[2 * c2], s0); s0 = fma(g0.y, rr[2 * c2 + 1], s0);
+                s1 = fma(g1.x, rr[2 * c2], s1); s1 = fma(g1.y, rr[2 * c2 + 1], s1);
+                s2 = fma(g2.x, rr[2 * c2], s2); s2 = fma(g2.y, rr[2 * c2 + 1], s2);
+                s3 = fma(g3.x, rr[2 * c2], s3); s3 = fma(g3.y, rr[2 * c2 + 1], s3);
+            }
+            out[(a + 0) * os] = s0;
+            out[(a + 1) * os] = s1;
+            out[(a + 2) * os] = s2;
+            out[(a + 3) * os] = s3;
         }
     }
 }
@@ -888,6 +908,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// as mbar_wait, backing off between polls (a waiting warp then leaves the issue slots to others)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(64);
+    }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // 3-D TMA box load (dims: column, row, plane) completing on `bar`
 __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
     asm volatile(
@@ -1064,11 +1102,27 @@ constexpr int M2SMEM = (M2XR * M2ROW + M2BR * M2ROW + M2CR * 20 * M2C) * 8 + 64;
 static_assert(M2T + 2 <= 32 && M2R * 32 == M2NT, "one warp per row, one residual position per thread");
 static_assert(M2T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
 
-template <bool XZERO>
-__global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_constant__ CUtensorMap tmx,
+// register slot of the coarse value e_H(I + dI, J + dJ, pl) in the fused prolongation: planes 0-4
+// use 13 slots, planes 5-9 use 7 (the union over both fine-row parities of MG_PROLONG's operands)
+__host__ __device__ constexpr int pslot(int dI, int dJ, int pl) {
+    return pl >= 5 ? (dI == 0 && dJ == 0 ? pl - 5 : (dJ == 1 ? 5 : 6))
+                   : (dI == 0 && dJ == 0 ? pl : dI == 0 ? 5 + pl : dJ == 0 ? (pl == 3 ? 10 : 8 + pl) : 11 + pl);
+}
+static_assert(pslot(0, 1, 2) == 7 && pslot(1, 0, 3) == 10 && pslot(1, 1, 1) == 12 && pslot(1, 0, 6) == 6, "pslot");
+
+constexpr int M2NP = 2;   // producer warps of the fused-prolongation sweep (one per row parity of a group)
+__host__ __device__ constexpr int pslot20(int dI, int dJ, int pl) { return pl >= 5 ? 13 + pslot(dI, dJ, pl) : pslot(dI, dJ, pl); }
+
+// PROL: the sweep relaxes x + P e_H instead of x (the coarse-grid correction of the V-cycle fused
+// into the first post-smoothing sweep): every x row is corrected in the ring right
+// after its TMA box lands, with the same arithmetic as prolong_kernel (v = sum of w e_H in table
+// order, x + v), so the result is bitwise that of prolong_kernel followed by the sweep, and x + P e_H
+// never goes through HBM.
+template <bool XZERO, bool PROL>
+__global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march2_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                const __grid_constant__ CUtensorMap tmb,
                                                                const VankaParams P, double* __restrict__ xo,
-                                                               NormSink S, int MH) {
+                                                               NormSink S, int MH, const ProlSrc E) {
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                        // [M2XR][10][M2W]
     double* br = xr + M2XR * M2ROW;         // [M2BR][10][M2W]   b, overwritten by r
@@ -1076,6 +1130,11 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
     uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M2CR * 20 * M2C);
     const LevelParams& L = P.L;
     if (*L.stop) return;
+    // barrier of the four compute warps (the PROL producer warp never joins it)
+    auto csync = [&]() {
+        if (PROL) asm volatile("bar.sync 1, %0;" ::"n"(M2NT) : "memory");
+        else __syncthreads();
+    };
     const int n = L.n;
     const int i0 = blockIdx.x * M2T, j0 = blockIdx.y * MH;
     const int rows = min(MH, n + 1 - j0);
@@ -1093,23 +1152,114 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
         const int nx = XZERO ? 0 : (g < 0 ? M2R + 2 : M2R);
         mbar_expect_tx(bar, (nx + M2R) * M2ROW * 8);
         const int xfirst = g < 0 ? j0 - M2R : j0 + g * M2R + 2;
+#pragma unroll 1
         for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * M2ROW, &tmx, i0 - 2, xfirst + k, 0, bar);
         const int bfirst = j0 + g * M2R + 1;
+#pragma unroll 1
         for (int k = 0; k < M2R; ++k) tma_load3(br + sb(bfirst + k) * M2ROW, &tmb, i0 - 2, bfirst + k, 0, bar);
     };
     if (t == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], M2NP);
+        mbar_init(&bars[3], M2NP);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // PROL: a fifth warp (the producer) corrects the x rows of group g (x += P e_H) as soon as their
+    // TMA boxes land -- during step g - 1 of the four compute warps -- and arrives on ready[g]; the
+    // compute warps wait on ready[] instead of the TMA barrier, so the prolongation runs on issue
+    // slots the latency-bound sweep leaves idle.  Lanes 0-15 take the column pairs (2I, 2I+1) of row
+    // y, lanes 16-31 those of row y + 2 (same parity: the table branch is warp uniform).
+    // producer task k of a group part (y0, count): lanes 0-15 row y0 + k, lanes 16-31 row y0 + k + 2,
+    // column pair (2I, 2I+1); pe[k][] holds the 20 coarse values of the task (pslot20)
+    auto prol_task = [&](int y0, int count, int k, int& y, int& I, int& J) {
+        const int lane = t & 31;
+        const int rsel = k + 2 * (lane >> 4);
+        y = y0 + rsel;
+        I = (i0 >> 1) - 1 + (lane & 15);
+        J = y >> 1;
+        return rsel < count && I >= 0 && I < E.nc && J >= 0 && J < E.nc;
+    };
+    // producer warp k (= M2NT / 32 + k) takes task k of every group part
+    const int kp = (t >> 5) - M2NT / 32;
+    auto prol_load = [&](int y0, int count, double (&pe)[20]) {
+        {
+            const int k = kp;
+            int y, I, J;
+            if (!prol_task(y0, count, k, y, I, J)) return;
+            const double* e0 = E.e + (int64_t)J * E.pitchc + I;
+#define PL(dI, dJ, pl) pe[pslot20(dI, dJ, pl)] = __ldg(e0 + (pl) * E.planec + (dJ) * E.pitchc + (dI));
+            PL(0, 0, 0) PL(0, 0, 1) PL(0, 0, 2) PL(0, 0, 3) PL(0, 0, 4) PL(0, 1, 0) PL(0, 1, 1)
+            PL(0, 1, 2) PL(1, 0, 0) PL(1, 0, 1) PL(1, 0, 3) PL(1, 1, 0) PL(1, 1, 1)
+            PL(0, 0, 5) PL(0, 0, 6) PL(0, 0, 7) PL(0, 0, 8) PL(0, 0, 9) PL(0, 1, 5) PL(1, 0, 6)
+#undef PL
+        }
+    };
+    auto prol_apply = [&](int y0, int count, const double (&pe)[20]) {
+#ifdef MG_PROL_NOOP
+        return;   // diagnostic build: the pipeline without the arithmetic (wrong results)
+#endif
+        {
+            const int k = kp;
+            int y, I, J;
+            if (!prol_task(y0, count, k, y, I, J)) return;
+            double* xrow = xr + sx(y) * M2ROW + 2 * (t & 15);
+            const int fi = 2 * I;
+            const unsigned m0 = active_mask(fi, y, n), m1 = active_mask(fi + 1, y, n);
+#define PQ(dI, dJ, pl, wt) v = fma(wt, pe[pslot20(dI, dJ, pl)], v);
+#define PX(dj, kf)                                                                    \
+    {                                                                                 \
+        double v = 0.0;                                                               \
+        MG_PROLONG_0_##dj##_##kf(PQ) const double v0 = v;                             \
+        v = 0.0;                                                                      \
+        MG_PROLONG_1_##dj##_##kf(PQ) double2* x2 = reinterpret_cast<double2*>(xrow + (kf) * M2W); \
+        double2 xv = *x2;                                                             \
+        if (m0 & (1u << (kf))) xv.x += v0;                                            \
+        if (m1 & (1u << (kf))) xv.y += v;                                             \
+        *x2 = xv;                                                                     \
+    }
+            if (y & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
+            else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+#undef PX
+#undef PQ
+        }
+    };
+    uint64_t* ready = bars + 2;
+    if (PROL && t >= M2NT) {
+        // ---- producer warp: the coarse values of a group are loaded before its TMA boxes are
+        // awaited, so their latency overlaps the wait
+        double pe[20];
+        auto publish = [&](int g) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // ring slots are refilled by TMA later
+            __syncwarp();
+            if ((t & 31) == 0) mbar_arrive(&ready[(g + 1) & 1]);
+        };
+        mbar_wait_sleep(&bars[0], 0);
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {   // group -1: rows j0 - R .. j0 + 1
+            prol_load(part ? j0 : j0 - M2R, part ? 2 : M2R, pe);
+            prol_apply(part ? j0 : j0 - M2R, part ? 2 : M2R, pe);
+        }
+        publish(-1);
+#pragma unroll 1
+        for (int g = 0; g < nsteps; ++g) {
+            prol_load(j0 + g * M2R + 2, M2R, pe);
+            mbar_wait_sleep(&bars[(g + 1) & 1], ((g + 1) >> 1) & 1);
+            prol_apply(j0 + g * M2R + 2, M2R, pe);
+            publish(g);
+        }
+        if (S.out || S.state) norm_finish<M2NT + 32 * M2NP>(S, 0.0);
+        return;
+    }
     if (t == 0) {
         issue(-1);
         issue(0);
     }
     double nrm = 0.0;
     for (int s = -1; s < nsteps; ++s) {
-        mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
+        // TMA group s landed (and, PROL, its x rows were corrected by the producer warp)
+        mbar_wait(PROL ? &ready[(s + 1) & 1] : &bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
         // ---- residual rows y = j0 + s R + 1 + q
         // one warp per row (lanes beyond the row idle): no bank conflicts from rows wrapping in a warp
         if ((t & 31) < M2T + 2) {
@@ -1137,7 +1287,7 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
                 for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
             }
         }
-        __syncthreads();
+        csync();
         // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
         if ((t & 31) < M2C) {
             const int q = t >> 5, px = t & 31;
@@ -1162,7 +1312,7 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
                 for (int k = 0; k < 20; ++k) out[k * M2C] = 0.0;
             }
         }
-        __syncthreads();
+        csync();
         // ---- owners y = j0 + s R + q: patch rows y and y + 1
         if (s >= 0 && (t & 31) < M2T) {
             const int q = t >> 5, lx = t & 31;
@@ -1192,13 +1342,13 @@ __global__ void __launch_bounds__(M2NT, 3) vanka_march2_kernel(const __grid_cons
                 }
             }
         }
-        __syncthreads();
+        csync();
         if (t == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(s + 2);
         }
     }
-    if (S.out || S.state) norm_finish<M2NT>(S, nrm);
+    if (S.out || S.state) norm_finish<PROL ? M2NT + 32 * M2NP : M2NT>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1523,8 +1673,9 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
 void kernels_init() {
     set_smem(vanka_march3_kernel<false>, M3SMEM);
     set_smem(vanka_march3_kernel<true>, M3SMEM);
-    set_smem(vanka_march2_kernel<false>, M2SMEM);
-    set_smem(vanka_march2_kernel<true>, M2SMEM);
+    set_smem(vanka_march2_kernel<false, false>, M2SMEM);
+    set_smem(vanka_march2_kernel<true, false>, M2SMEM);
+    set_smem(vanka_march2_kernel<false, true>, M2SMEM);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
     set_smem(restrict_march_kernel<true>, Q_SMEM);
     set_smem(vanka_march_kernel<false>, M_SMEM);
@@ -1696,7 +1847,7 @@ cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const doub
     return cudaGetLastError();
 }
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
-                                NormSink S, cudaStream_t s) {
+                                NormSink S, cudaStream_t s, const ProlSrc* E) {
     const LevelParams& L = P.L;
     CUtensorMap mx, mb;
     cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, M2W, 1);
@@ -1707,8 +1858,11 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     // (measured: 2048^2 sweep 0.45 -> 0.37 ms, 4096^2 1.24 -> 1.19 ms against ~128-row segments)
     const int MH = march_height(L.n, M2T, M2R, 3, std::max(32, L.n / 64));
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
-    if (x_zero) vanka_march2_kernel<true><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH);
-    else vanka_march2_kernel<false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH);
+    const ProlSrc none{nullptr, 0, 0, 0};
+    if (E && x_zero) return cudaErrorInvalidValue;
+    if (x_zero) vanka_march2_kernel<true, false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH, none);
+    else if (E) vanka_march2_kernel<false, true><<<grid, M2NT + 32 * M2NP, M2SMEM, s>>>(mx, mb, P, xo, S, MH, *E);
+    else vanka_march2_kernel<false, false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH, none);
     return cudaGetLastError();
 }
 int blocks_vanka_march2(int n) {

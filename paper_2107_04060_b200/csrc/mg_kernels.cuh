@@ -34,8 +34,9 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
 cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const double* b, double* xout,
                                bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march(int n);
+// E != nullptr: relax x + P e_H (prolongation of the coarse iterate E->e fused into the sweep)
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
-                                bool x_zero, NormSink norm, cudaStream_t s);
+                                bool x_zero, NormSink norm, cudaStream_t s, const ProlSrc* E = nullptr);
 int blocks_vanka_march2(int n);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);

@@ -38,19 +38,23 @@ def hierarchy(n, levels, pname, relax, het_seed=None):
     return OHierarchy(n, levels, lam, mu, tau, alpha, invM, 1.0, K=K, Kinv_field=kinv, relax=relax)
 
 
-def gpu_hierarchy(n, levels, pname, het_seed=None, march=False):
+def gpu_hierarchy(n, levels, pname, het_seed=None, march=False, env=None):
     """march=True forces the row-marching TMA kernels (production path of the levels with n >= 512)
-    on every level, so that small parity cases exercise them (MG_MARCH_MIN_N is read by mg_setup)."""
+    on every level, so that small parity cases exercise them (MG_MARCH_MIN_N is read by mg_setup);
+    env: further MG_* knobs read at setup (e.g. MG_FUSE_PROLONG)."""
     import os
     from paper_2107_04060_b200 import Hierarchy
+    knobs = dict(env or {})
     if march:
-        os.environ["MG_MARCH_MIN_N"] = "0"
+        knobs["MG_MARCH_MIN_N"] = "0"
+    os.environ.update(knobs)
     lam, mu, K, tau, alpha, invM = PARAMS[pname]
     kf = None if het_seed is None else mg_inputs.lognormal_K(n, het_seed)
     try:
         return Hierarchy(n, levels, lam, mu, K=K, tau=tau, alpha=alpha, inv_M=invM, mu_f=1.0, K_field=kf)
     finally:
-        os.environ.pop("MG_MARCH_MIN_N", None)
+        for k in knobs:
+            os.environ.pop(k, None)
 
 
 def abs_matvec(op, x):

@@ -230,6 +230,25 @@ def test_cycle_history(n, levels, pname, relax, het, cycles, march):
     assert np.all(np.abs(rG - rO)[ok] <= 1e-3)
 
 
+@pytest.mark.parametrize("n,levels,pname,nu2", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (64, 3, "stiff", 1)])
+def test_fused_prolong_bitwise(n, levels, pname, nu2):
+    """The prolongation fused into the first post-sweep of the marching kernel
+    gives bitwise the iterates of prolong_kernel followed by the sweep (same arithmetic, same
+    order), over several cycles and with a second, unfused post-sweep (nu2 = 2)."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    b = mg_inputs.uniform_rhs(n, 3)
+    out = []
+    for fuse in ("1", "0"):
+        H = C.gpu_hierarchy(n, levels, pname, march=True, env={"MG_FUSE_PROLONG": fuse})
+        xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+        hist = [H.cycle(xd, bd, Opts(1, nu2, "vanka", 0.7)) for _ in range(3)]
+        out.append((H.to_host(xd), hist))
+        H.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 def test_solve_matches_cycles():
     """mg_solve (device-side stop flag, fused norms) reproduces the cycle-by-cycle history and stops at rtol."""
     torch = _torch()
