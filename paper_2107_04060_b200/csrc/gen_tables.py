@@ -345,6 +345,76 @@ def emit(path):
             if e < len(per_row[k]):
                 il.append(per_row[k][e])
     w("#define MG_STENCIL_INTERLEAVED(X) " + " ".join(il))
+    # factored form.  Every merged coefficient is a linear combination of the material terms
+    # (mu, lambda, alpha h, tau h, h^2 / M) with weights fixed by the reference integrals
+    # (elem_entry in mg_setup.cpp).  Coefficients with a zero weight vector vanish for every
+    # material (dropped); coefficients with equal weight vectors up to sign share one value cg[g].
+    # Row k then reads sum_g (+-cg[g]) * (sum of +-x over the entries of group g): one FMA per
+    # group and one add per further entry instead of one FMA (and coefficient load) per entry.
+    def wvec(lst):
+        v = np.zeros(5)
+        for (sh, q, q2) in lst:
+            a, b = block(q), block(q2)
+            if (a, b) == ("u", "u"):
+                v[0] += 2.0 * snap(E[sh]["Aeps"][q][q2])
+                v[1] += 2.0 * snap(E[sh]["Bu"][q]) * snap(E[sh]["Bu"][q2])
+            elif (a, b) == ("u", "p"):
+                v[2] += snap(E[sh]["Bu"][q])
+            elif (a, b) == ("p", "u"):
+                v[2] += snap(E[sh]["Bu"][q2])
+            elif (a, b) == ("w", "p"):
+                v[3] += snap(E[sh]["Bw"][q - 9])
+            elif (a, b) == ("p", "w"):
+                v[3] += snap(E[sh]["Bw"][q2 - 9])
+            elif (a, b) == ("p", "p"):
+                v[4] -= snap(E[sh]["Mp"])
+        v[np.abs(v) < 1e-12] = 0.0
+        return v
+    groups = []          # [weight vector (first nonzero > 0), representative coef index, its sign]
+    fact_rows = [[] for _ in range(10)]   # per row: list of (g, [(dx, dy, pl, sign)])
+    ci = 0
+    for k, r in enumerate(rows):
+        order = []
+        terms = {}
+        for (col, lst) in r["entries"]:
+            v = wvec(lst)
+            if np.any(v != 0.0):
+                lead = v[np.nonzero(v)[0][0]]
+                sg = 1 if lead > 0 else -1
+                vn = v * sg
+                g = next((gi for gi, (gv, _, _) in enumerate(groups) if np.allclose(gv, vn, rtol=1e-12, atol=0)), None)
+                if g is None:
+                    g = len(groups)
+                    groups.append((vn, ci, sg))
+                if g not in terms:
+                    terms[g] = []
+                    order.append(g)
+                terms[g].append((col[0], col[1], col[2], sg))
+            ci += 1
+        fact_rows[k] = [(g, terms[g]) for g in order]
+    w("// factored stencil: A(row, g, sign, expr) adds sign cg[g] * expr to row; XS(dx, dy, plane) is")
+    w("// supplied by the user (rows interleaved round-robin: independent accumulator chains)")
+    w("#define MG_STENCIL_NGROUP %d" % len(groups))
+    w("// cg[g] = sign * coef[ci] for R(g, ci, sign)")
+    w("#define MG_STENCIL_GROUP_REP(R) " + " ".join("R(%d,%d,%d)" % (g, rep, sg) for g, (_, rep, sg) in enumerate(groups)))
+    fitems = [[] for _ in range(10)]
+    for k in range(10):
+        for g, lst in fact_rows[k]:
+            if all(t[3] < 0 for t in lst):
+                msign, lst2 = "-", [(a, b, c, -d) for (a, b, c, d) in lst]
+            else:
+                msign, lst2 = "+", sorted(lst, key=lambda t: -t[3])   # a positive entry first
+            expr = ""
+            for j, (dx, dy, pl, sg) in enumerate(lst2):
+                op = "" if j == 0 else (" + " if sg > 0 else " - ")
+                expr += op + "XS(%d,%d,%d)" % (dx, dy, pl)
+            fitems[k].append("A(%d,%d,%s,(%s))" % (k, g, msign, expr))
+    fil = []
+    for e in range(max(len(x) for x in fitems)):
+        for k in range(10):
+            if e < len(fitems[k]):
+                fil.append(fitems[k][e])
+    w("#define MG_STENCIL_FACT(A) " + " ".join(fil))
     w("// coefficient contributions: Y(coef_index, shape, q, q') -- coef = sum of element entries")
     w("#define MG_STENCIL_CONTRIB(Y) " + " ".join("Y(%d,%d,%d,%d)" % c for c in contribs))
     w("// M_w part of the RT0 rows, per triangle: W(row, cell_dx, cell_dy, shape, dx, dy, plane, e, e')")

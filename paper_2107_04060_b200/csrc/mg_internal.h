@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #define MG_NCOEF 141      // merged stencil coefficients (mg_tables.h MG_STENCIL_NCOEF)
+#define MG_NGROUP 17      // distinct coefficients of the factored stencil (mg_tables.h MG_STENCIL_NGROUP)
 #define MG_PSLOTS 20      // Vanka patch slots
 #define MG_USLOTS 8       // displacement patch slots (BSR)
 #define MG_NCLASS 9       // vertex classes: cx + 3 cy, cx = 0 interior, 1 at i = 0, 2 at i = n
@@ -24,6 +25,7 @@ struct LevelParams {
     int32_t n, pitch;
     int64_t plane;               // (n+1) * pitch
     double coef[MG_NCOEF];       // merged stencil of A^RQ without M_w (mg_tables.h order)
+    double cg[MG_NGROUP];        // factored stencil: cg[g] = coef[representative of group g]
     double ww[2][3][3];          // tau mu_f h^2 (M_w1)_{shape,e,e'}; multiplied by K^{-1}_T
     double kinv;                 // scalar K^{-1} (used when kinv_field == nullptr)
     const double* kinv_field;    // 2 planes [shape][j][i] with row pitch `pitch`, or nullptr

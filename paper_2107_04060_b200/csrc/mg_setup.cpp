@@ -280,6 +280,10 @@ int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, i
 #define Y(ci, s, q, q2) L.coef[ci] += elem_entry(s, q, q2, m, h, kinv);
     MG_STENCIL_CONTRIB(Y)
 #undef Y
+    static_assert(MG_STENCIL_NGROUP == MG_NGROUP, "factored stencil size");
+#define R(g, ci, sg) L.cg[g] = (sg) * L.coef[ci];
+    MG_STENCIL_GROUP_REP(R)
+#undef R
     for (int s = 0; s < 2; ++s)
         for (int e = 0; e < 3; ++e) {
             for (int e2 = 0; e2 < 3; ++e2) L.ww[s][e][e2] = m.tau * m.mu_f * h * h * REF_MW1[s][e][e2];

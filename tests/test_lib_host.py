@@ -232,3 +232,36 @@ def test_host_patch_inverses_equal_oracle(lib, params):
         mine = t["vanka"][cls]
         err = np.abs(mine - ref).max() / np.abs(ref).max()
         assert err < 1e-9, (cls, err)
+
+
+@pytest.mark.parametrize("params", [(64, 100.0, 1.0, 1e-2, 1.0, 1.0, 1.0), (37, 2.5, 0.7, 0.3, 0.8, 1.3, 0.05),
+                                    (100, 1e6, 1.3, 1e-6, 2.0, 0.3, 7.0)])
+def test_factored_stencil_equals_merged(lib, params):
+    """MG_STENCIL_FACT (the form the kernels evaluate) reproduces every merged stencil entry
+    coef[ci] of MG_STENCIL_ROW_k: entries it drops are exactly zero for this material, the others
+    equal +-cg[g] = +-coef[representative] to rounding (eq. block_form_rq)."""
+    from paper_2107_04060_b200.mg import host_level_tables
+    hdr = open(os.path.join(ROOT, "paper_2107_04060_b200", "csrc", "mg_tables.h")).read()
+    coef = host_level_tables(*params)["coef"]
+    merged = {}
+    for k in range(10):
+        body = re.search(r"#define MG_STENCIL_ROW_%d\(X\)(.*)" % k, hdr).group(1)
+        for (row, dx, dy, pl, ci) in re.findall(r"X\((\d+),(-?\d+),(-?\d+),(\d+),(\d+)\)", body):
+            merged[(int(row), int(dx), int(dy), int(pl))] = coef[int(ci)]
+    rep = {int(g): (int(ci), int(sg)) for g, ci, sg in re.findall(
+        r"R\((\d+),(\d+),(-?\d+)\)", re.search(r"#define MG_STENCIL_GROUP_REP\(R\)(.*)", hdr).group(1))}
+    fact = {}
+    body = re.search(r"#define MG_STENCIL_FACT\(A\)(.*)", hdr).group(1)
+    for row, g, ms, expr in re.findall(r"A\((\d+),(\d+),([+-]),\(([^()]*(?:\([^()]*\)[^()]*)*)\)\)", body):
+        cg = rep[int(g)][1] * coef[rep[int(g)][0]] * (1.0 if ms == "+" else -1.0)
+        for sgn, dx, dy, pl in re.findall(r"([+-]?)\s*XS\((-?\d+),(-?\d+),(\d+)\)", expr):
+            key = (int(row), int(dx), int(dy), int(pl))
+            assert key not in fact
+            fact[key] = cg * (-1.0 if sgn == "-" else 1.0)
+    scale = np.abs(coef).max()
+    assert set(fact) <= set(merged)
+    assert len(fact) == 113 and len(merged) == 141
+    for key, v in merged.items():
+        assert abs(fact.get(key, 0.0) - v) <= 1e-13 * scale, (key, v, fact.get(key))
+        if key not in fact:
+            assert v == 0.0
