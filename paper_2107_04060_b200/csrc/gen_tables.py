@@ -442,7 +442,9 @@ def emit(path):
         w("#define MG_PROLONG_%d_%d_%d(Q) %s" % (di, dj, kf, items))
     # restriction entries of planes 0-4 and 5-9, interleaved round-robin over the planes:
     # U(kc, cell_dI, cell_dJ, di, dj, kf, weight)
-    for name, planes in (("LO", range(0, 5)), ("HI", range(5, 10))):
+    # LO / HI: planes 0-4 / 5-9; G0-G3: four groups of ~23 entries each (one warp per group)
+    for name, planes in (("LO", range(0, 5)), ("HI", range(5, 10)), ("G0", (0, 8)), ("G1", (1, 9)),
+                         ("G2", (2, 3, 4)), ("G3", (5, 6, 7))):
         lists = []
         for kc in planes:
             lst = []

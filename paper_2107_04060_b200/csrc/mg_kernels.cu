@@ -1504,6 +1504,11 @@ __global__ void __launch_bounds__(M3NT, 4) vanka_march3_kernel(const __grid_cons
 }
 
 // ------------------------------------------------------------------------------------------
+// accumulator slot of coarse plane kc within its restriction group (MG_RESTRICT_G0..G3)
+__host__ __device__ constexpr int rslot(int kc) {
+    return kc >= 8 ? 1 : (kc <= 1 ? 0 : (kc <= 4 ? kc - 2 : kc - 5));
+}
+
 // Row-marching fused residual + restriction b_H = P^T (b - A x) with TMA row chunks.
 // A CTA owns coarse columns [I0, I0+QT) and coarse rows [J0, J0+MH); step s produces coarse rows
 // J0 + s QR .. J0 + (s+1) QR - 1 from the fine residual rows 2(J0 + s QR) - 2 .. 2(J0 + s QR) + 2QR - 1,
@@ -1580,9 +1585,11 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
         }
         __syncthreads();
         // coarse rows J = J0 + s QR + q: fine rows 2J - 2 .. 2J + 1 = rows 2q - 2 .. 2q + 1 of this step
-        // (negative: the carried rows of b/r chunk s).  Warps: (q, plane half) uniform.
+        // (negative: the carried rows of b/r chunk s).  Warp w takes coarse plane group w
+        // (MG_RESTRICT_G0..G3: planes {0,8}, {1,9}, {2,3,4}, {5,6,7}, ~23 entries each); lanes 0-14
+        // coarse row q = 0, lanes 16-30 row q = 1.
         if (s >= 0) {
-            const int q = (t >> 5) & 1, half = t >> 6, cx = t & 31;
+            const int grp = t >> 5, q = (t >> 4) & 1, cx = t & 15;
             const int I = I0 + cx, J = J0 + s * QR + q;
             if (cx < QT && I <= nc && J < J0 + crow) {
                 const double* cur = br + bslot * Q_BCH + (2 * cx + 2);
@@ -1591,24 +1598,16 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
                 // row pointer for fine-row offset f = 2q - 2cdJ + dj in [-2, 3]
 #define ROWP(f) ((f) < 0 ? car + (QF + (f)) * Q_RW : cur + (f) * Q_RW)
 #define RF(cdI, cdJ, di, dj, kf) ROWP(2 * q - 2 * (cdJ) + (dj))[(kf) * (QF * Q_RW) - 2 * (cdI) + (di)]
-#define MG_T(cdI, cdJ, di, dj, kf, w) acc = fma(w, RF(cdI, cdJ, di, dj, kf), acc);
-                // planes 0-4 or 5-9, their entries interleaved (5 independent chains)
-                double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#define MG_U0(kc, cdI, cdJ, di, dj, kf, w) acc[kc] = fma(w, RF(cdI, cdJ, di, dj, kf), acc[kc]);
-#define MG_U5(kc, cdI, cdJ, di, dj, kf, w) acc[(kc) - 5] = fma(w, RF(cdI, cdJ, di, dj, kf), acc[(kc) - 5]);
-                if (half == 0) {
-                    MG_RESTRICT_IL_LO(MG_U0)
-                } else {
-                    MG_RESTRICT_IL_HI(MG_U5)
+                double acc[3] = {0.0, 0.0, 0.0};
+#define MG_UG(kc, cdI, cdJ, di, dj, kf, w) acc[rslot(kc)] = fma(w, RF(cdI, cdJ, di, dj, kf), acc[rslot(kc)]);
+                auto put = [&](int k, double v) { bc[k * planec + o] = is_active(k, I, J, nc) ? v : 0.0; };
+                switch (grp) {
+                    case 0: MG_RESTRICT_IL_G0(MG_UG) put(0, acc[0]); put(8, acc[1]); break;
+                    case 1: MG_RESTRICT_IL_G1(MG_UG) put(1, acc[0]); put(9, acc[1]); break;
+                    case 2: MG_RESTRICT_IL_G2(MG_UG) put(2, acc[0]); put(3, acc[1]); put(4, acc[2]); break;
+                    default: MG_RESTRICT_IL_G3(MG_UG) put(5, acc[0]); put(6, acc[1]); put(7, acc[2]); break;
                 }
-#undef MG_U0
-#undef MG_U5
-#pragma unroll
-                for (int kk = 0; kk < 5; ++kk) {
-                    const int k = 5 * half + kk;
-                    bc[k * planec + o] = is_active(k, I, J, nc) ? acc[kk] : 0.0;
-                }
-#undef MG_T
+#undef MG_UG
 #undef RF
 #undef ROWP
             }
