@@ -151,6 +151,28 @@ __device__ __forceinline__ void apply_rows(const LevelParams& L, const double* x
     av[5] = a5; av[6] = a6; av[7] = a7; av[8] = a8; av[9] = a9;
 }
 
+// apply_rows with K^{-1} of the per-triangle M_w terms read from a shared-memory ring instead of
+// global memory (marching kernels, heterogeneous K): km / k0 point at cell (i, j-1) / (i, j) of
+// plane LL, plane UR is KPS doubles further (cells outside the mesh hold 0, like kinv_at)
+template <int PS, int KPS>
+__device__ __forceinline__ void apply_rows_kr(const LevelParams& L, const double* xm, const double* x0,
+                                              const double* xp, const double* km, const double* k0, double av[10]) {
+#define XS(dx, dy, pl) ((dy) < 0 ? xm : ((dy) > 0 ? xp : x0))[(pl) * PS + (dx)]
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0, a8 = 0, a9 = 0;
+#define MG_A(row, g, sg, e) a##row = fma(sg L.cg[g], e, a##row);
+    MG_STENCIL_FACT(MG_A)
+#undef MG_A
+#define MG_W(row, cdx, cdy, sh, dx, dy, pl, e, e2) \
+    a##row = fma(L.ww[sh][e][e2] * ((cdy) < 0 ? km : k0)[(sh) * KPS + (cdx)], XS(dx, dy, pl), a##row);
+    MG_STENCIL_WW_5(MG_W)
+    MG_STENCIL_WW_6(MG_W)
+    MG_STENCIL_WW_7(MG_W)
+#undef MG_W
+#undef XS
+    av[0] = a0; av[1] = a1; av[2] = a2; av[3] = a3; av[4] = a4;
+    av[5] = a5; av[6] = a6; av[7] = a7; av[8] = a8; av[9] = a9;
+}
+
 // r = b - A x for the 10 DoFs of index (i, j); xs is a W x HT x 10 tile holding (i, j) at
 // (lx, ly) with a ring of at least 1.  Inactive rows give 0.
 template <int W, int HT, bool HET>
@@ -1621,6 +1643,383 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Row-marching inexact Braess-Sarazin relaxation, the structure of
+// vanka_march2_kernel: 128 threads, one warp per row, 4 rows per step, single-row TMA rings
+// (x, b / r, and for a K field the two K^{-1} planes) refilled one step ahead, 3 CTAs / SM.
+//
+// Stage A (bsr_a_march_kernel): r = b - A x, z_u = F_u^{-1} r_u (8-DoF displacement patches),
+// g = alpha B_u z_u + tau B_w (tau D_w)^{-1} r_w - r_p and the first Jacobi sweep dp = omega_J g /
+// diag(S) on the cells of a strip of BQ_T columns.  Step s computes the residual and patch rows
+// j0 + sR + 2 .. + 5, the z_u rows j0 + sR + 1 .. + 4 and the g / dp cell rows j0 + sR .. + 3
+// (lower rows carried from step s - 1).  Stage B (bsr_b_march_kernel): r again, y_u = r_u -
+// alpha B_u^T dp, du = F_u^{-1} y_u, dw = (r_w - tau B_w^T dp) / (tau D_w), x + omega (du, dw, dp),
+// rows as in vanka_march2_kernel (dp and K^{-1} arrive as 2-plane TMA rows).
+constexpr int BQ_R = 4, BQ_NT = 128, BQ_W = 32, BQ_ROW = 10 * BQ_W, BQ_KROW = 2 * BQ_W;
+constexpr int BMA_T = 26;                              // stage A: owned cells / strip (x box i0-2 .. i0+29)
+constexpr int BMA_XR = 10, BMA_BR = 10, BMA_KR = 11, BMA_PR = 5, BMA_ZR = 5;
+constexpr int BMA_PC = BMA_T + 2, BMA_ZC = BMA_T + 1;     // patch vertices i0 .. i0+27, z_u i0 .. i0+26
+constexpr int BMA_SMEM = (BMA_XR * BQ_ROW + BMA_BR * BQ_ROW + BMA_KR * BQ_KROW + BMA_PR * 8 * BMA_PC + BMA_ZR * 5 * BMA_ZC) * 8 + 64;
+constexpr int BB_T = 28;                              // stage B: owned indices / strip
+constexpr int BB2_XR = 10, BB2_BR = 9, BB2_DR = 10, BB2_PR = 5, BB2_PC = BB_T + 1;
+constexpr int BB2_SMEM = (BB2_XR * BQ_ROW + BB2_BR * BQ_ROW + 2 * BB2_DR * BQ_KROW + BB2_PR * 8 * BB2_PC) * 8 + 64;
+static_assert(3 * (BMA_SMEM + 1024) <= 228 * 1024 && 3 * (BB2_SMEM + 1024) <= 228 * 1024, "three CTAs per SM");
+static_assert(BMA_T % 2 == 0 && BB_T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
+
+// 8-DoF displacement-patch residuals of vertex (a, b) from two r rows (r0: row b, rm: row b - 1,
+// both at the vertex column): gather8's slot order
+#define MG_GATHER8(rr, r0, rm, PS)                                                                  \
+    rr[0] = (r0)[0 * (PS)];  rr[1] = (r0)[1 * (PS)];                                                \
+    rr[2] = (r0)[2 * (PS)];  rr[3] = (r0)[2 * (PS) - 1]; rr[4] = (r0)[3 * (PS)]; rr[5] = (rm)[3 * (PS)]; \
+    rr[6] = (r0)[4 * (PS) - 1]; rr[7] = (rm)[4 * (PS)];
+
+template <bool HET, bool XZERO>
+__global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const __grid_constant__ CUtensorMap tmb,
+                                                               const __grid_constant__ CUtensorMap tmk,
+                                                               const LevelParams L, const DispParams U, double omJ,
+                                                               double* __restrict__ g, double* __restrict__ dp,
+                                                               NormSink S, int MH) {
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;                          // [BMA_XR][10][32]
+    double* br = xr + BMA_XR * BQ_ROW;         // [BMA_BR][10][32]  b, overwritten by r
+    double* kr = br + BMA_BR * BQ_ROW;         // [BMA_KR][2][32]   K^{-1} (HET)
+    double* pr = kr + BMA_KR * BQ_KROW;        // [BMA_PR][8][BMA_PC] displacement patch outputs
+    double* zr = pr + BMA_PR * 8 * BMA_PC;      // [BMA_ZR][5][BMA_ZC] z_u
+    uint64_t* bars = reinterpret_cast<uint64_t*>(zr + BMA_ZR * 5 * BMA_ZC);
+    if (*L.stop) return;
+    const int n = L.n;
+    const int i0 = blockIdx.x * BMA_T, j0 = blockIdx.y * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int nsteps = (rows + BQ_R - 1) / BQ_R;
+    const int t = threadIdx.x;
+    auto sx = [&](int y) { return (y - j0 + 2 * BQ_R) % BMA_XR; };
+    auto sb = [&](int y) { return (y - j0 + 2 * BQ_R) % BMA_BR; };
+    auto sk = [&](int y) { return (y - j0 + 2 * BQ_R) % BMA_KR; };
+    auto sp = [&](int y) { return (y - j0 + 2 * BQ_R) % BMA_PR; };
+    auto sz = [&](int y) { return (y - j0 + 2 * BQ_R) % BMA_ZR; };
+    // group g: x rows j0+gR+3 .. +6 (g = -1: j0-3 .. j0+2), b rows j0+gR+2 .. +5, K rows j0+gR+2 .. +5
+    // (g = -1: j0-3 .. j0+1)
+    auto issue = [&](int g) {
+        if (g >= nsteps) return;
+        uint64_t* bar = &bars[(g + 1) & 1];
+        const int nx = XZERO ? 0 : (g < 0 ? 6 : BQ_R);
+        const int nk = HET ? (g < 0 ? 5 : BQ_R) : 0;
+        mbar_expect_tx(bar, ((nx + BQ_R) * BQ_ROW + nk * BQ_KROW) * 8);
+        const int xfirst = g < 0 ? j0 - 3 : j0 + g * BQ_R + 3;
+#pragma unroll 1
+        for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * BQ_ROW, &tmx, i0 - 2, xfirst + k, 0, bar);
+#pragma unroll 1
+        for (int k = 0; k < BQ_R; ++k) {
+            const int y = j0 + g * BQ_R + 2 + k;
+            tma_load3(br + sb(y) * BQ_ROW, &tmb, i0 - 2, y, 0, bar);
+        }
+        const int kfirst = g < 0 ? j0 - 3 : j0 + g * BQ_R + 2;
+#pragma unroll 1
+        for (int k = 0; k < nk; ++k) tma_load3(kr + sk(kfirst + k) * BQ_KROW, &tmk, i0 - 2, kfirst + k, 0, bar);
+    };
+    // K^{-1} of triangle sh of cell (ci, cj) (0 outside the mesh: TMA zero fill / zeroed pyramid)
+    auto kinv = [&](int ci, int cj, int sh) -> double {
+        if (!HET) return L.kinv;
+        return kr[sk(cj) * BQ_KROW + sh * BQ_W + (ci - (i0 - 2))];
+    };
+    auto Dw = [&](int k, int i, int j) -> double {   // D_w of the RT0 DoF of plane k at index (i, j)
+        double d = 0.0;
+#define MG_I(kk, cdx, cdy, sh, q) d = fma(L.mw1d[sh][(q) - 9], kinv(i + (cdx), j + (cdy), sh), d);
+        if (k == 5) { MG_INCIDENT_5(MG_I) }
+        else if (k == 6) { MG_INCIDENT_6(MG_I) }
+        else { MG_INCIDENT_7(MG_I) }
+#undef MG_I
+        return d;
+    };
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue(-1);
+        issue(0);
+    }
+    const int64_t plane = L.plane;
+    double nrm = 0.0;
+    for (int s = -1; s < nsteps; ++s) {
+        mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
+        const int q = t >> 5, lane = t & 31;
+        // ---- residual rows y = j0 + sR + 2 + q at columns i0-1 .. i0+27
+        if (lane < BMA_T + 3) {
+            const int y = j0 + s * BQ_R + 2 + q, i = i0 - 1 + lane;
+            double* bp = br + sb(y) * BQ_ROW + (lane + 1);
+            double rv[10];
+            if (!XZERO) {
+                const double* xm = xr + sx(y - 1) * BQ_ROW + (lane + 1);
+                const double* x0 = xr + sx(y) * BQ_ROW + (lane + 1);
+                const double* xp = xr + sx(y + 1) * BQ_ROW + (lane + 1);
+                double av[10];
+                if (HET) apply_rows_kr<BQ_W, BQ_W>(L, xm, x0, xp, kr + sk(y - 1) * BQ_KROW + (lane + 1),
+                                                   kr + sk(y) * BQ_KROW + (lane + 1), av);
+                else apply_rows<BQ_W, false>(L, xm, x0, xp, i, y, av);
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, y, n) ? bp[k * BQ_W] - av[k] : 0.0;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) bp[k * BQ_W] = rv[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) rv[k] = bp[k * BQ_W];
+            }
+            if (lane >= 1 && lane <= BMA_T && i <= n && y >= j0 && y < j0 + rows) {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+            }
+        }
+        __syncthreads();
+        // ---- displacement patches at vertex rows bb = j0 + sR + 2 + q, vertices i0 .. i0+27
+        if (lane < BMA_PC) {
+            const int a = i0 + lane, bb = j0 + s * BQ_R + 2 + q;
+            double* out = pr + sp(bb) * (8 * BMA_PC) + lane;
+            if (a <= n && bb >= 0 && bb <= n) {
+                const double* r0 = br + sb(bb) * BQ_ROW + (lane + 2);
+                const double* rm = br + sb(bb - 1) * BQ_ROW + (lane + 2);
+                double rr[8];
+                MG_GATHER8(rr, r0, rm, BQ_W)
+                patch_apply8(U, vertex_class(a, bb, n), rr, out, BMA_PC);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) out[k * BMA_PC] = 0.0;
+            }
+        }
+        __syncthreads();
+        // ---- z_u rows y = j0 + sR + 1 + q at columns i0 .. i0+26 (patch rows y, y + 1)
+        if (lane < BMA_ZC) {
+            const int y = j0 + s * BQ_R + 1 + q;
+            const double* c0 = pr + sp(y) * (8 * BMA_PC) + lane;
+            const double* c1 = pr + sp(y + 1) * (8 * BMA_PC) + lane;
+            double* zo = zr + sz(y) * (5 * BMA_ZC) + lane;
+#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * BMA_PC + (dx)]
+            zo[0 * BMA_ZC] = CC(0, 0, 0);
+            zo[1 * BMA_ZC] = CC(1, 0, 0);
+            zo[2 * BMA_ZC] = CC(2, 0, 0) + CC(3, 1, 0);
+            zo[3 * BMA_ZC] = CC(4, 0, 0) + CC(5, 0, 1);
+            zo[4 * BMA_ZC] = CC(6, 1, 0) + CC(7, 0, 1);
+#undef CC
+        }
+        __syncthreads();
+        // ---- g and the first Jacobi sweep on the cells of rows y = j0 + sR + q, columns i0 .. i0+25
+        if (s >= 0 && lane < BMA_T) {
+            const int y = j0 + s * BQ_R + q, i = i0 + lane;
+            if (i <= n && y < j0 + rows) {
+                const int64_t o = (int64_t)y * L.pitch + i;
+                if (i < n && y < n) {
+                    const double* z0 = zr + sz(y) * (5 * BMA_ZC) + lane;
+                    const double* z1 = zr + sz(y + 1) * (5 * BMA_ZC) + lane;
+                    const double* r0 = br + sb(y) * BQ_ROW + (lane + 2);
+                    const double* r1 = br + sb(y + 1) * BQ_ROW + (lane + 2);
+#pragma unroll
+                    for (int sh = 0; sh < 2; ++sh) {
+                        double dw[3];
+                        bool act[3];
+                        if (sh == 0) { dw[0] = Dw(5, i, y); dw[1] = Dw(6, i, y); }
+                        else { dw[0] = Dw(5, i, y + 1); dw[1] = Dw(6, i + 1, y); }
+                        dw[2] = Dw(7, i, y);
+                        tri_edges_active(sh, i, y, n, act);
+                        double gu = 0.0, gw = 0.0, ds = L.s0h2;
+#define MG_L(s_, q_, dx, dy, pl)                                                                  \
+    if ((s_) == sh) {                                                                             \
+        if ((q_) < 9) gu = fma(L.bu[s_][(q_) < 9 ? (q_) : 0], ((dy) ? z1 : z0)[(pl) * BMA_ZC + (dx)], gu); \
+        else if ((q_) < 12) {                                                                     \
+            const int e = (q_) < 12 ? (q_) - 9 : 0;                                               \
+            if (act[e]) {                                                                         \
+                const double rw = ((dy) ? r1 : r0)[(pl) * BQ_W + (dx)];                           \
+                gw = fma(L.bw[s_][e], rw / (L.tau * dw[e]), gw);                                  \
+                ds += L.tau * L.bw[s_][e] * L.bw[s_][e] / dw[e];                                  \
+            }                                                                                     \
+        }                                                                                         \
+    }
+                        MG_LOCAL_0(MG_L)
+                        MG_LOCAL_1(MG_L)
+#undef MG_L
+                        const double rp = r0[(8 + sh) * BQ_W];
+                        const double gv = L.alpha * gu + L.tau * gw - rp;
+                        g[sh * plane + o] = gv;
+                        dp[sh * plane + o] = omJ * gv / ds;
+                    }
+                } else {
+                    g[o] = 0.0;
+                    g[plane + o] = 0.0;
+                    dp[o] = 0.0;
+                    dp[plane + o] = 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s + 2);
+        }
+    }
+    if (S.out || S.state) norm_finish<BQ_NT>(S, nrm);
+}
+
+template <bool HET, bool XZERO>
+__global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const __grid_constant__ CUtensorMap tmb,
+                                                               const __grid_constant__ CUtensorMap tmd,
+                                                               const __grid_constant__ CUtensorMap tmk,
+                                                               const LevelParams L, const DispParams U, double omega,
+                                                               double* __restrict__ xo, int MH) {
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;                          // [BB2_XR][10][32]
+    double* br = xr + BB2_XR * BQ_ROW;        // [BB2_BR][10][32]  b, overwritten by (y_u, r_w)
+    double* dr = br + BB2_BR * BQ_ROW;        // [BB2_DR][2][32]   dp
+    double* kr = dr + BB2_DR * BQ_KROW;       // [BB2_DR][2][32]   K^{-1} (HET)
+    double* pr = kr + BB2_DR * BQ_KROW;       // [BB2_PR][8][BB2_PC]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(pr + BB2_PR * 8 * BB2_PC);
+    if (*L.stop) return;
+    const int n = L.n;
+    const int i0 = blockIdx.x * BB_T, j0 = blockIdx.y * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int nsteps = (rows + BQ_R - 1) / BQ_R;
+    const int t = threadIdx.x;
+    auto sx = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_XR; };
+    auto sb = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_BR; };
+    auto sd = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_DR; };
+    auto sp = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_PR; };
+    // group g: x rows j0+gR+2 .. +5 (g = -1: j0-R .. j0+1), b rows j0+gR+1 .. +4, dp and K rows
+    // j0+gR+1 .. +4 (g = -1: j0-4 .. j0)
+    auto issue = [&](int g) {
+        if (g >= nsteps) return;
+        uint64_t* bar = &bars[(g + 1) & 1];
+        const int nx = XZERO ? 0 : (g < 0 ? BQ_R + 2 : BQ_R);
+        const int nd = g < 0 ? 5 : BQ_R;
+        mbar_expect_tx(bar, ((nx + BQ_R) * BQ_ROW + (HET ? 2 : 1) * nd * BQ_KROW) * 8);
+        const int xfirst = g < 0 ? j0 - BQ_R : j0 + g * BQ_R + 2;
+#pragma unroll 1
+        for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * BQ_ROW, &tmx, i0 - 2, xfirst + k, 0, bar);
+#pragma unroll 1
+        for (int k = 0; k < BQ_R; ++k) {
+            const int y = j0 + g * BQ_R + 1 + k;
+            tma_load3(br + sb(y) * BQ_ROW, &tmb, i0 - 2, y, 0, bar);
+        }
+        const int dfirst = g < 0 ? j0 - 4 : j0 + g * BQ_R + 1;
+#pragma unroll 1
+        for (int k = 0; k < nd; ++k) {
+            tma_load3(dr + sd(dfirst + k) * BQ_KROW, &tmd, i0 - 2, dfirst + k, 0, bar);
+            if (HET) tma_load3(kr + sd(dfirst + k) * BQ_KROW, &tmk, i0 - 2, dfirst + k, 0, bar);
+        }
+    };
+    auto kinv = [&](int ci, int cj, int sh) -> double {
+        if (!HET) return L.kinv;
+        return kr[sd(cj) * BQ_KROW + sh * BQ_W + (ci - (i0 - 2))];
+    };
+    auto dpc = [&](int ci, int cj, int sh) -> double { return dr[sd(cj) * BQ_KROW + sh * BQ_W + (ci - (i0 - 2))]; };
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue(-1);
+        issue(0);
+    }
+    for (int s = -1; s < nsteps; ++s) {
+        mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
+        const int q = t >> 5, lane = t & 31;
+        // ---- rows y = j0 + sR + 1 + q at columns i0-1 .. i0+28: r, then y_u = r_u - alpha B_u^T dp
+        if (lane < BB_T + 2) {
+            const int y = j0 + s * BQ_R + 1 + q, i = i0 - 1 + lane;
+            double* bp = br + sb(y) * BQ_ROW + (lane + 1);
+            double rv[8];
+            if (!XZERO) {
+                const double* xm = xr + sx(y - 1) * BQ_ROW + (lane + 1);
+                const double* x0 = xr + sx(y) * BQ_ROW + (lane + 1);
+                const double* xp = xr + sx(y + 1) * BQ_ROW + (lane + 1);
+                double av[10];
+                if (HET) apply_rows_kr<BQ_W, BQ_W>(L, xm, x0, xp, kr + sd(y - 1) * BQ_KROW + (lane + 1),
+                                                   kr + sd(y) * BQ_KROW + (lane + 1), av);
+                else apply_rows<BQ_W, false>(L, xm, x0, xp, i, y, av);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) rv[k] = is_active(k, i, y, n) ? bp[k * BQ_W] - av[k] : 0.0;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) rv[k] = bp[k * BQ_W];
+            }
+            double bt[5] = {0, 0, 0, 0, 0};
+#define MG_I(k, cdx, cdy, sh, qq) bt[k] = fma(L.bu[sh][qq], dpc(i + (cdx), y + (cdy), sh), bt[k]);
+            MG_INCIDENT_0(MG_I) MG_INCIDENT_1(MG_I) MG_INCIDENT_2(MG_I) MG_INCIDENT_3(MG_I) MG_INCIDENT_4(MG_I)
+#undef MG_I
+#pragma unroll
+            for (int k = 0; k < 5; ++k) bp[k * BQ_W] = is_active(k, i, y, n) ? rv[k] - L.alpha * bt[k] : rv[k];
+#pragma unroll
+            for (int k = 5; k < 8; ++k) bp[k * BQ_W] = rv[k];
+        }
+        __syncthreads();
+        // ---- displacement patches at vertex rows bb = j0 + sR + 1 + q, vertices i0 .. i0+28
+        if (lane < BB2_PC) {
+            const int a = i0 + lane, bb = j0 + s * BQ_R + 1 + q;
+            double* out = pr + sp(bb) * (8 * BB2_PC) + lane;
+            if (a <= n && bb >= 0 && bb <= n) {
+                const double* r0 = br + sb(bb) * BQ_ROW + (lane + 2);
+                const double* rm = br + sb(bb - 1) * BQ_ROW + (lane + 2);
+                double rr[8];
+                MG_GATHER8(rr, r0, rm, BQ_W)
+                patch_apply8(U, vertex_class(a, bb, n), rr, out, BB2_PC);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) out[k * BB2_PC] = 0.0;
+            }
+        }
+        __syncthreads();
+        // ---- owners y = j0 + sR + q: x + omega (du, dw, dp)
+        if (s >= 0 && lane < BB_T) {
+            const int y = j0 + s * BQ_R + q, i = i0 + lane;
+            if (i <= n && y < j0 + rows) {
+                const double* c0 = pr + sp(y) * (8 * BB2_PC) + lane;
+                const double* c1 = pr + sp(y + 1) * (8 * BB2_PC) + lane;
+#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * BB2_PC + (dx)]
+                double d[10];
+                d[0] = CC(0, 0, 0);
+                d[1] = CC(1, 0, 0);
+                d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+                d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+                d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+#undef CC
+                double bw[3] = {0, 0, 0};
+#define MG_I(k, cdx, cdy, sh, qq) bw[(k) - 5] = fma(L.bw[sh][(qq) - 9], dpc(i + (cdx), y + (cdy), sh), bw[(k) - 5]);
+                MG_INCIDENT_5(MG_I) MG_INCIDENT_6(MG_I) MG_INCIDENT_7(MG_I)
+#undef MG_I
+                const double* rw = br + sb(y) * BQ_ROW + (lane + 2);
+#pragma unroll
+                for (int k = 5; k < 8; ++k) {
+                    double dwk = 0.0;
+#define MG_I(kk, cdx, cdy, sh, qq) dwk = fma(L.mw1d[sh][(qq) - 9], kinv(i + (cdx), y + (cdy), sh), dwk);
+                    if (k == 5) { MG_INCIDENT_5(MG_I) }
+                    else if (k == 6) { MG_INCIDENT_6(MG_I) }
+                    else { MG_INCIDENT_7(MG_I) }
+#undef MG_I
+                    d[k] = is_active(k, i, y, n) ? (rw[k * BQ_W] - L.tau * bw[k - 5]) / (L.tau * dwk) : 0.0;
+                }
+                d[8] = dpc(i, y, 0);
+                d[9] = dpc(i, y, 1);
+                const double* xv = xr + sx(y) * BQ_ROW + (lane + 2);
+                const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) {
+                    const double xk = XZERO ? 0.0 : xv[k * BQ_W];
+                    xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(omega, d[k], xk) : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s + 2);
+        }
+    }
+}
+#undef MG_GATHER8
+
 // Rows marched by one CTA.  All CTAs of a marching launch carry equal work, so the number of row
 // segments per strip is chosen to make the launch an (almost) whole number of waves of resident
 // CTAs (SMs x CTAs per SM), with segments of about `target` rows: a fractional last wave left ~35% of
@@ -1654,7 +2053,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 static EncodeTiledFn g_encode = nullptr;
 
 static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int pitch, int64_t plane, int boxw,
-                                  int boxh) {
+                                  int boxh, int planes = 10) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -1662,9 +2061,9 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
         if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
         g_encode = reinterpret_cast<EncodeTiledFn>(fn);
     }
-    cuuint64_t dims[3] = {(cuuint64_t)(n + 1), (cuuint64_t)(n + 1), 10};
+    cuuint64_t dims[3] = {(cuuint64_t)(n + 1), (cuuint64_t)(n + 1), (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)plane * 8};
-    cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, 10};
+    cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, (cuuint32_t)planes};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1678,6 +2077,14 @@ void kernels_init() {
     set_smem(vanka_march2_kernel<false, false>, M2SMEM);
     set_smem(vanka_march2_kernel<true, false>, M2SMEM);
     set_smem(vanka_march2_kernel<false, true>, M2SMEM);
+    set_smem(bsr_a_march_kernel<false, false>, BMA_SMEM);
+    set_smem(bsr_a_march_kernel<false, true>, BMA_SMEM);
+    set_smem(bsr_a_march_kernel<true, false>, BMA_SMEM);
+    set_smem(bsr_a_march_kernel<true, true>, BMA_SMEM);
+    set_smem(bsr_b_march_kernel<false, false>, BB2_SMEM);
+    set_smem(bsr_b_march_kernel<false, true>, BB2_SMEM);
+    set_smem(bsr_b_march_kernel<true, false>, BB2_SMEM);
+    set_smem(bsr_b_march_kernel<true, true>, BB2_SMEM);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
     set_smem(restrict_march_kernel<true>, Q_SMEM);
     set_smem(vanka_march_kernel<false>, M_SMEM);
@@ -1892,6 +2299,45 @@ int blocks_vanka_march3(int n) {
 int blocks_vanka_march(int n) {
     const int MH = march_height(n, MT, MR, 2);
     return ((n + MT) / MT) * ((n + MH) / MH);
+}
+
+cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
+                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s) {
+    CUtensorMap mx, mb, mk;
+    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, BQ_W, 1);
+    if (e == cudaSuccess) e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, BQ_W, 1);
+    const bool het = L.kinv_field != nullptr;
+    if (e == cudaSuccess) e = encode_vec_map(&mk, het ? L.kinv_field : b, L.n, L.pitch, L.plane, BQ_W, 1, 2);
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(L.n, BMA_T, BQ_R, 3, std::max(32, L.n / 64));
+    dim3 grid((L.n + BMA_T) / BMA_T, (L.n + MH) / MH);
+#define BA_LAUNCH(H_, Z_) bsr_a_march_kernel<H_, Z_><<<grid, BQ_NT, BMA_SMEM, s>>>(mx, mb, mk, L, U, omJ, g, dp, S, MH)
+    if (het && x_zero) BA_LAUNCH(true, true);
+    else if (het) BA_LAUNCH(true, false);
+    else if (x_zero) BA_LAUNCH(false, true);
+    else BA_LAUNCH(false, false);
+#undef BA_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double omega, const double* x,
+                               const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s) {
+    CUtensorMap mx, mb, md, mk;
+    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, BQ_W, 1);
+    if (e == cudaSuccess) e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, BQ_W, 1);
+    if (e == cudaSuccess) e = encode_vec_map(&md, dp, L.n, L.pitch, L.plane, BQ_W, 1, 2);
+    const bool het = L.kinv_field != nullptr;
+    if (e == cudaSuccess) e = encode_vec_map(&mk, het ? L.kinv_field : dp, L.n, L.pitch, L.plane, BQ_W, 1, 2);
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(L.n, BB_T, BQ_R, 3, std::max(32, L.n / 64));
+    dim3 grid((L.n + BB_T) / BB_T, (L.n + MH) / MH);
+#define BB_LAUNCH(H_, Z_) bsr_b_march_kernel<H_, Z_><<<grid, BQ_NT, BB2_SMEM, s>>>(mx, mb, md, mk, L, U, omega, xo, MH)
+    if (het && x_zero) BB_LAUNCH(true, true);
+    else if (het) BB_LAUNCH(true, false);
+    else if (x_zero) BB_LAUNCH(false, true);
+    else BB_LAUNCH(false, false);
+#undef BB_LAUNCH
+    return cudaGetLastError();
 }
 
 cudaError_t launch_restrict_march(const LevelParams& Lf, int nc, int pitchc, const double* x, const double* b,

@@ -41,6 +41,11 @@ int blocks_vanka_march2(int n);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march3(int n);
+// row-marching TMA variants of the two BSR stages (same arithmetic as launch_bsr_a / launch_bsr_b)
+cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
+                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s);
+cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double omega, const double* x,
+                               const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s);
 // row-marching TMA variant of the fused residual + restriction (mode 1)
 cudaError_t launch_restrict_march(const LevelParams& Lf, int n_coarse, int pitch_coarse, const double* x_fine,
                                   const double* b_fine, double* b_coarse, cudaStream_t s);

@@ -137,12 +137,17 @@ def test_coarse_solve(nc, pname, het):
     assert np.linalg.norm(res) <= 1e-12 * (np.linalg.norm(mc.to_active(b)) + np.linalg.norm(C.abs_matvec(opc, xG)))
 
 
-@pytest.mark.parametrize("n,pname,het,nJ", [(8, "unit", None, 1), (16, "mixed", None, 3), (40, "unit", None, 3),
-                                            (16, "unit", 3, 3), (34, "mixed", 9, 2)])
-def test_bsr_sweep(n, pname, het, nJ):
+@pytest.mark.parametrize("n,pname,het,nJ,march", [(8, "unit", None, 1, False), (16, "mixed", None, 3, False),
+                                                  (40, "unit", None, 3, False), (16, "unit", 3, 3, False),
+                                                  (34, "mixed", 9, 2, False), (16, "mixed", None, 3, True),
+                                                  (40, "unit", None, 3, True), (16, "unit", 3, 3, True),
+                                                  (34, "mixed", 9, 2, True), (58, "stiff", 5, 3, True)])
+def test_bsr_sweep(n, pname, het, nJ, march):
+    """One BSR sweep vs the oracle; march=True runs the row-marching TMA stages (production path of
+    the levels with n >= 512) on small grids, strips and segments included."""
     torch = _torch()
     from oracle.relax import BSR
-    H = C.gpu_hierarchy(n, 1, pname, het)
+    H = C.gpu_hierarchy(n, 1, pname, het, march=march)
     op = C.operator(n, pname, het)
     S = BSR(op)
     m = C.mesh(n)
