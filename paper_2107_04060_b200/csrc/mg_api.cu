@@ -104,6 +104,8 @@ struct mg_ctx {
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
+    int jacobi_pair = 0;          // 1: two Jacobi sweeps per launch (bsr_jacobi2_kernel; measured slower:
+                                  //    292 us vs 2 x 110 us at 2048^2, the per-tile halo work dominates)
     int bsr_impl = 1;             // 1: row-marching BSR stages on levels with n >= march_min_n, 0: 2-D tiles
     int fuse_prolong = 1;         // 1: prolongation fused into the first post-sweep of marching Vanka levels
     int cgs_passes = 2;           // FGMRES Gram-Schmidt passes (MG_CGS_PASSES)
@@ -172,8 +174,14 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     else CK(launch_bsr_a(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s));
     double* cur = Lv.dpa;
     double* nxt = Lv.dpb;
-    for (int k = 1; k < o.jacobi_sweeps; ++k) {
-        CK(launch_bsr_jacobi(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
+    for (int k = 1; k < o.jacobi_sweeps;) {
+        if (c->jacobi_pair && k + 1 < o.jacobi_sweeps) {
+            CK(launch_bsr_jacobi2(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
+            k += 2;
+        } else {
+            CK(launch_bsr_jacobi(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
+            k += 1;
+        }
         std::swap(cur, nxt);
     }
     if (march) CK(launch_bsr_b_march(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
@@ -366,6 +374,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
     if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_BSR_IMPL")) c->bsr_impl = atoi(v);
+    if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v) != 0;
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
     auto bail = [&](int rc) {
         mg_free(c);

@@ -771,6 +771,112 @@ __global__ void __launch_bounds__(256) bsr_jacobi_kernel(const LevelParams L, do
     }
 }
 
+// Two Jacobi sweeps on S dp = g in one pass.  Per tile: dp0 on the tile + 2 rings of
+// cells, K^{-1} on the tile + 2 (low) / 3 (high) rings, g and the intermediate dp1 on the tile + 1
+// ring.  The edge factors tau / D_w(e) and 1 / diag(S) are formed once per tile (one division per
+// edge and per triangle) and shared by both sweeps.
+constexpr int JT_X = 32, JT_Y = 8, JNT = 256;
+constexpr int J0W = JT_X + 4, J0H = JT_Y + 4, J1W = JT_X + 2, J1H = JT_Y + 2;
+constexpr int JKW = JT_X + 5, JKH = JT_Y + 5, JEW = JT_X + 3, JEH = JT_Y + 3;
+
+template <bool HET>
+__global__ void __launch_bounds__(JNT) bsr_jacobi2_kernel(const LevelParams L, double omJ,
+                                                          const double* __restrict__ g,
+                                                          const double* __restrict__ dpi, double* __restrict__ dpo) {
+    __shared__ double d0[2][J0H][J0W];                            // cells [i0-2, i0+34) x [j0-2, j0+10)
+    __shared__ double kk[HET ? 2 : 1][HET ? JKH : 1][HET ? JKW : 1];   // cells [i0-2, i0+35) x [j0-2, j0+11)
+    __shared__ double tw[3][JEH][JEW];                            // tau / D_w of edges H, V, D at [i0-1, i0+34) x [j0-1, j0+10)
+    __shared__ double gg[2][J1H][J1W];                            // cells [i0-1, i0+33) x [j0-1, j0+9)
+    __shared__ double dsg[2][J1H][J1W];                           // diag(S)
+    __shared__ double ids[2][J1H][J1W];                           // 1 / diag(S)
+    __shared__ double d1[2][J1H][J1W];
+    if (*L.stop) return;
+    const int n = L.n;
+    const int64_t plane = L.plane, pitch = L.pitch;
+    const int i0 = blockIdx.x * JT_X, j0 = blockIdx.y * JT_Y;
+    auto inmesh = [&](int ci, int cj) { return ci >= 0 && cj >= 0 && ci < n && cj < n; };
+    for (int t = threadIdx.x; t < 2 * J0H * J0W; t += JNT) {
+        const int sh = t / (J0H * J0W), rem = t - sh * (J0H * J0W), ly = rem / J0W, lx = rem - ly * J0W;
+        const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
+        d0[sh][ly][lx] = inmesh(ci, cj) ? __ldg(dpi + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+    }
+    if (HET)
+        for (int t = threadIdx.x; t < 2 * JKH * JKW; t += JNT) {
+            const int sh = t / (JKH * JKW), rem = t - sh * (JKH * JKW), ly = rem / JKW, lx = rem - ly * JKW;
+            const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
+            kk[sh][ly][lx] = inmesh(ci, cj) ? __ldg(L.kinv_field + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+        }
+    for (int t = threadIdx.x; t < 2 * J1H * J1W; t += JNT) {
+        const int sh = t / (J1H * J1W), rem = t - sh * (J1H * J1W), ly = rem / J1W, lx = rem - ly * J1W;
+        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
+        gg[sh][ly][lx] = inmesh(ci, cj) ? __ldg(g + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+    }
+    __syncthreads();
+    auto kinv = [&](int ci, int cj, int sh) -> double {
+        if (!HET) return L.kinv;
+        return kk[sh][cj - (j0 - 2)][ci - (i0 - 2)];
+    };
+    // tau / D_w of the edges owned by index (ci, cj) (planes 5, 6, 7 -> H, V, D); 0 if inactive
+    for (int t = threadIdx.x; t < 3 * JEH * JEW; t += JNT) {
+        const int e = t / (JEH * JEW), rem = t - e * (JEH * JEW), ly = rem / JEW, lx = rem - ly * JEW;
+        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
+        double d = 0.0;
+#define MG_I(kk_, cdx, cdy, sh, q) d = fma(L.mw1d[sh][(q) - 9], kinv(ci + (cdx), cj + (cdy), sh), d);
+        if (e == 0) { MG_INCIDENT_5(MG_I) }
+        else if (e == 1) { MG_INCIDENT_6(MG_I) }
+        else { MG_INCIDENT_7(MG_I) }
+#undef MG_I
+        tw[e][ly][lx] = is_active(5 + e, ci, cj, n) ? L.tau / d : 0.0;
+    }
+    __syncthreads();
+    // edge factor of local edge e of triangle sh in cell (i, j): LL -> H(i,j), V(i,j), D(i,j);
+    // UR -> H(i,j+1), V(i+1,j), D(i,j)
+    auto tew = [&](int i, int j, int sh, int e) -> double {
+        const int ci = sh == 0 ? i : (e == 1 ? i + 1 : i), cj = sh == 0 ? j : (e == 0 ? j + 1 : j);
+        return tw[e][cj - (j0 - 1)][ci - (i0 - 1)];
+    };
+    for (int t = threadIdx.x; t < 2 * J1H * J1W; t += JNT) {
+        const int sh = t / (J1H * J1W), rem = t - sh * (J1H * J1W), ly = rem / J1W, lx = rem - ly * J1W;
+        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
+        double ds = L.s0h2;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) ds += tew(ci, cj, sh, e) * L.bw[sh][e] * L.bw[sh][e];
+        dsg[sh][ly][lx] = ds;
+        ids[sh][ly][lx] = inmesh(ci, cj) ? 1.0 / ds : 0.0;
+    }
+    __syncthreads();
+    // one Jacobi update of triangle sh of cell (i, j) (in the mesh) from dp values src(ci, cj, sh)
+    auto jac = [&](int i, int j, int sh, int ly, int lx, auto src) -> double {
+        const double dself = src(i, j, sh);
+        double off = 0.0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const double c = tew(i, j, sh, e) * L.bw[sh][e];   // 0 for an inactive edge
+            int ni, nj;
+            if (sh == 0) { ni = e == 1 ? i - 1 : i; nj = e == 0 ? j - 1 : j; }
+            else         { ni = e == 1 ? i + 1 : i; nj = e == 0 ? j + 1 : j; }
+            off = fma(c * L.bw[1 - sh][e], src(ni, nj, 1 - sh), off);
+        }
+        const double sd = fma(dsg[sh][ly][lx], dself, off);
+        return dself + omJ * (gg[sh][ly][lx] - sd) * ids[sh][ly][lx];
+    };
+    auto s0 = [&](int ci, int cj, int sh) { return d0[sh][cj - (j0 - 2)][ci - (i0 - 2)]; };
+    auto s1 = [&](int ci, int cj, int sh) { return d1[sh][cj - (j0 - 1)][ci - (i0 - 1)]; };
+    for (int t = threadIdx.x; t < 2 * J1H * J1W; t += JNT) {
+        const int sh = t / (J1H * J1W), rem = t - sh * (J1H * J1W), ly = rem / J1W, lx = rem - ly * J1W;
+        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
+        d1[sh][ly][lx] = inmesh(ci, cj) ? jac(ci, cj, sh, ly, lx, s0) : 0.0;
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+    const int i = i0 + lx, j = j0 + ly;
+    if (i > n || j > n) return;
+    const int64_t o = (int64_t)j * pitch + i;
+#pragma unroll
+    for (int sh = 0; sh < 2; ++sh)
+        dpo[sh * plane + o] = (i < n && j < n) ? jac(i, j, sh, ly + 1, lx + 1, s1) : 0.0;
+}
+
 // stage B: du = F_u^{-1}(r_u - alpha B_u^T dp), dw = (r_w - tau B_w^T dp)/(tau D_w),
 // xout = x + omega (du, dw, dp)
 constexpr int BB_XW = BTX + 4, BB_XH = BTY + 4, BB_RW = BTX + 2, BB_RH = BTY + 2;
@@ -1815,13 +1921,17 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                     const double* z1 = zr + sz(y + 1) * (5 * BMA_ZC) + lane;
                     const double* r0 = br + sb(y) * BQ_ROW + (lane + 2);
                     const double* r1 = br + sb(y + 1) * BQ_ROW + (lane + 2);
+                    // 1 / D_w of the five edges of the cell: H(i,y), V(i,y), D(i,y), H(i,y+1), V(i+1,y)
+                    const double rH0 = 1.0 / Dw(5, i, y), rV0 = 1.0 / Dw(6, i, y), rD = 1.0 / Dw(7, i, y);
+                    const double rH1 = 1.0 / Dw(5, i, y + 1), rV1 = 1.0 / Dw(6, i + 1, y);
+                    const double itau = 1.0 / L.tau;
 #pragma unroll
                     for (int sh = 0; sh < 2; ++sh) {
-                        double dw[3];
+                        double rdw[3];
                         bool act[3];
-                        if (sh == 0) { dw[0] = Dw(5, i, y); dw[1] = Dw(6, i, y); }
-                        else { dw[0] = Dw(5, i, y + 1); dw[1] = Dw(6, i + 1, y); }
-                        dw[2] = Dw(7, i, y);
+                        rdw[0] = sh == 0 ? rH0 : rH1;
+                        rdw[1] = sh == 0 ? rV0 : rV1;
+                        rdw[2] = rD;
                         tri_edges_active(sh, i, y, n, act);
                         double gu = 0.0, gw = 0.0, ds = L.s0h2;
 #define MG_L(s_, q_, dx, dy, pl)                                                                  \
@@ -1831,8 +1941,8 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
             const int e = (q_) < 12 ? (q_) - 9 : 0;                                               \
             if (act[e]) {                                                                         \
                 const double rw = ((dy) ? r1 : r0)[(pl) * BQ_W + (dx)];                           \
-                gw = fma(L.bw[s_][e], rw / (L.tau * dw[e]), gw);                                  \
-                ds += L.tau * L.bw[s_][e] * L.bw[s_][e] / dw[e];                                  \
+                gw = fma(L.bw[s_][e], rw * rdw[e] * itau, gw);                                    \
+                ds += L.tau * L.bw[s_][e] * L.bw[s_][e] * rdw[e];                                 \
             }                                                                                     \
         }                                                                                         \
     }
@@ -2398,6 +2508,14 @@ cudaError_t launch_bsr_jacobi(const LevelParams& L, double omJ, const double* g,
     dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
     if (L.kinv_field) bsr_jacobi_kernel<true><<<grid, 256, 0, s>>>(L, omJ, g, dpi, dpo);
     else bsr_jacobi_kernel<false><<<grid, 256, 0, s>>>(L, omJ, g, dpi, dpo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
+                               cudaStream_t s) {
+    dim3 grid((L.n + JT_X) / JT_X, (L.n + JT_Y) / JT_Y);
+    if (L.kinv_field) bsr_jacobi2_kernel<true><<<grid, JNT, 0, s>>>(L, omJ, g, dpi, dpo);
+    else bsr_jacobi2_kernel<false><<<grid, JNT, 0, s>>>(L, omJ, g, dpi, dpo);
     return cudaGetLastError();
 }
 

@@ -41,6 +41,9 @@ int blocks_vanka_march2(int n);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march3(int n);
+// two Jacobi sweeps in one launch (same arithmetic as two launch_bsr_jacobi)
+cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
+                               cudaStream_t s);
 // row-marching TMA variants of the two BSR stages (same arithmetic as launch_bsr_a / launch_bsr_b)
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
                                double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s);

@@ -1,3 +1,3 @@
-python -m pytest tests/test_gpu_parity.py -q -x -k "bsr" 2>&1 | tail -15 > gpurun_out/q_test.txt
+python -m pytest tests/test_gpu_parity.py -q -x -k "bsr" 2>&1 | tail -2 > gpurun_out/q_test.txt
+MG_JACOBI_PAIR=1 python -m pytest tests/test_gpu_parity.py -q -x -k "bsr_sweep" 2>&1 | tail -2 >> gpurun_out/q_test.txt
 python bench.py --config 4 --no-cpu-baseline --no-solve --no-e2e --steps 50 > gpurun_out/bq_c4.log 2>&1
-MG_BSR_IMPL=0 python bench.py --config 4 --no-cpu-baseline --no-solve --no-e2e --steps 50 > gpurun_out/bq_c4_0.log 2>&1
