@@ -1,3 +1,6 @@
-python -m pytest tests/test_gpu_parity.py -q -x -k "bsr" 2>&1 | tail -2 > gpurun_out/q_test.txt
-MG_JACOBI_PAIR=1 python -m pytest tests/test_gpu_parity.py -q -x -k "bsr_sweep" 2>&1 | tail -2 >> gpurun_out/q_test.txt
-python bench.py --config 4 --no-cpu-baseline --no-solve --no-e2e --steps 50 > gpurun_out/bq_c4.log 2>&1
+python bench.py > gpurun_out/bench_r01c.log 2>&1
+python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1
+python bench.py --config 4 --no-cpu-baseline --no-solve > gpurun_out/bench_c4.log 2>&1
+python bench.py --config 2 --no-cpu-baseline --no-solve > gpurun_out/bench_c2.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"march2_kernelILb0ELb0|restrict_march_kernelILb0" -c 2 -o gpurun_out/prof_r01c python tools/two_cycles.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"march2_kernelILb0ELb1" --launch-skip 3 -c 1 -o gpurun_out/prof_r01c_post python tools/two_cycles.py > /dev/null 2>&1
