@@ -229,6 +229,16 @@ __global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, cons
 // ------------------------------------------------------------------------------------------
 // additive Vanka sweep: xout = x + omega sum_v V^T D K_v^{-1} V (b - A x)
 constexpr int VTX = 32, VTY = 8, VNT = 352;   // (VTX+2)(VTY+2) = 340 residual positions, one per thread
+// 2-D tile geometry of the single-pass Vanka sweep for a TX x TY owner tile (x tile +2 ring,
+// residual +1 ring, patches +1 high ring); small tiles for the latency-bound coarse levels
+template <int TX, int TY>
+struct VTile {
+    static constexpr int XW = TX + 4, XH = TY + 4, RW = TX + 2, RH = TY + 2, PW = TX + 1, PH = TY + 1;
+    static constexpr int XSZ = 10 * XW * XH, CSZ = 20 * PW * PH, USZ = XSZ > CSZ ? XSZ : CSZ;
+    static constexpr int SMEM = (USZ + 10 * RW * RH) * 8;
+    static constexpr int NT = ((RW * RH + 31) / 32) * 32;   // >= PW * PH, TX * TY
+};
+constexpr int VSX = 8, VSY = 4;                // small tiles: 64 threads
 constexpr int V_XW = VTX + 4, V_XH = VTY + 4, V_RW = VTX + 2, V_RH = VTY + 2, V_PW = VTX + 1, V_PH = VTY + 1;
 constexpr int V_XSZ = 10 * V_XW * V_XH, V_CSZ = 20 * V_PW * V_PH;
 constexpr int V_USZ = V_XSZ > V_CSZ ? V_XSZ : V_CSZ;
@@ -320,58 +330,59 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
     }
 }
 
-template <bool XZERO>
-__global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
+template <bool XZERO, int TX = VTX, int TY = VTY>
+__global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
                                                        const double* __restrict__ b, double* __restrict__ xo,
                                                        NormSink S) {
+    using T = VTile<TX, TY>;
     extern __shared__ double sm[];
     double* xs = sm;          // x tile (phase 1)
     double* cs = sm;          // patch corrections (phase 2-3), overlays xs
-    double* rs = sm + V_USZ;  // residual tile
+    double* rs = sm + T::USZ;  // residual tile
     const LevelParams& L = P.L;
     if (*L.stop) return;
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
-    const int i0 = blockIdx.x * VTX, j0 = blockIdx.y * VTY;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
     const int t = threadIdx.x;
     // phase 1: r = b - A x on the tile + 1 ring (one index per thread; straight-line code keeps
     // the stencil coefficients as constant-bank operands instead of hoisted registers)
     if (!XZERO) {
-        load_tile<V_XW, V_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        load_tile<T::XW, T::XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
-        if (t < V_RW * V_RH) {
-            const int ly = t / V_RW, lx = t - ly * V_RW;
+        if (t < T::RW * T::RH) {
+            const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<V_XW, V_XH, false>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            residual_at<T::XW, T::XH, false>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
-            for (int k = 0; k < 10; ++k) rs[k * V_RW * V_RH + t] = rv[k];
+            for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
     } else {
-        load_tile<V_RW, V_RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);  // r = b (x = 0)
+        load_tile<T::RW, T::RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);  // r = b (x = 0)
     }
     __syncthreads();
     // phase 2: patch solves at the vertices of the tile + high ring
-    if (t < V_PW * V_PH) {
-        const int py = t / V_PW, px = t - py * V_PW;
+    if (t < T::PW * T::PH) {
+        const int py = t / T::PW, px = t - py * T::PW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
             double rr[20];
-            gather20<V_RW, V_RH>(rs + (py + 1) * V_RW + (px + 1), rr);
-            patch_apply20(P, vertex_class(a, bb, n), rr, cs + t, V_PW * V_PH);
+            gather20<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
+            patch_apply20(P, vertex_class(a, bb, n), rr, cs + t, T::PW * T::PH);
         } else {
 #pragma unroll
-            for (int q = 0; q < 20; ++q) cs[q * V_PW * V_PH + t] = 0.0;
+            for (int q = 0; q < 20; ++q) cs[q * T::PW * T::PH + t] = 0.0;
         }
     }
     __syncthreads();
     // phase 3: owners sum the corrections of the (up to) 4 patches touching their DoFs
     double nrm = 0.0;
-    if (t < VTX * VTY) {
-        const int lx = t % VTX, ly = t / VTX;
+    if (t < TX * TY) {
+        const int lx = t % TX, ly = t / TX;
         const int i = i0 + lx, j = j0 + ly;
         if (i <= n && j <= n) {
-            const double* c00 = cs + ly * V_PW + lx;
-#define CC(s, dx, dy) c00[(s) * (V_PW * V_PH) + (dy) * V_PW + (dx)]
+            const double* c00 = cs + ly * T::PW + lx;
+#define CC(s, dx, dy) c00[(s) * (T::PW * T::PH) + (dy) * T::PW + (dx)]
             double d[10];
             d[0] = CC(0, 0, 0);
             d[1] = CC(1, 0, 0);
@@ -385,17 +396,17 @@ __global__ void __launch_bounds__(VNT, 2) vanka_kernel(const VankaParams P, cons
             d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
 #undef CC
             const int64_t o = (int64_t)j * pitch + i;
-            const double* r00 = rs + (ly + 1) * V_RW + (lx + 1);
+            const double* r00 = rs + (ly + 1) * T::RW + (lx + 1);
 #pragma unroll
             for (int k = 0; k < 10; ++k) {
                 const double xv = XZERO ? 0.0 : __ldg(x + k * plane + o);
                 xo[k * plane + o] = is_active(k, i, j, n) ? fma(P.omega, d[k], xv) : 0.0;
-                const double rv = r00[k * V_RW * V_RH];
+                const double rv = r00[k * T::RW * T::RH];
                 nrm = fma(rv, rv, nrm);
             }
         }
     }
-    if (S.out || S.state) norm_finish<VNT>(S, nrm);
+    if (S.out || S.state) norm_finish<T::NT>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -404,43 +415,53 @@ constexpr int CX = 16, CY = 4, CNT = 352;   // fine residual region 34 x 10 = 34
 constexpr int C_RW = 2 * CX + 2, C_RH = 2 * CY + 2, C_XW = C_RW + 2, C_XH = C_RH + 2;
 constexpr int C_SMEM_FUSED = (10 * C_RW * C_RH + 10 * C_XW * C_XH) * 8;
 constexpr int C_SMEM_PLAIN = 10 * C_RW * C_RH * 8;
+// geometry of a restriction tile of CX x CY coarse indices (small tiles for the coarse levels)
+template <int CX_, int CY_>
+struct CTile {
+    static constexpr int RW = 2 * CX_ + 2, RH = 2 * CY_ + 2, XW = RW + 2, XH = RH + 2;
+    static constexpr int SMEM_FUSED = (10 * RW * RH + 10 * XW * XH) * 8, SMEM_PLAIN = 10 * RW * RH * 8;
+    static constexpr int NT0 = RW * RH > 5 * CX_ * CY_ ? RW * RH : 5 * CX_ * CY_;
+    static constexpr int NT = ((NT0 + 31) / 32) * 32;
+};
+constexpr int CSX = 4, CSY = 2;             // small restriction tiles: 64 threads
 
-template <int MODE, bool HET>
-__global__ void __launch_bounds__(CNT, 2) restrict_kernel(const LevelParams L, int nc, int pitchc,
+template <int MODE, bool HET, int TX = CX, int TY = CY>
+__global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const LevelParams L, int nc, int pitchc,
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ br,
                                                           double* __restrict__ bc) {
+    using T = CTile<TX, TY>;
     extern __shared__ double sm[];
     double* rs = sm;
-    double* xs = sm + 10 * C_RW * C_RH;
+    double* xs = sm + 10 * T::RW * T::RH;
     if (*L.stop) return;
-    const int I0 = blockIdx.x * CX, J0 = blockIdx.y * CY;
+    const int I0 = blockIdx.x * TX, J0 = blockIdx.y * TY;
     const int fi0 = 2 * I0 - 2, fj0 = 2 * J0 - 2;
     const int t = threadIdx.x;
     if (MODE == 1) {
-        load_tile<C_XW, C_XH, 10>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane);
+        load_tile<T::XW, T::XH, 10>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane);
         __syncthreads();
-        if (t < C_RW * C_RH) {
-            const int ly = t / C_RW, lx = t - ly * C_RW;
+        if (t < T::RW * T::RH) {
+            const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<C_XW, C_XH, HET>(L, xs, lx + 1, ly + 1, fi0 + lx, fj0 + ly, br, rv);
+            residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, fi0 + lx, fj0 + ly, br, rv);
 #pragma unroll
-            for (int k = 0; k < 10; ++k) rs[k * C_RW * C_RH + t] = rv[k];
+            for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
     } else {
-        load_tile<C_RW, C_RH, 10>(rs, br, fi0, fj0, L.n, L.pitch, L.plane);
+        load_tile<T::RW, T::RH, 10>(rs, br, fi0, fj0, L.n, L.pitch, L.plane);
     }
     __syncthreads();
     // coarse outputs: (coarse index, pair of planes) per thread; the plane pair is warp uniform
-    if (t >= 5 * CX * CY) return;
-    const int c = t % (CX * CY), grp = t / (CX * CY);
-    const int cy = c / CX, cx = c - cy * CX;
+    if (t >= 5 * TX * TY) return;
+    const int c = t % (TX * TY), grp = t / (TX * TY);
+    const int cy = c / TX, cx = c - cy * TX;
     const int I = I0 + cx, J = J0 + cy;
     if (I > nc || J > nc) return;
-    const double* r00 = rs + (2 * cy + 2) * C_RW + (2 * cx + 2);
+    const double* r00 = rs + (2 * cy + 2) * T::RW + (2 * cx + 2);
     const int64_t planec = (int64_t)(nc + 1) * pitchc;
     const int64_t o = (int64_t)J * pitchc + I;
-#define RF(cdI, cdJ, di, dj, kf) r00[(kf) * (C_RW * C_RH) + (-2 * (cdJ) + (dj)) * C_RW + (-2 * (cdI) + (di))]
+#define RF(cdI, cdJ, di, dj, kf) r00[(kf) * (T::RW * T::RH) + (-2 * (cdJ) + (dj)) * T::RW + (-2 * (cdI) + (di))]
 #define MG_T(cdI, cdJ, di, dj, kf, w) acc = fma(w, RF(cdI, cdJ, di, dj, kf), acc);
 #define OUT(k)                                                       \
     {                                                                \
@@ -2201,10 +2222,14 @@ void kernels_init() {
     set_smem(vanka_march_kernel<true>, M_SMEM);
     set_smem(vanka_kernel<false>, V_SMEM);
     set_smem(vanka_kernel<true>, V_SMEM);
+    set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
+    set_smem(vanka_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(restrict_kernel<0, false>, C_SMEM_PLAIN);
     set_smem(restrict_kernel<2, false>, C_SMEM_PLAIN);
     set_smem(restrict_kernel<1, false>, C_SMEM_FUSED);
     set_smem(restrict_kernel<1, true>, C_SMEM_FUSED);
+    set_smem(restrict_kernel<1, false, CSX, CSY>, CTile<CSX, CSY>::SMEM_FUSED);
+    set_smem(restrict_kernel<1, true, CSX, CSY>, CTile<CSX, CSY>::SMEM_FUSED);
     set_smem(coarse_kernel, 4096 * 8);
     set_smem(bsr_a_kernel<false, false>, BA_SMEM);
     set_smem(bsr_a_kernel<false, true>, BA_SMEM);
@@ -2222,7 +2247,11 @@ static_assert(BANT >= BA_RW * BA_RH && BANT % 32 == 0, "bsr_a thread mapping");
 static_assert(BBNT >= BB_RW * BB_RH && BBNT % 32 == 0, "bsr_b thread mapping");
 
 int blocks_residual(int n) { return ((n + RTX) / RTX) * ((n + RTY) / RTY); }
-int blocks_vanka(int n) { return ((n + VTX) / VTX) * ((n + VTY) / VTY); }
+int g_small_tile_n = 128;   // levels with n <= this use the small 2-D tiles (mg_setup: MG_SMALL_TILE_N)
+void set_small_tile_n(int n) { g_small_tile_n = n; }
+int blocks_vanka(int n) {
+    return n <= g_small_tile_n ? ((n + VSX) / VSX) * ((n + VSY) / VSY) : ((n + VTX) / VTX) * ((n + VTY) / VTY);
+}
 int blocks_bsr(int n) { return ((n + BTX) / BTX) * ((n + BTY) / BTY); }
 
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
@@ -2345,6 +2374,13 @@ int dot_partials_needed() { return VK * DOT_BLOCKS; }
 
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
                          NormSink S, cudaStream_t s) {
+    if (P.L.n <= g_small_tile_n) {
+        using T = VTile<VSX, VSY>;
+        dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
+        if (x_zero) vanka_kernel<true, VSX, VSY><<<grid, T::NT, T::SMEM, s>>>(P, x, b, xo, S);
+        else vanka_kernel<false, VSX, VSY><<<grid, T::NT, T::SMEM, s>>>(P, x, b, xo, S);
+        return cudaGetLastError();
+    }
     dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
     if (x_zero) vanka_kernel<true><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
     else vanka_kernel<false><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
@@ -2466,6 +2502,19 @@ cudaError_t launch_restrict_march(const LevelParams& Lf, int nc, int pitchc, con
 
 cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode, const double* x,
                             const double* br, double* bc, cudaStream_t s) {
+    if (nc <= g_small_tile_n / 2) {
+        using T = CTile<CSX, CSY>;
+        dim3 grid((nc + CSX) / CSX, (nc + CSY) / CSY);
+        if (mode == 1) {
+            if (Lf.kinv_field) restrict_kernel<1, true, CSX, CSY><<<grid, T::NT, T::SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
+            else restrict_kernel<1, false, CSX, CSY><<<grid, T::NT, T::SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
+        } else if (mode == 0) {
+            restrict_kernel<0, false, CSX, CSY><<<grid, T::NT, T::SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+        } else {
+            restrict_kernel<2, false, CSX, CSY><<<grid, T::NT, T::SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+        }
+        return cudaGetLastError();
+    }
     dim3 grid((nc + CX) / CX, (nc + CY) / CY);
     if (mode == 1) {
         if (Lf.kinv_field) restrict_kernel<1, true><<<grid, CNT, C_SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);

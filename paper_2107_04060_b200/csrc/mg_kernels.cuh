@@ -38,6 +38,9 @@ int blocks_vanka_march(int n);
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s, const ProlSrc* E = nullptr);
 int blocks_vanka_march2(int n);
+// levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
+// kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)
+void set_small_tile_n(int N);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march3(int n);

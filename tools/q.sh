@@ -1,6 +1,4 @@
-python bench.py > gpurun_out/bench_r01c.log 2>&1
-python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1
-python bench.py --config 4 --no-cpu-baseline --no-solve > gpurun_out/bench_c4.log 2>&1
-python bench.py --config 2 --no-cpu-baseline --no-solve > gpurun_out/bench_c2.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"march2_kernelILb0ELb0|restrict_march_kernelILb0" -c 2 -o gpurun_out/prof_r01c python tools/two_cycles.py > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"march2_kernelILb0ELb1" --launch-skip 3 -c 1 -o gpurun_out/prof_r01c_post python tools/two_cycles.py > /dev/null 2>&1
+python -m pytest tests/test_gpu_parity.py -q -x -k "vanka_sweep or cycle_history or restrict or solve_matches or fgmres" 2>&1 | tail -2 > gpurun_out/q_test.txt
+MG_SMALL_TILE_N=0 python -m pytest tests/test_gpu_parity.py -q -x -k "vanka_sweep or cycle_history" 2>&1 | tail -2 >> gpurun_out/q_test.txt
+for n in 64 256; do for st in 0 128; do MG_SMALL_TILE_N=$st python bench.py --no-cpu-baseline --no-e2e --no-solve --steps 200 --n $n > gpurun_out/bq_n${n}_$st.log 2>&1; done; done
+for st in 0 64 128 256; do MG_SMALL_TILE_N=$st python bench.py --no-cpu-baseline --no-e2e --no-solve --steps 100 > gpurun_out/bq_st$st.log 2>&1; done
