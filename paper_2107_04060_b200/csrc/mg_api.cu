@@ -375,6 +375,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_BSR_IMPL")) c->bsr_impl = atoi(v);
     if (const char* v = getenv("MG_SMALL_TILE_N")) set_small_tile_n(atoi(v));
+    if (const char* v = getenv("MG_PDL")) set_pdl(atoi(v) != 0);
     if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v) != 0;
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
     auto bail = [&](int rc) {
@@ -667,7 +668,8 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
     if (!c) return fail(MG_EINVAL, "null context");
     if (int rc = check_opts(o)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
-    if (max_iters < 0 || restart < 1 || restart > 64) return fail(MG_EINVAL, "need max_iters >= 0, 1 <= restart <= 64");
+    if (max_iters < 0 || restart < 1 || restart > 31)
+        return fail(MG_EINVAL, "need max_iters >= 0, 1 <= restart <= 31");
     if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (!c->Ginv || c->levels < 2) return fail(MG_EINVAL, "mg_fgmres needs levels >= 2 and a coarsest solve");
     Level& L0 = c->L[0];
@@ -692,45 +694,33 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
     }
     if (!c->kw) {
         c->kw = (double*)dalloc(c, vb);
-        c->kdots = (double*)dalloc(c, sizeof(double) * 160);
-        c->kpart = (double*)dalloc(c, sizeof(double) * dot_partials_needed());
+        c->kdots = (double*)dalloc(c, sizeof(double) * 256);
+        c->kpart = (double*)dalloc(c, sizeof(double) * std::max(dot_partials_needed(), gs_partials_needed()));
         c->kcnt = (unsigned*)dalloc(c, 64);
         if (!c->kw || !c->kdots || !c->kpart || !c->kcnt) return fail(MG_ENOMEM, "FGMRES work allocation failed");
         CK(cudaMemsetAsync(c->kcnt, 0, 64, s));
         CK(cudaMemsetAsync(c->kw, 0, vb, s));
     }
     const LevelParams& LP = L0.vp.L;
-    auto dots = [&](const double* w, const std::vector<double*>& vs, int first, int k, double* out) -> int {
-        for (int q0 = 0; q0 < k; q0 += 8) {
-            VecPtrs P{};
-            const int kk = std::min(8, k - q0);
-            for (int q = 0; q < kk; ++q) P.p[q] = vs[first + q0 + q];
-            CK(launch_dots(w, P, kk, len, c->kpart, c->kcnt, out + q0, s));
-        }
-        return MG_OK;
-    };
-    auto update = [&](double* w, const std::vector<double*>& vs, int first, int k, const double* coef) -> int {
-        for (int q0 = 0; q0 < k; q0 += 8) {
-            VecPtrs P{};
-            const int kk = std::min(8, k - q0);
-            for (int q = 0; q < kk; ++q) P.p[q] = vs[first + q0 + q];
-            CK(launch_update(w, P, kk, coef + q0, len, s));
-        }
-        return MG_OK;
-    };
-    double* hd = c->kdots;           // [0..63] first CGS pass, [64..127] second, [128] norm^2
-    std::vector<double> hist;
+    // Device scratch (doubles): [0, 33) pass-1 dots + |U|^2, [40, 73) pass-2 dots + |U'|^2, [80] |U''|^2,
+    // [96, 128) s_i^2, [128, 160) solution-update coefficients, [160] |r|^2.
+    double* hd = c->kdots;
+    double* d1 = hd, * d2 = hd + 40, * d3 = hd + 80, * s2d = hd + 96, * yd = hd + 128, * rn = hd + 160;
+    // Basis kept UNSCALED: W_i (kv[i]) with v_i = s_i W_i of unit norm; Z'_i = M^-1 W_i (kz[i]) so
+    // z_i = s_i Z'_i; the scaling passes of textbook GMRES disappear into host-side bookkeeping.
+    // Classical Gram-Schmidt twice, fused: pass 1 dots (mode 0); pass-1 update written to W_{j+1}
+    // together with the pass-2 dots (mode 1); pass-2 update with the norm (mode 2).
+    std::vector<double> hist, sv(restart + 2), hh(96);
     int iters = 0;
     double beta0 = -1.0, target = 0.0;
     bool done = false;
-    std::vector<double> H, cs, sn, g, hcol(130);
+    std::vector<double> H, cs, sn, g;
     while (!done) {
-        // r = b - A x -> v_0, beta = ||r||
-        CK(launch_residual(LP, x, b, c->kv[0], no_norm(), s));
-        if (int rc = dots(c->kv[0], c->kv, 0, 1, hd + 128)) return rc;
-        CK(cudaMemcpyAsync(hcol.data() + 128, hd + 128, sizeof(double), cudaMemcpyDeviceToHost, s));
+        // r = b - A x -> W_0, |r|^2 fused into the residual kernel
+        CK(launch_residual(LP, x, b, c->kv[0], NormSink{rn, c->partials, c->counter, nullptr}, s));
+        CK(cudaMemcpyAsync(hh.data(), rn, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        const double beta = std::sqrt(hcol[128]);
+        const double beta = std::sqrt(hh[0]);
         if (beta0 < 0.0) {
             beta0 = beta;
             target = rtol * beta0;
@@ -738,7 +728,9 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
         }
         if (!std::isfinite(beta)) return fail(MG_ECUDA, "non-finite residual in FGMRES");
         if (beta <= target || beta == 0.0 || iters >= max_iters) break;
-        CK(launch_scale(c->kv[0], c->kv[0], 1.0 / beta, len, s));
+        sv[0] = 1.0 / beta;
+        hh[0] = sv[0] * sv[0];
+        CK(cudaMemcpyAsync(s2d, hh.data(), sizeof(double), cudaMemcpyHostToDevice, s));
         const int m = std::min(restart, max_iters - iters);
         H.assign((m + 1) * m, 0.0);
         cs.assign(m, 0.0);
@@ -747,28 +739,30 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
         g[0] = beta;
         int k = 0;
         for (int j = 0; j < m; ++j) {
-            // z_j = one V-cycle from zero on v_j; w = A z_j
+            // Z'_j = one V-cycle from zero on W_j; U = A Z'_j
             cudaGraphExec_t ge;
             if (int rc = get_graph(c, c->kz[j], c->kv[j], *o, 3, nullptr, &ge)) return rc;
             CK(cudaGraphLaunch(ge, s));
             CK(launch_apply(LP, c->kz[j], c->kw, no_norm(), s));
-            // classical Gram-Schmidt, twice (the second pass only if c->cgs_passes == 2)
-            if (int rc = dots(c->kw, c->kv, 0, j + 1, hd)) return rc;
-            if (int rc = update(c->kw, c->kv, 0, j + 1, hd)) return rc;
-            if (c->cgs_passes == 2) {
-                if (int rc = dots(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
-                if (int rc = update(c->kw, c->kv, 0, j + 1, hd + 64)) return rc;
-            } else {
-                CK(cudaMemsetAsync(hd + 64, 0, sizeof(double) * 64, s));
-            }
-            std::vector<double*> wv{c->kw};
-            if (int rc = dots(c->kw, wv, 0, 1, hd + 128)) return rc;
-            CK(cudaMemcpyAsync(hcol.data(), hd, sizeof(double) * 129, cudaMemcpyDeviceToHost, s));
+            GsPtrs V{};
+            for (int i = 0; i <= j; ++i) V.p[i] = c->kv[i];
+            const int kk = j + 1;
+            // coefficients of W_i: c_i = <U, W_i> s_i^2 (the kernels scale by s2d)
+            CK(launch_gs(0, c->kw, nullptr, V, kk, nullptr, nullptr, len, c->kpart, c->kcnt, d1, s));
+            CK(launch_gs(1, c->kw, c->kv[j + 1], V, kk, d1, s2d, len, c->kpart, c->kcnt, d2, s));
+            const bool two = c->cgs_passes == 2;
+            if (two) CK(launch_gs(2, c->kv[j + 1], c->kv[j + 1], V, kk, d2, s2d, len, c->kpart, c->kcnt, d3, s));
+            CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            const double hn = std::sqrt(hcol[128]);
-            for (int i = 0; i <= j; ++i) H[i * m + j] = hcol[i] + hcol[64 + i];
-            H[(j + 1) * m + j] = hn;
-            if (hn > 0.0) CK(launch_scale(c->kv[j + 1], c->kw, 1.0 / hn, len, s));
+            const double rho = std::sqrt(two ? hh[80] : hh[40 + kk]);
+            // h_ij = (A z_j) . v_i = s_j s_i <U, W_i> = s_j (c1_i + c2_i) / s_i
+            for (int i = 0; i <= j; ++i)
+                H[i * m + j] = sv[j] * sv[i] * (hh[i] + (two ? hh[40 + i] : 0.0));
+            H[(j + 1) * m + j] = sv[j] * rho;
+            sv[j + 1] = rho > 0.0 ? 1.0 / rho : 0.0;
+            hh[90] = sv[j + 1] * sv[j + 1];
+            CK(cudaMemcpyAsync(s2d + j + 1, hh.data() + 90, sizeof(double), cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));   // hh[90] is host scratch reused next iteration
             for (int i = 0; i < j; ++i) {   // previous Givens rotations
                 const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
                 H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
@@ -787,21 +781,19 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
             if (!std::isfinite(hist.back())) return fail(MG_ECUDA, "non-finite FGMRES residual estimate");
             if (hist.back() <= target) break;
         }
-        // y = H^{-1} g (upper triangular), x += Z y
+        // y = H^{-1} g (upper triangular), x += sum_i y_i z_i = sum_i (y_i s_i) Z'_i in one pass
         std::vector<double> y(k);
         for (int i = k - 1; i >= 0; --i) {
             double t = g[i];
             for (int l = i + 1; l < k; ++l) t -= H[i * m + l] * y[l];
             y[i] = t / H[i * m + i];
         }
-        for (int i = 0; i < k; ++i) y[i] = -y[i];   // the update kernel subtracts
-        CK(cudaMemcpyAsync(hd + 130, y.data(), sizeof(double) * std::min(k, 8), cudaMemcpyHostToDevice, s));
-        for (int q0 = 0; q0 < k; q0 += 8) {
-            const int kk = std::min(8, k - q0);
-            CK(cudaMemcpyAsync(hd + 130, y.data() + q0, sizeof(double) * kk, cudaMemcpyHostToDevice, s));
-            if (int rc = update(x, c->kz, q0, kk, hd + 130)) return rc;
-            CK(cudaStreamSynchronize(s));   // hd + 130 is reused by the next chunk
-        }
+        for (int i = 0; i < k; ++i) y[i] = -y[i] * sv[i];   // the update kernel subtracts
+        CK(cudaMemcpyAsync(yd, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+        GsPtrs Z{};
+        for (int i = 0; i < k; ++i) Z.p[i] = c->kz[i];
+        CK(launch_gs(3, x, x, Z, k, yd, nullptr, len, nullptr, nullptr, nullptr, s));
+        CK(cudaStreamSynchronize(s));   // y is host memory read by the async copy
         if (hist.back() <= target || iters >= max_iters) done = true;
     }
     CK(cudaStreamSynchronize(s));

@@ -24,6 +24,15 @@
 
 namespace {
 
+// Programmatic dependent launch (sm_90+): every kernel waits for the completion (and memory) of the
+// grid it depends on before touching memory, so the host may launch it with programmatic stream
+// serialization -- the next grid is scheduled while the previous one drains, which removes most of
+// the launch gap between the short kernels of the coarse levels.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the dependent grid to be scheduled: once every CTA of this grid has started, the next
+// grid's CTAs fill the SMs this grid's tail frees (they block in pdl_wait until it completes)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ bool is_active(int p, int i, int j, int n) {
     if (i < 0 || j < 0 || i > n || j > n) return false;
     switch (p) {
@@ -196,6 +205,8 @@ template <bool HET, bool APPLY>
 __global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, const double* __restrict__ x,
                                                        const double* __restrict__ b, double* __restrict__ r,
                                                        NormSink S) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int XW = RTX + 2, XH = RTY + 2;
     __shared__ double xs[10 * XW * XH];
     if (*L.stop) return;
@@ -334,6 +345,8 @@ template <bool XZERO, int TX = VTX, int TY = VTY>
 __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
                                                        const double* __restrict__ b, double* __restrict__ xo,
                                                        NormSink S) {
+    pdl_wait();
+    pdl_trigger();
     using T = VTile<TX, TY>;
     extern __shared__ double sm[];
     double* xs = sm;          // x tile (phase 1)
@@ -430,6 +443,8 @@ __global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const Le
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ br,
                                                           double* __restrict__ bc) {
+    pdl_wait();
+    pdl_trigger();
     using T = CTile<TX, TY>;
     extern __shared__ double sm[];
     double* rs = sm;
@@ -485,6 +500,8 @@ __global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const Le
 __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc, int pitchc,
                                                       const double* __restrict__ e, double* __restrict__ x,
                                                       const int* __restrict__ stop) {
+    pdl_wait();
+    pdl_trigger();
     if (*stop) return;
     const int I = blockIdx.x * 32 + (threadIdx.x & 31), J = blockIdx.y * 8 + (threadIdx.x >> 5);
     if (I >= nc || J >= nc) return;
@@ -522,6 +539,8 @@ __global__ void __launch_bounds__(256) coarse_kernel(int N, const double* __rest
                                                      const int64_t* __restrict__ slots,
                                                      const double* __restrict__ b, double* __restrict__ x,
                                                      const int* __restrict__ stop) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double rb[];
     if (*stop) return;
     for (int k = threadIdx.x; k < N; k += blockDim.x) rb[k] = __ldg(b + slots[k]);
@@ -649,6 +668,8 @@ template <bool HET, bool XZERO>
 __global__ void __launch_bounds__(BANT, 2) bsr_a_kernel(const LevelParams L, const DispParams U, double omJ,
                                                        const double* __restrict__ x, const double* __restrict__ b,
                                                        double* __restrict__ g, double* __restrict__ dp, NormSink S) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double sm[];
     double* xs = sm;
     double* zs = sm;                              // disp patch outputs, overlays xs
@@ -756,6 +777,8 @@ template <bool HET>
 __global__ void __launch_bounds__(256) bsr_jacobi_kernel(const LevelParams L, double omJ,
                                                          const double* __restrict__ g,
                                                          const double* __restrict__ dpi, double* __restrict__ dpo) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
     const int n = L.n;
     if (i > n || j > n || *L.stop) return;
@@ -804,6 +827,8 @@ template <bool HET>
 __global__ void __launch_bounds__(JNT) bsr_jacobi2_kernel(const LevelParams L, double omJ,
                                                           const double* __restrict__ g,
                                                           const double* __restrict__ dpi, double* __restrict__ dpo) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double d0[2][J0H][J0W];                            // cells [i0-2, i0+34) x [j0-2, j0+10)
     __shared__ double kk[HET ? 2 : 1][HET ? JKH : 1][HET ? JKW : 1];   // cells [i0-2, i0+35) x [j0-2, j0+11)
     __shared__ double tw[3][JEH][JEW];                            // tau / D_w of edges H, V, D at [i0-1, i0+34) x [j0-1, j0+10)
@@ -910,6 +935,8 @@ template <bool HET, bool XZERO>
 __global__ void __launch_bounds__(BBNT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
                                                        const double* __restrict__ x, const double* __restrict__ b,
                                                        const double* __restrict__ dp, double* __restrict__ xo) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double sm[];
     double* xs = sm;
     double* zs = sm;
@@ -1002,6 +1029,8 @@ __global__ void __launch_bounds__(BBNT, 2) bsr_b_kernel(const LevelParams L, con
 // ------------------------------------------------------------------------------------------
 // K^{-1} pyramid (reading A11): level 0 from the user's K [shape][j][i] (n x n), then averages
 __global__ void kinv_from_K_kernel(int n, int pitch, const double* __restrict__ K, double* __restrict__ kinv) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
     if (i >= n || j >= n) return;
     const int64_t plane = (int64_t)(n + 1) * pitch;
@@ -1011,6 +1040,8 @@ __global__ void kinv_from_K_kernel(int n, int pitch, const double* __restrict__ 
 
 __global__ void kinv_coarsen_kernel(int nf, int pitchf, const double* __restrict__ kf, int pitchc,
                                     double* __restrict__ kc) {
+    pdl_wait();
+    pdl_trigger();
     const int I = blockIdx.x * 32 + (threadIdx.x & 31), J = blockIdx.y * 8 + (threadIdx.x >> 5);
     const int nc = nf / 2;
     if (I >= nc || J >= nc) return;
@@ -1090,6 +1121,8 @@ __global__ void __launch_bounds__(MNT, 2) vanka_march_kernel(const __grid_consta
                                                              const __grid_constant__ CUtensorMap tmb,
                                                              const VankaParams P, double* __restrict__ xo,
                                                              NormSink S, int MH) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                    // [3][10][MR][M_XW]
     double* br = xr + 3 * M_XCH;        // [3][10][MR][M_BW]  (b, overwritten by r)
@@ -1275,6 +1308,8 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
                                                                const __grid_constant__ CUtensorMap tmb,
                                                                const VankaParams P, double* __restrict__ xo,
                                                                NormSink S, int MH, const ProlSrc E) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                        // [M2XR][10][M2W]
     double* br = xr + M2XR * M2ROW;         // [M2BR][10][M2W]   b, overwritten by r
@@ -1518,6 +1553,8 @@ template <bool XZERO>
 __global__ void __launch_bounds__(M3NT, 4) vanka_march3_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                const VankaParams P, const double* __restrict__ b,
                                                                double* __restrict__ xo, NormSink S, int MH) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                        // [M3XR][10][M3W]
     double* rr_ = xr + M3XR * M3XROW;       // [M3RR][10][M3RW]   residual rows
@@ -1673,6 +1710,8 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
                                                                 const __grid_constant__ CUtensorMap tmb,
                                                                 const LevelParams L, int nc, int pitchc,
                                                                 double* __restrict__ bc, int MH) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                    // [3][10][QF][Q_XW]
     double* br = xr + 3 * Q_XCH;        // [3][10][QF][Q_RW]  (b, overwritten by r)
@@ -1807,6 +1846,8 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                                                                const LevelParams L, const DispParams U, double omJ,
                                                                double* __restrict__ g, double* __restrict__ dp,
                                                                NormSink S, int MH) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                          // [BMA_XR][10][32]
     double* br = xr + BMA_XR * BQ_ROW;         // [BMA_BR][10][32]  b, overwritten by r
@@ -1999,6 +2040,8 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmk,
                                                                const LevelParams L, const DispParams U, double omega,
                                                                double* __restrict__ xo, int MH) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                          // [BB2_XR][10][32]
     double* br = xr + BB2_XR * BQ_ROW;        // [BB2_BR][10][32]  b, overwritten by (y_u, r_w)
@@ -2183,6 +2226,25 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFn g_encode = nullptr;
 
+static int g_pdl = 1;   // programmatic dependent launch on (mg_setup: MG_PDL=0 turns it off)
+void set_pdl(int on) { g_pdl = on; }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int pitch, int64_t plane, int boxw,
                                   int boxh, int planes = 10) {
     if (!g_encode) {
@@ -2257,15 +2319,15 @@ int blocks_bsr(int n) { return ((n + BTX) / BTX) * ((n + BTY) / BTY); }
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
                             cudaStream_t s) {
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
-    if (L.kinv_field) residual_kernel<true, false><<<grid, RNT, 0, s>>>(L, x, b, r, S);
-    else residual_kernel<false, false><<<grid, RNT, 0, s>>>(L, x, b, r, S);
+    if (L.kinv_field) launch_k(residual_kernel<true, false>, grid, RNT, 0, s, L, x, b, r, S);
+    else launch_k(residual_kernel<false, false>, grid, RNT, 0, s, L, x, b, r, S);
     return cudaGetLastError();
 }
 
 cudaError_t launch_apply(const LevelParams& L, const double* x, double* y, NormSink S, cudaStream_t s) {
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
-    if (L.kinv_field) residual_kernel<true, true><<<grid, RNT, 0, s>>>(L, x, nullptr, y, S);
-    else residual_kernel<false, true><<<grid, RNT, 0, s>>>(L, x, nullptr, y, S);
+    if (L.kinv_field) launch_k(residual_kernel<true, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
+    else launch_k(residual_kernel<false, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
     return cudaGetLastError();
 }
 
@@ -2277,6 +2339,8 @@ constexpr int DOT_BLOCKS = 296, DOT_NT = 256, VK = 8;
 __global__ void __launch_bounds__(DOT_NT) vec_dots_kernel(const double* __restrict__ w, VecPtrs V, int k,
                                                           int64_t len, double* __restrict__ partials,
                                                           unsigned* __restrict__ counter, double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     double acc[VK];
 #pragma unroll
     for (int q = 0; q < VK; ++q) acc[q] = 0.0;
@@ -2326,6 +2390,8 @@ __global__ void __launch_bounds__(DOT_NT) vec_dots_kernel(const double* __restri
 // w = w - sum_q c[q] v_q   (c in device memory)
 __global__ void __launch_bounds__(DOT_NT) vec_update_kernel(double* __restrict__ w, VecPtrs V, int k,
                                                             const double* __restrict__ c, int64_t len) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t n2 = len / 2;
     double2* w2 = reinterpret_cast<double2*>(w);
     double cq[VK];
@@ -2348,6 +2414,8 @@ __global__ void __launch_bounds__(DOT_NT) vec_update_kernel(double* __restrict__
 // y = s * x
 __global__ void __launch_bounds__(DOT_NT) vec_scale_kernel(double* __restrict__ y, const double* __restrict__ x,
                                                            double s, int64_t len) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t n2 = len / 2;
     for (int64_t e = (int64_t)blockIdx.x * DOT_NT + threadIdx.x; e < n2; e += (int64_t)gridDim.x * DOT_NT) {
         double2 a = __ldg(reinterpret_cast<const double2*>(x) + e);
@@ -2357,17 +2425,155 @@ __global__ void __launch_bounds__(DOT_NT) vec_scale_kernel(double* __restrict__ 
     }
 }
 
+// fused Gram-Schmidt pass (see mg_kernels.cuh): KB >= k basis vectors (register accumulators sized
+// to the bucket, so short bases keep occupancy high), two double2 element pairs per thread and step
+// for memory-level parallelism
+constexpr int GS_BLOCKS = 592, GS_NT = 256;
+template <int MODE, int KB>
+__global__ void __launch_bounds__(GS_NT) vec_gs_kernel(const double* __restrict__ w, double* wo, GsPtrs V, int k,
+                                                       const double* __restrict__ c, const double* __restrict__ sc,
+                                                       int64_t len, double* __restrict__ partials,
+                                                       unsigned* __restrict__ counter, double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NA = MODE == 0 || MODE == 1 ? KB + 1 : (MODE == 2 ? 1 : 0);
+    double acc[NA > 0 ? NA : 1];
+#pragma unroll
+    for (int q = 0; q < (NA > 0 ? NA : 1); ++q) acc[q] = 0.0;
+    __shared__ double cq[KB];   // update coefficients (broadcast reads)
+    if (threadIdx.x < KB)
+        cq[threadIdx.x] = (MODE != 0 && (int)threadIdx.x < k) ? c[threadIdx.x] * (sc ? sc[threadIdx.x] : 1.0) : 0.0;
+    __syncthreads();
+    const int64_t n2 = len / 2;
+    const int64_t stride = (int64_t)gridDim.x * GS_NT;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    for (int64_t e0 = (int64_t)blockIdx.x * GS_NT + threadIdx.x; e0 < n2; e0 += 2 * stride) {
+        const int64_t e1 = e0 + stride;
+        const bool has1 = e1 < n2;
+        double2 a0 = w2[e0], a1 = has1 ? w2[e1] : make_double2(0.0, 0.0);
+        if (MODE == 0) {
+#pragma unroll
+            for (int q = 0; q < KB; ++q)
+                if (q < k) {
+                    const double2* vp = reinterpret_cast<const double2*>(V.p[q]);
+                    const double2 v0 = __ldg(vp + e0), v1 = has1 ? __ldg(vp + e1) : make_double2(0.0, 0.0);
+                    acc[q] = fma(a0.x, v0.x, acc[q]);
+                    acc[q] = fma(a0.y, v0.y, acc[q]);
+                    acc[q] = fma(a1.x, v1.x, acc[q]);
+                    acc[q] = fma(a1.y, v1.y, acc[q]);
+                }
+        } else {
+            // loads in groups of 4 vectors ahead of their FMAs (keeps 8 loads in flight per thread)
+#pragma unroll
+            for (int q0 = 0; q0 < KB; q0 += 4) {
+                double2 v0[4], v1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = q0 + u;
+                    const double2* vp = reinterpret_cast<const double2*>(V.p[q]);
+                    v0[u] = q < k ? __ldg(vp + e0) : make_double2(0.0, 0.0);
+                    v1[u] = (q < k && has1) ? __ldg(vp + e1) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = q0 + u;
+                    if (q < k) {
+                        a0.x = fma(-cq[q], v0[u].x, a0.x);
+                        a0.y = fma(-cq[q], v0[u].y, a0.y);
+                        a1.x = fma(-cq[q], v1[u].x, a1.x);
+                        a1.y = fma(-cq[q], v1[u].y, a1.y);
+                    }
+                }
+            }
+            reinterpret_cast<double2*>(wo)[e0] = a0;
+            if (has1) reinterpret_cast<double2*>(wo)[e1] = a1;
+            if (MODE == 1) {
+                // dots of the updated pairs with the basis (re-read: an L1 / L2 hit)
+#pragma unroll
+                for (int q = 0; q < KB; ++q)
+                    if (q < k) {
+                        const double2* vp = reinterpret_cast<const double2*>(V.p[q]);
+                        const double2 v0 = __ldg(vp + e0), v1 = has1 ? __ldg(vp + e1) : make_double2(0.0, 0.0);
+                        acc[q] = fma(a0.x, v0.x, acc[q]);
+                        acc[q] = fma(a0.y, v0.y, acc[q]);
+                        acc[q] = fma(a1.x, v1.x, acc[q]);
+                        acc[q] = fma(a1.y, v1.y, acc[q]);
+                    }
+            }
+        }
+        if (MODE != 3) {
+            acc[NA - 1] = fma(a0.x, a0.x, acc[NA - 1]);
+            acc[NA - 1] = fma(a0.y, a0.y, acc[NA - 1]);
+            acc[NA - 1] = fma(a1.x, a1.x, acc[NA - 1]);
+            acc[NA - 1] = fma(a1.y, a1.y, acc[NA - 1]);
+        }
+    }
+    if (NA == 0) return;
+    __shared__ double red[NA > 0 ? NA : 1][GS_NT / 32];
+    __shared__ unsigned last;
+#pragma unroll
+    for (int q = 0; q < (NA > 0 ? NA : 1); ++q) {
+        double v = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    const int nres = MODE == 2 ? 1 : k + 1;   // results: dots 0..k-1, norm at slot k (mode 2: slot 0)
+    auto slot = [&](int r) { return MODE == 2 ? 0 : (r < k ? r : NA - 1); };
+    for (int r = threadIdx.x; r < nres; r += GS_NT) {
+        double t = 0.0;
+        for (int u = 0; u < GS_NT / 32; ++u) t += red[slot(r)][u];
+        partials[r * GS_BLOCKS + blockIdx.x] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == GS_BLOCKS - 1);
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        for (int r = threadIdx.x; r < nres; r += GS_NT) {
+            double t = 0.0;
+            for (int u = 0; u < GS_BLOCKS; ++u) t += __ldcg(partials + r * GS_BLOCKS + u);
+            out[r] = t;
+        }
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+template <int KB>
+static void launch_gs_kb(int mode, const double* w, double* wo, const GsPtrs& V, int k, const double* c,
+                         const double* sc, int64_t len, double* partials, unsigned* counter, double* out, cudaStream_t s) {
+    switch (mode) {
+        case 0: launch_k(vec_gs_kernel<0, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        case 1: launch_k(vec_gs_kernel<1, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        case 2: launch_k(vec_gs_kernel<2, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        default: launch_k(vec_gs_kernel<3, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+    }
+}
+
+cudaError_t launch_gs(int mode, const double* w, double* wo, const GsPtrs& V, int k, const double* c,
+                      const double* sc, int64_t len, double* partials, unsigned* counter, double* out, cudaStream_t s) {
+    if (k < 0 || k > GS_KMAX) return cudaErrorInvalidValue;
+    if (k <= 4) launch_gs_kb<4>(mode, w, wo, V, k, c, sc, len, partials, counter, out, s);
+    else if (k <= 8) launch_gs_kb<8>(mode, w, wo, V, k, c, sc, len, partials, counter, out, s);
+    else if (k <= 16) launch_gs_kb<16>(mode, w, wo, V, k, c, sc, len, partials, counter, out, s);
+    else launch_gs_kb<GS_KMAX>(mode, w, wo, V, k, c, sc, len, partials, counter, out, s);
+    return cudaGetLastError();
+}
+int gs_partials_needed() { return (GS_KMAX + 1) * GS_BLOCKS; }
+
 cudaError_t launch_dots(const double* w, const VecPtrs& V, int k, int64_t len, double* partials, unsigned* counter,
                         double* out, cudaStream_t s) {
-    vec_dots_kernel<<<DOT_BLOCKS, DOT_NT, 0, s>>>(w, V, k, len, partials, counter, out);
+    launch_k(vec_dots_kernel, DOT_BLOCKS, DOT_NT, 0, s, w, V, k, len, partials, counter, out);
     return cudaGetLastError();
 }
 cudaError_t launch_update(double* w, const VecPtrs& V, int k, const double* c, int64_t len, cudaStream_t s) {
-    vec_update_kernel<<<2 * DOT_BLOCKS, DOT_NT, 0, s>>>(w, V, k, c, len);
+    launch_k(vec_update_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, w, V, k, c, len);
     return cudaGetLastError();
 }
 cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cudaStream_t s) {
-    vec_scale_kernel<<<2 * DOT_BLOCKS, DOT_NT, 0, s>>>(y, x, sc, len);
+    launch_k(vec_scale_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, y, x, sc, len);
     return cudaGetLastError();
 }
 int dot_partials_needed() { return VK * DOT_BLOCKS; }
@@ -2377,13 +2583,13 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
     if (P.L.n <= g_small_tile_n) {
         using T = VTile<VSX, VSY>;
         dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
-        if (x_zero) vanka_kernel<true, VSX, VSY><<<grid, T::NT, T::SMEM, s>>>(P, x, b, xo, S);
-        else vanka_kernel<false, VSX, VSY><<<grid, T::NT, T::SMEM, s>>>(P, x, b, xo, S);
+        if (x_zero) launch_k(vanka_kernel<true, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+        else launch_k(vanka_kernel<false, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
         return cudaGetLastError();
     }
     dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
-    if (x_zero) vanka_kernel<true><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
-    else vanka_kernel<false><<<grid, VNT, V_SMEM, s>>>(P, x, b, xo, S);
+    if (x_zero) launch_k(vanka_kernel<true>, grid, VNT, V_SMEM, s, P, x, b, xo, S);
+    else launch_k(vanka_kernel<false>, grid, VNT, V_SMEM, s, P, x, b, xo, S);
     return cudaGetLastError();
 }
 
@@ -2397,8 +2603,8 @@ cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const doub
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, MT, MR, 2);
     dim3 grid((L.n + MT) / MT, (L.n + MH) / MH);
-    if (x_zero) vanka_march_kernel<true><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
-    else vanka_march_kernel<false><<<grid, MNT, M_SMEM, s>>>(mx, mb, P, xo, S, MH);
+    if (x_zero) launch_k(vanka_march_kernel<true>, grid, MNT, M_SMEM, s, mx, mb, P, xo, S, MH);
+    else launch_k(vanka_march_kernel<false>, grid, MNT, M_SMEM, s, mx, mb, P, xo, S, MH);
     return cudaGetLastError();
 }
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
@@ -2415,9 +2621,9 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
-    if (x_zero) vanka_march2_kernel<true, false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH, none);
-    else if (E) vanka_march2_kernel<false, true><<<grid, M2NT + 32 * M2NP, M2SMEM, s>>>(mx, mb, P, xo, S, MH, *E);
-    else vanka_march2_kernel<false, false><<<grid, M2NT, M2SMEM, s>>>(mx, mb, P, xo, S, MH, none);
+    if (x_zero) launch_k(vanka_march2_kernel<true, false>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
+    else if (E) launch_k(vanka_march2_kernel<false, true>, grid, M2NT + 32 * M2NP, M2SMEM, s, mx, mb, P, xo, S, MH, *E);
+    else launch_k(vanka_march2_kernel<false, false>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
     return cudaGetLastError();
 }
 int blocks_vanka_march2(int n) {
@@ -2433,8 +2639,8 @@ cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const dou
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, M3T, M3R, 4);
     dim3 grid((L.n + M3T) / M3T, (L.n + MH) / MH);
-    if (x_zero) vanka_march3_kernel<true><<<grid, M3NT, M3SMEM, s>>>(mx, P, b, xo, S, MH);
-    else vanka_march3_kernel<false><<<grid, M3NT, M3SMEM, s>>>(mx, P, b, xo, S, MH);
+    if (x_zero) launch_k(vanka_march3_kernel<true>, grid, M3NT, M3SMEM, s, mx, P, b, xo, S, MH);
+    else launch_k(vanka_march3_kernel<false>, grid, M3NT, M3SMEM, s, mx, P, b, xo, S, MH);
     return cudaGetLastError();
 }
 int blocks_vanka_march3(int n) {
@@ -2457,7 +2663,7 @@ cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, BMA_T, BQ_R, 3, std::max(32, L.n / 64));
     dim3 grid((L.n + BMA_T) / BMA_T, (L.n + MH) / MH);
-#define BA_LAUNCH(H_, Z_) bsr_a_march_kernel<H_, Z_><<<grid, BQ_NT, BMA_SMEM, s>>>(mx, mb, mk, L, U, omJ, g, dp, S, MH)
+#define BA_LAUNCH(H_, Z_) launch_k(bsr_a_march_kernel<H_, Z_>, grid, BQ_NT, BMA_SMEM, s, mx, mb, mk, L, U, omJ, g, dp, S, MH)
     if (het && x_zero) BA_LAUNCH(true, true);
     else if (het) BA_LAUNCH(true, false);
     else if (x_zero) BA_LAUNCH(false, true);
@@ -2477,7 +2683,7 @@ cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, BB_T, BQ_R, 3, std::max(32, L.n / 64));
     dim3 grid((L.n + BB_T) / BB_T, (L.n + MH) / MH);
-#define BB_LAUNCH(H_, Z_) bsr_b_march_kernel<H_, Z_><<<grid, BQ_NT, BB2_SMEM, s>>>(mx, mb, md, mk, L, U, omega, xo, MH)
+#define BB_LAUNCH(H_, Z_) launch_k(bsr_b_march_kernel<H_, Z_>, grid, BQ_NT, BB2_SMEM, s, mx, mb, md, mk, L, U, omega, xo, MH)
     if (het && x_zero) BB_LAUNCH(true, true);
     else if (het) BB_LAUNCH(true, false);
     else if (x_zero) BB_LAUNCH(false, true);
@@ -2495,8 +2701,8 @@ cudaError_t launch_restrict_march(const LevelParams& Lf, int nc, int pitchc, con
     if (e != cudaSuccess) return e;
     const int MH = march_height(nc, QT, QR, 3, 128);
     dim3 grid((nc + QT) / QT, (nc + MH) / MH);
-    if (Lf.kinv_field) restrict_march_kernel<true><<<grid, QNT, Q_SMEM, s>>>(mx, mb, Lf, nc, pitchc, bc, MH);
-    else restrict_march_kernel<false><<<grid, QNT, Q_SMEM, s>>>(mx, mb, Lf, nc, pitchc, bc, MH);
+    if (Lf.kinv_field) launch_k(restrict_march_kernel<true>, grid, QNT, Q_SMEM, s, mx, mb, Lf, nc, pitchc, bc, MH);
+    else launch_k(restrict_march_kernel<false>, grid, QNT, Q_SMEM, s, mx, mb, Lf, nc, pitchc, bc, MH);
     return cudaGetLastError();
 }
 
@@ -2506,23 +2712,23 @@ cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode,
         using T = CTile<CSX, CSY>;
         dim3 grid((nc + CSX) / CSX, (nc + CSY) / CSY);
         if (mode == 1) {
-            if (Lf.kinv_field) restrict_kernel<1, true, CSX, CSY><<<grid, T::NT, T::SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
-            else restrict_kernel<1, false, CSX, CSY><<<grid, T::NT, T::SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
+            if (Lf.kinv_field) launch_k(restrict_kernel<1, true, CSX, CSY>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+            else launch_k(restrict_kernel<1, false, CSX, CSY>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
         } else if (mode == 0) {
-            restrict_kernel<0, false, CSX, CSY><<<grid, T::NT, T::SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+            launch_k(restrict_kernel<0, false, CSX, CSY>, grid, T::NT, T::SMEM_PLAIN, s, Lf, nc, pitchc, x, br, bc);
         } else {
-            restrict_kernel<2, false, CSX, CSY><<<grid, T::NT, T::SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+            launch_k(restrict_kernel<2, false, CSX, CSY>, grid, T::NT, T::SMEM_PLAIN, s, Lf, nc, pitchc, x, br, bc);
         }
         return cudaGetLastError();
     }
     dim3 grid((nc + CX) / CX, (nc + CY) / CY);
     if (mode == 1) {
-        if (Lf.kinv_field) restrict_kernel<1, true><<<grid, CNT, C_SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
-        else restrict_kernel<1, false><<<grid, CNT, C_SMEM_FUSED, s>>>(Lf, nc, pitchc, x, br, bc);
+        if (Lf.kinv_field) launch_k(restrict_kernel<1, true>, grid, CNT, C_SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+        else launch_k(restrict_kernel<1, false>, grid, CNT, C_SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
     } else if (mode == 0) {
-        restrict_kernel<0, false><<<grid, CNT, C_SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+        launch_k(restrict_kernel<0, false>, grid, CNT, C_SMEM_PLAIN, s, Lf, nc, pitchc, x, br, bc);
     } else {
-        restrict_kernel<2, false><<<grid, CNT, C_SMEM_PLAIN, s>>>(Lf, nc, pitchc, x, br, bc);
+        launch_k(restrict_kernel<2, false>, grid, CNT, C_SMEM_PLAIN, s, Lf, nc, pitchc, x, br, bc);
     }
     return cudaGetLastError();
 }
@@ -2530,14 +2736,14 @@ cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode,
 cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double* e, double* x, const int* stop,
                            cudaStream_t s) {
     dim3 grid((nc + 31) / 32, (nc + 7) / 8);
-    prolong_kernel<<<grid, 256, 0, s>>>(nf, pitchf, nc, pitchc, e, x, stop);
+    launch_k(prolong_kernel, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
     return cudaGetLastError();
 }
 
 cudaError_t launch_coarse(int N, const double* G, const int64_t* slots, const double* b, double* x,
                           const int* stop, cudaStream_t s) {
     int blocks = N <= 1024 ? 1 : (N + 255) / 256;
-    coarse_kernel<<<blocks, 256, N * 8, s>>>(N, G, slots, b, x, stop);
+    launch_k(coarse_kernel, blocks, 256, N * 8, s, N, G, slots, b, x, stop);
     return cudaGetLastError();
 }
 
@@ -2545,26 +2751,26 @@ cudaError_t launch_bsr_a(const LevelParams& L, const DispParams& U, double omJ, 
                          double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s) {
     dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     const bool het = L.kinv_field != nullptr;
-    if (het && x_zero) bsr_a_kernel<true, true><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
-    else if (het) bsr_a_kernel<true, false><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
-    else if (x_zero) bsr_a_kernel<false, true><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
-    else bsr_a_kernel<false, false><<<grid, BANT, BA_SMEM, s>>>(L, U, omJ, x, b, g, dp, S);
+    if (het && x_zero) launch_k(bsr_a_kernel<true, true>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
+    else if (het) launch_k(bsr_a_kernel<true, false>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
+    else if (x_zero) launch_k(bsr_a_kernel<false, true>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
+    else launch_k(bsr_a_kernel<false, false>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bsr_jacobi(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
                               cudaStream_t s) {
     dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
-    if (L.kinv_field) bsr_jacobi_kernel<true><<<grid, 256, 0, s>>>(L, omJ, g, dpi, dpo);
-    else bsr_jacobi_kernel<false><<<grid, 256, 0, s>>>(L, omJ, g, dpi, dpo);
+    if (L.kinv_field) launch_k(bsr_jacobi_kernel<true>, grid, 256, 0, s, L, omJ, g, dpi, dpo);
+    else launch_k(bsr_jacobi_kernel<false>, grid, 256, 0, s, L, omJ, g, dpi, dpo);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
                                cudaStream_t s) {
     dim3 grid((L.n + JT_X) / JT_X, (L.n + JT_Y) / JT_Y);
-    if (L.kinv_field) bsr_jacobi2_kernel<true><<<grid, JNT, 0, s>>>(L, omJ, g, dpi, dpo);
-    else bsr_jacobi2_kernel<false><<<grid, JNT, 0, s>>>(L, omJ, g, dpi, dpo);
+    if (L.kinv_field) launch_k(bsr_jacobi2_kernel<true>, grid, JNT, 0, s, L, omJ, g, dpi, dpo);
+    else launch_k(bsr_jacobi2_kernel<false>, grid, JNT, 0, s, L, omJ, g, dpi, dpo);
     return cudaGetLastError();
 }
 
@@ -2572,21 +2778,21 @@ cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega
                          const double* dp, double* xo, bool x_zero, cudaStream_t s) {
     dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     const bool het = L.kinv_field != nullptr;
-    if (het && x_zero) bsr_b_kernel<true, true><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
-    else if (het) bsr_b_kernel<true, false><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
-    else if (x_zero) bsr_b_kernel<false, true><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
-    else bsr_b_kernel<false, false><<<grid, BBNT, BB_SMEM, s>>>(L, U, omega, x, b, dp, xo);
+    if (het && x_zero) launch_k(bsr_b_kernel<true, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
+    else if (het) launch_k(bsr_b_kernel<true, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
+    else if (x_zero) launch_k(bsr_b_kernel<false, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
+    else launch_k(bsr_b_kernel<false, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
     return cudaGetLastError();
 }
 
 cudaError_t launch_kinv_from_K(int n, int pitch, const double* K, double* kinv, cudaStream_t s) {
     dim3 grid((n + 31) / 32, (n + 7) / 8);
-    kinv_from_K_kernel<<<grid, 256, 0, s>>>(n, pitch, K, kinv);
+    launch_k(kinv_from_K_kernel, grid, 256, 0, s, n, pitch, K, kinv);
     return cudaGetLastError();
 }
 
 cudaError_t launch_kinv_coarsen(int nf, int pitchf, const double* kf, int pitchc, double* kc, cudaStream_t s) {
     dim3 grid((nf / 2 + 31) / 32, (nf / 2 + 7) / 8);
-    kinv_coarsen_kernel<<<grid, 256, 0, s>>>(nf, pitchf, kf, pitchc, kc);
+    launch_k(kinv_coarsen_kernel, grid, 256, 0, s, nf, pitchf, kf, pitchc, kc);
     return cudaGetLastError();
 }

@@ -17,6 +17,21 @@ struct VecPtrs {
     const double* p[8];
 };
 
+// Gram-Schmidt pass over up to GS_KMAX basis vectors in one sweep of memory (vec_gs_kernel):
+//   mode 0: out[q] = <w, V_q> (q < k), out[k] = <w, w>
+//   mode 1: o = w - sum_q c_q V_q (written to wo, may alias w), out[q] = <o, V_q>, out[k] = <o, o>
+// (c_q is scaled by sc[q] when sc != nullptr)
+//   mode 2: o = w - sum_q c_q V_q (written to wo), out[0] = <o, o>
+//   mode 3: o = w - sum_q c_q V_q (written to wo), no reduction
+// Reductions are deterministic (per-block partials summed in block order by the last block).
+constexpr int GS_KMAX = 32;
+struct GsPtrs {
+    const double* p[GS_KMAX];
+};
+cudaError_t launch_gs(int mode, const double* w, double* wo, const GsPtrs& V, int k, const double* c,
+                      const double* sc, int64_t len, double* partials, unsigned* counter, double* out, cudaStream_t s);
+int gs_partials_needed();
+
 // All launchers return cudaGetLastError() of the launch.
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r,
                             NormSink norm, cudaStream_t s);
@@ -41,6 +56,8 @@ int blocks_vanka_march2(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)
 void set_small_tile_n(int N);
+// programmatic dependent launch of every kernel (1, default) or plain stream order (0)
+void set_pdl(int on);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march3(int n);
