@@ -2226,7 +2226,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFn g_encode = nullptr;
 
-static int g_pdl = 1;   // programmatic dependent launch on (mg_setup: MG_PDL=0 turns it off)
+static int g_pdl = 0;   // programmatic dependent launch (MG_PDL=1; measured no gain on the cycle graph)
 void set_pdl(int on) { g_pdl = on; }
 
 template <typename... KArgs, typename... Args>
