@@ -1475,6 +1475,14 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
             }
         }
         csync();
+        // every warp is past the owner phase of step s - 1 (the last reader of the x and r ring rows
+        // that group s + 1 replaces): refill them.  The owner phase of a step and the residual phase
+        // of the next need no barrier between them (disjoint ring rows), so this is the only one.
+        // (PROL keeps the end-of-step refill: its producer warps need the longer lead time)
+        if (!PROL && t == 0 && s >= 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s + 1);
+        }
         // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
         if ((t & 31) < M2C) {
             const int q = t >> 5, px = t & 31;
@@ -1529,10 +1537,12 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
                 }
             }
         }
-        csync();
-        if (t == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(s + 2);
+        if (PROL) {
+            csync();
+            if (t == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(s + 2);
+            }
         }
     }
     if (S.out || S.state) norm_finish<PROL ? M2NT + 32 * M2NP : M2NT>(S, nrm);
