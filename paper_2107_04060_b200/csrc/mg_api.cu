@@ -104,6 +104,8 @@ struct mg_ctx {
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
+    int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one CTA
+                                  // (measured slower: 442 vs 250 us per 256^2 cycle -- one SM is compute bound)
     int jacobi_pair = 0;          // 1: two Jacobi sweeps per launch (bsr_jacobi2_kernel; measured slower:
                                   //    292 us vs 2 x 110 us at 2048^2, the per-tile halo work dominates)
     int bsr_impl = 1;             // 1: row-marching BSR stages on levels with n >= march_min_n, 0: 2-D tiles
@@ -189,6 +191,16 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     return MG_OK;
 }
 
+// first level handled by the single-CTA bottom kernel, or -1
+int bottom_level(const mg_ctx* c, const mg_cycle_opts& o) {
+    const int Lc = c->levels - 1;
+    if (c->bottom_n <= 0 || o.relax != MG_VANKA || o.nu1 < 1 || o.nu2 < 1 || !c->Ginv || c->het) return -1;
+    int lb = -1;
+    for (int l = Lc - 1; l >= 1; --l)
+        if (c->L[l].n <= c->bottom_n && Lc - l <= BOT_MAXL) lb = l;
+    return lb;
+}
+
 // enqueue one V(nu1, nu2) cycle (PAPER.md:471-476 recursed).  solve != 0: the
 // first level-0 operation appends ||b - A x||^2 to the solve state.
 int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& o, int solve, double* nout,
@@ -214,7 +226,9 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         CK(launch_residual(c->L[0].vp.L, x0, b0, nullptr, S, s));
         S = no_norm();
     }
+    const int lb = bottom_level(c, o);
     for (int l = 0; l < Lc; ++l) {
+        if (l == lb) break;
         Level& Lv = c->L[l];
         double* xl = l == 0 ? x0 : Lv.x;
         const double* bl = l == 0 ? b0 : Lv.b;
@@ -240,10 +254,46 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         if (int rc = lmark()) return rc;
         cur[l] = a;
     }
-    CK(launch_coarse(c->Nc, c->Ginv, c->slots, c->L[Lc].b, c->L[Lc].x, c->stop, s));
-    if (int rc = lmark()) return rc;
-    cur[Lc] = c->L[Lc].x;
+    if (lb >= 0) {
+        // levels lb .. Lc in one CTA; the host replays its buffer swaps to know where level lb ends
+        BottomArgs A{};
+        A.nl = Lc - lb;
+        A.nu1 = o.nu1;
+        A.nu2 = o.nu2;
+        for (int i = 0; i <= A.nl; ++i) {
+            Level& Lv = c->L[lb + i];
+            A.x[i] = Lv.x;
+            A.b[i] = Lv.b;
+            A.pitch[i] = Lv.pitch;
+            if (i < A.nl) {
+                A.vp[i] = Lv.vp;
+                A.vp[i].omega = o.omega;
+                A.t[i] = Lv.t;
+            }
+        }
+        A.N = c->Nc;
+        A.G = c->Ginv;
+        A.slots = c->slots;
+        A.stop = c->stop;
+        CK(launch_bottom(A, s));
+        for (int i = 0; i < A.nl; ++i) {
+            double* a = A.x[i];
+            double* t = A.t[i];
+            for (int k = 0; k < o.nu1; ++k) std::swap(a, t);
+            t = (a == A.x[i]) ? A.t[i] : A.x[i];
+            for (int k = 0; k < o.nu2; ++k) std::swap(a, t);
+            cur[lb + i] = a;
+        }
+        cur[Lc] = c->L[Lc].x;
+        for (int k = 0; k < 4 * A.nl + 1; ++k)   // the per-level timing slots of levels lb .. Lc
+            if (int rc = lmark()) return rc;
+    } else {
+        CK(launch_coarse(c->Nc, c->Ginv, c->slots, c->L[Lc].b, c->L[Lc].x, c->stop, s));
+        if (int rc = lmark()) return rc;
+        cur[Lc] = c->L[Lc].x;
+    }
     for (int l = Lc - 1; l >= 0; --l) {
+        if (lb >= 0 && l >= lb) continue;
         Level& Lv = c->L[l];
         if (l == 0)
             if (int rc = mark(3)) return rc;
@@ -377,6 +427,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_SMALL_TILE_N")) set_small_tile_n(atoi(v));
     if (const char* v = getenv("MG_PDL")) set_pdl(atoi(v) != 0);
     if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v) != 0;
+    if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
     auto bail = [&](int rc) {
         mg_free(c);

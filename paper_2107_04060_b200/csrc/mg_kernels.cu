@@ -106,16 +106,29 @@ __device__ void norm_finish(const NormSink& S, double v) {
 }
 
 // zero-padded tile load: dst[p][ly][lx] = src(p, j0+ly, i0+lx) for 0 <= i, j <= n, else 0
-template <int W, int HT, int NP>
+// global load through the read-only path (NC) or a plain load (coherent with earlier writes of the
+// same kernel on this SM: the single-CTA bottom kernel reads what it wrote)
+template <bool NC>
+__device__ __forceinline__ double gld(const double* p) {
+    if (NC) return __ldg(p);
+    return *p;
+}
+
+template <int W, int HT, int NP, bool NC = true>
 __device__ __forceinline__ void load_tile(double* __restrict__ dst, const double* __restrict__ src, int i0,
-                                          int j0, int n, int pitch, int64_t plane, int p0 = 0) {
-    for (int t = threadIdx.x; t < NP * W * HT; t += blockDim.x) {
+                                          int j0, int n, int pitch, int64_t plane, int p0 = 0, int t0 = -1,
+                                          int nt = 0) {
+    if (t0 < 0) {
+        t0 = threadIdx.x;
+        nt = blockDim.x;
+    }
+    for (int t = t0; t < NP * W * HT; t += nt) {
         int p = t / (W * HT);
         int rem = t - p * (W * HT);
         int ly = rem / W;
         int lx = rem - ly * W;
         int i = i0 + lx, j = j0 + ly;
-        dst[t] = (i >= 0 && i <= n && j >= 0 && j <= n) ? __ldg(src + (p0 + p) * plane + (int64_t)j * pitch + i)
+        dst[t] = (i >= 0 && i <= n && j >= 0 && j <= n) ? gld<NC>(src + (p0 + p) * plane + (int64_t)j * pitch + i)
                                                          : 0.0;
     }
 }
@@ -184,7 +197,7 @@ __device__ __forceinline__ void apply_rows_kr(const LevelParams& L, const double
 
 // r = b - A x for the 10 DoFs of index (i, j); xs is a W x HT x 10 tile holding (i, j) at
 // (lx, ly) with a ring of at least 1.  Inactive rows give 0.
-template <int W, int HT, bool HET>
+template <int W, int HT, bool HET, bool NC = true>
 __device__ __forceinline__ void residual_at(const LevelParams& L, const double* __restrict__ xs, int lx, int ly,
                                             int i, int j, const double* __restrict__ b, double r[10]) {
     const double* x0 = xs + ly * W + lx;
@@ -194,7 +207,7 @@ __device__ __forceinline__ void residual_at(const LevelParams& L, const double* 
     const int64_t o = (int64_t)j * L.pitch + i;
     const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
 #pragma unroll
-    for (int k = 0; k < 10; ++k) r[k] = is_active(k, i, j, n) ? (__ldg(b + k * L.plane + (in ? o : 0)) - av[k]) : 0.0;
+    for (int k = 0; k < 10; ++k) r[k] = is_active(k, i, j, n) ? (gld<NC>(b + k * L.plane + (in ? o : 0)) - av[k]) : 0.0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -341,41 +354,40 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
     }
 }
 
-template <bool XZERO, int TX = VTX, int TY = VTY>
-__global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
-                                                       const double* __restrict__ b, double* __restrict__ xo,
-                                                       NormSink S) {
-    pdl_wait();
-    pdl_trigger();
+// one TX x TY tile of the sweep, run by threads t = 0 .. T::NT-1 of a (virtual) block with shared
+// memory sm; every thread executes the three barriers, `active` = false skips the work (tiles of
+// the bottom kernel's last round).  Returns the thread's share of ||r||^2.
+template <bool XZERO, int TX, int TY, bool NC>
+__device__ __forceinline__ double vanka_tile(const VankaParams& P, const double* __restrict__ x,
+                                             const double* __restrict__ b, double* __restrict__ xo, int bx, int by,
+                                             int t, double* sm, bool active) {
     using T = VTile<TX, TY>;
-    extern __shared__ double sm[];
     double* xs = sm;          // x tile (phase 1)
     double* cs = sm;          // patch corrections (phase 2-3), overlays xs
     double* rs = sm + T::USZ;  // residual tile
     const LevelParams& L = P.L;
-    if (*L.stop) return;
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-    const int t = threadIdx.x;
+    const int i0 = bx * TX, j0 = by * TY;
+    const int tl = active ? t : 1 << 20;   // inactive: no thread takes a position
     // phase 1: r = b - A x on the tile + 1 ring (one index per thread; straight-line code keeps
     // the stencil coefficients as constant-bank operands instead of hoisted registers)
     if (!XZERO) {
-        load_tile<T::XW, T::XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        if (active) load_tile<T::XW, T::XH, 10, NC>(xs, x, i0 - 2, j0 - 2, n, pitch, plane, 0, t, T::NT);
         __syncthreads();
-        if (t < T::RW * T::RH) {
+        if (tl < T::RW * T::RH) {
             const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<T::XW, T::XH, false>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            residual_at<T::XW, T::XH, false, NC>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
             for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
     } else {
-        load_tile<T::RW, T::RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);  // r = b (x = 0)
+        if (active) load_tile<T::RW, T::RH, 10, NC>(rs, b, i0 - 1, j0 - 1, n, pitch, plane, 0, t, T::NT);  // r = b (x = 0)
     }
     __syncthreads();
     // phase 2: patch solves at the vertices of the tile + high ring
-    if (t < T::PW * T::PH) {
+    if (tl < T::PW * T::PH) {
         const int py = t / T::PW, px = t - py * T::PW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const Vanka
     __syncthreads();
     // phase 3: owners sum the corrections of the (up to) 4 patches touching their DoFs
     double nrm = 0.0;
-    if (t < TX * TY) {
+    if (tl < TX * TY) {
         const int lx = t % TX, ly = t / TX;
         const int i = i0 + lx, j = j0 + ly;
         if (i <= n && j <= n) {
@@ -412,14 +424,26 @@ __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const Vanka
             const double* r00 = rs + (ly + 1) * T::RW + (lx + 1);
 #pragma unroll
             for (int k = 0; k < 10; ++k) {
-                const double xv = XZERO ? 0.0 : __ldg(x + k * plane + o);
+                const double xv = XZERO ? 0.0 : gld<NC>(x + k * plane + o);
                 xo[k * plane + o] = is_active(k, i, j, n) ? fma(P.omega, d[k], xv) : 0.0;
                 const double rv = r00[k * T::RW * T::RH];
                 nrm = fma(rv, rv, nrm);
             }
         }
     }
-    if (S.out || S.state) norm_finish<T::NT>(S, nrm);
+    return nrm;
+}
+
+template <bool XZERO, int TX = VTX, int TY = VTY>
+__global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
+                                                       const double* __restrict__ b, double* __restrict__ xo,
+                                                       NormSink S) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double sm[];
+    if (*P.L.stop) return;
+    const double nrm = vanka_tile<XZERO, TX, TY, true>(P, x, b, xo, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
+    if (S.out || S.state) norm_finish<VTile<TX, TY>::NT>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -438,37 +462,33 @@ struct CTile {
 };
 constexpr int CSX = 4, CSY = 2;             // small restriction tiles: 64 threads
 
-template <int MODE, bool HET, int TX = CX, int TY = CY>
-__global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const LevelParams L, int nc, int pitchc,
-                                                          const double* __restrict__ x,
-                                                          const double* __restrict__ br,
-                                                          double* __restrict__ bc) {
-    pdl_wait();
-    pdl_trigger();
+// one tile of the restriction (see vanka_tile for t / sm / active); both barriers are executed by
+// every thread
+template <int MODE, bool HET, int TX, int TY, bool NC>
+__device__ __forceinline__ void restrict_tile(const LevelParams& L, int nc, int pitchc, const double* __restrict__ x,
+                                              const double* __restrict__ br, double* __restrict__ bc, int bx,
+                                              int by, int t, double* sm, bool active) {
     using T = CTile<TX, TY>;
-    extern __shared__ double sm[];
     double* rs = sm;
     double* xs = sm + 10 * T::RW * T::RH;
-    if (*L.stop) return;
-    const int I0 = blockIdx.x * TX, J0 = blockIdx.y * TY;
+    const int I0 = bx * TX, J0 = by * TY;
     const int fi0 = 2 * I0 - 2, fj0 = 2 * J0 - 2;
-    const int t = threadIdx.x;
     if (MODE == 1) {
-        load_tile<T::XW, T::XH, 10>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane);
+        if (active) load_tile<T::XW, T::XH, 10, NC>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane, 0, t, T::NT);
         __syncthreads();
-        if (t < T::RW * T::RH) {
+        if (active && t < T::RW * T::RH) {
             const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, fi0 + lx, fj0 + ly, br, rv);
+            residual_at<T::XW, T::XH, HET, NC>(L, xs, lx + 1, ly + 1, fi0 + lx, fj0 + ly, br, rv);
 #pragma unroll
             for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
     } else {
-        load_tile<T::RW, T::RH, 10>(rs, br, fi0, fj0, L.n, L.pitch, L.plane);
+        if (active) load_tile<T::RW, T::RH, 10, NC>(rs, br, fi0, fj0, L.n, L.pitch, L.plane, 0, t, T::NT);
     }
     __syncthreads();
     // coarse outputs: (coarse index, pair of planes) per thread; the plane pair is warp uniform
-    if (t >= 5 * TX * TY) return;
+    if (!active || t >= 5 * TX * TY) return;
     const int c = t % (TX * TY), grp = t / (TX * TY);
     const int cy = c / TX, cx = c - cy * TX;
     const int I = I0 + cx, J = J0 + cy;
@@ -493,6 +513,18 @@ __global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const Le
 #undef OUT
 #undef MG_T
 #undef RF
+}
+
+template <int MODE, bool HET, int TX = CX, int TY = CY>
+__global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const LevelParams L, int nc, int pitchc,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ br,
+                                                          double* __restrict__ bc) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double sm[];
+    if (*L.stop) return;
+    restrict_tile<MODE, HET, TX, TY, true>(L, nc, pitchc, x, br, bc, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -531,6 +563,117 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
 #undef PROL2
 #undef MG_Q
 #undef EC
+}
+
+// ------------------------------------------------------------------------------------------
+// Bottom of the V-cycle in ONE CTA (Vanka, levels with n <= 32 down to the coarsest): the same tile
+// functions as the per-level kernels, run by 16 virtual blocks of 64 threads over the tiles of a
+// level in rounds, with CTA barriers between the steps instead of kernel boundaries.  Loads are
+// plain (not read-only path): the kernel reads what it wrote.  Bitwise the per-level sequence.
+constexpr int BOT_VB = 12, BOT_NT = BOT_VB * 64;
+constexpr int BOT_VSM = VTile<VSX, VSY>::SMEM > CTile<CSX, CSY>::SMEM_FUSED ? VTile<VSX, VSY>::SMEM
+                                                                           : CTile<CSX, CSY>::SMEM_FUSED;
+constexpr int BOT_SMEM = BOT_VB * BOT_VSM;
+static_assert(VTile<VSX, VSY>::NT == 64 && CTile<CSX, CSY>::NT == 64, "virtual blocks of 64 threads");
+static_assert(BOT_SMEM <= 227 * 1024, "bottom kernel shared memory");
+
+__global__ void __launch_bounds__(BOT_NT, 1) bottom_kernel(const __grid_constant__ BottomArgs A) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double sm[];
+    if (*A.stop) return;
+    const int vb = threadIdx.x >> 6, t = threadIdx.x & 63;
+    double* vsm = sm + vb * (BOT_VSM / 8);
+    auto relax = [&](int l, const double* xin, double* xo, bool xzero) {
+        const VankaParams& P = A.vp[l];
+        const int n = P.L.n, tx = (n + VSX) / VSX, ntiles = tx * ((n + VSY) / VSY);
+        for (int r0 = 0; r0 < ntiles; r0 += BOT_VB) {
+            const int tile = r0 + vb;
+            const bool act = tile < ntiles;
+            const int bx = act ? tile % tx : 0, by = act ? tile / tx : 0;
+            if (xzero) vanka_tile<true, VSX, VSY, false>(P, xin, A.b[l], xo, bx, by, t, vsm, act);
+            else vanka_tile<false, VSX, VSY, false>(P, xin, A.b[l], xo, bx, by, t, vsm, act);
+            __syncthreads();
+        }
+    };
+    auto restrict_ = [&](int l, const double* xl) {
+        const LevelParams& L = A.vp[l].L;
+        const int nc = L.n / 2, tx = (nc + CSX) / CSX, ntiles = tx * ((nc + CSY) / CSY);
+        for (int r0 = 0; r0 < ntiles; r0 += BOT_VB) {
+            const int tile = r0 + vb;
+            const bool act = tile < ntiles;
+            const int bx = act ? tile % tx : 0, by = act ? tile / tx : 0;
+            restrict_tile<1, false, CSX, CSY, false>(L, nc, A.pitch[l + 1], xl, A.b[l], A.b[l + 1], bx, by, t, vsm, act);
+            __syncthreads();
+        }
+    };
+    // x_f += P e_c on level l from e on level l + 1 (prolong_kernel's arithmetic, plain loads)
+    auto prolong_ = [&](int l, const double* e, double* x) {
+        const int nf = A.vp[l].L.n, pitchf = A.vp[l].L.pitch, nc = nf / 2, pitchc = A.pitch[l + 1];
+        const int64_t planec = (int64_t)(nc + 1) * pitchc, planef = (int64_t)(nf + 1) * pitchf;
+        for (int cell = threadIdx.x; cell < nc * nc; cell += BOT_NT) {
+            const int I = cell % nc, J = cell / nc;
+            const double* e0 = e + (int64_t)J * pitchc + I;
+#define EC(dI, dJ, pl) e0[(pl) * planec + (dJ) * pitchc + (dI)]
+#define MG_Q(dI, dJ, pl, w) v = fma(w, EC(dI, dJ, pl), v);
+            const int fi = 2 * I, fj = 2 * J;
+            double* x0 = x + (int64_t)fj * pitchf + fi;
+#define PROL2(dj, kf)                                                                   \
+    {                                                                                   \
+        double v = 0.0;                                                                 \
+        MG_PROLONG_0_##dj##_##kf(MG_Q) const double v0 = v;                             \
+        v = 0.0;                                                                        \
+        MG_PROLONG_1_##dj##_##kf(MG_Q) const double v1 = v;                             \
+        double2* p2 = reinterpret_cast<double2*>(x0 + kf * planef + dj * pitchf);       \
+        double2 xv = *p2;                                                               \
+        if (is_active(kf, fi, fj + dj, nf)) xv.x += v0;                                 \
+        if (is_active(kf, fi + 1, fj + dj, nf)) xv.y += v1;                             \
+        *p2 = xv;                                                                       \
+    }
+#define PROL4(kf) PROL2(0, kf) PROL2(1, kf)
+            PROL4(0) PROL4(1) PROL4(2) PROL4(3) PROL4(4) PROL4(5) PROL4(6) PROL4(7) PROL4(8) PROL4(9)
+#undef PROL4
+#undef PROL2
+#undef MG_Q
+#undef EC
+        }
+        __syncthreads();
+    };
+    const int nl = A.nl;
+    double* cur[BOT_MAXL + 1];
+    for (int l = 0; l < nl; ++l) {
+        double* a = A.x[l];
+        double* tt = A.t[l];
+        for (int k = 0; k < A.nu1; ++k) {
+            relax(l, a, tt, k == 0);
+            double* sw = a; a = tt; tt = sw;
+        }
+        restrict_(l, a);
+        cur[l] = a;
+    }
+    // coarsest: x_c[slots] = G b_c[slots] (coarse_kernel's arithmetic)
+    {
+        double* rb = sm;
+        for (int k = threadIdx.x; k < A.N; k += BOT_NT) rb[k] = A.b[nl][A.slots[k]];
+        __syncthreads();
+        for (int row = threadIdx.x; row < A.N; row += BOT_NT) {
+            double acc = 0.0;
+            for (int k = 0; k < A.N; ++k) acc = fma(__ldg(A.G + (int64_t)k * A.N + row), rb[k], acc);
+            A.x[nl][A.slots[row]] = acc;
+        }
+        __syncthreads();
+        cur[nl] = A.x[nl];
+    }
+    for (int l = nl - 1; l >= 0; --l) {
+        prolong_(l, cur[l + 1], cur[l]);
+        double* a = cur[l];
+        double* tt = (a == A.x[l]) ? A.t[l] : A.x[l];
+        for (int k = 0; k < A.nu2; ++k) {
+            relax(l, a, tt, false);
+            double* sw = a; a = tt; tt = sw;
+        }
+        cur[l] = a;
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2275,6 +2418,7 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
 }
 
 void kernels_init() {
+    set_smem(bottom_kernel, BOT_SMEM);
     set_smem(vanka_march3_kernel<false>, M3SMEM);
     set_smem(vanka_march3_kernel<true>, M3SMEM);
     set_smem(vanka_march2_kernel<false, false>, M2SMEM);
@@ -2740,6 +2884,11 @@ cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode,
     } else {
         launch_k(restrict_kernel<2, false>, grid, CNT, C_SMEM_PLAIN, s, Lf, nc, pitchc, x, br, bc);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bottom(const BottomArgs& A, cudaStream_t s) {
+    launch_k(bottom_kernel, 1, BOT_NT, BOT_SMEM, s, A);
     return cudaGetLastError();
 }
 

@@ -32,6 +32,23 @@ cudaError_t launch_gs(int mode, const double* w, double* wo, const GsPtrs& V, in
                       const double* sc, int64_t len, double* partials, unsigned* counter, double* out, cudaStream_t s);
 int gs_partials_needed();
 
+// The bottom of a Vanka V-cycle in one CTA (bottom_kernel): levels lb .. lb + nl - 1 (n <= 32) and
+// the coarsest lb + nl.  Index l below is relative to lb.
+constexpr int BOT_MAXL = 4;
+struct BottomArgs {
+    int nl, nu1, nu2;
+    VankaParams vp[BOT_MAXL];          // omega set
+    double* x[BOT_MAXL + 1];           // per level: iterate buffer (context-owned Lv.x)
+    double* t[BOT_MAXL];               // scratch
+    double* b[BOT_MAXL + 1];           // right-hand sides (b[l+1] written by the restriction)
+    int pitch[BOT_MAXL + 1];
+    int N;                             // coarsest dense inverse (column major) and slots
+    const double* G;
+    const int64_t* slots;
+    const int* stop;
+};
+cudaError_t launch_bottom(const BottomArgs& A, cudaStream_t s);
+
 // All launchers return cudaGetLastError() of the launch.
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r,
                             NormSink norm, cudaStream_t s);
