@@ -33,16 +33,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // grid's CTAs fill the SMs this grid's tail frees (they block in pdl_wait until it completes)
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-__device__ __forceinline__ bool is_active(int p, int i, int j, int n) {
-    if (i < 0 || j < 0 || i > n || j > n) return false;
-    switch (p) {
-        case 0: case 1: return i > 0 && i < n && j > 0 && j < n;
-        case 2: case 5: return i < n && j > 0 && j < n;
-        case 3: case 6: return i > 0 && i < n && j < n;
-        default: return i < n && j < n;
-    }
-}
-
 // bit p set <=> is_active(p, i, j, n), for all ten planes at once
 __device__ __forceinline__ unsigned active_mask(int i, int j, int n) {
     if (i < 0 || j < 0 || i > n || j > n) return 0u;
@@ -50,6 +40,11 @@ __device__ __forceinline__ unsigned active_mask(int i, int j, int n) {
     return (ii && ij ? 0x003u : 0u) | (li && ij ? 0x024u : 0u) | (ii && lj ? 0x048u : 0u) |
            (li && lj ? 0x390u : 0u);
 }
+
+// plane p of index (i, j) is an unknown (not Dirichlet, not outside the mesh; SURVEY 8 layout table).
+// Through the ten-plane mask: the unrolled per-plane tests of one index share one mask.
+__device__ __forceinline__ bool is_active(int p, int i, int j, int n) { return (active_mask(i, j, n) >> p) & 1u; }
+
 
 template <int NT>
 __device__ __forceinline__ double block_sum(double v) {
