@@ -1583,20 +1583,25 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
     }
     double nrm = 0.0;
     for (int s = -1; s < nsteps; ++s) {
-        // TMA group s landed (and, PROL, its x rows were corrected by the producer warp)
+        // ring slots of rows j0 + sR + d (0 <= d <= 5) from per-step bases (no modulo per access)
+        const int bx0 = (s * M2R + 2 * M2R) % M2XR, bb0 = (s * M2R + 2 * M2R) % M2BR, bc0 = (s * M2R + 2 * M2R) % M2CR;
+        auto sxs = [&](int d) { const int v = bx0 + d; return v >= M2XR ? v - M2XR : v; };
+        auto sbs = [&](int d) { const int v = bb0 + d; return v >= M2BR ? v - M2BR : v; };
+        auto scs = [&](int d) { const int v = bc0 + d; return v >= M2CR ? v - M2CR : v; };
+        // TMA group s landed (and, PROL, its x rows were corrected by the producer warps)
         mbar_wait(PROL ? &ready[(s + 1) & 1] : &bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
         // ---- residual rows y = j0 + s R + 1 + q
         // one warp per row (lanes beyond the row idle): no bank conflicts from rows wrapping in a warp
         if ((t & 31) < M2T + 2) {
             const int q = t >> 5, lx = t & 31;
             const int y = j0 + s * M2R + 1 + q, i = i0 - 1 + lx;
-            double* bp = br + sb(y) * M2ROW + (lx + 1);
+            double* bp = br + sbs(1 + q) * M2ROW + (lx + 1);
             const bool own = lx >= 1 && lx <= M2T && i <= n && y >= j0 && y < j0 + rows;
             double rv[10];
             if (!XZERO) {
-                const double* xm = xr + sx(y - 1) * M2ROW + (lx + 1);
-                const double* x0 = xr + sx(y) * M2ROW + (lx + 1);
-                const double* xp = xr + sx(y + 1) * M2ROW + (lx + 1);
+                const double* xm = xr + sxs(q) * M2ROW + (lx + 1);
+                const double* x0 = xr + sxs(1 + q) * M2ROW + (lx + 1);
+                const double* xp = xr + sxs(2 + q) * M2ROW + (lx + 1);
                 double av[10];
                 apply_rows<M2W, false>(L, xm, x0, xp, i, y, av);
 #pragma unroll
@@ -1625,10 +1630,10 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
         if ((t & 31) < M2C) {
             const int q = t >> 5, px = t & 31;
             const int a = i0 + px, bb = j0 + s * M2R + 1 + q;
-            double* out = cr + sc(bb) * (20 * M2C) + px;
+            double* out = cr + scs(1 + q) * (20 * M2C) + px;
             if (a <= n && bb >= 0 && bb <= n) {
-                const double* r0 = br + sb(bb) * M2ROW + (px + 2);
-                const double* rm = br + sb(bb - 1) * M2ROW + (px + 2);
+                const double* r0 = br + sbs(1 + q) * M2ROW + (px + 2);
+                const double* rm = br + sbs(q) * M2ROW + (px + 2);
                 double rr[20];
 #define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * M2W + (dx)]
                 rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
@@ -1651,8 +1656,8 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
             const int q = t >> 5, lx = t & 31;
             const int y = j0 + s * M2R + q, i = i0 + lx;
             if (i <= n && y < j0 + rows) {
-                const double* c0 = cr + sc(y) * (20 * M2C) + lx;
-                const double* c1 = cr + sc(y + 1) * (20 * M2C) + lx;
+                const double* c0 = cr + scs(q) * (20 * M2C) + lx;
+                const double* c1 = cr + scs(q + 1) * (20 * M2C) + lx;
 #define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * M2C + (dx)]
                 double d[10];
                 d[0] = CC(0, 0, 0);
@@ -1666,7 +1671,7 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
                 d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
                 d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
 #undef CC
-                const double* xv = xr + sx(y) * M2ROW + (lx + 2);
+                const double* xv = xr + sxs(q) * M2ROW + (lx + 2);
                 const int64_t o = (int64_t)y * L.pitch + i;
 #pragma unroll
                 for (int k = 0; k < 10; ++k) {
