@@ -2361,6 +2361,17 @@ static int sm_count() {
     }
     return g_sms;
 }
+// segment target of the marching relaxations: ~n/64 rows, at least 32; 16 below n = 2048 (more, shorter
+// marches against the wave tail of the 2-3 wave grids there; MG_MARCH_SMALL overrides)
+static int relax_target(int n) {
+    static int small = -1;
+    if (small < 0) {
+        const char* v = getenv("MG_MARCH_SMALL");
+        small = v ? atoi(v) : 16;
+    }
+    return n >= 2048 ? std::max(32, n / 64) : small;
+}
+
 static int march_height(int n, int tcols, int rstep, int ctas_per_sm, int target = 128) {
     if (const char* v = getenv("MG_MARCH_TARGET")) target = atoi(v);
     const long strips = (n + tcols) / tcols;
@@ -2771,7 +2782,7 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     if (e != cudaSuccess) return e;
     // segments of ~max(32, n/64) rows: more, shorter marches keep CTAs of one SM out of lock step
     // (measured: 2048^2 sweep 0.45 -> 0.37 ms, 4096^2 1.24 -> 1.19 ms against ~128-row segments)
-    const int MH = march_height(L.n, M2T, M2R, 3, std::max(32, L.n / 64));
+    const int MH = march_height(L.n, M2T, M2R, 3, relax_target(L.n));
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
@@ -2781,7 +2792,7 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     return cudaGetLastError();
 }
 int blocks_vanka_march2(int n) {
-    const int MH = march_height(n, M2T, M2R, 3, std::max(32, n / 64));
+    const int MH = march_height(n, M2T, M2R, 3, relax_target(n));
     return ((n + M2T) / M2T) * ((n + MH) / MH);
 }
 
@@ -2815,7 +2826,7 @@ cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double
     const bool het = L.kinv_field != nullptr;
     if (e == cudaSuccess) e = encode_vec_map(&mk, het ? L.kinv_field : b, L.n, L.pitch, L.plane, BQ_W, 1, 2);
     if (e != cudaSuccess) return e;
-    const int MH = march_height(L.n, BMA_T, BQ_R, 3, std::max(32, L.n / 64));
+    const int MH = march_height(L.n, BMA_T, BQ_R, 3, relax_target(L.n));
     dim3 grid((L.n + BMA_T) / BMA_T, (L.n + MH) / MH);
 #define BA_LAUNCH(H_, Z_) launch_k(bsr_a_march_kernel<H_, Z_>, grid, BQ_NT, BMA_SMEM, s, mx, mb, mk, L, U, omJ, g, dp, S, MH)
     if (het && x_zero) BA_LAUNCH(true, true);
@@ -2835,7 +2846,7 @@ cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double
     const bool het = L.kinv_field != nullptr;
     if (e == cudaSuccess) e = encode_vec_map(&mk, het ? L.kinv_field : dp, L.n, L.pitch, L.plane, BQ_W, 1, 2);
     if (e != cudaSuccess) return e;
-    const int MH = march_height(L.n, BB_T, BQ_R, 3, std::max(32, L.n / 64));
+    const int MH = march_height(L.n, BB_T, BQ_R, 3, relax_target(L.n));
     dim3 grid((L.n + BB_T) / BB_T, (L.n + MH) / MH);
 #define BB_LAUNCH(H_, Z_) launch_k(bsr_b_march_kernel<H_, Z_>, grid, BQ_NT, BB2_SMEM, s, mx, mb, md, mk, L, U, omega, xo, MH)
     if (het && x_zero) BB_LAUNCH(true, true);
