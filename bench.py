@@ -167,15 +167,34 @@ def oracle_sample(c, cycles: int, warmup: int = 1, n_sample: int = 128):
                        f"numpy/scipy (sparse matvec single-threaded, BLAS threads {cores})")
 
 
+METRIC = "DoF-updates/s per V(1,1) cycle (fp64) at 4096^2; ms per cycle; % of HBM roofline"
+
+
+def workload_config(args, c):
+    """The workload description shared by both arms (the reference arm times a bounded sample of it,
+    stated in its cpu_baseline)."""
+    relax = c["relax_used"]   # no import of the product package here: the reference arm uses this too
+    omega = c["omega"] if relax == "vanka" else c["bsr_omega"]
+    n, L = c["n"], c["levels"]
+    pitch = ((n + 1 + 31) // 32) * 32
+    return {"workload": f"BASELINE config {args.config}: {n}^2 cells, {L} levels, V(1,1) {relax}, "
+                        f"lambda={c['lam']}, mu={c['mu']}, K={'exp(N(0,4)) field' if c['K_seed'] is not None else c['K']}, "
+                        f"tau=alpha=1/M=1, b~U(-1,1) seed {c['b_seed']}, x0=0",
+            "n": n, "levels": L, "relax": relax, "omega": omega,
+            "omega_J": c["omega_J"] if relax == "bsr" else None,
+            "active_dofs": mg_inputs.n_active(n),
+            "l2": "inputs larger than L2 (one vector = %.2f GB)" % (10 * (n + 1) * pitch * 8 / 1e9)}
+
+
 def run_reference(args, c, rank, world):
     if rank != 0:
         return
     s = oracle_sample(c, args.steps, args.warmup)
-    line = {"impl": "reference", "metric": "DoF-updates/s per V(1,1) cycle (fp64)", "value": s["value"],
+    line = {"impl": "reference", "metric": METRIC, "value": s["value"],
             "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": s["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {args.config} (bounded sample, see cpu_baseline)"},
+            "config": workload_config(args, c),
             "cpu_baseline": {"value": s["value"], "unit": "DoF/s", "cores": s["cores"], "kind": "oracle",
                              "sample": s["sample"]},
             "e2e": {"value": s["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -344,20 +363,14 @@ def main():
     cycle_bytes = 8.0 * sum(level_passes(l) * mg_inputs.n_active(n >> l) for l in range(L))
     ms_step = ms / args.steps
     line = {
-        "metric": "DoF-updates/s per V(1,1) cycle (fp64) at 4096^2; ms per cycle; % of HBM roofline",
+        "metric": METRIC,
         "value": aggregate_rate(nact, args.steps, world, ms),
         "unit": "DoF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: {n}^2 cells, {L} levels, V(1,1) {o.relax}, "
-                               f"lambda={c['lam']}, mu={c['mu']}, K={'exp(N(0,4)) field' if kf is not None else c['K']}, "
-                               f"tau=alpha=1/M=1, b~U(-1,1) seed {c['b_seed']}, x0=0",
-                   "n": n, "levels": L, "relax": o.relax, "omega": o.omega,
-                   "omega_J": o.omega_J if o.relax == "bsr" else None,
-                   "active_dofs": nact, "l2": "inputs larger than L2 (one vector = %.2f GB)" % (10 * (n + 1) * H.pitch(0) * 8 / 1e9),
-                   "final_residual_norm": res_norm},
+        "config": dict(workload_config(args, c), final_residual_norm=res_norm),
         "gpu_launches": launches_per_cycle * args.steps,
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
