@@ -1229,6 +1229,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
 }
 // as mbar_wait, backing off between polls (a waiting warp then leaves the issue slots to others)
+#ifndef MG_SLEEP_NS
+#define MG_SLEEP_NS 64
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
     unsigned ok;
     for (;;) {
@@ -1240,7 +1243,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
         if (ok) return;
-        __nanosleep(64);
+        __nanosleep(MG_SLEEP_NS);
     }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
