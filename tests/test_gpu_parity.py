@@ -194,6 +194,8 @@ def floor_parity(Oh, Oalt, b, xs_O, xs_alt, hO, hAlt):
     (32, 4, "unit", "bsr", None, 8, False),         # config 2 (BSR) regime
     (32, 4, "unit", "bsr", 3, 6, False),            # config 4 regime (heterogeneous K)
     (32, 4, "unit", "bsr", 3, 4, True),             # config 4 regime, marching restriction (K field)
+    (48, 3, "mixed", "vanka", None, 5, True),       # n not a power of two (coarsest 12), marching kernels
+    (48, 3, "mixed", "bsr", 7, 4, True),            # the same with BSR and a K field
 ])
 def test_cycle_history(n, levels, pname, relax, het, cycles, march):
     torch = _torch()

@@ -1,1 +1,1 @@
-for ns in 64 256 1000; do MG_NVCC_EXTRA=-DMG_SLEEP_NS=$ns python paper_2107_04060_b200/build.py > /dev/null 2>&1; python bench.py --no-cpu-baseline --no-e2e --no-solve --steps 100 > gpurun_out/bq_ns$ns.log 2>&1; done
+python -m pytest tests/test_gpu_parity.py -q -x -k "cycle_history" 2>&1 | tail -3 > gpurun_out/q_test.txt
