@@ -49,6 +49,7 @@ struct Level {
     double* dpa = nullptr;   // BSR: 2 planes
     double* dpb = nullptr;
     double* kinv = nullptr;  // 2 planes, heterogeneous K only
+    double* jtab = nullptr;  // BSR Jacobi table: 5 planes (tau / D_w per RT0 edge, 1 / diag S per triangle)
     double* gbnd = nullptr;  // 9 x 400
     double* ubnd = nullptr;  // 9 x 64
     VankaParams vp;
@@ -106,6 +107,7 @@ struct mg_ctx {
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one CTA
                                   // (measured slower: 442 vs 250 us per 256^2 cycle -- one SM is compute bound)
+    int jacobi_table = 1;         // 1: Jacobi sweeps from the per-level table (bsr_jacobi_t_kernel)
     int jacobi_pair = 0;          // 1: two Jacobi sweeps per launch (bsr_jacobi2_kernel; measured slower:
                                   //    292 us vs 2 x 110 us at 2048^2, the per-tile halo work dominates)
     int bsr_impl = 1;             // 1: row-marching BSR stages on levels with n >= march_min_n, 0: 2-D tiles
@@ -177,7 +179,10 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     double* cur = Lv.dpa;
     double* nxt = Lv.dpb;
     for (int k = 1; k < o.jacobi_sweeps;) {
-        if (c->jacobi_pair && k + 1 < o.jacobi_sweeps) {
+        if (c->jacobi_table) {
+            CK(launch_bsr_jacobi_t(Lv.vp.L, o.omega_J, Lv.g, Lv.jtab, cur, nxt, s));
+            k += 1;
+        } else if (c->jacobi_pair && k + 1 < o.jacobi_sweeps) {
             CK(launch_bsr_jacobi2(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
             k += 2;
         } else {
@@ -427,6 +432,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_SMALL_TILE_N")) set_small_tile_n(atoi(v));
     if (const char* v = getenv("MG_PDL")) set_pdl(atoi(v) != 0);
     if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v) != 0;
+    if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
     auto bail = [&](int rc) {
@@ -479,7 +485,8 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
             Lv.b = (double*)dalloc(c, vb);
         }
         if (c->het) Lv.kinv = (double*)dalloc(c, pb);
-        if (!Lv.t || !Lv.g || !Lv.dpa || !Lv.dpb || !Lv.gbnd || !Lv.ubnd || (l > 0 && (!Lv.x || !Lv.b)) ||
+        Lv.jtab = (double*)dalloc(c, sizeof(double) * 5 * Lv.plane);
+        if (!Lv.t || !Lv.g || !Lv.dpa || !Lv.dpb || !Lv.gbnd || !Lv.ubnd || !Lv.jtab || (l > 0 && (!Lv.x || !Lv.b)) ||
             (c->het && !Lv.kinv)) {
             delete t;
             return bail(fail(MG_ENOMEM, "device allocation failed at level %d", l));
@@ -511,6 +518,12 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
             if (launch_kinv_coarsen(c->L[l - 1].n, c->L[l - 1].pitch, c->L[l - 1].kinv, c->L[l].pitch, c->L[l].kinv, 0) !=
                 cudaSuccess)
                 return bail(fail(MG_ECUDA, "kinv coarsen launch failed"));
+    }
+    // BSR Jacobi tables (after the K^-1 pyramid they are formed from)
+    for (int l = 0; l < levels; ++l) {
+        cudaMemset(c->L[l].jtab, 0, sizeof(double) * 5 * c->L[l].plane);
+        if (launch_jtable(c->L[l].vp.L, c->L[l].jtab, 0) != cudaSuccess)
+            return bail(fail(MG_ECUDA, "jtable launch: %s", cudaGetErrorString(cudaGetLastError())));
     }
     // norms and solve state
     c->partials = (double*)dalloc(c, sizeof(double) * max_blocks);

@@ -953,6 +953,79 @@ __global__ void __launch_bounds__(256) bsr_jacobi_kernel(const LevelParams L, do
     }
 }
 
+// Per-level Jacobi table: tau / D_w(e) of the three RT0 edges owned by index
+// (i, j) (0 if inactive) and 1 / diag(S) of its two triangles -- fixed by K^{-1}, formed once at
+// setup so the Jacobi sweeps need neither the K^{-1} gathers nor divisions.  5 planes.
+template <bool HET>
+__global__ void __launch_bounds__(256) jtable_kernel(const LevelParams L, double* __restrict__ tab) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int n = L.n;
+    if (i > n || j > n) return;
+    const int64_t plane = L.plane, o = (int64_t)j * L.pitch + i;
+#pragma unroll
+    for (int e = 0; e < 3; ++e)
+        tab[e * plane + o] = is_active(5 + e, i, j, n) ? L.tau / Dw_at<HET>(L, 5 + e, i, j) : 0.0;
+#pragma unroll
+    for (int sh = 0; sh < 2; ++sh) {
+        double v = 0.0;
+        if (i < n && j < n) {
+            double dw[3];
+            bool act[3];
+            tri_Dw<HET>(L, sh, i, j, dw);
+            tri_edges_active(sh, i, j, n, act);
+            double ds = L.s0h2;
+#pragma unroll
+            for (int e = 0; e < 3; ++e)
+                if (act[e]) ds += L.tau * L.bw[sh][e] * L.bw[sh][e] / dw[e];
+            v = 1.0 / ds;
+        }
+        tab[(3 + sh) * plane + o] = v;
+    }
+}
+
+// Jacobi sweep with the table: dp' = dp + omega_J (g / diag S - dp - (S dp - diag(S) dp) / diag S)
+template <int DUMMY = 0>
+__global__ void __launch_bounds__(256) bsr_jacobi_t_kernel(const LevelParams L, double omJ,
+                                                           const double* __restrict__ g,
+                                                           const double* __restrict__ tab,
+                                                           const double* __restrict__ dpi, double* __restrict__ dpo) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int n = L.n;
+    if (i > n || j > n || *L.stop) return;
+    const int64_t plane = L.plane, pitch = L.pitch;
+    const int64_t o = (int64_t)j * pitch + i;
+    if (i == n || j == n) {
+        dpo[o] = 0.0;
+        dpo[plane + o] = 0.0;
+        return;
+    }
+    // edge factors of the cell's triangles: LL -> H(i,j), V(i,j), D(i,j); UR -> H(i,j+1), V(i+1,j), D(i,j)
+    const double tH0 = __ldg(tab + o), tV0 = __ldg(tab + plane + o), tD = __ldg(tab + 2 * plane + o);
+    const double tH1 = __ldg(tab + o + pitch), tV1 = __ldg(tab + plane + o + 1);
+#pragma unroll
+    for (int sh = 0; sh < 2; ++sh) {
+        const double te[3] = {sh == 0 ? tH0 : tH1, sh == 0 ? tV0 : tV1, tD};
+        const double dself = __ldg(dpi + sh * plane + o);
+        double off = 0.0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            int ni, nj;
+            if (sh == 0) { ni = e == 1 ? i - 1 : i; nj = e == 0 ? j - 1 : j; }
+            else         { ni = e == 1 ? i + 1 : i; nj = e == 0 ? j + 1 : j; }
+            if (te[e] != 0.0) {   // inactive edge: no coupling (and the neighbour may lie outside)
+                const double dn = __ldg(dpi + (1 - sh) * plane + (int64_t)nj * pitch + ni);
+                off = fma(te[e] * L.bw[sh][e] * L.bw[1 - sh][e], dn, off);
+            }
+        }
+        const double ids = __ldg(tab + (3 + sh) * plane + o);
+        dpo[sh * plane + o] = dself + omJ * (fma(__ldg(g + sh * plane + o), ids, -dself) - off * ids);
+    }
+}
+
 // Two Jacobi sweeps on S dp = g in one pass.  Per tile: dp0 on the tile + 2 rings of
 // cells, K^{-1} on the tile + 2 (low) / 3 (high) rings, g and the intermediate dp1 on the tile + 1
 // ring.  The edge factors tau / D_w(e) and 1 / diag(S) are formed once per tile (one division per
@@ -2936,6 +3009,20 @@ cudaError_t launch_bsr_jacobi(const LevelParams& L, double omJ, const double* g,
     dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
     if (L.kinv_field) launch_k(bsr_jacobi_kernel<true>, grid, 256, 0, s, L, omJ, g, dpi, dpo);
     else launch_k(bsr_jacobi_kernel<false>, grid, 256, 0, s, L, omJ, g, dpi, dpo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jtable(const LevelParams& L, double* tab, cudaStream_t s) {
+    dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
+    if (L.kinv_field) launch_k(jtable_kernel<true>, grid, 256, 0, s, L, tab);
+    else launch_k(jtable_kernel<false>, grid, 256, 0, s, L, tab);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_jacobi_t(const LevelParams& L, double omJ, const double* g, const double* tab,
+                                const double* dpi, double* dpo, cudaStream_t s) {
+    dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
+    launch_k(bsr_jacobi_t_kernel<0>, grid, 256, 0, s, L, omJ, g, tab, dpi, dpo);
     return cudaGetLastError();
 }
 

@@ -78,6 +78,10 @@ void set_pdl(int on);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march3(int n);
+// per-level Jacobi table (tau / D_w per RT0 edge, 1 / diag S per triangle; 5 planes) and the sweep using it
+cudaError_t launch_jtable(const LevelParams& L, double* tab, cudaStream_t s);
+cudaError_t launch_bsr_jacobi_t(const LevelParams& L, double omega_J, const double* g, const double* tab,
+                                const double* dp_in, double* dp_out, cudaStream_t s);
 // two Jacobi sweeps in one launch (same arithmetic as two launch_bsr_jacobi)
 cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
                                cudaStream_t s);
