@@ -802,77 +802,87 @@ constexpr int BA_XSZ = 10 * BA_XW * BA_XH, BA_ZSZ = 8 * BA_ZW * BA_ZH + 5 * BA_U
 constexpr int BA_USZ = BA_XSZ > BA_ZSZ ? BA_XSZ : BA_ZSZ;
 constexpr int BA_SMEM = (BA_USZ + 10 * BA_RW * BA_RH) * 8;
 
-template <bool HET, bool XZERO>
-__global__ void __launch_bounds__(BANT, 2) bsr_a_kernel(const LevelParams L, const DispParams U, double omJ,
+// stage-A tile geometry for TX x TY owned cells (small tiles on the latency-bound coarse levels)
+template <int TX, int TY>
+struct BATile {
+    static constexpr int XW = TX + 5, XH = TY + 5, RW = TX + 3, RH = TY + 3, ZW = TX + 2, ZH = TY + 2;
+    static constexpr int UW = TX + 1, UH = TY + 1;
+    static constexpr int XSZ = 10 * XW * XH, ZSZ = 8 * ZW * ZH + 5 * UW * UH, USZ = XSZ > ZSZ ? XSZ : ZSZ;
+    static constexpr int SMEM = (USZ + 10 * RW * RH) * 8;
+    static constexpr int NT = ((RW * RH + 31) / 32) * 32;
+};
+template <bool HET, bool XZERO, int TX = BTX, int TY = BTY>
+__global__ void __launch_bounds__(BATile<TX, TY>::NT, 2) bsr_a_kernel(const LevelParams L, const DispParams U, double omJ,
                                                        const double* __restrict__ x, const double* __restrict__ b,
                                                        double* __restrict__ g, double* __restrict__ dp, NormSink S) {
     pdl_wait();
     pdl_trigger();
+    using T = BATile<TX, TY>;
     extern __shared__ double sm[];
     double* xs = sm;
     double* zs = sm;                              // disp patch outputs, overlays xs
-    double* zu = sm + 8 * BA_ZW * BA_ZH;          // z_u on owned + high ring
-    double* rs = sm + BA_USZ;
+    double* zu = sm + 8 * T::ZW * T::ZH;          // z_u on owned + high ring
+    double* rs = sm + T::USZ;
     if (*L.stop) return;
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
-    const int i0 = blockIdx.x * BTX, j0 = blockIdx.y * BTY;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
     if (!XZERO) {
-        load_tile<BA_XW, BA_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        load_tile<T::XW, T::XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
-        if (const int t = threadIdx.x; t < BA_RW * BA_RH) {
-            const int ly = t / BA_RW, lx = t - ly * BA_RW;
+        if (const int t = threadIdx.x; t < T::RW * T::RH) {
+            const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<BA_XW, BA_XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
-            for (int k = 0; k < 10; ++k) rs[k * BA_RW * BA_RH + t] = rv[k];
+            for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
     } else {
-        load_tile<BA_RW, BA_RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);
+        load_tile<T::RW, T::RH, 10>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);
     }
     __syncthreads();
-    // displacement patches at vertices [i0, i0+BTX+1] x [j0, j0+BTY+1]
-    if (const int t = threadIdx.x; t < BA_ZW * BA_ZH) {
-        const int py = t / BA_ZW, px = t - py * BA_ZW;
+    // displacement patches at vertices [i0, i0+TX+1] x [j0, j0+TY+1]
+    if (const int t = threadIdx.x; t < T::ZW * T::ZH) {
+        const int py = t / T::ZW, px = t - py * T::ZW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
             double rr[8];
-            gather8<BA_RW, BA_RH>(rs + (py + 1) * BA_RW + (px + 1), rr);
-            patch_apply8(U, vertex_class(a, bb, n), rr, zs + t, BA_ZW * BA_ZH);
+            gather8<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
+            patch_apply8(U, vertex_class(a, bb, n), rr, zs + t, T::ZW * T::ZH);
         } else {
 #pragma unroll
-            for (int s = 0; s < 8; ++s) zs[s * BA_ZW * BA_ZH + t] = 0.0;
+            for (int s = 0; s < 8; ++s) zs[s * T::ZW * T::ZH + t] = 0.0;
         }
     }
     __syncthreads();
-    // z_u on indices [i0, i0+BTX] x [j0, j0+BTY]
-    if (const int t = threadIdx.x; t < BA_UW * BA_UH) {
-        const int ly = t / BA_UW, lx = t - ly * BA_UW;
-        const double* c00 = zs + ly * BA_ZW + lx;
-#define CC(s, dx, dy) c00[(s) * (BA_ZW * BA_ZH) + (dy) * BA_ZW + (dx)]
-        zu[0 * BA_UW * BA_UH + t] = CC(0, 0, 0);
-        zu[1 * BA_UW * BA_UH + t] = CC(1, 0, 0);
-        zu[2 * BA_UW * BA_UH + t] = CC(2, 0, 0) + CC(3, 1, 0);
-        zu[3 * BA_UW * BA_UH + t] = CC(4, 0, 0) + CC(5, 0, 1);
-        zu[4 * BA_UW * BA_UH + t] = CC(6, 1, 0) + CC(7, 0, 1);
+    // z_u on indices [i0, i0+TX] x [j0, j0+TY]
+    if (const int t = threadIdx.x; t < T::UW * T::UH) {
+        const int ly = t / T::UW, lx = t - ly * T::UW;
+        const double* c00 = zs + ly * T::ZW + lx;
+#define CC(s, dx, dy) c00[(s) * (T::ZW * T::ZH) + (dy) * T::ZW + (dx)]
+        zu[0 * T::UW * T::UH + t] = CC(0, 0, 0);
+        zu[1 * T::UW * T::UH + t] = CC(1, 0, 0);
+        zu[2 * T::UW * T::UH + t] = CC(2, 0, 0) + CC(3, 1, 0);
+        zu[3 * T::UW * T::UH + t] = CC(4, 0, 0) + CC(5, 0, 1);
+        zu[4 * T::UW * T::UH + t] = CC(6, 1, 0) + CC(7, 0, 1);
 #undef CC
     }
     __syncthreads();
-    const int lx = threadIdx.x % BTX, ly = threadIdx.x / BTX;
+    const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
     const int i = i0 + lx, j = j0 + ly;
     double nrm = 0.0;
-    if (threadIdx.x < BTX * BTY && i <= n && j <= n) {
-        const double* r00 = rs + (ly + 1) * BA_RW + (lx + 1);
+    if (threadIdx.x < TX * TY && i <= n && j <= n) {
+        const double* r00 = rs + (ly + 1) * T::RW + (lx + 1);
         if (S.out || S.state) {
 #pragma unroll
             for (int k = 0; k < 10; ++k) {
-                const double rv = r00[k * BA_RW * BA_RH];
+                const double rv = r00[k * T::RW * T::RH];
                 nrm = fma(rv, rv, nrm);
             }
         }
         const int64_t o = (int64_t)j * pitch + i;
         if (i < n && j < n) {
-            const double* u00 = zu + ly * BA_UW + lx;
+            const double* u00 = zu + ly * T::UW + lx;
 #pragma unroll
             for (int sh = 0; sh < 2; ++sh) {
                 double dw[3];
@@ -882,11 +892,11 @@ __global__ void __launch_bounds__(BANT, 2) bsr_a_kernel(const LevelParams L, con
                 double gu = 0.0, gw = 0.0, ds = L.s0h2;
 #define MG_L(s, q, dx, dy, pl)                                                              \
     if ((s) == sh) {                                                                        \
-        if ((q) < 9) gu = fma(L.bu[s][(q) < 9 ? (q) : 0], u00[(pl) * (BA_UW * BA_UH) + (dy) * BA_UW + (dx)], gu); \
+        if ((q) < 9) gu = fma(L.bu[s][(q) < 9 ? (q) : 0], u00[(pl) * (T::UW * T::UH) + (dy) * T::UW + (dx)], gu); \
         else if ((q) < 12) {                                                                \
             const int e = (q) < 12 ? (q) - 9 : 0;                                           \
             if (act[e]) {                                                                   \
-                const double rw = r00[(pl) * (BA_RW * BA_RH) + (dy) * BA_RW + (dx)];        \
+                const double rw = r00[(pl) * (T::RW * T::RH) + (dy) * T::RW + (dx)];        \
                 gw = fma(L.bw[s][e], rw / (L.tau * dw[e]), gw);                             \
                 ds += L.tau * L.bw[s][e] * L.bw[s][e] / dw[e];                              \
             }                                                                               \
@@ -895,7 +905,7 @@ __global__ void __launch_bounds__(BANT, 2) bsr_a_kernel(const LevelParams L, con
                 MG_LOCAL_0(MG_L)
                 MG_LOCAL_1(MG_L)
 #undef MG_L
-                const double rp = r00[(8 + sh) * (BA_RW * BA_RH)];
+                const double rp = r00[(8 + sh) * (T::RW * T::RH)];
                 const double gv = L.alpha * gu + L.tau * gw - rp;
                 g[sh * plane + o] = gv;
                 dp[sh * plane + o] = omJ * gv / ds;
@@ -907,7 +917,7 @@ __global__ void __launch_bounds__(BANT, 2) bsr_a_kernel(const LevelParams L, con
             dp[plane + o] = 0.0;
         }
     }
-    if (S.out || S.state) norm_finish<BANT>(S, nrm);
+    if (S.out || S.state) norm_finish<T::NT>(S, nrm);
 }
 
 // Jacobi sweep on S dp = g: dp' = dp + omega_J (g - S dp) / diag(S)
@@ -1142,73 +1152,82 @@ constexpr int BB_XSZ = 10 * BB_XW * BB_XH, BB_ZSZ = 8 * BB_PW * BB_PH;
 constexpr int BB_USZ = BB_XSZ > BB_ZSZ ? BB_XSZ : BB_ZSZ;
 constexpr int BB_SMEM = (BB_USZ + 10 * BB_RW * BB_RH + 2 * BB_DW * BB_DH) * 8;
 
-template <bool HET, bool XZERO>
-__global__ void __launch_bounds__(BBNT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
+template <int TX, int TY>
+struct BBTile {
+    static constexpr int XW = TX + 4, XH = TY + 4, RW = TX + 2, RH = TY + 2, PW = TX + 1, PH = TY + 1;
+    static constexpr int DW = TX + 3, DH = TY + 3;
+    static constexpr int XSZ = 10 * XW * XH, ZSZ = 8 * PW * PH, USZ = XSZ > ZSZ ? XSZ : ZSZ;
+    static constexpr int SMEM = (USZ + 10 * RW * RH + 2 * DW * DH) * 8;
+    static constexpr int NT = ((RW * RH + 31) / 32) * 32;
+};
+template <bool HET, bool XZERO, int TX = BTX, int TY = BTY>
+__global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
                                                        const double* __restrict__ x, const double* __restrict__ b,
                                                        const double* __restrict__ dp, double* __restrict__ xo) {
     pdl_wait();
     pdl_trigger();
+    using T = BBTile<TX, TY>;
     extern __shared__ double sm[];
     double* xs = sm;
     double* zs = sm;
-    double* rs = sm + BB_USZ;
-    double* ps = rs + 10 * BB_RW * BB_RH;   // dp on cells [i0-2, i0+BTX] x [j0-2, j0+BTY]
+    double* rs = sm + T::USZ;
+    double* ps = rs + 10 * T::RW * T::RH;   // dp on cells [i0-2, i0+TX] x [j0-2, j0+TY]
     if (*L.stop) return;
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
-    const int i0 = blockIdx.x * BTX, j0 = blockIdx.y * BTY;
-    for (int t = threadIdx.x; t < 2 * BB_DW * BB_DH; t += BBNT) {
-        const int sh = t / (BB_DW * BB_DH), rem = t - sh * (BB_DW * BB_DH);
-        const int ly = rem / BB_DW, lx = rem - ly * BB_DW;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    for (int t = threadIdx.x; t < 2 * T::DW * T::DH; t += T::NT) {
+        const int sh = t / (T::DW * T::DH), rem = t - sh * (T::DW * T::DH);
+        const int ly = rem / T::DW, lx = rem - ly * T::DW;
         const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
         ps[t] = (ci >= 0 && cj >= 0 && ci < n && cj < n) ? __ldg(dp + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
     }
     if (!XZERO) {
-        load_tile<BB_XW, BB_XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
+        load_tile<T::XW, T::XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
-        if (const int t = threadIdx.x; t < BB_RW * BB_RH) {
-            const int ly = t / BB_RW, lx = t - ly * BB_RW;
+        if (const int t = threadIdx.x; t < T::RW * T::RH) {
+            const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<BB_XW, BB_XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) rs[k * BB_RW * BB_RH + t] = rv[k];
+            for (int k = 0; k < 8; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
     } else {
-        load_tile<BB_RW, BB_RH, 8>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);
+        load_tile<T::RW, T::RH, 8>(rs, b, i0 - 1, j0 - 1, n, pitch, plane);
     }
     __syncthreads();
     // y_u = r_u - alpha B_u^T dp on the r tile (u planes, active DoFs)
-    if (const int t = threadIdx.x; t < BB_RW * BB_RH) {
-        const int ly = t / BB_RW, lx = t - ly * BB_RW;
+    if (const int t = threadIdx.x; t < T::RW * T::RH) {
+        const int ly = t / T::RW, lx = t - ly * T::RW;
         const int c = i0 - 1 + lx, d = j0 - 1 + ly;
-        const double* p00 = ps + (ly + 1) * BB_DW + (lx + 1);   // cell (c, d)
+        const double* p00 = ps + (ly + 1) * T::DW + (lx + 1);   // cell (c, d)
         double bt[5] = {0, 0, 0, 0, 0};
-#define MG_I(k, cdx, cdy, sh, q) bt[k] = fma(L.bu[sh][q], p00[(sh) * (BB_DW * BB_DH) + (cdy) * BB_DW + (cdx)], bt[k]);
+#define MG_I(k, cdx, cdy, sh, q) bt[k] = fma(L.bu[sh][q], p00[(sh) * (T::DW * T::DH) + (cdy) * T::DW + (cdx)], bt[k]);
         MG_INCIDENT_0(MG_I) MG_INCIDENT_1(MG_I) MG_INCIDENT_2(MG_I) MG_INCIDENT_3(MG_I) MG_INCIDENT_4(MG_I)
 #undef MG_I
 #pragma unroll
         for (int k = 0; k < 5; ++k)
-            if (is_active(k, c, d, n)) rs[k * BB_RW * BB_RH + t] -= L.alpha * bt[k];
+            if (is_active(k, c, d, n)) rs[k * T::RW * T::RH + t] -= L.alpha * bt[k];
     }
     __syncthreads();
-    if (const int t = threadIdx.x; t < BB_PW * BB_PH) {
-        const int py = t / BB_PW, px = t - py * BB_PW;
+    if (const int t = threadIdx.x; t < T::PW * T::PH) {
+        const int py = t / T::PW, px = t - py * T::PW;
         const int a = i0 + px, bb = j0 + py;
         if (a <= n && bb <= n) {
             double rr[8];
-            gather8<BB_RW, BB_RH>(rs + (py + 1) * BB_RW + (px + 1), rr);
-            patch_apply8(U, vertex_class(a, bb, n), rr, zs + t, BB_PW * BB_PH);
+            gather8<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
+            patch_apply8(U, vertex_class(a, bb, n), rr, zs + t, T::PW * T::PH);
         } else {
 #pragma unroll
-            for (int s = 0; s < 8; ++s) zs[s * BB_PW * BB_PH + t] = 0.0;
+            for (int s = 0; s < 8; ++s) zs[s * T::PW * T::PH + t] = 0.0;
         }
     }
     __syncthreads();
-    const int lx = threadIdx.x % BTX, ly = threadIdx.x / BTX;
+    const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
     const int i = i0 + lx, j = j0 + ly;
-    if (threadIdx.x >= BTX * BTY || i > n || j > n) return;
-    const double* c00 = zs + ly * BB_PW + lx;
-#define CC(s, dx, dy) c00[(s) * (BB_PW * BB_PH) + (dy) * BB_PW + (dx)]
+    if (threadIdx.x >= TX * TY || i > n || j > n) return;
+    const double* c00 = zs + ly * T::PW + lx;
+#define CC(s, dx, dy) c00[(s) * (T::PW * T::PH) + (dy) * T::PW + (dx)]
     double d[10];
     d[0] = CC(0, 0, 0);
     d[1] = CC(1, 0, 0);
@@ -1216,19 +1235,19 @@ __global__ void __launch_bounds__(BBNT, 2) bsr_b_kernel(const LevelParams L, con
     d[3] = CC(4, 0, 0) + CC(5, 0, 1);
     d[4] = CC(6, 1, 0) + CC(7, 0, 1);
 #undef CC
-    const double* p00 = ps + (ly + 2) * BB_DW + (lx + 2);   // cell (i, j)
-    const double* r00 = rs + (ly + 1) * BB_RW + (lx + 1);
+    const double* p00 = ps + (ly + 2) * T::DW + (lx + 2);   // cell (i, j)
+    const double* r00 = rs + (ly + 1) * T::RW + (lx + 1);
     double bw[3] = {0, 0, 0};
-#define MG_I(k, cdx, cdy, sh, q) bw[(k) - 5] = fma(L.bw[sh][(q) - 9], p00[(sh) * (BB_DW * BB_DH) + (cdy) * BB_DW + (cdx)], bw[(k) - 5]);
+#define MG_I(k, cdx, cdy, sh, q) bw[(k) - 5] = fma(L.bw[sh][(q) - 9], p00[(sh) * (T::DW * T::DH) + (cdy) * T::DW + (cdx)], bw[(k) - 5]);
     MG_INCIDENT_5(MG_I) MG_INCIDENT_6(MG_I) MG_INCIDENT_7(MG_I)
 #undef MG_I
 #pragma unroll
     for (int k = 5; k < 8; ++k) {
         const double dwk = Dw_at<HET>(L, k, i, j);
-        d[k] = is_active(k, i, j, n) ? (r00[k * BB_RW * BB_RH] - L.tau * bw[k - 5]) / (L.tau * dwk) : 0.0;
+        d[k] = is_active(k, i, j, n) ? (r00[k * T::RW * T::RH] - L.tau * bw[k - 5]) / (L.tau * dwk) : 0.0;
     }
     d[8] = p00[0];
-    d[9] = p00[BB_DW * BB_DH];
+    d[9] = p00[T::DW * T::DH];
     const int64_t o = (int64_t)j * pitch + i;
 #pragma unroll
     for (int k = 0; k < 10; ++k) {
@@ -2555,7 +2574,9 @@ void set_small_tile_n(int n) { g_small_tile_n = n; }
 int blocks_vanka(int n) {
     return n <= g_small_tile_n ? ((n + VSX) / VSX) * ((n + VSY) / VSY) : ((n + VTX) / VTX) * ((n + VTY) / VTY);
 }
-int blocks_bsr(int n) { return ((n + BTX) / BTX) * ((n + BTY) / BTY); }
+int blocks_bsr(int n) {
+    return n <= g_small_tile_n ? ((n + VSX) / VSX) * ((n + VSY) / VSY) : ((n + BTX) / BTX) * ((n + BTY) / BTY);
+}
 
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
                             cudaStream_t s) {
@@ -2995,8 +3016,19 @@ cudaError_t launch_coarse(int N, const double* G, const int64_t* slots, const do
 
 cudaError_t launch_bsr_a(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
                          double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s) {
-    dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     const bool het = L.kinv_field != nullptr;
+    if (L.n <= g_small_tile_n) {
+        using T = BATile<VSX, VSY>;
+        dim3 grid((L.n + VSX) / VSX, (L.n + VSY) / VSY);
+#define BAS(H_, Z_) launch_k(bsr_a_kernel<H_, Z_, VSX, VSY>, grid, T::NT, T::SMEM, s, L, U, omJ, x, b, g, dp, S)
+        if (het && x_zero) BAS(true, true);
+        else if (het) BAS(true, false);
+        else if (x_zero) BAS(false, true);
+        else BAS(false, false);
+#undef BAS
+        return cudaGetLastError();
+    }
+    dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     if (het && x_zero) launch_k(bsr_a_kernel<true, true>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
     else if (het) launch_k(bsr_a_kernel<true, false>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
     else if (x_zero) launch_k(bsr_a_kernel<false, true>, grid, BANT, BA_SMEM, s, L, U, omJ, x, b, g, dp, S);
@@ -3036,8 +3068,19 @@ cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g
 
 cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega, const double* x, const double* b,
                          const double* dp, double* xo, bool x_zero, cudaStream_t s) {
-    dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     const bool het = L.kinv_field != nullptr;
+    if (L.n <= g_small_tile_n) {
+        using T = BBTile<VSX, VSY>;
+        dim3 grid((L.n + VSX) / VSX, (L.n + VSY) / VSY);
+#define BBS(H_, Z_) launch_k(bsr_b_kernel<H_, Z_, VSX, VSY>, grid, T::NT, T::SMEM, s, L, U, omega, x, b, dp, xo)
+        if (het && x_zero) BBS(true, true);
+        else if (het) BBS(true, false);
+        else if (x_zero) BBS(false, true);
+        else BBS(false, false);
+#undef BBS
+        return cudaGetLastError();
+    }
+    dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
     if (het && x_zero) launch_k(bsr_b_kernel<true, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
     else if (het) launch_k(bsr_b_kernel<true, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
     else if (x_zero) launch_k(bsr_b_kernel<false, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
