@@ -174,7 +174,7 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     }
     const double omJ = o.jacobi_sweeps >= 1 ? o.omega_J : 0.0;
     const bool march = c->bsr_impl == 1 && Lv.n >= c->march_min_n;
-    if (march) CK(launch_bsr_a_march(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s));
+    if (march) CK(launch_bsr_a_march(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s, Lv.jtab));
     else CK(launch_bsr_a(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s));
     double* cur = Lv.dpa;
     double* nxt = Lv.dpb;

@@ -2093,7 +2093,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmk,
                                                                const LevelParams L, const DispParams U, double omJ,
                                                                double* __restrict__ g, double* __restrict__ dp,
-                                                               NormSink S, int MH) {
+                                                               NormSink S, int MH, const double* __restrict__ jtab) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) double sm[];
@@ -2231,29 +2231,23 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                     const double* z1 = zr + sz(y + 1) * (5 * BMA_ZC) + lane;
                     const double* r0 = br + sb(y) * BQ_ROW + (lane + 2);
                     const double* r1 = br + sb(y + 1) * BQ_ROW + (lane + 2);
-                    // 1 / D_w of the five edges of the cell: H(i,y), V(i,y), D(i,y), H(i,y+1), V(i+1,y)
-                    const double rH0 = 1.0 / Dw(5, i, y), rV0 = 1.0 / Dw(6, i, y), rD = 1.0 / Dw(7, i, y);
-                    const double rH1 = 1.0 / Dw(5, i, y + 1), rV1 = 1.0 / Dw(6, i + 1, y);
-                    const double itau = 1.0 / L.tau;
+                    // tau / D_w of the five edges of the cell (H(i,y), V(i,y), D(i,y), H(i,y+1),
+                    // V(i+1,y); 0 if inactive) and 1 / diag S of its triangles: the Jacobi table
+                    const double* tb = jtab + o;
+                    const double tH0 = __ldg(tb), tV0 = __ldg(tb + plane), tD = __ldg(tb + 2 * plane);
+                    const double tH1 = __ldg(tb + L.pitch), tV1 = __ldg(tb + plane + 1);
+                    const double itau2 = 1.0 / (L.tau * L.tau);
 #pragma unroll
                     for (int sh = 0; sh < 2; ++sh) {
-                        double rdw[3];
-                        bool act[3];
-                        rdw[0] = sh == 0 ? rH0 : rH1;
-                        rdw[1] = sh == 0 ? rV0 : rV1;
-                        rdw[2] = rD;
-                        tri_edges_active(sh, i, y, n, act);
-                        double gu = 0.0, gw = 0.0, ds = L.s0h2;
+                        const double te[3] = {sh == 0 ? tH0 : tH1, sh == 0 ? tV0 : tV1, tD};
+                        double gu = 0.0, gw = 0.0;
 #define MG_L(s_, q_, dx, dy, pl)                                                                  \
     if ((s_) == sh) {                                                                             \
         if ((q_) < 9) gu = fma(L.bu[s_][(q_) < 9 ? (q_) : 0], ((dy) ? z1 : z0)[(pl) * BMA_ZC + (dx)], gu); \
         else if ((q_) < 12) {                                                                     \
             const int e = (q_) < 12 ? (q_) - 9 : 0;                                               \
-            if (act[e]) {                                                                         \
-                const double rw = ((dy) ? r1 : r0)[(pl) * BQ_W + (dx)];                           \
-                gw = fma(L.bw[s_][e], rw * rdw[e] * itau, gw);                                    \
-                ds += L.tau * L.bw[s_][e] * L.bw[s_][e] * rdw[e];                                 \
-            }                                                                                     \
+            const double rw = ((dy) ? r1 : r0)[(pl) * BQ_W + (dx)];                               \
+            gw = fma(L.bw[s_][e], rw * te[e] * itau2, gw);                                        \
         }                                                                                         \
     }
                         MG_LOCAL_0(MG_L)
@@ -2262,7 +2256,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                         const double rp = r0[(8 + sh) * BQ_W];
                         const double gv = L.alpha * gu + L.tau * gw - rp;
                         g[sh * plane + o] = gv;
-                        dp[sh * plane + o] = omJ * gv / ds;
+                        dp[sh * plane + o] = omJ * gv * __ldg(tb + (3 + sh) * plane);
                     }
                 } else {
                     g[o] = 0.0;
@@ -2916,7 +2910,7 @@ int blocks_vanka_march(int n) {
 }
 
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
-                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s) {
+                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab) {
     CUtensorMap mx, mb, mk;
     cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, BQ_W, 1);
     if (e == cudaSuccess) e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, BQ_W, 1);
@@ -2925,7 +2919,7 @@ cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, BMA_T, BQ_R, 3, relax_target(L.n));
     dim3 grid((L.n + BMA_T) / BMA_T, (L.n + MH) / MH);
-#define BA_LAUNCH(H_, Z_) launch_k(bsr_a_march_kernel<H_, Z_>, grid, BQ_NT, BMA_SMEM, s, mx, mb, mk, L, U, omJ, g, dp, S, MH)
+#define BA_LAUNCH(H_, Z_) launch_k(bsr_a_march_kernel<H_, Z_>, grid, BQ_NT, BMA_SMEM, s, mx, mb, mk, L, U, omJ, g, dp, S, MH, jtab)
     if (het && x_zero) BA_LAUNCH(true, true);
     else if (het) BA_LAUNCH(true, false);
     else if (x_zero) BA_LAUNCH(false, true);

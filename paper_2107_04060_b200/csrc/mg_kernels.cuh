@@ -87,7 +87,7 @@ cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g
                                cudaStream_t s);
 // row-marching TMA variants of the two BSR stages (same arithmetic as launch_bsr_a / launch_bsr_b)
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
-                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s);
+                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab);
 cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double omega, const double* x,
                                const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s);
 // row-marching TMA variant of the fused residual + restriction (mode 1)
