@@ -2873,7 +2873,12 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     if (e != cudaSuccess) return e;
     // segments of ~max(32, n/64) rows: more, shorter marches keep CTAs of one SM out of lock step
     // (measured: 2048^2 sweep 0.45 -> 0.37 ms, 4096^2 1.24 -> 1.19 ms against ~128-row segments)
-    const int MH = march_height(L.n, M2T, M2R, 3, relax_target(L.n));
+    static int prol_scale = -1;   // segment length factor of the fused-prolongation sweep (MG_PROL_SEG)
+    if (prol_scale < 0) {
+        const char* v = getenv("MG_PROL_SEG");
+        prol_scale = v ? atoi(v) : 1;
+    }
+    const int MH = march_height(L.n, M2T, M2R, 3, relax_target(L.n) * (E ? prol_scale : 1));
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
