@@ -429,8 +429,10 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
     if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_BSR_IMPL")) c->bsr_impl = atoi(v);
-    if (const char* v = getenv("MG_SMALL_TILE_N")) set_small_tile_n(atoi(v));
-    if (const char* v = getenv("MG_PDL")) set_pdl(atoi(v) != 0);
+    // process-wide kernel knobs: every setup re-reads them (unset -> default), so they never stick
+    set_small_tile_n(getenv("MG_SMALL_TILE_N") ? atoi(getenv("MG_SMALL_TILE_N")) : 128);
+    set_pdl(getenv("MG_PDL") ? atoi(getenv("MG_PDL")) != 0 : 0);
+    set_resid_march_n(getenv("MG_RESID_MARCH_N") ? atoi(getenv("MG_RESID_MARCH_N")) : 512);
     if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v) != 0;
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
@@ -452,6 +454,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         max_blocks = std::max(max_blocks, std::max(blocks_vanka(Lv.n), std::max(blocks_residual(Lv.n), blocks_bsr(Lv.n))));
         max_blocks = std::max(max_blocks, std::max(blocks_vanka_march(Lv.n), blocks_vanka_march2(Lv.n)));
         max_blocks = std::max(max_blocks, blocks_vanka_march3(Lv.n));
+        max_blocks = std::max(max_blocks, blocks_residual_march(Lv.n));
         HostLevelTables* t = new HostLevelTables;
         if (host_level_tables(Lv.n, c->m, t, err, sizeof(err))) {
             delete t;

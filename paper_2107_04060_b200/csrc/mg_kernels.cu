@@ -2436,6 +2436,76 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
 }
 #undef MG_GATHER8
 
+// ------------------------------------------------------------------------------------------
+// Row-marching residual / operator application (levels with n >= 512, scalar K): x rows arrive as
+// TMA boxes (32 columns x 1 row x 10 planes) in a 10-row ring one step ahead, one warp per row,
+// 28 owned columns per strip; b is read straight from global (one coalesced pass).
+// MODE 0: r = b - A x (+||r||^2), MODE 1: y = A x on the active slots (FGMRES), MODE 2: ||b - A x||^2.
+constexpr int RM_T = 28, RM_R = 4, RM_NT = 128, RM_XR = 10, RM_W = 32, RM_ROW = 10 * RM_W;
+constexpr int RM_SMEM = RM_XR * RM_ROW * 8 + 64;
+
+template <int MODE>
+__global__ void __launch_bounds__(RM_NT) residual_march_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const LevelParams L, const double* __restrict__ b,
+                                                               double* __restrict__ r, NormSink S, int MH) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(128) double sm[];
+    double* xr = sm;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xr + RM_XR * RM_ROW);
+    if (*L.stop) return;
+    const int n = L.n;
+    const int i0 = blockIdx.x * RM_T, j0 = blockIdx.y * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int nsteps = (rows + RM_R - 1) / RM_R;
+    const int t = threadIdx.x;
+    auto sx = [&](int y) { return (y - j0 + 2 * RM_R) % RM_XR; };
+    // group g: x rows j0+gR+1 .. j0+gR+4 (g = 0: j0-1 .. j0+4)
+    auto issue = [&](int g) {
+        if (g >= nsteps) return;
+        uint64_t* bar = &bars[g & 1];
+        const int nx = g == 0 ? RM_R + 2 : RM_R;
+        const int first = g == 0 ? j0 - 1 : j0 + g * RM_R + 1;
+        mbar_expect_tx(bar, nx * RM_ROW * 8);
+#pragma unroll 1
+        for (int k = 0; k < nx; ++k) tma_load3(xr + sx(first + k) * RM_ROW, &tmx, i0 - 2, first + k, 0, bar);
+    };
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        issue(0);
+        issue(1);
+    }
+    double nrm = 0.0;
+    const int q = t >> 5, lane = t & 31;
+    for (int s = 0; s < nsteps; ++s) {
+        mbar_wait(&bars[s & 1], (s >> 1) & 1);
+        const int y = j0 + s * RM_R + q, i = i0 - 2 + lane;
+        if (lane >= 2 && lane < RM_T + 2 && i <= n && y < j0 + rows) {
+            const double* x0 = xr + sx(y) * RM_ROW + lane;
+            double av[10];
+            apply_rows<RM_W, false>(L, xr + sx(y - 1) * RM_ROW + lane, x0, xr + sx(y + 1) * RM_ROW + lane, i, y, av);
+            const unsigned am = active_mask(i, y, n);
+            const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                double v;
+                if (MODE == 1) v = (am >> k) & 1u ? av[k] : 0.0;
+                else v = (am >> k) & 1u ? __ldg(b + k * L.plane + o) - av[k] : 0.0;
+                if (MODE != 2) r[k * L.plane + o] = v;
+                nrm = fma(v, v, nrm);
+            }
+        }
+        __syncthreads();
+        if (t == 0) issue(s + 2);   // the rows group s + 2 replaces were last read by this step
+    }
+    if (S.out || S.state) norm_finish<RM_NT>(S, nrm);
+}
+
 // Rows marched by one CTA.  All CTAs of a marching launch carry equal work, so the number of row
 // segments per strip is chosen to make the launch an (almost) whole number of waves of resident
 // CTAs (SMs x CTAs per SM), with segments of about `target` rows: a fractional last wave left ~35% of
@@ -2479,6 +2549,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFn g_encode = nullptr;
 
+static int g_resid_march_n = 512;   // residual / apply on levels with n >= this: marching kernel (MG_RESID_MARCH_N)
+void set_resid_march_n(int n) { g_resid_march_n = n; }
 static int g_pdl = 0;   // programmatic dependent launch (MG_PDL=1; measured no gain on the cycle graph)
 void set_pdl(int on) { g_pdl = on; }
 
@@ -2572,8 +2644,26 @@ int blocks_bsr(int n) {
     return n <= g_small_tile_n ? ((n + VSX) / VSX) * ((n + VSY) / VSY) : ((n + BTX) / BTX) * ((n + BTY) / BTY);
 }
 
+static cudaError_t launch_residual_march(int mode, const LevelParams& L, const double* x, const double* b, double* r,
+                                         NormSink S, cudaStream_t s) {
+    CUtensorMap mx;
+    cudaError_t e = encode_vec_map(&mx, x, L.n, L.pitch, L.plane, RM_W, 1);
+    if (e != cudaSuccess) return e;
+    const int MH = march_height(L.n, RM_T, RM_R, 6, 64);
+    dim3 grid((L.n + RM_T) / RM_T, (L.n + MH) / MH);
+    if (mode == 0) launch_k(residual_march_kernel<0>, grid, RM_NT, RM_SMEM, s, mx, L, b, r, S, MH);
+    else if (mode == 1) launch_k(residual_march_kernel<1>, grid, RM_NT, RM_SMEM, s, mx, L, b, r, S, MH);
+    else launch_k(residual_march_kernel<2>, grid, RM_NT, RM_SMEM, s, mx, L, b, r, S, MH);
+    return cudaGetLastError();
+}
+int blocks_residual_march(int n) {
+    const int MH = march_height(n, RM_T, RM_R, 6, 64);
+    return ((n + RM_T) / RM_T) * ((n + MH) / MH);
+}
+
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
                             cudaStream_t s) {
+    if (!L.kinv_field && L.n >= g_resid_march_n) return launch_residual_march(r ? 0 : 2, L, x, b, r, S, s);
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
     if (L.kinv_field) launch_k(residual_kernel<true, false>, grid, RNT, 0, s, L, x, b, r, S);
     else launch_k(residual_kernel<false, false>, grid, RNT, 0, s, L, x, b, r, S);
@@ -2581,6 +2671,7 @@ cudaError_t launch_residual(const LevelParams& L, const double* x, const double*
 }
 
 cudaError_t launch_apply(const LevelParams& L, const double* x, double* y, NormSink S, cudaStream_t s) {
+    if (!L.kinv_field && L.n >= g_resid_march_n) return launch_residual_march(1, L, x, nullptr, y, S, s);
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
     if (L.kinv_field) launch_k(residual_kernel<true, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
     else launch_k(residual_kernel<false, true>, grid, RNT, 0, s, L, x, nullptr, y, S);

@@ -70,11 +70,14 @@ int blocks_vanka_march(int n);
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s, const ProlSrc* E = nullptr);
 int blocks_vanka_march2(int n);
+int blocks_residual_march(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)
 void set_small_tile_n(int N);
 // programmatic dependent launch of every kernel (1, default) or plain stream order (0)
 void set_pdl(int on);
+// residual / operator application on levels with n >= N through the marching kernel (scalar K)
+void set_resid_march_n(int N);
 cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s);
 int blocks_vanka_march3(int n);

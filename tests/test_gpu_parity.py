@@ -36,12 +36,16 @@ def _inactive_zero(H, v, level=0):
     assert np.all(a[~mask] == 0.0)
 
 
-@pytest.mark.parametrize("n,pname,het", [(4, "unit", None), (8, "mixed", None), (16, "stiff", None),
-                                         (40, "cfg5", None), (66, "mixed", None), (24, "unit", 3),
-                                         (34, "mixed", 7)])
-def test_residual(n, pname, het):
+@pytest.mark.parametrize("n,pname,het,march", [(4, "unit", None, False), (8, "mixed", None, False),
+                                               (16, "stiff", None, False), (40, "cfg5", None, False),
+                                               (66, "mixed", None, False), (24, "unit", 3, False),
+                                               (34, "mixed", 7, False), (40, "cfg5", None, True),
+                                               (66, "mixed", None, True), (130, "stiff", None, True)])
+def test_residual(n, pname, het, march):
+    """r = b - A x and its norm; march=True runs the row-marching residual kernel (production for
+    n >= 512, scalar K) on small grids."""
     torch = _torch()
-    H = C.gpu_hierarchy(n, 1, pname, het)
+    H = C.gpu_hierarchy(n, 1, pname, het, env={"MG_RESID_MARCH_N": "0"} if march else None)
     op = C.operator(n, pname, het)
     m = C.mesh(n)
     x = mg_inputs.uniform_vector(n, 11)
@@ -300,16 +304,19 @@ def test_solve_matches_cycles():
     assert np.all(np.abs(hist - hO[:4]) <= 1e-10 * hO[:4])
 
 
-@pytest.mark.parametrize("n,levels,pname,relax", [(16, 3, "unit", "vanka"), (32, 4, "cfg5", "vanka"),
-                                                 (32, 4, "unit", "bsr")])
-def test_fgmres_history(n, levels, pname, relax):
+@pytest.mark.parametrize("n,levels,pname,relax,march", [(16, 3, "unit", "vanka", False),
+                                                       (32, 4, "cfg5", "vanka", False),
+                                                       (32, 4, "unit", "bsr", False),
+                                                       (32, 4, "cfg5", "vanka", True)])
+def test_fgmres_history(n, levels, pname, relax, march):
     """FGMRES + one V-cycle per iteration: the GPU history equals the oracle's
     (oracle: modified Gram-Schmidt; GPU: classical Gram-Schmidt twice) to 1e-9 relative while
     above 1e3 x the rounding floor, and the final iterates agree."""
     torch = _torch()
     from paper_2107_04060_b200 import Opts
     from oracle.krylov import fgmres_mg
-    H = C.gpu_hierarchy(n, levels, pname)
+    # march: every kernel in its production (row-marching) variant, the residual / apply included
+    H = C.gpu_hierarchy(n, levels, pname, march=march, env={"MG_RESID_MARCH_N": "0"} if march else None)
     Oh = C.hierarchy(n, levels, pname, relax)
     m = Oh.meshes[0]
     b = mg_inputs.uniform_rhs(n, 3)
