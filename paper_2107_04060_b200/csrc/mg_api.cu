@@ -105,8 +105,9 @@ struct mg_ctx {
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
-    int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one CTA
-                                  // (measured slower: 442 vs 250 us per 256^2 cycle -- one SM is compute bound)
+    int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one kernel
+                                  // (measured slower: one CTA 442 us, grid-wide cooperative 323 us vs 247 us
+                                  //  per 256^2 cycle with the per-level kernels)
     int jacobi_table = 1;         // 1: Jacobi sweeps from the per-level table (bsr_jacobi_t_kernel)
     int jacobi_pair = 0;          // 1: two Jacobi sweeps per launch (bsr_jacobi2_kernel; measured slower:
                                   //    292 us vs 2 x 110 us at 2048^2, the per-tile halo work dominates)

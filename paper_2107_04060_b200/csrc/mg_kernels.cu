@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstdint>
 #include <cuda.h>
+#include <cooperative_groups.h>
 
 #include "mg_kernels.cuh"
 #include "mg_tables.h"
@@ -106,7 +107,7 @@ __device__ void norm_finish(const NormSink& S, double v) {
 template <bool NC>
 __device__ __forceinline__ double gld(const double* p) {
     if (NC) return __ldg(p);
-    return *p;
+    return __ldcg(p);   // L2: coherent with what other CTAs of this kernel wrote before a grid barrier
 }
 
 template <int W, int HT, int NP, bool NC = true>
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
 // functions as the per-level kernels, run by 16 virtual blocks of 64 threads over the tiles of a
 // level in rounds, with CTA barriers between the steps instead of kernel boundaries.  Loads are
 // plain (not read-only path): the kernel reads what it wrote.  Bitwise the per-level sequence.
-constexpr int BOT_VB = 12, BOT_NT = BOT_VB * 64;
+constexpr int BOT_VB = 8, BOT_NT = BOT_VB * 64;
 constexpr int BOT_VSM = VTile<VSX, VSY>::SMEM > CTile<CSX, CSY>::SMEM_FUSED ? VTile<VSX, VSY>::SMEM
                                                                            : CTile<CSX, CSY>::SMEM_FUSED;
 constexpr int BOT_SMEM = BOT_VB * BOT_VSM;
@@ -577,39 +578,48 @@ __global__ void __launch_bounds__(BOT_NT, 1) bottom_kernel(const __grid_constant
     pdl_trigger();
     extern __shared__ double sm[];
     if (*A.stop) return;
+    // grid-wide when launched cooperatively over several CTAs (gridDim.x > 1), one CTA otherwise
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    auto gsync = [&]() {
+        if (gridDim.x > 1) grid.sync();
+        else __syncthreads();
+    };
     const int vb = threadIdx.x >> 6, t = threadIdx.x & 63;
+    const int gvb = blockIdx.x * BOT_VB + vb, nvb = gridDim.x * BOT_VB;   // global virtual block
     double* vsm = sm + vb * (BOT_VSM / 8);
     auto relax = [&](int l, const double* xin, double* xo, bool xzero) {
         const VankaParams& P = A.vp[l];
         const int n = P.L.n, tx = (n + VSX) / VSX, ntiles = tx * ((n + VSY) / VSY);
-        for (int r0 = 0; r0 < ntiles; r0 += BOT_VB) {
-            const int tile = r0 + vb;
+        for (int r0 = 0; r0 < ntiles; r0 += nvb) {   // rounds: uniform over the grid
+            const int tile = r0 + gvb;
             const bool act = tile < ntiles;
             const int bx = act ? tile % tx : 0, by = act ? tile / tx : 0;
             if (xzero) vanka_tile<true, VSX, VSY, false>(P, xin, A.b[l], xo, bx, by, t, vsm, act);
             else vanka_tile<false, VSX, VSY, false>(P, xin, A.b[l], xo, bx, by, t, vsm, act);
             __syncthreads();
         }
+        gsync();
     };
     auto restrict_ = [&](int l, const double* xl) {
         const LevelParams& L = A.vp[l].L;
         const int nc = L.n / 2, tx = (nc + CSX) / CSX, ntiles = tx * ((nc + CSY) / CSY);
-        for (int r0 = 0; r0 < ntiles; r0 += BOT_VB) {
-            const int tile = r0 + vb;
+        for (int r0 = 0; r0 < ntiles; r0 += nvb) {
+            const int tile = r0 + gvb;
             const bool act = tile < ntiles;
             const int bx = act ? tile % tx : 0, by = act ? tile / tx : 0;
             restrict_tile<1, false, CSX, CSY, false>(L, nc, A.pitch[l + 1], xl, A.b[l], A.b[l + 1], bx, by, t, vsm, act);
             __syncthreads();
         }
+        gsync();
     };
-    // x_f += P e_c on level l from e on level l + 1 (prolong_kernel's arithmetic, plain loads)
+    // x_f += P e_c on level l from e on level l + 1 (prolong_kernel's arithmetic, L2 loads)
     auto prolong_ = [&](int l, const double* e, double* x) {
         const int nf = A.vp[l].L.n, pitchf = A.vp[l].L.pitch, nc = nf / 2, pitchc = A.pitch[l + 1];
         const int64_t planec = (int64_t)(nc + 1) * pitchc, planef = (int64_t)(nf + 1) * pitchf;
-        for (int cell = threadIdx.x; cell < nc * nc; cell += BOT_NT) {
+        for (int cell = blockIdx.x * BOT_NT + threadIdx.x; cell < nc * nc; cell += gridDim.x * BOT_NT) {
             const int I = cell % nc, J = cell / nc;
             const double* e0 = e + (int64_t)J * pitchc + I;
-#define EC(dI, dJ, pl) e0[(pl) * planec + (dJ) * pitchc + (dI)]
+#define EC(dI, dJ, pl) __ldcg(e0 + (pl) * planec + (dJ) * pitchc + (dI))
 #define MG_Q(dI, dJ, pl, w) v = fma(w, EC(dI, dJ, pl), v);
             const int fi = 2 * I, fj = 2 * J;
             double* x0 = x + (int64_t)fj * pitchf + fi;
@@ -620,7 +630,7 @@ __global__ void __launch_bounds__(BOT_NT, 1) bottom_kernel(const __grid_constant
         v = 0.0;                                                                        \
         MG_PROLONG_1_##dj##_##kf(MG_Q) const double v1 = v;                             \
         double2* p2 = reinterpret_cast<double2*>(x0 + kf * planef + dj * pitchf);       \
-        double2 xv = *p2;                                                               \
+        double2 xv = __ldcg(p2);                                                        \
         if (is_active(kf, fi, fj + dj, nf)) xv.x += v0;                                 \
         if (is_active(kf, fi + 1, fj + dj, nf)) xv.y += v1;                             \
         *p2 = xv;                                                                       \
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(BOT_NT, 1) bottom_kernel(const __grid_constant
 #undef MG_Q
 #undef EC
         }
-        __syncthreads();
+        gsync();
     };
     const int nl = A.nl;
     double* cur[BOT_MAXL + 1];
@@ -646,19 +656,19 @@ __global__ void __launch_bounds__(BOT_NT, 1) bottom_kernel(const __grid_constant
         restrict_(l, a);
         cur[l] = a;
     }
-    // coarsest: x_c[slots] = G b_c[slots] (coarse_kernel's arithmetic)
-    {
+    // coarsest: x_c[slots] = G b_c[slots] (coarse_kernel's arithmetic), by CTA 0
+    if (blockIdx.x == 0) {
         double* rb = sm;
-        for (int k = threadIdx.x; k < A.N; k += BOT_NT) rb[k] = A.b[nl][A.slots[k]];
+        for (int k = threadIdx.x; k < A.N; k += BOT_NT) rb[k] = __ldcg(A.b[nl] + A.slots[k]);
         __syncthreads();
         for (int row = threadIdx.x; row < A.N; row += BOT_NT) {
             double acc = 0.0;
             for (int k = 0; k < A.N; ++k) acc = fma(__ldg(A.G + (int64_t)k * A.N + row), rb[k], acc);
             A.x[nl][A.slots[row]] = acc;
         }
-        __syncthreads();
-        cur[nl] = A.x[nl];
     }
+    gsync();
+    cur[nl] = A.x[nl];
     for (int l = nl - 1; l >= 0; --l) {
         prolong_(l, cur[l + 1], cur[l]);
         double* a = cur[l];
@@ -3086,8 +3096,25 @@ cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode,
 }
 
 cudaError_t launch_bottom(const BottomArgs& A, cudaStream_t s) {
-    launch_k(bottom_kernel, 1, BOT_NT, BOT_SMEM, s, A);
-    return cudaGetLastError();
+    // grid-wide: as many CTAs as can be co-resident (one per SM), launched cooperatively
+    static int nblk = 0;
+    if (!nblk) {
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bottom_kernel, BOT_NT, BOT_SMEM);
+        nblk = std::max(1, per) * sm_count();
+        if (const char* v = getenv("MG_BOTTOM_CTAS")) nblk = std::max(1, std::min(nblk, atoi(v)));
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(BOT_NT);
+    cfg.dynamicSmemBytes = BOT_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, bottom_kernel, A);
 }
 
 cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double* e, double* x, const int* stop,

@@ -32,9 +32,9 @@ cudaError_t launch_gs(int mode, const double* w, double* wo, const GsPtrs& V, in
                       const double* sc, int64_t len, double* partials, unsigned* counter, double* out, cudaStream_t s);
 int gs_partials_needed();
 
-// The bottom of a Vanka V-cycle in one CTA (bottom_kernel): levels lb .. lb + nl - 1 (n <= 32) and
-// the coarsest lb + nl.  Index l below is relative to lb.
-constexpr int BOT_MAXL = 4;
+// The bottom of a Vanka V-cycle in one grid-wide kernel (bottom_kernel, cooperative launch): levels
+// lb .. lb + nl - 1 and the coarsest lb + nl.  Index l below is relative to lb.
+constexpr int BOT_MAXL = 6;
 struct BottomArgs {
     int nl, nu1, nu2;
     VankaParams vp[BOT_MAXL];          // omega set

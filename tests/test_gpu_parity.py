@@ -262,14 +262,14 @@ def test_fused_prolong_bitwise(n, levels, pname, nu2):
 
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (128, 6, "stiff", 1)])
 def test_bottom_kernel_bitwise(n, levels, pname, nu):
-    """The single-CTA bottom of the V-cycle (levels with n <= 32 and the coarsest solve in one
-    kernel) reproduces bitwise the per-level kernel sequence it replaces (same tile functions,
-    same order), over several cycles and for V(2,2)."""
+    """The grid-wide bottom of the V-cycle (levels with n <= 128 and the coarsest solve in one
+    cooperative kernel) reproduces bitwise the per-level kernel sequence it replaces (same tile
+    functions, same order), over several cycles and for V(2,2)."""
     torch = _torch()
     from paper_2107_04060_b200 import Opts
     b = mg_inputs.uniform_rhs(n, 4)
     out = []
-    for bottom in ("32", "0"):   # MG_BOTTOM_N=32 switches the (off by default) bottom kernel on
+    for bottom in ("128", "0"):   # MG_BOTTOM_N=128 switches the (off by default) bottom kernel on
         H = C.gpu_hierarchy(n, levels, pname, env={"MG_BOTTOM_N": bottom})
         xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
         hist = [H.cycle(xd, bd, Opts(nu, nu, "vanka", 0.7)) for _ in range(3)]

@@ -1,2 +1,3 @@
-for rm in 512 100000 512; do MG_RESID_MARCH_N=$rm python bench.py --no-cpu-baseline --no-e2e --steps 20 > gpurun_out/bq_rm$rm.log 2>&1; tail -1 gpurun_out/bq_rm$rm.log | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print($rm, round(d['ms_per_step'],3), d['solve']['iterations'], round(d['solve']['ms'],1))" >> gpurun_out/rm.txt; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "bottom" 2>&1 | tail -3 > gpurun_out/q_test.txt
+for bn in 128 64 0; do MG_BOTTOM_N=$bn timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-solve --steps 100 > gpurun_out/bq_b$bn.log 2>&1; done
+for bn in 128 0; do MG_BOTTOM_N=$bn timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-solve --steps 200 --n 256 > gpurun_out/bq_n256_b$bn.log 2>&1; done
