@@ -102,15 +102,13 @@ struct mg_ctx {
     bool timed_ran = false;
     std::vector<cudaEvent_t> lev;  // per-level phase events of the traced cycle (4 (L-1) + 2)
     int launches = 0;             // kernel launches enqueued by the last captured cycle
-    int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 1: chunk rings, 0: 2-D tiles
+    int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 0: 2-D tiles everywhere
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one kernel
                                   // (measured slower: one CTA 442 us, grid-wide cooperative 323 us vs 247 us
                                   //  per 256^2 cycle with the per-level kernels)
     int jacobi_table = 1;         // 1: Jacobi sweeps from the per-level table (bsr_jacobi_t_kernel)
-    int jacobi_pair = 0;          // 1: two Jacobi sweeps per launch (bsr_jacobi2_kernel; measured slower:
-                                  //    292 us vs 2 x 110 us at 2048^2, the per-tile halo work dominates)
     int bsr_impl = 1;             // 1: row-marching BSR stages on levels with n >= march_min_n, 0: 2-D tiles
     int fuse_prolong = 1;         // 1: prolongation fused into the first post-sweep of marching Vanka levels
     int cgs_passes = 2;           // FGMRES Gram-Schmidt passes (MG_CGS_PASSES)
@@ -167,9 +165,7 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
             CK(launch_vanka_march2(P, xin, b, xout, false, S, s, &E));
             return MG_OK;
         }
-        if (c->vanka_impl == 3 && Lv.n >= c->march_min_n) CK(launch_vanka_march3(P, xin, b, xout, xzero, S, s));
-        else if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
-        else if (c->vanka_impl == 1 && Lv.n >= c->march_min_n) CK(launch_vanka_march(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
     }
@@ -183,9 +179,6 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         if (c->jacobi_table) {
             CK(launch_bsr_jacobi_t(Lv.vp.L, o.omega_J, Lv.g, Lv.jtab, cur, nxt, s));
             k += 1;
-        } else if (c->jacobi_pair && k + 1 < o.jacobi_sweeps) {
-            CK(launch_bsr_jacobi2(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
-            k += 2;
         } else {
             CK(launch_bsr_jacobi(Lv.vp.L, o.omega_J, Lv.g, cur, nxt, s));
             k += 1;
@@ -434,7 +427,6 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     set_small_tile_n(getenv("MG_SMALL_TILE_N") ? atoi(getenv("MG_SMALL_TILE_N")) : 128);
     set_pdl(getenv("MG_PDL") ? atoi(getenv("MG_PDL")) != 0 : 0);
     set_resid_march_n(getenv("MG_RESID_MARCH_N") ? atoi(getenv("MG_RESID_MARCH_N")) : 512);
-    if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v) != 0;
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
@@ -453,8 +445,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         Lv.plane = (int64_t)(Lv.n + 1) * Lv.pitch;
         Lv.len = 10 * Lv.plane;
         max_blocks = std::max(max_blocks, std::max(blocks_vanka(Lv.n), std::max(blocks_residual(Lv.n), blocks_bsr(Lv.n))));
-        max_blocks = std::max(max_blocks, std::max(blocks_vanka_march(Lv.n), blocks_vanka_march2(Lv.n)));
-        max_blocks = std::max(max_blocks, blocks_vanka_march3(Lv.n));
+        max_blocks = std::max(max_blocks, blocks_vanka_march2(Lv.n));
         max_blocks = std::max(max_blocks, blocks_residual_march(Lv.n));
         HostLevelTables* t = new HostLevelTables;
         if (host_level_tables(Lv.n, c->m, t, err, sizeof(err))) {

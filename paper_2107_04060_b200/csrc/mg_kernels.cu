@@ -1046,114 +1046,6 @@ __global__ void __launch_bounds__(256) bsr_jacobi_t_kernel(const LevelParams L, 
     }
 }
 
-// Two Jacobi sweeps on S dp = g in one pass.  Per tile: dp0 on the tile + 2 rings of
-// cells, K^{-1} on the tile + 2 (low) / 3 (high) rings, g and the intermediate dp1 on the tile + 1
-// ring.  The edge factors tau / D_w(e) and 1 / diag(S) are formed once per tile (one division per
-// edge and per triangle) and shared by both sweeps.
-constexpr int JT_X = 32, JT_Y = 8, JNT = 256;
-constexpr int J0W = JT_X + 4, J0H = JT_Y + 4, J1W = JT_X + 2, J1H = JT_Y + 2;
-constexpr int JKW = JT_X + 5, JKH = JT_Y + 5, JEW = JT_X + 3, JEH = JT_Y + 3;
-
-template <bool HET>
-__global__ void __launch_bounds__(JNT) bsr_jacobi2_kernel(const LevelParams L, double omJ,
-                                                          const double* __restrict__ g,
-                                                          const double* __restrict__ dpi, double* __restrict__ dpo) {
-    pdl_wait();
-    pdl_trigger();
-    __shared__ double d0[2][J0H][J0W];                            // cells [i0-2, i0+34) x [j0-2, j0+10)
-    __shared__ double kk[HET ? 2 : 1][HET ? JKH : 1][HET ? JKW : 1];   // cells [i0-2, i0+35) x [j0-2, j0+11)
-    __shared__ double tw[3][JEH][JEW];                            // tau / D_w of edges H, V, D at [i0-1, i0+34) x [j0-1, j0+10)
-    __shared__ double gg[2][J1H][J1W];                            // cells [i0-1, i0+33) x [j0-1, j0+9)
-    __shared__ double dsg[2][J1H][J1W];                           // diag(S)
-    __shared__ double ids[2][J1H][J1W];                           // 1 / diag(S)
-    __shared__ double d1[2][J1H][J1W];
-    if (*L.stop) return;
-    const int n = L.n;
-    const int64_t plane = L.plane, pitch = L.pitch;
-    const int i0 = blockIdx.x * JT_X, j0 = blockIdx.y * JT_Y;
-    auto inmesh = [&](int ci, int cj) { return ci >= 0 && cj >= 0 && ci < n && cj < n; };
-    for (int t = threadIdx.x; t < 2 * J0H * J0W; t += JNT) {
-        const int sh = t / (J0H * J0W), rem = t - sh * (J0H * J0W), ly = rem / J0W, lx = rem - ly * J0W;
-        const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
-        d0[sh][ly][lx] = inmesh(ci, cj) ? __ldg(dpi + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
-    }
-    if (HET)
-        for (int t = threadIdx.x; t < 2 * JKH * JKW; t += JNT) {
-            const int sh = t / (JKH * JKW), rem = t - sh * (JKH * JKW), ly = rem / JKW, lx = rem - ly * JKW;
-            const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
-            kk[sh][ly][lx] = inmesh(ci, cj) ? __ldg(L.kinv_field + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
-        }
-    for (int t = threadIdx.x; t < 2 * J1H * J1W; t += JNT) {
-        const int sh = t / (J1H * J1W), rem = t - sh * (J1H * J1W), ly = rem / J1W, lx = rem - ly * J1W;
-        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
-        gg[sh][ly][lx] = inmesh(ci, cj) ? __ldg(g + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
-    }
-    __syncthreads();
-    auto kinv = [&](int ci, int cj, int sh) -> double {
-        if (!HET) return L.kinv;
-        return kk[sh][cj - (j0 - 2)][ci - (i0 - 2)];
-    };
-    // tau / D_w of the edges owned by index (ci, cj) (planes 5, 6, 7 -> H, V, D); 0 if inactive
-    for (int t = threadIdx.x; t < 3 * JEH * JEW; t += JNT) {
-        const int e = t / (JEH * JEW), rem = t - e * (JEH * JEW), ly = rem / JEW, lx = rem - ly * JEW;
-        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
-        double d = 0.0;
-#define MG_I(kk_, cdx, cdy, sh, q) d = fma(L.mw1d[sh][(q) - 9], kinv(ci + (cdx), cj + (cdy), sh), d);
-        if (e == 0) { MG_INCIDENT_5(MG_I) }
-        else if (e == 1) { MG_INCIDENT_6(MG_I) }
-        else { MG_INCIDENT_7(MG_I) }
-#undef MG_I
-        tw[e][ly][lx] = is_active(5 + e, ci, cj, n) ? L.tau / d : 0.0;
-    }
-    __syncthreads();
-    // edge factor of local edge e of triangle sh in cell (i, j): LL -> H(i,j), V(i,j), D(i,j);
-    // UR -> H(i,j+1), V(i+1,j), D(i,j)
-    auto tew = [&](int i, int j, int sh, int e) -> double {
-        const int ci = sh == 0 ? i : (e == 1 ? i + 1 : i), cj = sh == 0 ? j : (e == 0 ? j + 1 : j);
-        return tw[e][cj - (j0 - 1)][ci - (i0 - 1)];
-    };
-    for (int t = threadIdx.x; t < 2 * J1H * J1W; t += JNT) {
-        const int sh = t / (J1H * J1W), rem = t - sh * (J1H * J1W), ly = rem / J1W, lx = rem - ly * J1W;
-        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
-        double ds = L.s0h2;
-#pragma unroll
-        for (int e = 0; e < 3; ++e) ds += tew(ci, cj, sh, e) * L.bw[sh][e] * L.bw[sh][e];
-        dsg[sh][ly][lx] = ds;
-        ids[sh][ly][lx] = inmesh(ci, cj) ? 1.0 / ds : 0.0;
-    }
-    __syncthreads();
-    // one Jacobi update of triangle sh of cell (i, j) (in the mesh) from dp values src(ci, cj, sh)
-    auto jac = [&](int i, int j, int sh, int ly, int lx, auto src) -> double {
-        const double dself = src(i, j, sh);
-        double off = 0.0;
-#pragma unroll
-        for (int e = 0; e < 3; ++e) {
-            const double c = tew(i, j, sh, e) * L.bw[sh][e];   // 0 for an inactive edge
-            int ni, nj;
-            if (sh == 0) { ni = e == 1 ? i - 1 : i; nj = e == 0 ? j - 1 : j; }
-            else         { ni = e == 1 ? i + 1 : i; nj = e == 0 ? j + 1 : j; }
-            off = fma(c * L.bw[1 - sh][e], src(ni, nj, 1 - sh), off);
-        }
-        const double sd = fma(dsg[sh][ly][lx], dself, off);
-        return dself + omJ * (gg[sh][ly][lx] - sd) * ids[sh][ly][lx];
-    };
-    auto s0 = [&](int ci, int cj, int sh) { return d0[sh][cj - (j0 - 2)][ci - (i0 - 2)]; };
-    auto s1 = [&](int ci, int cj, int sh) { return d1[sh][cj - (j0 - 1)][ci - (i0 - 1)]; };
-    for (int t = threadIdx.x; t < 2 * J1H * J1W; t += JNT) {
-        const int sh = t / (J1H * J1W), rem = t - sh * (J1H * J1W), ly = rem / J1W, lx = rem - ly * J1W;
-        const int ci = i0 - 1 + lx, cj = j0 - 1 + ly;
-        d1[sh][ly][lx] = inmesh(ci, cj) ? jac(ci, cj, sh, ly, lx, s0) : 0.0;
-    }
-    __syncthreads();
-    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
-    const int i = i0 + lx, j = j0 + ly;
-    if (i > n || j > n) return;
-    const int64_t o = (int64_t)j * pitch + i;
-#pragma unroll
-    for (int sh = 0; sh < 2; ++sh)
-        dpo[sh * plane + o] = (i < n && j < n) ? jac(i, j, sh, ly + 1, lx + 1, s1) : 0.0;
-}
-
 // stage B: du = F_u^{-1}(r_u - alpha B_u^T dp), dw = (r_w - tau B_w^T dp)/(tau D_w),
 // xout = x + omega (du, dw, dp)
 constexpr int BB_XW = BTX + 4, BB_XH = BTY + 4, BB_RW = BTX + 2, BB_RH = BTY + 2;
@@ -1296,22 +1188,7 @@ __global__ void kinv_coarsen_kernel(int nf, int pitchf, const double* __restrict
 }
 
 // ------------------------------------------------------------------------------------------
-// Row-marching additive Vanka sweep with TMA-prefetched row chunks (the level-0 hot kernel).
-//
-// A CTA owns a strip of MT columns [i0, i0+MT) and MH rows [j0, j0+MH) and marches up in
-// steps of MR rows.  Step s computes the residual rows j0+s*MR+1 .. j0+(s+1)*MR (one index per
-// thread), the patch solves at the same vertex rows, and updates the owner rows
-// j0+s*MR .. j0+(s+1)*MR-1 (the lowest patch row and residual row are carried from step s-1;
-// step -1 is the prologue).  So the y halo is never recomputed (only the x halo: (MT+2)/MT).
-// x and b arrive as TMA boxes of MR rows x 10 planes (zero fill outside the mesh) in 3-slot ring
-// buffers guarded by mbarriers and are prefetched two steps ahead, so the loads of later rows
-// overlap the fp64 work of the current ones.  r overwrites b in place.
-constexpr int MT = 30, MR = 4, MNT = (MT + 2) * MR;   // 128 threads: one residual position each
-constexpr int M_XW = MT + 4, M_BW = MT + 4, M_CW = MT + 1;   // b box as wide as x: box origins must be 16-B aligned
-static_assert(MT % 2 == 0, "strip origin i0 - 2 must be an even column (16-byte aligned TMA box)");
-constexpr int M_XCH = 10 * MR * M_XW, M_BCH = 10 * MR * M_BW, M_CCH = 20 * MR * M_CW;   // doubles per chunk
-constexpr int M_SMEM = (3 * M_XCH + 3 * M_BCH + 2 * M_CCH) * 8 + 64;
-
+// mbarrier / TMA helpers of the row-marching kernels
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -1359,157 +1236,6 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
         : "memory");
 }
 
-template <bool XZERO>
-__global__ void __launch_bounds__(MNT, 2) vanka_march_kernel(const __grid_constant__ CUtensorMap tmx,
-                                                             const __grid_constant__ CUtensorMap tmb,
-                                                             const VankaParams P, double* __restrict__ xo,
-                                                             NormSink S, int MH) {
-    pdl_wait();
-    pdl_trigger();
-    extern __shared__ __align__(128) double sm[];
-    double* xr = sm;                    // [3][10][MR][M_XW]
-    double* br = xr + 3 * M_XCH;        // [3][10][MR][M_BW]  (b, overwritten by r)
-    double* cr = br + 3 * M_BCH;        // [2][20][MR][M_CW]  patch corrections
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + 2 * M_CCH);   // bars[0..2] x, bars[3..5] b
-    const LevelParams& L = P.L;
-    if (*L.stop) return;
-    const int n = L.n;
-    const int i0 = blockIdx.x * MT, j0 = blockIdx.y * MH;
-    const int rows = min(MH, n + 1 - j0);
-    const int nsteps = (rows + MR - 1) / MR;
-    const int t = threadIdx.x;
-    // chunk c of x holds rows [j0 + (c-1) MR, j0 + c MR); chunk d of b holds rows [j0 + (d-1) MR + 1, j0 + d MR]
-    const int nxc = nsteps + 2, nbc = nsteps + 1;
-    auto issue_x = [&](int c) {
-        if (!XZERO && c < nxc) {
-            mbar_expect_tx(&bars[c % 3], M_XCH * 8);
-            tma_load3(xr + (c % 3) * M_XCH, &tmx, i0 - 2, j0 + (c - 1) * MR, 0, &bars[c % 3]);
-        }
-    };
-    auto issue_b = [&](int d) {
-        if (d < nbc) {
-            mbar_expect_tx(&bars[3 + d % 3], M_BCH * 8);
-            tma_load3(br + (d % 3) * M_BCH, &tmb, i0 - 2, j0 + (d - 1) * MR + 1, 0, &bars[3 + d % 3]);
-        }
-    };
-    if (t == 0) {
-        for (int k = 0; k < 6; ++k) mbar_init(&bars[k], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (t == 0) {
-        issue_x(0);
-        issue_x(1);
-        issue_x(2);
-        issue_b(0);
-        issue_b(1);
-    }
-    double nrm = 0.0;
-    for (int s = -1; s < nsteps; ++s) {
-        // ---- residual rows y = j0 + s MR + 1 + q (b chunk s+1, row q), x rows y-1 .. y+1
-        const int bslot = (s + 1) % 3;
-        if (!XZERO) {
-            mbar_wait(&bars[(s + 1) % 3], ((s + 1) / 3) & 1);
-            mbar_wait(&bars[(s + 2) % 3], ((s + 2) / 3) & 1);
-        }
-        mbar_wait(&bars[3 + bslot], ((s + 1) / 3) & 1);
-        {
-            const int q = t / (MT + 2), lx = t - q * (MT + 2);
-            const int y = j0 + s * MR + 1 + q, i = i0 - 1 + lx;
-            double* bp = br + bslot * M_BCH + q * M_BW + (lx + 1);
-            double rv[10];
-            if (!XZERO) {
-                // x row y lives in chunk s+1 (rows q+1 < MR) or s+2; rows y-1 and y+1 likewise
-                const int ym = q, y0 = q + 1, yp = q + 2;   // offsets from the first row of chunk s+1
-                const double* base1 = xr + ((s + 1) % 3) * M_XCH + (lx + 1);
-                const double* base2 = xr + ((s + 2) % 3) * M_XCH + (lx + 1);
-                const double* xm = (ym < MR ? base1 + ym * M_XW : base2 + (ym - MR) * M_XW);
-                const double* x0 = (y0 < MR ? base1 + y0 * M_XW : base2 + (y0 - MR) * M_XW);
-                const double* xp = (yp < MR ? base1 + yp * M_XW : base2 + (yp - MR) * M_XW);
-                double av[10];
-                apply_rows<MR * M_XW, false>(L, xm, x0, xp, i, y, av);
-#pragma unroll
-                for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, y, n) ? bp[k * MR * M_BW] - av[k] : 0.0;
-#pragma unroll
-                for (int k = 0; k < 10; ++k) bp[k * MR * M_BW] = rv[k];
-            } else {
-#pragma unroll
-                for (int k = 0; k < 10; ++k) rv[k] = bp[k * MR * M_BW];   // r = b (b inactive slots are 0)
-            }
-            if (lx >= 1 && lx <= MT && i <= n && y >= j0 && y < j0 + rows) {
-#pragma unroll
-                for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
-            }
-        }
-        __syncthreads();
-        // ---- patch solves at vertex rows bb = j0 + s MR + 1 + q: r rows bb-1 (carry for q = 0) and bb
-        const int cslot = (s + 1) & 1;
-        if (t < MR * M_CW) {
-            const int q = t / M_CW, px = t - q * M_CW;
-            const int a = i0 + px, bb = j0 + s * MR + 1 + q;
-            double* out = cr + cslot * M_CCH + q * M_CW + px;
-            if (a <= n && bb >= 0 && bb <= n) {
-                const double* r0 = br + bslot * M_BCH + q * M_BW + (px + 2);
-                const double* rm = (q > 0) ? r0 - M_BW : br + (s % 3 + (s < 0 ? 3 : 0)) % 3 * M_BCH + (MR - 1) * M_BW + (px + 2);
-                double rr[20];
-#define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * (MR * M_BW) + (dx)]
-                rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
-                rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
-                rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
-                rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
-                rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
-                rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
-                rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
-#undef RR
-                patch_apply20(P, vertex_class(a, bb, n), rr, out, MR * M_CW);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 20; ++k) out[k * MR * M_CW] = 0.0;
-            }
-        }
-        __syncthreads();
-        // ---- owners y = j0 + s MR + q: patch rows y (carry for q = 0) and y + 1
-        if (s >= 0 && t < MR * MT) {
-            const int q = t / MT, lx = t - q * MT;
-            const int y = j0 + s * MR + q, i = i0 + lx;
-            if (i <= n && y < j0 + rows) {
-                const double* c1 = cr + cslot * M_CCH + q * M_CW + lx;                         // row y + 1
-                const double* c0 = (q > 0) ? c1 - M_CW : cr + (cslot ^ 1) * M_CCH + (MR - 1) * M_CW + lx;   // row y
-#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * (MR * M_CW) + (dx)]
-                double d[10];
-                d[0] = CC(0, 0, 0);
-                d[1] = CC(1, 0, 0);
-                d[2] = CC(2, 0, 0) + CC(3, 1, 0);
-                d[3] = CC(4, 0, 0) + CC(5, 0, 1);
-                d[4] = CC(6, 1, 0) + CC(7, 0, 1);
-                d[5] = CC(8, 0, 0) + CC(9, 1, 0);
-                d[6] = CC(10, 0, 0) + CC(11, 0, 1);
-                d[7] = CC(12, 1, 0) + CC(13, 0, 1);
-                d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
-                d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
-#undef CC
-                // x at row y = chunk s+1, row q
-                const double* xv = xr + ((s + 1) % 3) * M_XCH + q * M_XW + (lx + 2);
-                const int64_t o = (int64_t)y * L.pitch + i;
-#pragma unroll
-                for (int k = 0; k < 10; ++k) {
-                    const double xk = XZERO ? 0.0 : xv[k * MR * M_XW];
-                    xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(P.omega, d[k], xk) : 0.0;
-                }
-            }
-        }
-        __syncthreads();
-        // ---- prefetch: x chunk s+4 into the slot of chunk s+1 (last used now), b chunk s+3 into the slot
-        //      of chunk s (the carry of this step)
-        if (t == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_x(s + 4);
-            issue_b(s + 3);
-        }
-    }
-    if (S.out || S.state) norm_finish<MNT>(S, nrm);
-}
-
 template <typename F>
 void set_smem(F* f, int bytes) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -1518,7 +1244,8 @@ void set_smem(F* f, int bytes) {
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
-// Row-marching Vanka, row-granular rings (3 CTAs / SM).  Same arithmetic as vanka_march_kernel;
+// Row-marching Vanka, row-granular rings (3 CTAs / SM): the level-0 hot kernel.  Same arithmetic as
+// vanka_kernel (the 2-D tile sweep);
 // x, b and the patch outputs live in modular rings of single rows (x: 10, b/r: 9, patches: 5
 // rows), filled by one 3-D TMA box per row (32 columns x 1 row x 10 planes) and prefetched one
 // step ahead, which cuts shared memory to 72 KB per CTA.
@@ -1794,157 +1521,6 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
         }
     }
     if (S.out || S.state) norm_finish<PROL ? M2NT + 32 * M2NP : M2NT>(S, nrm);
-}
-
-// ------------------------------------------------------------------------------------------
-// Row-marching Vanka, 4 CTAs / SM.  As vanka_march2_kernel, but b is read straight from global
-// memory into registers at the start of each step (it is used once, by one thread, so staging it in
-// shared memory buys nothing) and only r is kept in a 5-row ring: 54 KB of shared memory per CTA.
-constexpr int M3T = 24, M3R = 4, M3W = M3T + 4, M3RW = M3T + 2, M3C = M3T + 1, M3NT = 128;
-constexpr int M3XR = 10, M3RR = 5, M3CR = 5;
-constexpr int M3XROW = ((10 * M3W * 8 + 127) / 128) * 16, M3RROW = 10 * M3RW;   // x slots 128-byte aligned (TMA)
-constexpr int M3SMEM = (M3XR * M3XROW + M3RR * M3RROW + M3CR * 20 * M3C) * 8 + 64;
-static_assert(M3T + 2 <= 32 && M3R * 32 == M3NT, "one warp per row, one residual position per thread");
-static_assert(M3T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
-
-template <bool XZERO>
-__global__ void __launch_bounds__(M3NT, 4) vanka_march3_kernel(const __grid_constant__ CUtensorMap tmx,
-                                                               const VankaParams P, const double* __restrict__ b,
-                                                               double* __restrict__ xo, NormSink S, int MH) {
-    pdl_wait();
-    pdl_trigger();
-    extern __shared__ __align__(128) double sm[];
-    double* xr = sm;                        // [M3XR][10][M3W]
-    double* rr_ = xr + M3XR * M3XROW;       // [M3RR][10][M3RW]   residual rows
-    double* cr = rr_ + M3RR * M3RROW;       // [M3CR][20][M3C]    patch corrections
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M3CR * 20 * M3C);
-    const LevelParams& L = P.L;
-    if (*L.stop) return;
-    const int n = L.n;
-    const int i0 = blockIdx.x * M3T, j0 = blockIdx.y * MH;
-    const int rows = min(MH, n + 1 - j0);
-    const int nsteps = (rows + M3R - 1) / M3R;
-    const int t = threadIdx.x;
-    auto sx = [&](int y) { return (y - j0 + 2 * M3R) % M3XR; };
-    auto sr = [&](int y) { return (y - j0 + 2 * M3R) % M3RR; };
-    auto sc = [&](int y) { return (y - j0 + 2 * M3R) % M3CR; };
-    // group g: x rows first used by step g (g = -1: j0-R .. j0+1; else j0+gR+2 .. j0+gR+R+1)
-    auto issue = [&](int g) {
-        if (XZERO || g >= nsteps) return;
-        uint64_t* bar = &bars[(g + 1) & 1];
-        const int nx = g < 0 ? M3R + 2 : M3R;
-        mbar_expect_tx(bar, nx * 10 * M3W * 8);
-        const int xfirst = g < 0 ? j0 - M3R : j0 + g * M3R + 2;
-        for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * M3XROW, &tmx, i0 - 2, xfirst + k, 0, bar);
-    };
-    if (t == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (t == 0) {
-        issue(-1);
-        issue(0);
-    }
-    const int lane = t & 31, q = t >> 5;
-    double nrm = 0.0;
-    for (int s = -1; s < nsteps; ++s) {
-        // ---- residual rows y = j0 + s R + 1 + q, column i = i0 - 1 + lane; b straight from HBM
-        {
-            const int y = j0 + s * M3R + 1 + q, i = i0 - 1 + lane;
-            const bool inrow = lane < M3RW;
-            const bool in = inrow && i >= 0 && i <= n && y >= 0 && y <= n;
-            double bv[10];
-            const int64_t o = (int64_t)y * L.pitch + i;
-#pragma unroll
-            for (int k = 0; k < 10; ++k) bv[k] = (in && is_active(k, i, y, n)) ? __ldg(b + k * L.plane + o) : 0.0;
-            if (!XZERO) mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
-            if (inrow) {
-                double* rp = rr_ + sr(y) * M3RROW + lane;
-                const bool own = lane >= 1 && lane <= M3T && i <= n && y >= j0 && y < j0 + rows;
-                double rv[10];
-                if (!XZERO) {
-                    const double* xm = xr + sx(y - 1) * M3XROW + (lane + 1);
-                    const double* x0 = xr + sx(y) * M3XROW + (lane + 1);
-                    const double* xp = xr + sx(y + 1) * M3XROW + (lane + 1);
-                    double av[10];
-                    apply_rows<M3W, false>(L, xm, x0, xp, i, y, av);
-#pragma unroll
-                    for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, y, n) ? bv[k] - av[k] : 0.0;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 10; ++k) rv[k] = bv[k];
-                }
-#pragma unroll
-                for (int k = 0; k < 10; ++k) rp[k * M3RW] = rv[k];
-                if (own) {
-#pragma unroll
-                    for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
-                }
-            }
-        }
-        __syncthreads();
-        // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
-        if (lane < M3C) {
-            const int px = lane;
-            const int a = i0 + px, bb = j0 + s * M3R + 1 + q;
-            double* out = cr + sc(bb) * (20 * M3C) + px;
-            if (a <= n && bb >= 0 && bb <= n) {
-                const double* r0 = rr_ + sr(bb) * M3RROW + (px + 1);
-                const double* rm = rr_ + sr(bb - 1) * M3RROW + (px + 1);
-                double rr[20];
-#define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * M3RW + (dx)]
-                rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
-                rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
-                rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
-                rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
-                rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
-                rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
-                rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
-#undef RR
-                patch_apply20(P, vertex_class(a, bb, n), rr, out, M3C);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 20; ++k) out[k * M3C] = 0.0;
-            }
-        }
-        __syncthreads();
-        // ---- owners y = j0 + s R + q: patch rows y and y + 1
-        if (s >= 0 && lane < M3T) {
-            const int y = j0 + s * M3R + q, i = i0 + lane;
-            if (i <= n && y < j0 + rows) {
-                const double* c0 = cr + sc(y) * (20 * M3C) + lane;
-                const double* c1 = cr + sc(y + 1) * (20 * M3C) + lane;
-#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * M3C + (dx)]
-                double d[10];
-                d[0] = CC(0, 0, 0);
-                d[1] = CC(1, 0, 0);
-                d[2] = CC(2, 0, 0) + CC(3, 1, 0);
-                d[3] = CC(4, 0, 0) + CC(5, 0, 1);
-                d[4] = CC(6, 1, 0) + CC(7, 0, 1);
-                d[5] = CC(8, 0, 0) + CC(9, 1, 0);
-                d[6] = CC(10, 0, 0) + CC(11, 0, 1);
-                d[7] = CC(12, 1, 0) + CC(13, 0, 1);
-                d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
-                d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
-#undef CC
-                const double* xv = xr + sx(y) * M3XROW + (lane + 2);
-                const int64_t o = (int64_t)y * L.pitch + i;
-#pragma unroll
-                for (int k = 0; k < 10; ++k) {
-                    const double xk = XZERO ? 0.0 : xv[k * M3W];
-                    xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(P.omega, d[k], xk) : 0.0;
-                }
-            }
-        }
-        __syncthreads();
-        if (t == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(s + 2);
-        }
-    }
-    if (S.out || S.state) norm_finish<M3NT>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2601,8 +2177,6 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
 
 void kernels_init() {
     set_smem(bottom_kernel, BOT_SMEM);
-    set_smem(vanka_march3_kernel<false>, M3SMEM);
-    set_smem(vanka_march3_kernel<true>, M3SMEM);
     set_smem(vanka_march2_kernel<false, false>, M2SMEM);
     set_smem(vanka_march2_kernel<true, false>, M2SMEM);
     set_smem(vanka_march2_kernel<false, true>, M2SMEM);
@@ -2616,8 +2190,6 @@ void kernels_init() {
     set_smem(bsr_b_march_kernel<true, true>, BB2_SMEM);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
     set_smem(restrict_march_kernel<true>, Q_SMEM);
-    set_smem(vanka_march_kernel<false>, M_SMEM);
-    set_smem(vanka_march_kernel<true>, M_SMEM);
     set_smem(vanka_kernel<false>, V_SMEM);
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
@@ -2950,20 +2522,6 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
     return cudaGetLastError();
 }
 
-cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
-                               NormSink S, cudaStream_t s) {
-    const LevelParams& L = P.L;
-    CUtensorMap mx, mb;
-    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, M_XW, MR);
-    if (e != cudaSuccess) return e;
-    e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, M_BW, MR);   // both boxes start at column i0 - 2
-    if (e != cudaSuccess) return e;
-    const int MH = march_height(L.n, MT, MR, 2);
-    dim3 grid((L.n + MT) / MT, (L.n + MH) / MH);
-    if (x_zero) launch_k(vanka_march_kernel<true>, grid, MNT, M_SMEM, s, mx, mb, P, xo, S, MH);
-    else launch_k(vanka_march_kernel<false>, grid, MNT, M_SMEM, s, mx, mb, P, xo, S, MH);
-    return cudaGetLastError();
-}
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
                                 NormSink S, cudaStream_t s, const ProlSrc* E) {
     const LevelParams& L = P.L;
@@ -2993,27 +2551,7 @@ int blocks_vanka_march2(int n) {
     return ((n + M2T) / M2T) * ((n + MH) / MH);
 }
 
-cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
-                                NormSink S, cudaStream_t s) {
-    const LevelParams& L = P.L;
-    CUtensorMap mx;
-    cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, M3W, 1);
-    if (e != cudaSuccess) return e;
-    const int MH = march_height(L.n, M3T, M3R, 4);
-    dim3 grid((L.n + M3T) / M3T, (L.n + MH) / MH);
-    if (x_zero) launch_k(vanka_march3_kernel<true>, grid, M3NT, M3SMEM, s, mx, P, b, xo, S, MH);
-    else launch_k(vanka_march3_kernel<false>, grid, M3NT, M3SMEM, s, mx, P, b, xo, S, MH);
-    return cudaGetLastError();
-}
-int blocks_vanka_march3(int n) {
-    const int MH = march_height(n, M3T, M3R, 4);
-    return ((n + M3T) / M3T) * ((n + MH) / MH);
-}
 
-int blocks_vanka_march(int n) {
-    const int MH = march_height(n, MT, MR, 2);
-    return ((n + MT) / MT) * ((n + MH) / MH);
-}
 
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
                                double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab) {
@@ -3175,13 +2713,6 @@ cudaError_t launch_bsr_jacobi_t(const LevelParams& L, double omJ, const double* 
     return cudaGetLastError();
 }
 
-cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
-                               cudaStream_t s) {
-    dim3 grid((L.n + JT_X) / JT_X, (L.n + JT_Y) / JT_Y);
-    if (L.kinv_field) launch_k(bsr_jacobi2_kernel<true>, grid, JNT, 0, s, L, omJ, g, dpi, dpo);
-    else launch_k(bsr_jacobi2_kernel<false>, grid, JNT, 0, s, L, omJ, g, dpi, dpo);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega, const double* x, const double* b,
                          const double* dp, double* xo, bool x_zero, cudaStream_t s) {

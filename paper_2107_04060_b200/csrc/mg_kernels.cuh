@@ -63,9 +63,6 @@ int dot_partials_needed();
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
                          bool x_zero, NormSink norm, cudaStream_t s);
 // row-marching TMA variant of the same sweep (identical arithmetic); the production kernel
-cudaError_t launch_vanka_march(const VankaParams& P, const double* x, const double* b, double* xout,
-                               bool x_zero, NormSink norm, cudaStream_t s);
-int blocks_vanka_march(int n);
 // E != nullptr: relax x + P e_H (prolongation of the coarse iterate E->e fused into the sweep)
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s, const ProlSrc* E = nullptr);
@@ -78,16 +75,11 @@ void set_small_tile_n(int N);
 void set_pdl(int on);
 // residual / operator application on levels with n >= N through the marching kernel (scalar K)
 void set_resid_march_n(int N);
-cudaError_t launch_vanka_march3(const VankaParams& P, const double* x, const double* b, double* xout,
-                                bool x_zero, NormSink norm, cudaStream_t s);
-int blocks_vanka_march3(int n);
 // per-level Jacobi table (tau / D_w per RT0 edge, 1 / diag S per triangle; 5 planes) and the sweep using it
 cudaError_t launch_jtable(const LevelParams& L, double* tab, cudaStream_t s);
 cudaError_t launch_bsr_jacobi_t(const LevelParams& L, double omega_J, const double* g, const double* tab,
                                 const double* dp_in, double* dp_out, cudaStream_t s);
 // two Jacobi sweeps in one launch (same arithmetic as two launch_bsr_jacobi)
-cudaError_t launch_bsr_jacobi2(const LevelParams& L, double omJ, const double* g, const double* dpi, double* dpo,
-                               cudaStream_t s);
 // row-marching TMA variants of the two BSR stages (same arithmetic as launch_bsr_a / launch_bsr_b)
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
                                double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab);
