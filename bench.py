@@ -291,11 +291,25 @@ def main():
         rc, hist = H.fgmres(xs, b, o, rtol=1e-8, max_iters=300, restart=restart)
         e1.record(stream)
         torch.cuda.synchronize()
-        solve = {"method": f"FGMRES({restart}) (classical Gram-Schmidt twice), right-preconditioned by one V(1,1) cycle per iteration",
+        first_ms = e0.elapsed_time(e1)
+        true_rel = H.residual(0, xs, b, norm=True) / float(hist[0])
+        # the same solve again: the per-iteration cycle graphs (one per basis slot) and the FGMRES
+        # work space now exist, as in any later solve on this context
+        xs.zero_()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        rc2, hist2 = H.fgmres(xs, b, o, rtol=1e-8, max_iters=300, restart=restart)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solve = {"method": f"FGMRES({restart}) (classical Gram-Schmidt, second pass by the DGKS criterion), "
+                           "right-preconditioned by one V(1,1) cycle per iteration",
                  "rtol": 1e-8, "iterations": len(hist) - 1, "converged": rc == 0,
                  "final_rel_residual_estimate": float(hist[-1] / hist[0]),
-                 "true_rel_residual": H.residual(0, xs, b, norm=True) / float(hist[0]),
-                 "ms": e0.elapsed_time(e1)}
+                 "true_rel_residual": true_rel,
+                 "ms": e0.elapsed_time(e1),
+                 "ms_first": first_ms,
+                 "note": "ms: a repeated solve on the same context; ms_first: the first one, which also allocates "
+                         "the Krylov work space and instantiates the per-basis-slot cycle graphs"}
         del xs
 
     # e2e through the public C ABI with host buffers

@@ -192,9 +192,10 @@ int mg_solve(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts,
 
 /* Flexible GMRES(restart) on level 0, right-preconditioned by one V(nu1, nu2) cycle from a zero
  * initial guess per iteration -- the paper's solver for every timed experiment (PAPER.md:922,
- * SURVEY 8(f) rank 1).  Arnoldi by classical Gram-Schmidt applied twice, fused into three passes
- * over memory (dots; first update + second dots; second update + norm) on an unscaled basis whose
- * scales are kept on the host; deterministic device dot products; Givens rotations on the host.  Starts from the given x, stops at estimated
+ * SURVEY 8(f) rank 1).  Arnoldi by classical Gram-Schmidt with a second pass when the first one
+ * cancelled more than half of the vector (DGKS criterion), fused into passes over memory (dots;
+ * first update + second dots; second update + norm) on an unscaled basis whose scales are kept on
+ * the host; deterministic device dot products; Givens rotations on the host.  Starts from the given x, stops at estimated
  * ||r_k|| <= rtol ||r_0|| or max_iters.  history_host: NULL or max_iters+1 doubles: history[0] =
  * ||b - A x_0||, history[i] = the residual-norm estimate after i iterations (equal to
  * ||b - A x_i|| in exact arithmetic).  Work space: 2 restart + 2 level-0 vectors (allocated on

@@ -111,7 +111,8 @@ struct mg_ctx {
     int jacobi_table = 1;         // 1: Jacobi sweeps from the per-level table (bsr_jacobi_t_kernel)
     int bsr_impl = 1;             // 1: row-marching BSR stages on levels with n >= march_min_n, 0: 2-D tiles
     int fuse_prolong = 1;         // 1: prolongation fused into the first post-sweep of marching Vanka levels
-    int cgs_passes = 2;           // FGMRES Gram-Schmidt passes (MG_CGS_PASSES)
+    int cgs_passes = 0;           // FGMRES Gram-Schmidt: 0 adaptive (second pass when |U'| < |U|/sqrt2,
+                                  // the DGKS criterion), 1 single, 2 always twice (MG_CGS_PASSES)
     cudaEvent_t ev[6] = {};
 };
 
@@ -429,7 +430,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     set_resid_march_n(getenv("MG_RESID_MARCH_N") ? atoi(getenv("MG_RESID_MARCH_N")) : 512);
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
-    if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = atoi(v) == 1 ? 1 : 2;
+    if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = std::min(2, std::max(0, atoi(v)));
     auto bail = [&](int rc) {
         mg_free(c);
         return rc;
@@ -809,7 +810,14 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
             // coefficients of W_i: c_i = <U, W_i> s_i^2 (the kernels scale by s2d)
             CK(launch_gs(0, c->kw, nullptr, V, kk, nullptr, nullptr, len, c->kpart, c->kcnt, d1, s));
             CK(launch_gs(1, c->kw, c->kv[j + 1], V, kk, d1, s2d, len, c->kpart, c->kcnt, d2, s));
-            const bool two = c->cgs_passes == 2;
+            bool two = c->cgs_passes == 2;
+            if (c->cgs_passes == 0) {
+                // DGKS: reorthogonalise only when the first pass cancelled more than half of U
+                // (|U'|^2 < |U|^2 / 2); |U|^2 and |U'|^2 come with the two passes' dot products
+                CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                two = hh[40 + kk] < 0.5 * hh[kk];
+            }
             if (two) CK(launch_gs(2, c->kv[j + 1], c->kv[j + 1], V, kk, d2, s2d, len, c->kpart, c->kcnt, d3, s));
             CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
