@@ -285,9 +285,10 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        # restart length: 20 at 4096^2 (35 iterations either way, shorter Gram-Schmidt), 30 for the
-        # near-incompressible config 3 (restart 20 stagnates: 180 iterations vs 54; tools/fgmres_sweep.py)
-        restart = 30 if args.config == 3 else 20
+        # restart length (tools/fgmres_sweep.py, repeated solves): 10 at 4096^2 (40 iterations, 0.40 s;
+        # 20: 35 iterations, 0.50 s; 30: 35, 0.74 s -- the Gram-Schmidt passes grow with the basis),
+        # 30 for the near-incompressible config 3 (20: 180 iterations; 15 and below stagnate)
+        restart = 30 if args.config == 3 else 10
         rc, hist = H.fgmres(xs, b, o, rtol=1e-8, max_iters=300, restart=restart)
         e1.record(stream)
         torch.cuda.synchronize()
