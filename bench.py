@@ -213,11 +213,20 @@ def main():
     ap.add_argument("--trace-cycles", type=int, default=10)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--n", type=int, default=0, help="experiment: override the grid size (levels keep n_c = 4)")
+    ap.add_argument("--relax", default="", choices=["", "vanka", "bsr"],
+                    help="override the relaxation (config 2 names both: Vanka by default, --relax bsr for BSR)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     c = workload(args.config)
+    if args.relax:
+        if args.relax == "vanka" and c["K_seed"] is not None:
+            raise SystemExit("Vanka needs a scalar K (reading A20)")
+        c["relax_used"] = args.relax
+        c.setdefault("bsr_omega", 0.75)
+        c.setdefault("omega_J", 1.0)
+        c.setdefault("omega", 0.74)
     if args.n:
         c["n"], c["levels"] = args.n, int(np.log2(args.n // 4)) + 1
     if args.impl == "reference":
