@@ -20,11 +20,14 @@ Modules
   relax     additive Vanka and inexact BSR
   cycle     hierarchy, coarsest solve, V-cycle, stationary solve, rho_N
   manufactured  steady manufactured problem and FE error norms
+  lfa       two-grid local Fourier analysis from the assembled stencils
 
 Pins: every function here is checked by ``tests/test_oracle_*.py`` against
 something the paper or mathematics fixes (Appendix A stencils, Appendix B
 transfer sums, exact Galerkin identities, brute-force dense two-grid
 operators, the printed two-grid convergence factors of tab:vanka22 and
-tab:bsr_vanka11, FE convergence rates).  Functions without such a pin are
+tab:bsr_vanka11, their printed LFA predictions rho_LFA (all 72 cells
+within 1e-3, which pins A_h, A_H, P, Vanka and BSR on the infinite grid), FE
+convergence rates).  Functions without such a pin are
 marked "parity unpinned" in their docstring and in DESIGN.md.
 """
