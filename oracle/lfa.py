@@ -28,7 +28,10 @@ from __future__ import annotations
 
 import numpy as np
 
-from .cycle import Hierarchy
+from .mesh import Mesh
+from .fem import Operator
+from .transfer import Transfer
+from .relax import Vanka, BSR
 
 ALPHAS = ((0, 0), (1, 0), (0, 1), (1, 1))
 
@@ -90,34 +93,44 @@ def _prolong_columns(P, fine, coarse, X0, Y0):
 
 
 class TwoGridLFA:
-    """Symbols of one two-grid method built by the oracle's Hierarchy (two levels, fine n).
+    """Symbols of the two-grid method the oracle builds (the two levels of oracle.cycle.Hierarchy:
+    Operator on both meshes, Transfer, Vanka or BSR on the fine one).
 
-    relax='vanka' or 'bsr'; smoother options as in Hierarchy.smooth.  n must leave the stencil
-    centre (n/2, n/2) far from the boundary (n >= 16); the symbols depend on h = 1/n."""
+    relax='vanka' or 'bsr' (then omega_J, jacobi_sweeps as in Hierarchy.smooth).  The stencils are
+    read at the centre (n/2, n/2) of an n x n patch of mesh; h (default 1/n) is the fine spacing
+    the symbols are for -- the element integrals only see the vertex coordinates i h, so a small
+    patch of a fine mesh gives the interior stencils of the unit square at 1/h cells (the prolongation
+    weights are scale invariant, oracle.transfer.build_P).  n = 16 leaves every stencil (radius <= 3
+    indices for C) clear of the patch boundary."""
 
     def __init__(self, n, lam, mu, tau, alpha, inv_M, mu_f=1.0, K=1.0, relax="vanka",
-                 omega_J=None, jacobi_sweeps=1):
+                 omega_J=None, jacobi_sweeps=1, h=None):
         if n % 4 != 0 or n < 16:
             raise ValueError("n must be a multiple of 4, n >= 16")
-        Hh = Hierarchy(n, 2, lam, mu, tau, alpha, inv_M, mu_f, K=K, relax=relax)
-        fine, coarse = Hh.meshes
+        fine, coarse = Mesh(n), Mesh(n // 2)
+        if h is not None:
+            fine.h, coarse.h = h, 2.0 * h
+        self.h = fine.h
+        op_f = Operator(fine, lam, mu, tau, alpha, inv_M, mu_f, K=K)
+        op_c = Operator(coarse, lam, mu, tau, alpha, inv_M, mu_f, K=K)
         x0 = n // 2
         self.relax = relax
-        self.A_cols = _columns(lambda e: Hh.ops[0].A @ e, fine, x0, x0)
-        self.AH_cols = _columns(lambda e: Hh.ops[1].A @ e, coarse, x0 // 2, x0 // 2)
-        self._Hh, self._x0, self.jacobi_sweeps = Hh, x0, jacobi_sweeps
+        self.A_cols = _columns(lambda e: op_f.A @ e, fine, x0, x0)
+        self.AH_cols = _columns(lambda e: op_c.A @ e, coarse, x0 // 2, x0 // 2)
+        self.P_cols = _prolong_columns(Transfer(fine, coarse).P, fine, coarse, x0 // 2, x0 // 2)
+        self._fine, self._x0, self.jacobi_sweeps = fine, x0, jacobi_sweeps
         if relax == "vanka":
-            self.C_cols = _columns(Hh.smoothers[0].apply_Minv, fine, x0, x0)     # C = M^{-1}
+            self.C_cols = _columns(Vanka(op_f).apply_Minv, fine, x0, x0)         # C = M^{-1}
         else:
             if omega_J is None:
                 raise ValueError("bsr needs omega_J")
+            self._bsr = BSR(op_f)
             self.set_omega_J(omega_J)
-        self.P_cols = _prolong_columns(Hh.transfers[0].P, fine, coarse, x0 // 2, x0 // 2)
 
     def set_omega_J(self, omega_J):
         """BSR: the correction operator C(omega_J) = one sweep from x = 0 with omega = 1, which is
         linear in the residual."""
-        sm, fine = self._Hh.smoothers[0], self._Hh.meshes[0]
+        sm, fine = self._bsr, self._fine
         z = np.zeros(fine.nact)
         self.omega_J = omega_J
         self.C_cols = _columns(lambda e: sm.sweep(z, e, 1.0, omega_J, self.jacobi_sweeps),
