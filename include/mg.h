@@ -130,7 +130,9 @@ int mg_residual(mg_ctx* ctx, int32_t level, const double* x, const double* b, do
  *   x <- x + omega sum_v V_v^T D_v (V_v A_l V_v^T)^{-1} V_v (b - A_l x),
  * one patch per vertex, truncated to active DoFs (reading A8), natural weights D (1, 1/2, 1/3;
  * PAPER.md:586-587), exactly deflated patch solves (reading A9).  In place on x; the context's
- * level-l scratch vector is used for the out-of-place sweep.  Constant K only (reading A20). */
+ * level-l scratch vector is used for the out-of-place sweep, so an odd sweep count ends with one
+ * device copy back into x (the cycle itself ping-pongs without copies).  Constant K only
+ * (reading A20). */
 int mg_relax_vanka(mg_ctx* ctx, int32_t level, double* x, const double* b, double omega,
                    int32_t sweeps, cudaStream_t s);
 
