@@ -86,7 +86,7 @@ def lognormal_K(n: int, seed: int, sigma: float = 2.0) -> np.ndarray:
 
 # BASELINE.json configs.  1/M = 1 and mu_f = 1 (readings A5, A6 of DESIGN.md;
 # with 1/M = 1e-6 the rediscretised V-cycle diverges like 1/gamma at these parameters, see E0).
-# omega / omega_J: the minimisers of experiment E0 (tools/e0_omega_scan.py,
+# omega / omega_J: the minimisers of experiment E0 (tests/scripts/e0_omega_scan.py,
 # tests/golden/e0_omega_scan.json; V(1,1) on 64^2, 5 levels): Vanka 0.74 (configs 1/2),
 # 0.70 (configs 3, 5); BSR (omega_J, omega) = (1.0, 0.75) (config 2) and (0.7, 0.3) for the
 # heterogeneous config 4, where every scanned pair diverges (reading A24).

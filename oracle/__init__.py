@@ -1,6 +1,7 @@
 """CPU ORACLE for the monolithic multigrid hot path of arXiv 2107.04060.
 
-*** TEST INFRASTRUCTURE ONLY ***  Only ``tests/``, ``__graft_entry__.smoke()``
+*** TEST INFRASTRUCTURE ONLY ***  Only ``tests/`` (incl. the golden-record scripts in
+``tests/scripts/``), ``__graft_entry__.smoke()``
 and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import or
 run anything in this package.  The product path (``paper_2107_04060_b200``)
 never imports it, and this package never imports the product path: the two
