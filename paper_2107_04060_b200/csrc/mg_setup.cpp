@@ -60,16 +60,17 @@ bool invert(std::vector<long double>& A, int m) {
                 std::swap(A[c * (size_t)m + k], A[piv * (size_t)m + k]);
                 std::swap(I[c * (size_t)m + k], I[piv * (size_t)m + k]);
             }
+        // columns < c of A are never read again (pivot search and multipliers look at columns
+        // >= c only), so they are not updated: the result I is the same, with 3/4 of the work
         long double d = 1.0L / A[c * (size_t)m + c];
-        for (int k = 0; k < m; ++k) { A[c * (size_t)m + k] *= d; I[c * (size_t)m + k] *= d; }
+        for (int k = c; k < m; ++k) A[c * (size_t)m + k] *= d;
+        for (int k = 0; k < m; ++k) I[c * (size_t)m + k] *= d;
         for (int r = 0; r < m; ++r) {
             if (r == c) continue;
             long double f = A[r * (size_t)m + c];
             if (f == 0.0L) continue;
-            for (int k = 0; k < m; ++k) {
-                A[r * (size_t)m + k] -= f * A[c * (size_t)m + k];
-                I[r * (size_t)m + k] -= f * I[c * (size_t)m + k];
-            }
+            for (int k = c; k < m; ++k) A[r * (size_t)m + k] -= f * A[c * (size_t)m + k];
+            for (int k = 0; k < m; ++k) I[r * (size_t)m + k] -= f * I[c * (size_t)m + k];
         }
     }
     A.swap(I);

@@ -38,6 +38,21 @@ def hierarchy(n, levels, pname, relax, het_seed=None):
     return OHierarchy(n, levels, lam, mu, tau, alpha, invM, 1.0, K=K, Kinv_field=kinv, relax=relax)
 
 
+def small_coarse_levels(n, min_levels=1):
+    """Levels for a test of level-0 (or level 0 -> 1) operations: the fewest levels >= min_levels
+    whose coarsest n_c is either > 20 (mg_setup builds no dense coarsest inverse) or <= 8, so the
+    host's dense inverse (O(n_c^6) work for 8 < n_c <= 20) stays small; the operations under
+    test do not depend on the levels below."""
+    L, m = 1, n
+    while True:
+        if L >= min_levels and (m > 20 or m <= 8):
+            return L
+        if m % 2 or m // 2 < 2:
+            return max(L, min_levels)
+        m //= 2
+        L += 1
+
+
 def gpu_hierarchy(n, levels, pname, het_seed=None, march=False, env=None):
     """march=True forces the row-marching TMA kernels (production path of the levels with n >= 512)
     on every level, so that small parity cases exercise them (MG_MARCH_MIN_N is read by mg_setup);

@@ -45,7 +45,7 @@ def test_residual(n, pname, het, march):
     """r = b - A x and its norm; march=True runs the row-marching residual kernel (production for
     n >= 512, scalar K) on small grids."""
     torch = _torch()
-    H = C.gpu_hierarchy(n, 1, pname, het, env={"MG_RESID_MARCH_N": "0"} if march else None)
+    H = C.gpu_hierarchy(n, C.small_coarse_levels(n), pname, het, env={"MG_RESID_MARCH_N": "0"} if march else None)
     op = C.operator(n, pname, het)
     m = C.mesh(n)
     x = mg_inputs.uniform_vector(n, 11)
@@ -73,7 +73,7 @@ def test_vanka_sweep(n, pname, omega, march):
     """One Vanka sweep; march=True runs the production row-marching TMA kernel on small grids
     (ragged strips: n + 1 not a multiple of the strip width, several row segments)."""
     torch = _torch()
-    H = C.gpu_hierarchy(n, 1, pname, march=march)
+    H = C.gpu_hierarchy(n, C.small_coarse_levels(n), pname, march=march)
     from oracle.relax import Vanka
     op = C.operator(n, pname)
     V = Vanka(op)
@@ -95,7 +95,7 @@ def test_vanka_sweep(n, pname, omega, march):
 def test_restrict_prolong(n, pname):
     torch = _torch()
     from oracle.transfer import Transfer
-    H = C.gpu_hierarchy(n, 2, pname)
+    H = C.gpu_hierarchy(n, C.small_coarse_levels(n, 2), pname)
     mf, mc = C.mesh(n), C.mesh(n // 2)
     T = Transfer(mf, mc)
     r = mg_inputs.uniform_vector(n, 31)
@@ -151,7 +151,7 @@ def test_bsr_sweep(n, pname, het, nJ, march):
     the levels with n >= 512) on small grids, strips and segments included."""
     torch = _torch()
     from oracle.relax import BSR
-    H = C.gpu_hierarchy(n, 1, pname, het, march=march)
+    H = C.gpu_hierarchy(n, C.small_coarse_levels(n), pname, het, march=march)
     op = C.operator(n, pname, het)
     S = BSR(op)
     m = C.mesh(n)
@@ -241,7 +241,7 @@ def test_cycle_history(n, levels, pname, relax, het, cycles, march):
     assert np.all(np.abs(rG - rO)[ok] <= 1e-3)
 
 
-@pytest.mark.parametrize("n,levels,pname,nu2", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (64, 3, "stiff", 1)])
+@pytest.mark.parametrize("n,levels,pname,nu2", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (64, 4, "stiff", 1)])
 def test_fused_prolong_bitwise(n, levels, pname, nu2):
     """The prolongation fused into the first post-sweep of the marching kernel
     gives bitwise the iterates of prolong_kernel followed by the sweep (same arithmetic, same
