@@ -109,8 +109,8 @@ void mg_set_allocator(mg_alloc_fn alloc, mg_free_fn free_, void* user);
  * 1 <= levels, n_{levels-1} = n / 2^(levels-1) >= 2.  The dense coarsest solve needs
  * n_{levels-1} <= 20; a context with a larger coarsest level supports the per-level operations
  * only (mg_coarse_solve / mg_cycle / mg_solve then return MG_EINVAL).  The dense inverse is formed
- * on the host in long double, O(m^3) for m ~ 10 n_c^2 unknowns: milliseconds at the paper's n_c = 4
- * (PAPER.md:945), about a minute at n_c = 16 -- keep the coarsest level small.
+ * on the host in long double, O(m^3) for m ~ 10 n_c^2 unknowns: milliseconds at n_c = 4 (every
+ * BASELINE config), about a second at the paper's n_c = 8, a minute at n_c = 16.
  * Errors: MG_EINVAL, MG_ECUDA, MG_ENOMEM. */
 int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau, double alpha,
              int32_t levels, mg_ctx** out);
