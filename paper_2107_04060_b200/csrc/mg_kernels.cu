@@ -283,7 +283,10 @@ __device__ __forceinline__ int vertex_class(int a, int b, int n) {
 }
 
 // out[s * os] = (D K^{-1} r)_s for one 20-DoF patch (interior: +/- blocks; boundary class: dense
-// table), written straight to shared memory
+// table), written straight to shared memory.  UNROLL_BND: the five passes over the dense table are
+// unrolled (the small-tile kernels of the latency-bound coarse levels, where the boundary patches
+// are the critical path); same summation order either way
+template <bool UNROLL_BND = false>
 __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, const double rr[20], double* out, int os) {
     if (cls == 0) {
         double hp[9], hm[11];
@@ -330,8 +333,7 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
         // boundary class: dense 20 x 20 (row major in gbnd), four output rows per pass so four
         // independent chains hide the load and fp64 latency (each output sums c = 0 .. 19 in order)
         const double2* G = reinterpret_cast<const double2*>(P.gbnd + cls * 400);
-#pragma unroll 1
-        for (int a = 0; a < 20; a += 4) {
+        auto pass = [&](int a) {
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
             for (int c2 = 0; c2 < 10; ++c2) {
@@ -346,6 +348,13 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
             out[(a + 1) * os] = s1;
             out[(a + 2) * os] = s2;
             out[(a + 3) * os] = s3;
+        };
+        if (UNROLL_BND) {
+#pragma unroll
+            for (int a = 0; a < 20; a += 4) pass(a);
+        } else {
+#pragma unroll 1
+            for (int a = 0; a < 20; a += 4) pass(a);
         }
     }
 }
@@ -389,7 +398,7 @@ __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double*
         if (a <= n && bb <= n) {
             double rr[20];
             gather20<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
-            patch_apply20(P, vertex_class(a, bb, n), rr, cs + t, T::PW * T::PH);
+            patch_apply20<(TX <= 8)>(P, vertex_class(a, bb, n), rr, cs + t, T::PW * T::PH);
         } else {
 #pragma unroll
             for (int q = 0; q < 20; ++q) cs[q * T::PW * T::PH + t] = 0.0;
