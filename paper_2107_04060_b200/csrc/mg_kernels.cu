@@ -703,8 +703,18 @@ __global__ void __launch_bounds__(256) coarse_kernel(int N, const double* __rest
     for (int k = threadIdx.x; k < N; k += blockDim.x) rb[k] = __ldg(b + slots[k]);
     __syncthreads();
     for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < N; row += gridDim.x * blockDim.x) {
+        // one FMA chain per row in k order; unrolled so the column loads of G are issued 16 ahead
+        // instead of exposing one L2 round trip per k (the kernel is a 130-long latency chain)
         double acc = 0.0;
-        for (int k = 0; k < N; ++k) acc = fma(__ldg(G + (int64_t)k * N + row), rb[k], acc);
+        int k = 0;
+        for (; k + 16 <= N; k += 16) {
+            double g[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) g[q] = __ldg(G + (int64_t)(k + q) * N + row);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc = fma(g[q], rb[k + q], acc);
+        }
+        for (; k < N; ++k) acc = fma(__ldg(G + (int64_t)k * N + row), rb[k], acc);
         x[slots[row]] = acc;
     }
 }
