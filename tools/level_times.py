@@ -1,6 +1,6 @@
 """Warm per-kernel times of every level of a hierarchy (CUDA events around R back-to-back
-launches of one C-ABI call; diagnostic only, not a bench line).  The vanka column is one
-mg_relax_vanka call: the out-of-place sweep plus the copy back into x (level 0: ~0.45 ms of it).
+launches of one C-ABI call; diagnostic only, not a bench line).  The vanka column is half of an
+mg_relax_vanka call with 2 sweeps (an even count ends in x: no copy back).
 
     python tools/level_times.py [--n 4096] [--levels 11] [--reps 50]
 """
@@ -48,7 +48,7 @@ def main():
         x, b, r = H.zeros(l), H.zeros(l), H.zeros(l)
         b.normal_()
         x.normal_()
-        tv = timed(lambda: H.relax_vanka(l, x, b, 0.7, sweeps=1), a.reps)
+        tv = timed(lambda: H.relax_vanka(l, x, b, 0.7, sweeps=2), a.reps) / 2
         tr = timed(lambda: H.residual(l, x, b, r), a.reps)
         if l + 1 < a.levels:
             bc = H.zeros(l + 1)
