@@ -161,6 +161,11 @@ def test_tab_vanka22_rho(cell):
     H = Hierarchy(64, 2, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], relax="vanka")
     rho, rhos = H.measure_rho(dict(nu1=2, nu2=2, omega=c["omega"]), seed=0, min_cycles=60, max_cycles=60)
     assert abs(np.mean(rhos[-2:]) - c["rho_N"]) <= 0.03, (rhos[-4:], c)
+    # the paper's validation of LFA against measurement, on the oracle's own
+    # numbers: |rho_N - rho_LFA| <= 0.05 (SURVEY acceptance band)
+    from oracle.lfa import TwoGridLFA
+    r_lfa = TwoGridLFA(16, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], h=1.0 / 64).rho(c["omega"], 2, 2)
+    assert abs(np.mean(rhos[-2:]) - r_lfa) <= 0.05, (rhos[-4:], r_lfa)
 
 
 @pytest.mark.slow
@@ -174,6 +179,10 @@ def test_tab_bsr_vanka11_rho(cell):
     opts = dict(nu1=1, nu2=1, omega=c["omega"], omega_J=c["omega_J"], jacobi_sweeps=1)
     rho, rhos = H.measure_rho(opts, seed=0, min_cycles=150, max_cycles=150)
     assert abs(rhos[-1] - c["rho_N"]) <= 0.03, (rhos[-4:], c)
+    from oracle.lfa import TwoGridLFA
+    r_lfa = TwoGridLFA(16, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], relax="bsr", omega_J=c["omega_J"],
+                       h=1.0 / 64).rho(c["omega"], 1, 1)
+    assert abs(rhos[-1] - r_lfa) <= 0.05, (rhos[-4:], r_lfa)
 
 
 def test_manufactured_rates():
