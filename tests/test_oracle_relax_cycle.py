@@ -161,7 +161,7 @@ def test_tab_vanka22_rho(cell):
     H = Hierarchy(64, 2, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], relax="vanka")
     rho, rhos = H.measure_rho(dict(nu1=2, nu2=2, omega=c["omega"]), seed=0, min_cycles=60, max_cycles=60)
     assert abs(np.mean(rhos[-2:]) - c["rho_N"]) <= 0.03, (rhos[-4:], c)
-    # the paper's validation of LFA against measurement (PAPER.md:907-909), on the oracle's own
+    # the paper's validation of LFA against measurement (PAPER.md:911), on the oracle's own
     # numbers: |rho_N - rho_LFA| <= 0.05 (SURVEY acceptance band)
     from oracle.lfa import TwoGridLFA
     r_lfa = TwoGridLFA(16, lam, mu, 1.0, 1.0, 1e-6, 1.0, K=c["k"], h=1.0 / 64).rho(c["omega"], 2, 2)
