@@ -177,7 +177,8 @@ class TwoGridLFA:
     @staticmethod
     def thetas(m=32):
         """m x m grid of theta in [-pi/2, pi/2)^2 shifted by half a step, so that theta = 0
-        (where A_H is singular) is never sampled (PAPER.md:749 discrete sampling; 32 points per direction, offset from the origin)."""
+        (where A_H is singular) is never sampled (discrete sampling; PAPER.md:822:
+        32 points per direction, offset from the origin)."""
         t = -np.pi / 2 + (np.arange(m) + 0.5) * np.pi / m
         t1, t2 = np.meshgrid(t, t, indexing="ij")
         return np.stack([t1.ravel(), t2.ravel()], axis=1)
