@@ -44,12 +44,15 @@
  * coarsened by averaging K^{-1} over the four children (reading A11).
  *
  * OWNERSHIP.  The caller owns every pointer passed in (x, b, r, e: DEVICE
- * pointers to mg_vec_len(ctx, level) doubles, 8-byte aligned; *_host: host
+ * pointers to mg_vec_len(ctx, level) doubles, 16-byte aligned -- the kernels
+ * move column pairs as double2 and the TMA descriptors need 16-byte global
+ * addresses; a misaligned pointer is rejected with MG_EINVAL; *_host: host
  * pointers) and every stream.  The context owns all per-level tables, the
  * level >= 1 work vectors, one scratch vector per level, the K^{-1} pyramid
  * and the coarsest inverse; they are allocated in mg_setup through the
  * allocator installed with mg_set_allocator (default cudaMalloc) and released
- * by mg_free.  A context must not be used from two host threads or two
+ * by mg_free.  The allocator in force at mg_setup is recorded in the context and
+ * used for all of its later allocations (FGMRES work space, history) and frees.  A context must not be used from two host threads or two
  * streams at the same time.
  *
  * ERRORS.  Every int function returns MG_OK (0) on success, a negative code on
@@ -85,7 +88,12 @@ typedef struct {
     const double* K_field;  /* NULL -> scalar K of mg_setup.  Else DEVICE pointer to 2 x n x n
                                doubles [shape (0 = LL, 1 = UR)][j][i], the permeability of each
                                triangle (> 0, finite); copied during mg_setup                     */
-    double inv_M;           /* 1/M >= 0 (Biot modulus); BASELINE configs use 1   */
+    double inv_M;           /* 1/M > 0 (Biot modulus); 0 is rejected (MG_EINVAL):
+                               the exactly deflated patch and coarsest solves divide by the
+                               constant-pressure eigenvalue gamma = (1/M) h^2/2 (reading A9).
+                               BASELINE configs run 1/M = 1 (reading A5), not SURVEY 8(b)'s
+                               proposed 1e-6: at 1e-6 the rediscretised V(1,1) cycle diverges
+                               (factor ~ 1/gamma growth, tests/golden/a5_invM_scan.json).        */
     double mu_f;            /* fluid viscosity > 0; 1                            */
 } mg_grid;
 
@@ -97,8 +105,9 @@ typedef struct {
     int32_t jacobi_sweeps;  /* BSR: sweeps on S from dp = 0 (BASELINE: 3; paper: 1)          */
 } mg_cycle_opts;
 
-/* Device memory hooks: alloc(bytes, user) -> device pointer or NULL; free(ptr, user).
- * Installed for the contexts created afterwards.  NULL, NULL restores cudaMalloc/cudaFree. */
+/* Device memory hooks: alloc(bytes, user) -> device pointer (16-byte aligned) or NULL;
+ * free(ptr, user).  Installed for the contexts created afterwards; each context keeps the pair it
+ * was created with until mg_free.  NULL, NULL restores cudaMalloc/cudaFree. */
 typedef void* (*mg_alloc_fn)(size_t bytes, void* user);
 typedef void  (*mg_free_fn)(void* ptr, void* user);
 void mg_set_allocator(mg_alloc_fn alloc, mg_free_fn free_, void* user);

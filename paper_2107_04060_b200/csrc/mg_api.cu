@@ -96,6 +96,9 @@ struct mg_ctx {
     unsigned* kcnt = nullptr;
     int kcap = 0;
     std::vector<void*> allocs;
+    mg_alloc_fn alloc = nullptr;  // allocator in force at mg_setup: every later allocation and free of
+    mg_free_fn dfree = nullptr;   // this context uses it, whatever mg_set_allocator installs afterwards
+    void* alloc_user = nullptr;
     std::vector<GraphEntry> graphs;
     cudaStream_t cap = nullptr;   // capture stream
     bool timing = false;
@@ -120,7 +123,7 @@ namespace {
 
 void* dalloc(mg_ctx* c, size_t bytes) {
     void* p = nullptr;
-    if (g_alloc) p = g_alloc(bytes, g_user);
+    if (c->alloc) p = c->alloc(bytes, c->alloc_user);
     else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
     if (p) c->allocs.push_back(p);
     return p;
@@ -128,7 +131,7 @@ void* dalloc(mg_ctx* c, size_t bytes) {
 
 void dfree_all(mg_ctx* c) {
     for (void* p : c->allocs) {
-        if (g_free) g_free(p, g_user);
+        if (c->dfree) c->dfree(p, c->alloc_user);
         else cudaFree(p);
     }
     c->allocs.clear();
@@ -136,7 +139,9 @@ void dfree_all(mg_ctx* c) {
 
 int pitch_of(int n) { return ((n + 1 + 31) / 32) * 32; }
 
-bool aligned(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) % 8 == 0); }
+// every vector pointer must be 16-byte aligned: the kernels move column pairs as double2 and TMA
+// descriptors need 16-byte global addresses (include/mg.h OWNERSHIP)
+bool aligned(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) % 16 == 0); }
 
 int check_level(const mg_ctx* c, int level, int maxl) {
     if (!c) return fail(MG_EINVAL, "null context");
@@ -311,7 +316,9 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
             if (rc) return rc;
             std::swap(a, t);
         }
-        if (l == 0 && a != x0) CK(cudaMemcpyAsync(x0, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+        // odd sweep count: copy back with a kernel that honours mg_solve's stop flag (a memcpy node
+        // would also run in the stopping cycle and return the pre-sweep's output)
+        if (l == 0 && a != x0) CK(launch_copy(x0, a, Lv.len, c->stop, s));
         if (int rc = lmark()) return rc;
         cur[l] = a;
     }
@@ -407,13 +414,16 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (!(grid->inv_M > 0) || !std::isfinite(grid->inv_M))
         return fail(MG_EINVAL, "inv_M must be > 0 (the deflated solves need the -(1/M) M_p block)");
     if (!(grid->mu_f > 0)) return fail(MG_EINVAL, "mu_f must be > 0");
-    if (grid->K_field && !aligned(grid->K_field)) return fail(MG_EINVAL, "K_field not 8-byte aligned");
+    if (grid->K_field && !aligned(grid->K_field)) return fail(MG_EINVAL, "K_field not 16-byte aligned");
     const int nc = n >> (levels - 1);
     // the dense coarsest solve needs n_c <= 20; a context with a larger coarsest level offers the
     // per-level operations only (mg_coarse_solve, mg_cycle and mg_solve return MG_EINVAL)
     const bool dense_ok = 10LL * nc * nc - 8LL * nc + 2 <= 4096;
 
     mg_ctx* c = new mg_ctx;
+    c->alloc = g_alloc;
+    c->dfree = g_free;
+    c->alloc_user = g_user;
     c->levels = levels;
     c->het = grid->K_field != nullptr;
     c->m = Material{lambda, mu, grid->K_field ? 1.0 : K, tau, alpha, grid->inv_M, grid->mu_f};
@@ -888,6 +898,16 @@ int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, doub
         c->hist_cap = cap;
     }
     SolveState st{0, max_cycles, rtol * rtol, c->hist, c->stop};
+    // whatever path leaves this function, the stop flag is cleared: a flag left raised would make
+    // every later kernel on the context return at entry
+    struct StopGuard {
+        mg_ctx* c;
+        cudaStream_t s;
+        ~StopGuard() {
+            cudaMemsetAsync(c->stop, 0, sizeof(int), s);
+            cudaStreamSynchronize(s);
+        }
+    } guard{c, s};
     CK(cudaMemcpyAsync(c->state, &st, sizeof(st), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(c->stop, 0, sizeof(int), s));
     cudaGraphExec_t g;
@@ -908,8 +928,6 @@ int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, doub
     if (!stop) return fail(MG_ECUDA, "solve state inconsistent (no stop after %d launches)", launched);
     std::vector<double> h(k);
     CK(cudaMemcpy(h.data(), c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
-    CK(cudaMemsetAsync(c->stop, 0, sizeof(int), s));
-    CK(cudaStreamSynchronize(s));
     if (history_host)
         for (int i = 0; i < k; ++i) history_host[i] = std::sqrt(h[i]);
     if (n_cycles) *n_cycles = k - 1;

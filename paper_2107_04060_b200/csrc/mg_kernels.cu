@@ -2371,6 +2371,20 @@ __global__ void __launch_bounds__(DOT_NT) vec_update_kernel(double* __restrict__
     }
 }
 
+// dst = src over a whole padded vector (len doubles, 16-B aligned), skipped when the solve's stop
+// flag is raised: the level-0 copy-back of an odd sweep count must not run in the cycle that
+// stops mg_solve (its pre-sweep already wrote the scratch vector past the recorded iterate)
+__global__ void __launch_bounds__(DOT_NT) vec_copy_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                                          int64_t len, const int* __restrict__ stop) {
+    pdl_wait();
+    pdl_trigger();
+    if (*stop) return;
+    const int64_t n2 = len / 2;
+    for (int64_t e = (int64_t)blockIdx.x * DOT_NT + threadIdx.x; e < n2; e += (int64_t)gridDim.x * DOT_NT)
+        reinterpret_cast<double2*>(dst)[e] = __ldg(reinterpret_cast<const double2*>(src) + e);
+    if ((len & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[len - 1] = src[len - 1];
+}
+
 // y = s * x
 __global__ void __launch_bounds__(DOT_NT) vec_scale_kernel(double* __restrict__ y, const double* __restrict__ x,
                                                            double s, int64_t len) {
@@ -2534,6 +2548,10 @@ cudaError_t launch_update(double* w, const VecPtrs& V, int k, const double* c, i
 }
 cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cudaStream_t s) {
     launch_k(vec_scale_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, y, x, sc, len);
+    return cudaGetLastError();
+}
+cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* stop, cudaStream_t s) {
+    launch_k(vec_copy_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, dst, src, len, stop);
     return cudaGetLastError();
 }
 int dot_partials_needed() { return VK * DOT_BLOCKS; }

@@ -59,6 +59,8 @@ cudaError_t launch_dots(const double* w, const VecPtrs& V, int k, int64_t len, d
                         double* out, cudaStream_t s);
 cudaError_t launch_update(double* w, const VecPtrs& V, int k, const double* c, int64_t len, cudaStream_t s);
 cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cudaStream_t s);
+// dst = src (len doubles), skipped when *stop != 0 (mg_solve's flag)
+cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* stop, cudaStream_t s);
 int dot_partials_needed();
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
                          bool x_zero, NormSink norm, cudaStream_t s);

@@ -125,11 +125,20 @@ def _install_torch_allocator(lib):
     lib.mg_set_allocator(ctypes.cast(_alloc_cbs[0], _VP), ctypes.cast(_alloc_cbs[1], _VP), None)
 
 
-def _ptr(t):
+def _ptr(t, numel=None):
+    """Device pointer of a CUDA float64 tensor; numel: the element count the C call will touch
+    (mg_vec_len of the level), checked so that a short or strided tensor never reaches a kernel."""
     if t is None:
         return None
-    if not t.is_cuda or t.dtype.itemsize != 8:
+    import torch
+    if not t.is_cuda or t.dtype != torch.float64:
         raise MGError("expected a CUDA float64 tensor")
+    if not t.is_contiguous():
+        raise MGError("expected a contiguous tensor (the C ABI takes plain pointers)")
+    if numel is not None and t.numel() != numel:
+        raise MGError(f"tensor has {t.numel()} elements, the level vector has {numel} (10 x (n_l+1) x pitch_l)")
+    if t.data_ptr() % 16:
+        raise MGError("tensor storage is not 16-byte aligned")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -189,6 +198,12 @@ class Hierarchy:
             pass
 
     # ---- layout helpers (marshalling only) -------------------------------------------------
+    def vec_len(self, level: int) -> int:
+        return self.lib.mg_vec_len(self.ctx, level)
+
+    def _v(self, t, level: int = 0):
+        return _ptr(t, self.vec_len(level))
+
     def level_n(self, level: int) -> int:
         return self.lib.mg_level_n(self.ctx, level)
 
@@ -219,38 +234,38 @@ class Hierarchy:
     def residual(self, level, x, b, r=None, norm=False, stream=None):
         import torch
         nd = torch.zeros(1, dtype=torch.float64, device="cuda") if norm else None
-        _check(self.lib.mg_residual(self.ctx, level, _ptr(x), _ptr(b), _ptr(r), _ptr(nd), _stream(stream)),
+        _check(self.lib.mg_residual(self.ctx, level, self._v(x, level), self._v(b, level), self._v(r, level), _ptr(nd, 1), _stream(stream)),
                "mg_residual")
         return float(nd.sqrt().item()) if norm else None
 
     def relax_vanka(self, level, x, b, omega, sweeps=1, stream=None):
-        _check(self.lib.mg_relax_vanka(self.ctx, level, _ptr(x), _ptr(b), float(omega), int(sweeps),
+        _check(self.lib.mg_relax_vanka(self.ctx, level, self._v(x, level), self._v(b, level), float(omega), int(sweeps),
                                        _stream(stream)), "mg_relax_vanka")
 
     def relax_bsr(self, level, x, b, omega, omega_J, jacobi_sweeps, sweeps=1, stream=None):
-        _check(self.lib.mg_relax_bsr(self.ctx, level, _ptr(x), _ptr(b), float(omega), float(omega_J),
+        _check(self.lib.mg_relax_bsr(self.ctx, level, self._v(x, level), self._v(b, level), float(omega), float(omega_J),
                                      int(jacobi_sweeps), int(sweeps), _stream(stream)), "mg_relax_bsr")
 
     def restrict(self, fine_level, r, bc, stream=None):
-        _check(self.lib.mg_restrict(self.ctx, fine_level, _ptr(r), _ptr(bc), _stream(stream)), "mg_restrict")
+        _check(self.lib.mg_restrict(self.ctx, fine_level, self._v(r, fine_level), self._v(bc, fine_level + 1), _stream(stream)), "mg_restrict")
 
     def prolong(self, fine_level, e, xf, stream=None):
-        _check(self.lib.mg_prolong(self.ctx, fine_level, _ptr(e), _ptr(xf), _stream(stream)), "mg_prolong")
+        _check(self.lib.mg_prolong(self.ctx, fine_level, self._v(e, fine_level + 1), self._v(xf, fine_level), _stream(stream)), "mg_prolong")
 
     def coarse_solve(self, b, x, stream=None):
-        _check(self.lib.mg_coarse_solve(self.ctx, _ptr(b), _ptr(x), _stream(stream)), "mg_coarse_solve")
+        _check(self.lib.mg_coarse_solve(self.ctx, self._v(b, self.levels - 1), self._v(x, self.levels - 1), _stream(stream)), "mg_coarse_solve")
 
     def cycle(self, x, b, opts: Opts, norm=True, stream=None):
         out = ctypes.c_double(0.0)
         o = opts.c()
-        _check(self.lib.mg_cycle(self.ctx, _ptr(x), _ptr(b), ctypes.byref(o), ctypes.byref(out) if norm else None,
+        _check(self.lib.mg_cycle(self.ctx, self._v(x), self._v(b), ctypes.byref(o), ctypes.byref(out) if norm else None,
                                  _stream(stream)), "mg_cycle")
         return out.value if norm else None
 
     def cycle_async(self, x, b, opts: Opts, norm2_out=None, stream=None):
         """One cycle, no host sync; norm2_out: optional 1-element CUDA tensor receiving ||b - A x_in||^2."""
         o = opts.c()
-        _check(self.lib.mg_cycle_async(self.ctx, _ptr(x), _ptr(b), ctypes.byref(o), _ptr(norm2_out),
+        _check(self.lib.mg_cycle_async(self.ctx, self._v(x), self._v(b), ctypes.byref(o), _ptr(norm2_out, None if norm2_out is None else norm2_out.numel()),
                                        _stream(stream)), "mg_cycle_async")
 
     def cycle_kernels(self) -> int:
@@ -288,7 +303,7 @@ class Hierarchy:
         hist = np.zeros(max_cycles + 1)
         nc = ctypes.c_int32(0)
         o = opts.c()
-        rc = _check(self.lib.mg_solve(self.ctx, _ptr(x), _ptr(b), ctypes.byref(o), float(rtol), int(max_cycles),
+        rc = _check(self.lib.mg_solve(self.ctx, self._v(x), self._v(b), ctypes.byref(o), float(rtol), int(max_cycles),
                                       hist.ctypes.data_as(_D), ctypes.byref(nc), _stream(stream)), "mg_solve")
         return rc, hist[: nc.value + 1]
 
@@ -297,7 +312,7 @@ class Hierarchy:
         hist = np.zeros(max_iters + 1)
         nc = ctypes.c_int32(0)
         o = opts.c()
-        rc = _check(self.lib.mg_fgmres(self.ctx, _ptr(x), _ptr(b), ctypes.byref(o), float(rtol), int(max_iters),
+        rc = _check(self.lib.mg_fgmres(self.ctx, self._v(x), self._v(b), ctypes.byref(o), float(rtol), int(max_iters),
                                        int(restart), hist.ctypes.data_as(_D), ctypes.byref(nc), _stream(stream)),
                     "mg_fgmres")
         return rc, hist[: nc.value + 1]
@@ -305,8 +320,10 @@ class Hierarchy:
     def solve_host(self, x_host: np.ndarray, b_host: np.ndarray, opts: Opts, rtol=1e-8, max_cycles=100,
                    stream=None):
         """End-to-end solve from host arrays (10, n+1, n+1); x_host is overwritten with the solution."""
-        assert x_host.dtype == np.float64 and b_host.dtype == np.float64
-        assert x_host.flags.c_contiguous and b_host.flags.c_contiguous
+        shape = (10, self.n + 1, self.n + 1)
+        for a in (x_host, b_host):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.shape == shape):
+                raise MGError(f"host vectors must be C-contiguous float64 arrays of shape {shape}")
         hist = np.zeros(max_cycles + 1)
         nc = ctypes.c_int32(0)
         o = opts.c()

@@ -97,3 +97,54 @@ def test_fgmres_argument_checks():
         with pytest.raises(MGError):
             H.fgmres(xd, bd, Opts(1, 1, "vanka", 0.74), rtol=1e-8, max_iters=10, restart=restart)
     H.close()
+
+
+@pytest.mark.parametrize("nu1,nu2,relax", [(1, 0, "vanka"), (2, 1, "vanka"), (1, 2, "bsr"), (0, 1, "vanka")])
+def test_odd_sweep_solve_returns_recorded_iterate(nu1, nu2, relax):
+    """mg_solve with an odd number of level-0 sweeps (the cycle ends with a copy back into x): the
+    returned x is the iterate whose residual is the last history entry, not one smoothing step
+    past it (the copy honours the stop flag).  ||b - A x_returned|| = hist[-1] to one
+    rounding of the residual norm, and a second solve on the same context still computes (the
+    stop flag was cleared)."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    n, levels = 64, 5
+    o = Opts(nu1, nu2, "vanka", 0.72) if relax == "vanka" else Opts(nu1, nu2, "bsr", 0.75, 1.0, 3)
+    b = mg_inputs.uniform_rhs(n, 26)
+    H = C.gpu_hierarchy(n, levels, "cfg5")
+    xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+    for rtol, cap in ((1e-3, 60), (1e-30, 5)):     # converged stop, then the max_cycles stop
+        xd.zero_()
+        rc, hist = H.solve(xd, bd, o, rtol=rtol, max_cycles=cap)
+        torch.cuda.synchronize()
+        r = H.residual(0, xd, bd, norm=True)
+        assert abs(r - hist[-1]) <= 1e-12 * hist[-1], (nu1, nu2, r, hist[-1], rc)
+    # max_cycles = 0: x is left untouched
+    x0 = mg_inputs.uniform_vector(n, 27)
+    xd = H.to_device(x0)
+    rc, hist = H.solve(xd, bd, o, rtol=1e-8, max_cycles=0)
+    torch.cuda.synchronize()
+    assert len(hist) == 1 and torch.equal(xd, H.to_device(x0))
+    H.close()
+
+
+def test_binding_rejects_bad_vectors():
+    """The binding refuses tensors the C call would read out of bounds (wrong element count,
+    non-contiguous views) and the library refuses misaligned pointers (MG_EINVAL, no launch)."""
+    torch = _torch()
+    from paper_2107_04060_b200.mg import MGError
+    import ctypes
+    n, levels = 16, 3
+    H = C.gpu_hierarchy(n, levels, "unit")
+    good = H.zeros()
+    with pytest.raises(MGError):
+        H.residual(0, good[:, :, : n + 1], good, norm=True)            # strided view
+    with pytest.raises(MGError):
+        H.residual(0, good.reshape(-1)[:-32], good, norm=True)         # too short
+    raw = torch.zeros(good.numel() + 1, dtype=torch.float64, device="cuda")
+    rc = H.lib.mg_residual(H.ctx, 0, ctypes.c_void_p(raw.data_ptr() + 8), ctypes.c_void_p(good.data_ptr()),
+                           None, None, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == -1                                                      # 8-byte aligned only
+    with pytest.raises(MGError):
+        H.solve_host(np.zeros((10, n + 1, n)), np.zeros((10, n + 1, n + 1)), None)
+    H.close()
