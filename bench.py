@@ -162,6 +162,7 @@ def oracle_sample(c, cycles: int, warmup: int = 1, n_sample: int = 128):
         cores = 1
     nact = mg_inputs.n_active(n_sample)
     return dict(value=nact * len(times) / sum(times), ms=1e3 * sum(times) / len(times), cores=cores,
+                n=n_sample, levels=levels,
                 sample=f"oracle V(1,1) on {n_sample}^2 ({levels} levels, {nact} active DoFs), same parameters and "
                        f"RHS recipe, {len(times)} cycles after {warmup} warm-up; host has {os.cpu_count()} cores, "
                        f"numpy/scipy (sparse matvec single-threaded, BLAS threads {cores})")
@@ -190,11 +191,18 @@ def run_reference(args, c, rank, world):
     if rank != 0:
         return
     s = oracle_sample(c, args.steps, args.warmup)
+    # the config names what was actually timed: the oracle on an n_sample^2 sample with the
+    # workload's parameters (the 4096^2 operator does not fit the oracle), not the workload itself
+    cfg = workload_config(args, c)
+    cfg.update({"workload": f"SAMPLE of BASELINE config {args.config}: the CPU oracle on {s['n']}^2 cells, "
+                            f"{s['levels']} levels{'' if s['n'] == c['n'] else ' (not %d^2)' % c['n']}, same parameters, RHS recipe and V(1,1) cycle",
+                "n": s["n"], "levels": s["levels"], "active_dofs": mg_inputs.n_active(s["n"]),
+                "sample_of": cfg["workload"], "l2": "host CPU run (no L2 flush)"})
     line = {"impl": "reference", "metric": METRIC, "value": s["value"],
             "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": s["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, c),
+            "config": cfg,
             "cpu_baseline": {"value": s["value"], "unit": "DoF/s", "cores": s["cores"], "kind": "oracle",
                              "sample": s["sample"]},
             "e2e": {"value": s["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
