@@ -38,6 +38,20 @@ from .mesh import Mesh
 from .fem import Operator
 
 
+def principal_submatrices(A, I, chunk=20000):
+    """K[q] = A[I[q]][:, I[q]] (dense) for the stacked index sets I (P, m): V_l A V_l^T of every patch.
+    Element lookups A[i, j] of the CSR matrix (scipy csr_sample_values), in chunks of patches; the
+    values are the stored entries themselves, so this is the same matrix as slicing patch by patch."""
+    P, m = I.shape
+    out = np.empty((P, m, m))
+    for s0 in range(0, P, chunk):
+        J = I[s0:s0 + chunk]
+        rows = np.repeat(J, m, axis=1).ravel()
+        cols = np.tile(J, (1, m)).ravel()
+        out[s0:s0 + chunk] = np.asarray(A[rows, cols]).reshape(-1, m, m)
+    return out
+
+
 def vertex_patches(mesh: Mesh, kind: str):
     """Patch DoF lists (positions in the active vector), one per vertex.
 
@@ -86,9 +100,7 @@ class Vanka:
         self.data = []
         for m, plist in sorted(self.groups.items()):
             I = np.array(plist)                                 # (P, m)
-            Ks = np.empty((len(plist), m, m))
-            for q, idx in enumerate(plist):
-                Ks[q] = A[idx][:, idx].toarray()                # V_l A V_l^T
+            Ks = principal_submatrices(A, I)                    # V_l A V_l^T
             pm = ispress[I]                                     # (P, m) pressure mask
             npress = pm.sum(axis=1)
             Kdef = Ks.copy()
@@ -170,7 +182,7 @@ class DispVanka:
         self.data = []
         for m, plist in sorted(groups.items()):
             I = np.array(plist)
-            Ks = np.array([Au[idx][:, idx].toarray() for idx in plist])
+            Ks = principal_submatrices(Au, I)
             self.data.append(dict(I=I, K=Ks))
         self.n = Au.shape[0]
 
