@@ -216,6 +216,19 @@ int mg_solve(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts,
 int mg_fgmres(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts, double rtol,
               int32_t max_iters, int32_t restart, double* history_host, int32_t* n_iters, cudaStream_t s);
 
+/* Backward-Euler time stepping.  At step m the system matrix is the same
+ * A^RQ (tau is the step size of mg_setup) and the previous step enters the right-hand side only
+ * through the pressure rows, eq. discrete3 scaled by -1 with
+ *   (f_hat, q) = tau (f, q) + (1/M)(p^{m-1}, q) + (alpha div u^{m-1}, q):
+ *   b^m = b_load^m + [0; 0; -(1/M) M_p p^{m-1} + alpha B_u u^{m-1}],
+ * b_load^m = [(rho g, v); tau (rho_f g, r); -tau (f^m, q)] being the caller's loads at t_m.
+ * mg_step_rhs writes b^m to b_out (DEVICE, level-0 layout; may alias b_load, not x_prev).
+ * mg_time_step forms b^m from x = x^{m-1} and b_load, then runs mg_fgmres from x as the initial
+ * guess, leaving x^m in x (work vector allocated on first use).  Returns as mg_fgmres. */
+int mg_step_rhs(mg_ctx* ctx, const double* x_prev, const double* b_load, double* b_out, cudaStream_t s);
+int mg_time_step(mg_ctx* ctx, double* x, const double* b_load, const mg_cycle_opts* opts, double rtol,
+                 int32_t max_iters, int32_t restart, double* history_host, int32_t* n_iters, cudaStream_t s);
+
 /* mg_solve with HOST vectors in the unpadded layout [10][n+1][n+1] (the end-to-end path):
  * b_host is copied to the device, x starts at x_host, the solution is copied back to x_host.
  * Host buffers should be pinned for full copy bandwidth.  Synchronous. */

@@ -51,6 +51,8 @@ struct Level {
     double* kinv = nullptr;  // 2 planes, heterogeneous K only
     double* jtab = nullptr;  // BSR Jacobi table: 5 planes (tau / D_w per RT0 edge, 1 / diag S per triangle)
     double* gbnd = nullptr;  // 9 x 400
+    double* hv_cls = nullptr;   // heterogeneous Vanka: 9 x MG_HV_CLS class tables
+    double* hv_sinv = nullptr;  // heterogeneous Vanka: MG_HV_NSINV planes of per-vertex S_v^{-1}
     double* ubnd = nullptr;  // 9 x 64
     VankaParams vp;
     DispParams up;
@@ -91,6 +93,7 @@ struct mg_ctx {
     // FGMRES work space (allocated on first use, grown with the restart length)
     std::vector<double*> kv, kz;
     double* kw = nullptr;
+    double* kb = nullptr;         // mg_time_step: the step's right-hand side
     double* kdots = nullptr;      // device: 2 x 72 dot results + 8 coefficients
     double* kpart = nullptr;
     unsigned* kcnt = nullptr;
@@ -153,7 +156,7 @@ NormSink no_norm() { return NormSink{nullptr, nullptr, nullptr, nullptr}; }
 
 // does the first post-sweep on level l absorb the prolongation (relax_once with e_coarse)?
 bool fused_prolong(const mg_ctx* c, int l, const mg_cycle_opts& o) {
-    return c->fuse_prolong && o.relax == MG_VANKA && o.nu2 >= 1 && c->vanka_impl == 2 &&
+    return c->fuse_prolong && o.relax == MG_VANKA && o.nu2 >= 1 && c->vanka_impl == 2 && !c->het &&
            c->L[l].n >= c->march_min_n;
 }
 
@@ -171,7 +174,7 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
             CK(launch_vanka_march2(P, xin, b, xout, false, S, s, &E));
             return MG_OK;
         }
-        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n && !c->het) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
     }
@@ -428,6 +431,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     c->het = grid->K_field != nullptr;
     c->m = Material{lambda, mu, grid->K_field ? 1.0 : K, tau, alpha, grid->inv_M, grid->mu_f};
     c->L.resize(levels);
+    set_carveout(getenv("MG_CARVEOUT") ? atoi(getenv("MG_CARVEOUT")) : 100);
     kernels_init();
     if (const char* v = getenv("MG_VANKA_IMPL")) c->vanka_impl = atoi(v);
     if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
@@ -464,6 +468,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
             return bail(fail(MG_EINVAL, "level %d: %s", l, err));
         }
         Lv.vp.L = t->L;
+        Lv.vp.hv = HetVankaTabs{nullptr, nullptr};   // set below for a K field
         Lv.vp.L.pitch = Lv.pitch;
         Lv.vp.L.plane = Lv.plane;
         for (int a = 0; a < 9; ++a)
@@ -530,6 +535,27 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         cudaMemset(c->L[l].jtab, 0, sizeof(double) * 5 * c->L[l].plane);
         if (launch_jtable(c->L[l].vp.L, c->L[l].jtab, 0) != cudaSuccess)
             return bail(fail(MG_ECUDA, "jtable launch: %s", cudaGetErrorString(cudaGetLastError())));
+    }
+    // heterogeneous Vanka: condensed class tables + per-vertex S_v^{-1}
+    if (c->het) {
+        std::vector<double> hcls(MG_NCLASS * MG_HV_CLS), hw(MG_NCLASS * MG_HV_W), hc(MG_NCLASS * 36);
+        for (int l = 0; l < levels; ++l) {
+            Level& Lv = c->L[l];
+            if (host_hv_tables(Lv.n, c->m, hcls.data(), hw.data(), hc.data(), err, sizeof(err)))
+                return bail(fail(MG_EINVAL, "level %d heterogeneous Vanka tables: %s", l, err));
+            Lv.hv_cls = (double*)dalloc(c, sizeof(double) * hcls.size());
+            Lv.hv_sinv = (double*)dalloc(c, sizeof(double) * MG_HV_NSINV * Lv.plane);
+            double* dw = (double*)dalloc(c, sizeof(double) * (hw.size() + hc.size()));
+            if (!Lv.hv_cls || !Lv.hv_sinv || !dw) return bail(fail(MG_ENOMEM, "heterogeneous Vanka tables (level %d)", l));
+            if (cudaMemcpy(Lv.hv_cls, hcls.data(), sizeof(double) * hcls.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(dw, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(dw + hw.size(), hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+                return bail(fail(MG_ECUDA, "heterogeneous Vanka table upload failed"));
+            cudaMemset(Lv.hv_sinv, 0, sizeof(double) * MG_HV_NSINV * Lv.plane);
+            if (launch_hv_sinv(Lv.vp.L, dw, dw + hw.size(), Lv.hv_sinv, 0) != cudaSuccess)
+                return bail(fail(MG_ECUDA, "hv_sinv launch: %s", cudaGetErrorString(cudaGetLastError())));
+            Lv.vp.hv = HetVankaTabs{Lv.hv_cls, Lv.hv_sinv};
+        }
     }
     // norms and solve state
     c->partials = (double*)dalloc(c, sizeof(double) * max_blocks);
@@ -609,7 +635,6 @@ int mg_relax_vanka(mg_ctx* c, int32_t level, double* x, const double* b, double 
                    cudaStream_t s) {
     if (int rc = check_level(c, level, c ? c->levels - 1 : 0)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
-    if (c->het) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (sweeps < 0) return fail(MG_EINVAL, "sweeps < 0");
     mg_cycle_opts o{1, 1, MG_VANKA, omega, 0.0, 0};
     Level& Lv = c->L[level];
@@ -667,7 +692,6 @@ int mg_cycle(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, doub
     if (!c) return fail(MG_EINVAL, "null context");
     if (int rc = check_opts(o)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
-    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (!c->Ginv) return fail(MG_EINVAL, "no dense coarsest solve on this context (n_c > 20)");
     if (c->levels == 1) {
         CK(launch_coarse(c->Nc, c->Ginv, c->slots, b, x, c->stop, s));
@@ -692,7 +716,6 @@ int mg_cycle_async(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o
     if (int rc = check_opts(o)) return rc;
     if (!aligned(x) || !aligned(b) || (in_norm2_dev && !aligned(in_norm2_dev)))
         return fail(MG_EINVAL, "null or misaligned pointer");
-    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (!c->Ginv || c->levels < 2) return fail(MG_EINVAL, "mg_cycle_async needs levels >= 2 and a coarsest solve");
     cudaGraphExec_t g;
     if (int rc = get_graph(c, x, b, *o, in_norm2_dev ? 2 : 0, in_norm2_dev, &g)) return rc;
@@ -740,7 +763,6 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (max_iters < 0 || restart < 1 || restart > 31)
         return fail(MG_EINVAL, "need max_iters >= 0, 1 <= restart <= 31");
-    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (!c->Ginv || c->levels < 2) return fail(MG_EINVAL, "mg_fgmres needs levels >= 2 and a coarsest solve");
     Level& L0 = c->L[0];
     const int64_t len = L0.len;
@@ -881,13 +903,34 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
     return hist.back() <= target ? MG_OK : MG_NOTCONV;
 }
 
+int mg_step_rhs(mg_ctx* c, const double* x_prev, const double* b_load, double* b_out, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (!aligned(x_prev) || !aligned(b_load) || !aligned(b_out)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (b_out == x_prev) return fail(MG_EINVAL, "b_out must not alias x_prev");
+    const Level& L0 = c->L[0];
+    if (b_out != b_load) CK(cudaMemcpyAsync(b_out, b_load, sizeof(double) * L0.len, cudaMemcpyDeviceToDevice, s));
+    CK(launch_step_rhs(L0.vp.L, c->m.inv_M, c->m.alpha, x_prev, b_out, s));
+    return MG_OK;
+}
+
+int mg_time_step(mg_ctx* c, double* x, const double* b_load, const mg_cycle_opts* o, double rtol, int32_t max_iters,
+                 int32_t restart, double* history_host, int32_t* n_iters, cudaStream_t s) {
+    if (!c) return fail(MG_EINVAL, "null context");
+    if (!aligned(x) || !aligned(b_load)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (!c->kb) {
+        c->kb = (double*)dalloc(c, sizeof(double) * c->L[0].len);
+        if (!c->kb) return fail(MG_ENOMEM, "time-step right-hand side allocation failed");
+    }
+    if (int rc = mg_step_rhs(c, x, b_load, c->kb, s)) return rc;
+    return mg_fgmres(c, x, c->kb, o, rtol, max_iters, restart, history_host, n_iters, s);
+}
+
 int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_cycles,
              double* history_host, int32_t* n_cycles, cudaStream_t s) {
     if (!c) return fail(MG_EINVAL, "null context");
     if (int rc = check_opts(o)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (max_cycles < 0) return fail(MG_EINVAL, "max_cycles < 0");
-    if (c->het && o->relax == MG_VANKA) return fail(MG_EINVAL, "Vanka needs a scalar K (reading A20)");
     if (c->levels == 1) return fail(MG_EINVAL, "mg_solve needs levels >= 2");
     if (!c->Ginv) return fail(MG_EINVAL, "no dense coarsest solve on this context (n_c > 20)");
     if (max_cycles + 1 > c->hist_cap) {

@@ -59,8 +59,36 @@ struct ProlSrc {                  // coarse iterate e_H for a sweep with fused p
     int64_t planec;
 };
 
+// Heterogeneous-K Vanka (DESIGN.md section 4 "Heterogeneous Vanka"): every
+// patch matrix K_v = K0_v + blockdiag(0, tau M_w,v(K)) differs only in its 6x6 RT0 block, so the
+// patch solve is condensed onto the RT0 slots r = {8..13}: with y = the other 14 slots (order
+// 0..7, 14..19),  a = G_def r_y,  c = -(1^T r_p)/(m gamma),  s = r_r - K_ry a,  z_r = S_v^{-1} s,
+// z_y = a + c 1_p - Q z_r,  out = D z,  where G_def = K_yy^{-1} + v v^T / gamma is the deflated
+// (well-conditioned) part of K_yy^{-1} (reading A9), Q = G_def K_yr, and
+// S_v = tau M_w,v(K) - K_ry G_def K_yr is the per-vertex 6x6 RT0 Schur complement.
+// The RT0 block is handled in an orthonormal basis U = [N, R] of the patch's RT0 slots, N spanning
+// the kernel of K_yr (the divergence-free circulation around the vertex: B_w N = 0), R its
+// complement.  In that basis the N rows of K_ry U and the N columns of Q U and of U^T C U are
+// exactly 0, so the small circulation eigenvalue of S_v (~ tau mu_f h^2 K^{-1}) is formed from
+// M_w alone, free of the rounding of the large K_ry G_def K_yr part (cond(S_v) reaches 1e6-1e9 for
+// lognormal K fields).  S~_v = U^T S_v U is stored inverted per vertex.
+#define MG_HV_CLS 384             // doubles per vertex-class table
+#define MG_HV_G 0                 // [14][14] G_def (row major, y order)
+#define MG_HV_Q 196               // [14][6]  Q U
+#define MG_HV_KRP 280             // [6][6]   U^T K_ry restricted to the P0 columns ([basis row][P0 slot 14 + k])
+#define MG_HV_PINV 316            // 1 / (m gamma), m = active P0 slots of the class (0 if none)
+#define MG_HV_D 320               // [20] natural weights D (1, 1/2, 1/3) on the active slots, 0 elsewhere
+#define MG_HV_U 344               // [6][6] U (row = RT0 slot, column = basis vector)
+#define MG_HV_NSINV 21            // per-vertex planes: upper triangle of S~_v^{-1}, row by row
+#define MG_HV_W 288               // setup: per class 8 triangles x [6][6] U^T M_w,v U per unit K^{-1}
+struct HetVankaTabs {
+    const double* cls;            // device: MG_NCLASS x MG_HV_CLS
+    const double* sinv;           // device: MG_HV_NSINV planes of (n+1) x pitch
+};
+
 struct VankaParams {
     LevelParams L;
+    HetVankaTabs hv;              // heterogeneous K only (cls == nullptr otherwise)
     double gpT[9][9];            // transposed: gpT[c][a] = G+[a][c] (column-outer FMA loops read pairs)
     double gmT[11][11];
     const double* gbnd;          // device: MG_NCLASS x 20 x 20 (weighted, deflated), row major
@@ -90,6 +118,10 @@ struct Material {
 
 // mg_setup.cpp
 int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, int errlen);
+// condensed heterogeneous-Vanka tables of one level (see HetVankaTabs): cls[MG_NCLASS][MG_HV_CLS],
+// W[MG_NCLASS][MG_HV_W] (tau mu_f h^2 M_w1 of triangle (cell a-1+tx, b-1+ty, shape sh), tri = 4 sh + 2 ty + tx,
+// mapped onto the 6 RT0 patch slots), C[MG_NCLASS][36] (K_ry G_def K_yr)
+int host_hv_tables(int n, const Material& m, double* cls, double* W, double* C, char* err, int errlen);
 // dense coarsest operator: Ginv (N x N, column major: G[col*N + row]) of the deflated inverse and
 // the slot offsets (k*(n+1)*pitch + j*pitch + i) of the N active unknowns.  kinv: nullptr (scalar)
 // or 2 x n x n [shape][j][i].

@@ -23,6 +23,11 @@
 #include "mg_kernels.cuh"
 #include "mg_tables.h"
 
+// displacement DoFs (q = 0..8: P1 x/y of the 3 vertices, 3 bubbles) of triangle `sh` of a cell as
+// (dx, dy, plane) -- mg_tables.h LOCAL_DOF (generated geometry), copied to the constant bank by
+// kernels_init
+__constant__ int c_local_dof[2][9][3];
+
 namespace {
 
 // Programmatic dependent launch (sm_90+): every kernel waits for the completion (and memory) of the
@@ -359,10 +364,139 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
     }
 }
 
+// Heterogeneous-K patch solve (mg_internal.h HetVankaTabs): the class-constant condensed tables
+// and the per-vertex inverse RT0 Schur complement S_v^{-1} (upper triangle, MG_HV_NSINV planes).
+// out[s * os] = (D K_v^{-1} r)_s for the vertex (a, b) of class cls.
+__device__ __forceinline__ void patch_apply_het(const VankaParams& P, int cls, int a, int b, const double rr[20],
+                                                double* out, int os) {
+    const double* T = P.hv.cls + cls * MG_HV_CLS;
+    double ry[14];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ry[q] = rr[q];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) ry[8 + q] = rr[14 + q];
+    // a = G_def r_y (column-outer: 14 independent chains)
+    double ad[14];
+#pragma unroll
+    for (int q = 0; q < 14; ++q) ad[q] = 0.0;
+    const double2* G2 = reinterpret_cast<const double2*>(T + MG_HV_G);
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {
+#pragma unroll
+        for (int c2 = 0; c2 < 7; ++c2) {
+            const double2 g = __ldg(G2 + q * 7 + c2);
+            ad[q] = fma(g.x, ry[2 * c2], ad[q]);
+            ad[q] = fma(g.y, ry[2 * c2 + 1], ad[q]);
+        }
+    }
+    // constant-pressure part of K_yy^{-1} r_y: -(1^T r_p) / (m gamma) on every active P0 slot
+    double psum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) psum += ry[8 + k];
+    const double cp = -psum * __ldg(T + MG_HV_PINV);
+    // s~ = U^T r_r - (U^T K_ry) a_def  (in the basis U; K_ry: P0 columns only)
+    double sv[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        double v = 0.0;
+#pragma unroll
+        for (int e = 0; e < 6; ++e) v = fma(__ldg(T + MG_HV_U + e * 6 + j), rr[8 + e], v);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v = fma(-__ldg(T + MG_HV_KRP + j * 6 + k), ad[8 + k], v);
+        sv[j] = v;
+    }
+    // z~ = S~_v^{-1} s~ (symmetric, upper triangle per vertex)
+    const int64_t o = (int64_t)b * P.L.pitch + a;
+    double si[21];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) si[k] = __ldg(P.hv.sinv + k * P.L.plane + o);
+    double zr[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+        double v = 0.0;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            const int lo = e < f ? e : f, hi = e < f ? f : e;
+            v = fma(si[lo * 6 - lo * (lo - 1) / 2 + (hi - lo)], sv[f], v);
+        }
+        zr[e] = v;
+    }
+    // z_y = a_def + cp 1_p - (Q U) z~; weights
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {
+        double v = ad[q] + (q >= 8 ? cp : 0.0);
+#pragma unroll
+        for (int e = 0; e < 6; ++e) v = fma(-__ldg(T + MG_HV_Q + q * 6 + e), zr[e], v);
+        const int sl = q < 8 ? q : q + 6;
+        out[sl * os] = __ldg(T + MG_HV_D + sl) * v;
+    }
+    // z_r = U z~
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) v = fma(__ldg(T + MG_HV_U + e * 6 + j), zr[j], v);
+        out[(8 + e) * os] = __ldg(T + MG_HV_D + 8 + e) * v;
+    }
+}
+
+// per-vertex S~_v^{-1} of the heterogeneous Vanka patches of one level (setup), in the basis U of
+// the class (mg_internal.h): S~_v = sum over the star triangles of K^{-1}_T W~[cls][tri] - C~[cls];
+// inactive RT0 slots get a unit diagonal (their right-hand side is always 0).  Gauss-Jordan with
+// partial pivoting in fp64.
+__global__ void __launch_bounds__(256) hv_sinv_kernel(const LevelParams L, const double* __restrict__ W,
+                                                      const double* __restrict__ C, double* __restrict__ sinv) {
+    const int a = blockIdx.x * 32 + (threadIdx.x & 31), b = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int n = L.n;
+    if (a > n || b > n) return;
+    const int cls = (a == 0 ? 1 : (a == n ? 2 : 0)) + 3 * (b == 0 ? 1 : (b == n ? 2 : 0));
+    double S[6][6], I[6][6];
+    for (int e = 0; e < 6; ++e)
+        for (int f = 0; f < 6; ++f) {
+            S[e][f] = -C[cls * 36 + e * 6 + f];
+            I[e][f] = e == f ? 1.0 : 0.0;
+        }
+    for (int sh = 0; sh < 2; ++sh)
+        for (int ty = 0; ty < 2; ++ty)
+            for (int tx = 0; tx < 2; ++tx) {
+                const int ci = a - 1 + tx, cj = b - 1 + ty;
+                if (ci < 0 || cj < 0 || ci >= n || cj >= n) continue;
+                const double k = L.kinv_field[sh * L.plane + (int64_t)cj * L.pitch + ci];
+                const double* Wt = W + cls * MG_HV_W + (4 * sh + 2 * ty + tx) * 36;
+                for (int e = 0; e < 36; ++e) S[e / 6][e % 6] = fma(k, Wt[e], S[e / 6][e % 6]);
+            }
+    for (int e = 0; e < 6; ++e) {
+        bool zero = true;
+        for (int f = 0; f < 6; ++f) zero = zero && S[e][f] == 0.0 && S[f][e] == 0.0;
+        if (zero) S[e][e] = 1.0;
+    }
+    for (int c = 0; c < 6; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < 6; ++r)
+            if (fabs(S[r][c]) > fabs(S[piv][c])) piv = r;
+        if (piv != c)
+            for (int k = 0; k < 6; ++k) {
+                double t = S[c][k]; S[c][k] = S[piv][k]; S[piv][k] = t;
+                t = I[c][k]; I[c][k] = I[piv][k]; I[piv][k] = t;
+            }
+        const double d = 1.0 / S[c][c];
+        for (int k = 0; k < 6; ++k) { S[c][k] *= d; I[c][k] *= d; }
+        for (int r = 0; r < 6; ++r) {
+            if (r == c) continue;
+            const double f = S[r][c];
+            for (int k = 0; k < 6; ++k) { S[r][k] = fma(-f, S[c][k], S[r][k]); I[r][k] = fma(-f, I[c][k], I[r][k]); }
+        }
+    }
+    const int64_t o = (int64_t)b * L.pitch + a;
+    int k = 0;
+    for (int e = 0; e < 6; ++e)
+        for (int f = e; f < 6; ++f) sinv[(k++) * L.plane + o] = 0.5 * (I[e][f] + I[f][e]);
+}
+
 // one TX x TY tile of the sweep, run by threads t = 0 .. T::NT-1 of a (virtual) block with shared
 // memory sm; every thread executes the three barriers, `active` = false skips the work (tiles of
 // the bottom kernel's last round).  Returns the thread's share of ||r||^2.
-template <bool XZERO, int TX, int TY, bool NC>
+template <bool XZERO, int TX, int TY, bool NC, bool HET = false>
 __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double* __restrict__ x,
                                              const double* __restrict__ b, double* __restrict__ xo, int bx, int by,
                                              int t, double* sm, bool active) {
@@ -383,7 +517,7 @@ __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double*
         if (tl < T::RW * T::RH) {
             const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<T::XW, T::XH, false, NC>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            residual_at<T::XW, T::XH, HET, NC>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
             for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
@@ -398,7 +532,8 @@ __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double*
         if (a <= n && bb <= n) {
             double rr[20];
             gather20<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
-            patch_apply20<(TX <= 8)>(P, vertex_class(a, bb, n), rr, cs + t, T::PW * T::PH);
+            if (HET) patch_apply_het(P, vertex_class(a, bb, n), a, bb, rr, cs + t, T::PW * T::PH);
+            else patch_apply20<(TX <= 8)>(P, vertex_class(a, bb, n), rr, cs + t, T::PW * T::PH);
         } else {
 #pragma unroll
             for (int q = 0; q < 20; ++q) cs[q * T::PW * T::PH + t] = 0.0;
@@ -439,7 +574,7 @@ __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double*
     return nrm;
 }
 
-template <bool XZERO, int TX = VTX, int TY = VTY>
+template <bool XZERO, int TX = VTX, int TY = VTY, bool HET = false>
 __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
                                                        const double* __restrict__ b, double* __restrict__ xo,
                                                        NormSink S) {
@@ -447,7 +582,8 @@ __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const Vanka
     pdl_trigger();
     extern __shared__ double sm[];
     if (*P.L.stop) return;
-    const double nrm = vanka_tile<XZERO, TX, TY, true>(P, x, b, xo, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
+    const double nrm =
+        vanka_tile<XZERO, TX, TY, true, HET>(P, x, b, xo, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
     if (S.out || S.state) norm_finish<VTile<TX, TY>::NT>(S, nrm);
 }
 
@@ -1206,6 +1342,8 @@ __global__ void kinv_coarsen_kernel(int nf, int pitchf, const double* __restrict
     kc[pc + (int64_t)J * pitchc + I] = ur / 4.0;
 }
 
+int g_carveout = cudaSharedmemCarveoutMaxShared;   // MG_CARVEOUT (-1: driver default)
+
 // ------------------------------------------------------------------------------------------
 // mbarrier / TMA helpers of the row-marching kernels
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1255,9 +1393,17 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
         : "memory");
 }
 
+// Every kernel of the cycle asks for the same L1 / shared-memory split (the maximum shared
+// carveout): kernels with different preferred splits force the SM to drain and reconfigure between
+// consecutive launches, which the latency-bound coarse levels pay on every kernel boundary.
+template <typename F>
+void carve(F* f) {
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
+}
 template <typename F>
 void set_smem(F* f, int bytes) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    carve(f);
 }
 
 }  // namespace
@@ -2206,7 +2352,17 @@ static cudaError_t encode_vec_map(CUtensorMap* m, const double* ptr, int n, int 
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static void carve_all();
+void set_carveout(int pct) { g_carveout = pct; }
 void kernels_init() {
+    carve_all();
+    {
+        int ld[2][9][3];
+        for (int sh = 0; sh < 2; ++sh)
+            for (int q = 0; q < 9; ++q)
+                for (int k = 0; k < 3; ++k) ld[sh][q][k] = LOCAL_DOF[sh][q][k];
+        cudaMemcpyToSymbol(c_local_dof, ld, sizeof(ld));
+    }
     set_smem(bottom_kernel, BOT_SMEM);
     set_smem(vanka_march2_kernel<false, false>, M2SMEM);
     set_smem(vanka_march2_kernel<true, false>, M2SMEM);
@@ -2225,6 +2381,10 @@ void kernels_init() {
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
+    set_smem(vanka_kernel<false, VTX, VTY, true>, V_SMEM);
+    set_smem(vanka_kernel<true, VTX, VTY, true>, V_SMEM);
+    set_smem(vanka_kernel<false, VSX, VSY, true>, VTile<VSX, VSY>::SMEM);
+    set_smem(vanka_kernel<true, VSX, VSY, true>, VTile<VSX, VSY>::SMEM);
     set_smem(restrict_kernel<0, false>, C_SMEM_PLAIN);
     set_smem(restrict_kernel<2, false>, C_SMEM_PLAIN);
     set_smem(restrict_kernel<1, false>, C_SMEM_FUSED);
@@ -2550,6 +2710,40 @@ cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cud
     launch_k(vec_scale_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, y, x, sc, len);
     return cudaGetLastError();
 }
+// Backward-Euler history term (eq. discrete3 scaled by -1): the pressure rows of
+// b^m get -(1/M) M_p p^{m-1} + alpha B_u u^{m-1}, B_u u = -(div u, 1_T) of the 9 displacement DoFs
+// of triangle T (L.bu = h REF_BU in LOCAL_DOF order), M_p = h^2/2.  One thread per cell.
+__global__ void __launch_bounds__(256) step_rhs_kernel(const LevelParams L, double inv_M, double alpha,
+                                                       const double* __restrict__ x, double* __restrict__ b) {
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int n = L.n;
+    if (i >= n || j >= n) return;
+    const double h = 1.0 / n;
+#pragma unroll
+    for (int sh = 0; sh < 2; ++sh) {
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            const int ii = i + c_local_dof[sh][q][0], jj = j + c_local_dof[sh][q][1], p = c_local_dof[sh][q][2];
+            d = fma(L.bu[sh][q], x[p * L.plane + (int64_t)jj * L.pitch + ii], d);
+        }
+        const int64_t o = (8 + sh) * L.plane + (int64_t)j * L.pitch + i;
+        b[o] += fma(-inv_M * (h * h * 0.5), x[o], alpha * d);   // M_p = |T| = h^2/2 (REF_MP)
+    }
+}
+
+cudaError_t launch_step_rhs(const LevelParams& L, double inv_M, double alpha, const double* x, double* b,
+                            cudaStream_t s) {
+    dim3 grid((L.n + 31) / 32, (L.n + 7) / 8);
+    step_rhs_kernel<<<grid, 256, 0, s>>>(L, inv_M, alpha, x, b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hv_sinv(const LevelParams& L, const double* W, const double* C, double* sinv, cudaStream_t s) {
+    dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
+    hv_sinv_kernel<<<grid, 256, 0, s>>>(L, W, C, sinv);
+    return cudaGetLastError();
+}
 cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* stop, cudaStream_t s) {
     launch_k(vec_copy_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, dst, src, len, stop);
     return cudaGetLastError();
@@ -2558,6 +2752,19 @@ int dot_partials_needed() { return VK * DOT_BLOCKS; }
 
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
                          NormSink S, cudaStream_t s) {
+    if (P.hv.cls) {   // heterogeneous K: condensed patch solves, K^{-1} field in the residual
+        if (P.L.n <= g_small_tile_n) {
+            using T = VTile<VSX, VSY>;
+            dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
+            if (x_zero) launch_k(vanka_kernel<true, VSX, VSY, true>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+            else launch_k(vanka_kernel<false, VSX, VSY, true>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+            return cudaGetLastError();
+        }
+        dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
+        if (x_zero) launch_k(vanka_kernel<true, VTX, VTY, true>, grid, VNT, V_SMEM, s, P, x, b, xo, S);
+        else launch_k(vanka_kernel<false, VTX, VTY, true>, grid, VNT, V_SMEM, s, P, x, b, xo, S);
+        return cudaGetLastError();
+    }
     if (P.L.n <= g_small_tile_n) {
         using T = VTile<VSX, VSY>;
         dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
@@ -2795,4 +3002,21 @@ cudaError_t launch_kinv_coarsen(int nf, int pitchf, const double* kf, int pitchc
     dim3 grid((nf / 2 + 31) / 32, (nf / 2 + 7) / 8);
     launch_k(kinv_coarsen_kernel, grid, 256, 0, s, nf, pitchf, kf, pitchc, kc);
     return cudaGetLastError();
+}
+
+// the kernels launched without a dynamic shared-memory attribute (set_smem carves the others)
+static void carve_all() {
+    carve(prolong_kernel);
+    carve(residual_kernel<false, false>);
+    carve(residual_kernel<true, false>);
+    carve(residual_kernel<false, true>);
+    carve(residual_kernel<true, true>);
+    carve(residual_march_kernel<0>);
+    carve(residual_march_kernel<1>);
+    carve(residual_march_kernel<2>);
+    carve(bsr_jacobi_kernel<false>);
+    carve(bsr_jacobi_kernel<true>);
+    carve(bsr_jacobi_t_kernel<0>);
+    carve(vec_copy_kernel);
+    carve(step_rhs_kernel);
 }

@@ -11,6 +11,8 @@ struct NormSink {
     SolveState* state;    // non-null: append the norm to state->hist and decide state->stop
 };
 void kernels_init();
+// preferred L1 / shared carveout (percent) of every kernel, applied by kernels_init (-1: driver default)
+void set_carveout(int pct);
 
 // up to 8 vector pointers for the FGMRES multi-vector kernels
 struct VecPtrs {
@@ -62,6 +64,12 @@ cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cud
 // dst = src (len doubles), skipped when *stop != 0 (mg_solve's flag)
 cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* stop, cudaStream_t s);
 int dot_partials_needed();
+// backward-Euler history term added to the pressure rows of b (x = the previous step's iterate)
+cudaError_t launch_step_rhs(const LevelParams& L, double inv_M, double alpha, const double* x, double* b,
+                            cudaStream_t s);
+// per-vertex S_v^{-1} planes of the heterogeneous Vanka patches (setup; L.kinv_field set)
+cudaError_t launch_hv_sinv(const LevelParams& L, const double* W, const double* C, double* sinv, cudaStream_t s);
+// P.hv.cls != nullptr: heterogeneous-K sweep (condensed patch solves, 2-D tiles on every level)
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
                          bool x_zero, NormSink norm, cudaStream_t s);
 // row-marching TMA variant of the same sweep (identical arithmetic); the production kernel

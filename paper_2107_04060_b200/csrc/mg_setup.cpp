@@ -197,6 +197,192 @@ bool patch_inverse(int a, int b, int n, int ns, const Material& m, double h, dou
 
 int class_coord(int c, int n) { return c == 0 ? 1 : (c == 1 ? 0 : n); }
 
+// Eigen-decomposition of a symmetric m x m matrix (m <= 6) by cyclic Jacobi rotations in long
+// double: A is destroyed (its diagonal ends up holding the eigenvalues), V receives the eigenvectors
+// as columns.
+void jacobi_eigen(long double A[6][6], long double V[6][6], int m) {
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) V[i][j] = i == j ? 1.0L : 0.0L;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        long double off = 0.0L, tot = 0.0L;
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) {
+                tot += A[i][j] * A[i][j];
+                if (i != j) off += A[i][j] * A[i][j];
+            }
+        if (off <= 1e-38L * tot) break;
+        for (int p = 0; p < m; ++p)
+            for (int q = p + 1; q < m; ++q) {
+                if (A[p][q] == 0.0L) continue;
+                const long double th = (A[q][q] - A[p][p]) / (2.0L * A[p][q]);
+                const long double t = (th >= 0 ? 1.0L : -1.0L) / (fabsl(th) + sqrtl(th * th + 1.0L));
+                const long double c = 1.0L / sqrtl(t * t + 1.0L), sn = t * c;
+                for (int k = 0; k < m; ++k) {       // A <- A J
+                    const long double akp = A[k][p], akq = A[k][q];
+                    A[k][p] = c * akp - sn * akq;
+                    A[k][q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < m; ++k) {       // A <- J^T A
+                    const long double apk = A[p][k], aqk = A[q][k];
+                    A[p][k] = c * apk - sn * aqk;
+                    A[q][k] = sn * apk + c * aqk;
+                }
+                for (int k = 0; k < m; ++k) {       // V <- V J
+                    const long double vkp = V[k][p], vkq = V[k][q];
+                    V[k][p] = c * vkp - sn * vkq;
+                    V[k][q] = sn * vkp + c * vkq;
+                }
+            }
+    }
+}
+
+// Condensed heterogeneous-Vanka tables of the vertex (a, b) (mg_internal.h HetVankaTabs): the patch
+// matrix without its M_w block (K0 with kinv = 0) split into y = slots 0..7, 14..19 and r = 8..13.
+bool hv_class_tables(int a, int b, int n, const Material& m, double h, double* cls, double* W, double* C,
+                     char* err, int errlen) {
+    Material m0 = m;
+    m0.K = INFINITY;                                           // kinv = 0: K0 has no M_w block
+    std::vector<double> K;
+    std::vector<int> act;
+    patch_matrix(a, b, n, MG_PSLOTS, m0, h, K, act);
+    static const int YS[14] = {0, 1, 2, 3, 4, 5, 6, 7, 14, 15, 16, 17, 18, 19};
+    std::vector<int> yi;                                       // active y slots (positions in YS)
+    for (int q = 0; q < 14; ++q)
+        if (act[YS[q]]) yi.push_back(q);
+    const int my = (int)yi.size();
+    memset(cls, 0, sizeof(double) * MG_HV_CLS);
+    memset(W, 0, sizeof(double) * MG_HV_W);
+    memset(C, 0, sizeof(double) * 36);
+    // G_def over the active y slots (long double): deflated_inverse gives G = G_def - v v^T / gamma
+    std::vector<double> Ky(my * (size_t)my), G;
+    std::vector<int> isp(my);
+    int mp = 0;
+    for (int r = 0; r < my; ++r) {
+        isp[r] = YS[yi[r]] >= 14;
+        mp += isp[r];
+        for (int c = 0; c < my; ++c) Ky[r * (size_t)my + c] = K[YS[yi[r]] * MG_PSLOTS + YS[yi[c]]];
+    }
+    std::vector<long double> Gd(14 * 14, 0.0L);
+    if (my > 0) {
+        if (!deflated_inverse(Ky, isp, my, G, err, errlen)) return false;
+        const long double gamma = (long double)m.inv_M * h * h * 0.5L;   // -(1/M) M_p on v, M_p = h^2/2
+        for (int r = 0; r < my; ++r)
+            for (int c = 0; c < my; ++c) {
+                long double g = G[r * (size_t)my + c];
+                if (isp[r] && isp[c]) g += 1.0L / (mp * gamma);           // + v v^T / gamma
+                Gd[yi[r] * 14 + yi[c]] = g;
+            }
+        if (mp > 0) cls[MG_HV_PINV] = (double)(1.0L / (mp * gamma));
+    }
+    // K_yr (y x 6) and K_ry on the active slots; Q = G_def K_yr; C = K_ry Q
+    long double Kyr[14][6] = {}, Q[14][6] = {};
+    for (int q = 0; q < 14; ++q)
+        for (int e = 0; e < 6; ++e)
+            if (act[YS[q]] && act[8 + e]) Kyr[q][e] = K[YS[q] * MG_PSLOTS + 8 + e];
+    for (int q = 0; q < 14; ++q)
+        for (int e = 0; e < 6; ++e) {
+            long double s2 = 0.0L;
+            for (int t = 0; t < 14; ++t) s2 += Gd[q * 14 + t] * Kyr[t][e];
+            Q[q][e] = s2;
+        }
+    // orthonormal basis U of the active RT0 slots: kernel of K_yr first (eigenvalue ~ 0 of
+    // K_yr^T K_yr), then its complement; inactive slots keep unit vectors (they carry no data)
+    int ar[6], na = 0;
+    for (int e = 0; e < 6; ++e)
+        if (act[8 + e]) ar[na++] = e;
+    long double U[6][6] = {};
+    for (int e = 0; e < 6; ++e) U[e][e] = 1.0L;
+    bool isnull[6] = {false, false, false, false, false, false};
+    if (na > 0) {
+        long double M[6][6] = {}, E[6][6];
+        long double mmax = 0.0L;
+        for (int i = 0; i < na; ++i)
+            for (int j = 0; j < na; ++j) {
+                long double s2 = 0.0L;
+                for (int t = 0; t < 14; ++t) s2 += Kyr[t][ar[i]] * Kyr[t][ar[j]];
+                M[i][j] = s2;
+                mmax = fmaxl(mmax, fabsl(s2));
+            }
+        jacobi_eigen(M, E, na);
+        int order[6], k = 0;
+        for (int i = 0; i < na; ++i)
+            if (M[i][i] <= 1e-14L * mmax) order[k++] = i;
+        const int nnull = k;
+        for (int i = 0; i < na; ++i)
+            if (!(M[i][i] <= 1e-14L * mmax)) order[k++] = i;
+        for (int e = 0; e < 6; ++e)
+            if (act[8 + e])
+                for (int j = 0; j < 6; ++j) U[e][j] = 0.0L;
+        // basis vector j (j < na) occupies column ar[j]; inactive slots keep their unit column
+        for (int j = 0; j < na; ++j) {
+            for (int i = 0; i < na; ++i) U[ar[i]][ar[j]] = E[i][order[j]];
+            isnull[ar[j]] = j < nnull;
+        }
+    }
+    // U^T C U (C = K_ry G_def K_yr) with the kernel rows / columns exactly 0
+    long double KU[14][6] = {}, QU[14][6] = {};
+    for (int t = 0; t < 14; ++t)
+        for (int j = 0; j < 6; ++j) {
+            long double s2 = 0.0L, s3 = 0.0L;
+            for (int e = 0; e < 6; ++e) {
+                s2 += Kyr[t][e] * U[e][j];
+                s3 += Q[t][e] * U[e][j];
+            }
+            KU[t][j] = isnull[j] ? 0.0L : s2;
+            QU[t][j] = isnull[j] ? 0.0L : s3;
+        }
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) {
+            long double s2 = 0.0L;
+            for (int t = 0; t < 14; ++t) s2 += KU[t][i] * QU[t][j];
+            C[i * 6 + j] = (double)s2;
+        }
+    for (int q = 0; q < MG_PSLOTS; ++q)   // natural weights
+        cls[MG_HV_D + q] = act[q] ? (q < 2 ? 1.0 : (q < 14 ? 0.5 : 1.0 / 3.0)) : 0.0;
+    for (int q = 0; q < 14; ++q)
+        for (int c = 0; c < 14; ++c) cls[MG_HV_G + q * 14 + c] = (double)Gd[q * 14 + c];
+    for (int q = 0; q < 14; ++q)
+        for (int j = 0; j < 6; ++j) cls[MG_HV_Q + q * 6 + j] = (double)QU[q][j];
+    for (int j = 0; j < 6; ++j)
+        for (int k = 0; k < 6; ++k) {
+            for (int q = 0; q < 8; ++q)   // K_ry has no u / bubble columns (zero (w, u) block of A^RQ)
+                if (Kyr[q][j] != 0.0L) { snprintf(err, errlen, "K_ry has a displacement column"); return false; }
+            cls[MG_HV_KRP + j * 6 + k] = (double)KU[8 + k][j];
+        }
+    for (int e = 0; e < 6; ++e)
+        for (int j = 0; j < 6; ++j) cls[MG_HV_U + e * 6 + j] = (double)U[e][j];
+    // U^T M_w,v U of each star triangle per unit K^{-1}: tau mu_f h^2 REF_MW1 on the RT0 slots
+    for (int ty = 0; ty < 2; ++ty)
+        for (int tx = 0; tx < 2; ++tx) {
+            const int ci = a - 1 + tx, cj = b - 1 + ty;
+            if (ci < 0 || cj < 0 || ci >= n || cj >= n) continue;
+            for (int sh = 0; sh < 2; ++sh) {
+                int loc[3];
+                for (int e = 0; e < 3; ++e) {
+                    loc[e] = -1;
+                    const int q = 9 + e;                       // RT0 local DoFs of the triangle
+                    const int dx = tx - 1 + LOCAL_DOF[sh][q][0], dy = ty - 1 + LOCAL_DOF[sh][q][1], p = LOCAL_DOF[sh][q][2];
+                    for (int s2 = 8; s2 < 14; ++s2)
+                        if (VSLOT[s2][0] == dx && VSLOT[s2][1] == dy && VSLOT[s2][2] == p && act[s2]) loc[e] = s2 - 8;
+                }
+                long double Wl[6][6] = {};
+                for (int e = 0; e < 3; ++e)
+                    for (int f = 0; f < 3; ++f)
+                        if (loc[e] >= 0 && loc[f] >= 0)
+                            Wl[loc[e]][loc[f]] += (long double)m.tau * m.mu_f * h * h * REF_MW1[sh][e][f];
+                double* Wt = W + (4 * sh + 2 * ty + tx) * 36;
+                for (int i = 0; i < 6; ++i)
+                    for (int j = 0; j < 6; ++j) {
+                        long double s2 = 0.0L;
+                        for (int e = 0; e < 6; ++e)
+                            for (int f = 0; f < 6; ++f) s2 += U[e][i] * Wl[e][f] * U[f][j];
+                        Wt[i * 6 + j] = (double)s2;
+                    }
+            }
+        }
+    return true;
+}
+
 // +/- basis of the 180-degree rotation for ns = 20 (Vanka) or 8 (displacement).  comp[t] lists
 // hat component t as (slot a, slot b, sign): hat_t = r_a + sign r_b (b < 0: single).
 struct HatComp { int a, b, sg; };
@@ -307,6 +493,18 @@ int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, i
         }
     if (!split_pm(t->vanka[0], MG_PSLOTS, &t->gp[0][0], &t->gm[0][0], err, errlen)) return -1;
     if (!split_pm(t->disp[0], MG_USLOTS, &t->up[0][0], &t->um[0][0], err, errlen)) return -1;
+    return 0;
+}
+
+int host_hv_tables(int n, const Material& m, double* cls, double* W, double* C, char* err, int errlen) {
+    const double h = 1.0 / n;
+    for (int cy = 0; cy < 3; ++cy)
+        for (int cx = 0; cx < 3; ++cx) {
+            const int c = cx + 3 * cy;
+            if (!hv_class_tables(class_coord(cx, n), class_coord(cy, n), n, m, h, cls + c * MG_HV_CLS,
+                                 W + c * MG_HV_W, C + c * 36, err, errlen))
+                return -1;
+        }
     return 0;
 }
 

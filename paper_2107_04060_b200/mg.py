@@ -63,6 +63,9 @@ SIGNATURES = {
                                 _D, ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_fgmres": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
                                  ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32), _VP]),
+    "mg_step_rhs": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "mg_time_step": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
+                                    ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_solve_host": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
                                      _D, ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_cycle_async": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), _VP, _VP]),
@@ -315,6 +318,21 @@ class Hierarchy:
         rc = _check(self.lib.mg_fgmres(self.ctx, self._v(x), self._v(b), ctypes.byref(o), float(rtol), int(max_iters),
                                        int(restart), hist.ctypes.data_as(_D), ctypes.byref(nc), _stream(stream)),
                     "mg_fgmres")
+        return rc, hist[: nc.value + 1]
+
+    def step_rhs(self, x_prev, b_load, b_out, stream=None):
+        """b_out = b_load + backward-Euler history of x_prev (mg_step_rhs)."""
+        _check(self.lib.mg_step_rhs(self.ctx, self._v(x_prev), self._v(b_load), self._v(b_out), _stream(stream)),
+               "mg_step_rhs")
+
+    def time_step(self, x, b_load, opts: Opts, rtol=1e-10, max_iters=100, restart=30, stream=None):
+        """One backward-Euler step in place on x (x^{m-1} -> x^m): mg_time_step; returns (rc, history)."""
+        hist = np.zeros(max_iters + 1)
+        nc = ctypes.c_int32(0)
+        o = opts.c()
+        rc = _check(self.lib.mg_time_step(self.ctx, self._v(x), self._v(b_load), ctypes.byref(o), float(rtol),
+                                          int(max_iters), int(restart), hist.ctypes.data_as(_D), ctypes.byref(nc),
+                                          _stream(stream)), "mg_time_step")
         return rc, hist[: nc.value + 1]
 
     def solve_host(self, x_host: np.ndarray, b_host: np.ndarray, opts: Opts, rtol=1e-8, max_cycles=100,
