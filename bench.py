@@ -71,7 +71,9 @@ def workload(cfg_id: int):
 def opts_for(c):
     from paper_2107_04060_b200 import Opts
     if c["relax_used"] == "vanka":
-        return Opts(1, 1, "vanka", c["omega"])
+        return Opts(1, 1, "vanka", c.get("omega", 0.74))
+    if c["relax_used"] == "bsr_exact":
+        return Opts(1, 1, "bsr_exact", c.get("bsr_omega", 0.75), 1.0, 0)
     return Opts(1, 1, "bsr", c["bsr_omega"], c["omega_J"], 3)
 
 
@@ -221,16 +223,18 @@ def main():
     ap.add_argument("--trace-cycles", type=int, default=10)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--n", type=int, default=0, help="experiment: override the grid size (levels keep n_c = 4)")
-    ap.add_argument("--relax", default="", choices=["", "vanka", "bsr"],
-                    help="override the relaxation (config 2 names both: Vanka by default, --relax bsr for BSR)")
+    ap.add_argument("--relax", default="", choices=["", "vanka", "bsr", "bsr_exact"],
+                    help="override the relaxation (config 2 names both: Vanka by default, --relax bsr for BSR; "
+                         "--relax vanka on config 4 runs the heterogeneous-K Vanka of SURVEY 8(f) rank 4; "
+                         "bsr_exact: exact BSR, n <= 1024)")
+    ap.add_argument("--quadrature", default="rq", choices=["rq", "exact"],
+                    help="exact: the exact-integration operator of eq. block_form (SURVEY 8(f) rank 3)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     c = workload(args.config)
     if args.relax:
-        if args.relax == "vanka" and c["K_seed"] is not None:
-            raise SystemExit("Vanka needs a scalar K (reading A20)")
         c["relax_used"] = args.relax
         c.setdefault("bsr_omega", 0.75)
         c.setdefault("omega_J", 1.0)
@@ -250,7 +254,7 @@ def main():
     n, L = c["n"], c["levels"]
     kf = None if c["K_seed"] is None else mg_inputs.lognormal_K(n, c["K_seed"])
     H = Hierarchy(n, L, c["lam"], c["mu"], K=c["K"] if c["K"] is not None else 1.0, tau=c["tau"],
-                  alpha=c["alpha"], inv_M=c["inv_M"], mu_f=c["mu_f"], K_field=kf)
+                  alpha=c["alpha"], inv_M=c["inv_M"], mu_f=c["mu_f"], K_field=kf, quadrature=args.quadrature)
     o = opts_for(c)
     b_host = mg_inputs.uniform_rhs(n, c["b_seed"])
     b = H.to_device(b_host)
@@ -358,9 +362,15 @@ def main():
     # levels whose first post-sweep absorbs the prolongation (marching Vanka levels, mg_api.cu
     # fused_prolong): that sweep also reads the coarse iterate, 1/4 of a fine pass
     march_min = int(os.environ.get("MG_MARCH_MIN_N", "512"))
+    het = c["K_seed"] is not None
     fused = o.relax == "vanka" and os.environ.get("MG_FUSE_PROLONG", "1") != "0" and \
-        os.environ.get("MG_VANKA_IMPL", "2") == "2"
-    if o.relax == "vanka":
+        os.environ.get("MG_VANKA_IMPL", "2") == "2" and not het and args.quadrature == "rq"
+    if o.relax == "vanka" and het:
+        # heterogeneous Vanka (2-D tile kernel): read x, b, write x + the per-vertex S~^{-1} table
+        # (21 doubles per vertex = 16.8 B per active DoF at 10 DoFs per vertex) + K^{-1} (2 per cell)
+        alg_bytes = (24.0 + 16.8 + 1.6) * nact
+        dom = "vanka_kernel<HET> (level 0: residual with the K^{-1} field + condensed patch solves + update)"
+    elif o.relax == "vanka":
         # read x, read b, write x over the active DoFs; averaged over the pre-sweep and the post-sweep
         # (which with the fused prolongation also reads e_H: + 8 B x N_1 ~ 2 B per fine DoF)
         alg_bytes = (24.0 * nact + (24.0 * nact + 8.0 * mg_inputs.n_active(n >> 1) if fused and n >= march_min
@@ -386,12 +396,14 @@ def main():
             return 14.7 if c["K_seed"] is not None else 14.1
         if l == L - 1:
             return 0.0 if L > 1 else 6.0
+        if het:                       # + the S~^{-1} table and K^{-1} in both sweeps (2 x 2.3 passes)
+            return 15.1
         return 8.5 if fused and (n >> l) >= march_min else 10.5
     # B_alg of SURVEY 8(d) (10.5 Vanka / 14.1 BSR / 14.7 BSR + K field passes on every level): the
     # roofline figure of the method; the fused schedule (prolongation inside the post-sweep) needs
     # fewer bytes, reported beside it
     sum_levels = sum(mg_inputs.n_active(n >> l) for l in range(L))
-    b_alg = 8.0 * (10.5 if o.relax == "vanka" else 14.7 if c["K_seed"] is not None else 14.1) * sum_levels
+    b_alg = 8.0 * ((15.1 if het else 10.5) if o.relax == "vanka" else 14.7 if het else 14.1) * sum_levels
     cycle_bytes = 8.0 * sum(level_passes(l) * mg_inputs.n_active(n >> l) for l in range(L))
     ms_step = ms / args.steps
     line = {

@@ -80,6 +80,10 @@ extern "C" {
 
 #define MG_VANKA 0       /* additive Vanka, 20-DoF vertex patches    */
 #define MG_BSR   1       /* inexact Braess-Sarazin                   */
+#define MG_BSR_EXACT 2   /* exact Braess-Sarazin: S dp = g solved exactly */
+
+#define MG_RQ    0       /* reduced quadrature of lambda (div u, div v): A^RQ, eq. block_form_rq */
+#define MG_EXACT 1       /* exact integration: A of eq. block_form (tab:naive) */
 
 typedef struct mg_ctx mg_ctx;
 
@@ -95,11 +99,15 @@ typedef struct {
                                proposed 1e-6: at 1e-6 the rediscretised V(1,1) cycle diverges
                                (factor ~ 1/gamma growth, tests/golden/a5_invM_scan.json).        */
     double mu_f;            /* fluid viscosity > 0; 1                            */
+    int32_t quadrature;     /* MG_RQ (0, the paper's method) or MG_EXACT: lambda (div u, div v)
+                               integrated exactly (eq. block_form), the "solver-incompatible"
+                               operator of PAPER.md:169-198.  MG_EXACT contexts run the 2-D tile
+                               kernels on every level (the row-marching kernels are RQ only)     */
 } mg_grid;
 
 typedef struct {
     int32_t nu1, nu2;       /* pre / post relaxation sweeps (BASELINE: 1, 1)                 */
-    int32_t relax;          /* MG_VANKA or MG_BSR                                             */
+    int32_t relax;          /* MG_VANKA, MG_BSR or MG_BSR_EXACT (n <= 1024)                   */
     double  omega;          /* outer damping                              */
     double  omega_J;        /* BSR: weight of the Jacobi sweeps on S          */
     int32_t jacobi_sweeps;  /* BSR: sweeps on S from dp = 0 (BASELINE: 3; paper: 1)          */
@@ -156,6 +164,14 @@ int mg_relax_vanka(mg_ctx* ctx, int32_t level, double* x, const double* b, doubl
  *   x += omega (du, dw, dp).   In place on x.  `sweeps` repetitions. */
 int mg_relax_bsr(mg_ctx* ctx, int32_t level, double* x, const double* b, double omega,
                  double omega_J, int32_t jacobi_sweeps, int32_t sweeps, cudaStream_t s);
+
+/* `sweeps` exact Braess-Sarazin relaxations on level l: as mg_relax_bsr with
+ * the Jacobi sweeps replaced by the exact solution of S dp = g (eq. bsr_p), computed on the device
+ * by Jacobi-preconditioned conjugate gradients to 1e-14 in the D_S^{-1} norm (at most 24 n + 64
+ * iterations).  Level n <= 1024 (a full S solve per relaxation is the cost the paper avoids with
+ * inexact BSR).  Work space allocated on first use.  In place on x. */
+int mg_relax_bsr_exact(mg_ctx* ctx, int32_t level, double* x, const double* b, double omega, int32_t sweeps,
+                       cudaStream_t s);
 
 /* b_coarse = P^T r_fine between levels fine_level and fine_level+1 (R = P^T, PAPER.md:484;
  * P_u divergence preserving PAPER.md:510-566, P_w / P_p canonical).  Overwrites b_coarse. */

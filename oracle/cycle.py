@@ -85,14 +85,16 @@ def reversed_rows(A):
 class Hierarchy:
     """Per-level operators, transfers and smoothers.
 
-    relax: 'vanka' or 'bsr'.  levels = number of levels L (level 0 finest).
+    relax: 'vanka', 'bsr' (inexact BSR) or 'bsr_exact' (exact BSR).  levels = number
+    of levels L (level 0 finest).  quadrature: 'rq' (A^RQ, eq. block_form_rq) or 'exact' (A of
+    eq. block_form) on every level.
     alt_order=True builds the same method with every summation order reversed (CSR rows,
     patch DoF order, hence the pivot order of the patch solves): the spread between the two
     runs calibrates the fp64 rounding floor of the parity criterion (SURVEY.md 8(c) c-11,
     DESIGN.md reading A22).  It changes no arithmetic of the method."""
 
     def __init__(self, n, levels, lam, mu, tau, alpha, inv_M, mu_f=1.0, K=1.0, Kinv_field=None,
-                 relax="vanka", alt_order=False):
+                 relax="vanka", alt_order=False, quadrature="rq"):
         if levels < 1 or n % (2 ** (levels - 1)) != 0 or n // (2 ** (levels - 1)) < 2:
             raise ValueError("n must be divisible by 2^(levels-1) with coarsest n >= 2")
         self.levels = levels
@@ -102,7 +104,7 @@ class Hierarchy:
             m = Mesh(n // 2 ** l)
             if l > 0 and Kinv is not None:
                 Kinv = coarsen_Kinv(self.meshes[-1], m, Kinv)
-            op = Operator(m, lam, mu, tau, alpha, inv_M, mu_f, K=K, Kinv_field=Kinv)
+            op = Operator(m, lam, mu, tau, alpha, inv_M, mu_f, K=K, Kinv_field=Kinv, quadrature=quadrature)
             self.meshes.append(m)
             self.ops.append(op)
             if l > 0:
@@ -113,7 +115,7 @@ class Hierarchy:
                 pat = [p[::-1] for p in vertex_patches(self.meshes[l], "full")] if alt_order else None
                 self.smoothers.append(Vanka(self.ops[l], pat))
             else:
-                self.smoothers.append(BSR(self.ops[l], reverse=alt_order))
+                self.smoothers.append(BSR(self.ops[l], reverse=alt_order, exact=relax == "bsr_exact"))
         self.coarse = CoarseSolver(self.ops[-1])
         if alt_order:
             for op in self.ops:
@@ -125,7 +127,7 @@ class Hierarchy:
     def smooth(self, l, x, b, opts):
         if self.relax == "vanka":
             return self.smoothers[l].sweep(x, b, opts["omega"])
-        return self.smoothers[l].sweep(x, b, opts["omega"], opts["omega_J"], opts["jacobi_sweeps"])
+        return self.smoothers[l].sweep(x, b, opts["omega"], opts.get("omega_J", 1.0), opts.get("jacobi_sweeps", 1))
 
     def cycle(self, x, b, opts, l=0):
         """One V(nu1, nu2) cycle on level l."""

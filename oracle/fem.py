@@ -61,6 +61,8 @@ def element_matrices(P, eloc, ekind):
       Mw1  (3, 3)  (psi_e, psi_e')    (multiply by mu_f / K_T)
       Bw   (3,)    -(div psi_e, 1_T)
       Mp   float   |T|
+      Ddiv (9, 9)  (div phi_i, div phi_j), integrated exactly (exact-integration lambda term,
+                   eq. block_form; div of P1 + bubble is linear on T)
     """
     g, area = p1_geometry(P)
     nrm = NORMALS[ekind]
@@ -69,6 +71,7 @@ def element_matrices(P, eloc, ekind):
     s = np.array([1.0 if np.dot(0.5 * (P[eloc[e, 0]] + P[eloc[e, 1]]) - centroid, nrm[e]) > 0 else -1.0
                   for e in range(3)])
     Aeps = np.zeros((9, 9))
+    Ddiv = np.zeros((9, 9))
     Bu = np.zeros(9)
     Mw1 = np.zeros((3, 3))
     Bw = np.zeros(3)
@@ -87,13 +90,15 @@ def element_matrices(P, eloc, ekind):
             G[6 + e] = np.outer(nrm[e], gpsi)
         eps = 0.5 * (G + G.transpose(0, 2, 1))
         Aeps += w * np.einsum("icd,jcd->ij", eps, eps)
-        Bu += -w * np.trace(G, axis1=1, axis2=2)
+        dv = np.trace(G, axis1=1, axis2=2)
+        Ddiv += w * np.outer(dv, dv)
+        Bu += -w * dv
         # RT0 values at x
         psi = np.array([s[e] * elen[e] / (2.0 * area) * (x - P[eloc[e, 2]]) for e in range(3)])
         Mw1 += w * psi @ psi.T
         divpsi = np.array([s[e] * elen[e] / (2.0 * area) * 2.0 for e in range(3)])
         Bw += -w * divpsi
-    return dict(Aeps=Aeps, Bu=Bu, Mw1=Mw1, Bw=Bw, Mp=area, sign=s, elen=elen, grad=g, area=area)
+    return dict(Aeps=Aeps, Ddiv=Ddiv, Bu=Bu, Mw1=Mw1, Bw=Bw, Mp=area, sign=s, elen=elen, grad=g, area=area)
 
 
 class Operator:
@@ -103,9 +108,18 @@ class Operator:
     per-triangle 1/K ([shape, j, i]).  Matrices are assembled on the full slot
     space (10 (n+1)^2) and then restricted to the active DoFs (symmetric
     elimination of the Dirichlet rows and columns).
+
+    quadrature: "rq" (default) -- lambda (P_Q div u, P_Q div v) = lambda B_u^T M_p^{-1} B_u, the
+    reduced-quadrature operator A^RQ of eq. block_form_rq; "exact" -- lambda (div u, div v)
+    integrated exactly, the operator A of eq. block_form, whose solver
+    incompatibility tab:naive shows.  Only A_u differs.
     """
 
-    def __init__(self, mesh: Mesh, lam, mu, tau, alpha, inv_M, mu_f=1.0, K=1.0, Kinv_field=None):
+    def __init__(self, mesh: Mesh, lam, mu, tau, alpha, inv_M, mu_f=1.0, K=1.0, Kinv_field=None,
+                 quadrature="rq"):
+        if quadrature not in ("rq", "exact"):
+            raise ValueError("quadrature must be 'rq' or 'exact'")
+        self.quadrature = quadrature
         self.mesh = mesh
         self.lam, self.mu, self.tau, self.alpha, self.inv_M, self.mu_f = lam, mu, tau, alpha, inv_M, mu_f
         T = mesh.ntri
@@ -116,7 +130,7 @@ class Operator:
         else:
             kinv_t = Kinv_field[mesh.tri_shape, mesh.tri_cj, mesh.tri_ci]
         self.kinv_t = kinv_t
-        rows = {k: [] for k in ("Aeps", "Bu", "Mw", "Bw", "Mp")}
+        rows = {k: [] for k in ("Aeps", "Ddiv", "Bu", "Mw", "Bw", "Mp")}
         cols = {k: [] for k in rows}
         vals = {k: [] for k in rows}
         self.elem = {}
@@ -136,6 +150,9 @@ class Operator:
             rows["Aeps"].append(np.repeat(us, 9, axis=1).ravel())
             cols["Aeps"].append(np.tile(us, (1, 9)).ravel())
             vals["Aeps"].append(np.tile(E["Aeps"].ravel(), nt))
+            rows["Ddiv"].append(np.repeat(us, 9, axis=1).ravel())
+            cols["Ddiv"].append(np.tile(us, (1, 9)).ravel())
+            vals["Ddiv"].append(np.tile(E["Ddiv"].ravel(), nt))
             rows["Bu"].append(np.repeat(ps, 9))
             cols["Bu"].append(us.ravel())
             vals["Bu"].append(np.tile(E["Bu"], nt))
@@ -157,7 +174,10 @@ class Operator:
         mpd = blk["Mp"].diagonal()
         mpinv = np.zeros(N)
         mpinv[mpd > 0] = 1.0 / mpd[mpd > 0]
-        Au = 2.0 * mu * blk["Aeps"] + lam * (blk["Bu"].T @ sp.diags(mpinv) @ blk["Bu"])
+        if quadrature == "rq":
+            Au = 2.0 * mu * blk["Aeps"] + lam * (blk["Bu"].T @ sp.diags(mpinv) @ blk["Bu"])
+        else:
+            Au = 2.0 * mu * blk["Aeps"] + lam * blk["Ddiv"]
         A = (Au + alpha * (blk["Bu"].T + blk["Bu"]) + tau * blk["Mw"] + tau * (blk["Bw"].T + blk["Bw"])
              - inv_M * blk["Mp"])
         act = mesh.act_idx

@@ -196,15 +196,21 @@ class DispVanka:
 
 
 class BSR:
-    """Inexact Braess-Sarazin relaxation."""
+    """Inexact Braess-Sarazin relaxation; exact=True: exact BSR, the Schur
+    complement system S dp = g of eq. bsr_p solved exactly (sparse LU) instead of by n_J Jacobi
+    sweeps -- "the method with exact inversion of this system in eq. bsr_p" (PAPER.md:684-685)."""
 
-    def __init__(self, op: Operator, d: int = 2, reverse: bool = False):
+    def __init__(self, op: Operator, d: int = 2, reverse: bool = False, exact: bool = False):
         self.op = op
+        self.exact = exact
         self.Fu = DispVanka(op, reverse)
         self.Dw = op.Mw.diagonal()                              # D_w = diag(M_w)
         s0 = op.inv_M + op.alpha ** 2 / (op.lam + 2.0 * op.mu / d)
         self.S = (s0 * op.Mp + op.tau * (op.Bw @ sp.diags(1.0 / self.Dw) @ op.Bw.T)).tocsr()
         self.diagS = self.S.diagonal()
+        if exact:
+            import scipy.sparse.linalg as spla
+            self.Slu = spla.splu(self.S.tocsc())
 
     def sweep(self, x, b, omega, omega_J, n_J):
         op = self.op
@@ -215,8 +221,11 @@ class BSR:
         zw = rw / (tau * self.Dw)                               # (tau D_w)^{-1} r_w
         g = alpha * (op.Bu @ zu) + tau * (op.Bw @ zw) - rp      # B F^{-1} r_y - r_p
         dp = np.zeros_like(g)
-        for _ in range(n_J):                                    # weighted Jacobi on S dp = g
-            dp = dp + omega_J * (g - self.S @ dp) / self.diagS
+        if self.exact:                                          # exact BSR: S dp = g (eq. bsr_p)
+            dp = self.Slu.solve(g)
+        else:
+            for _ in range(n_J):                                # weighted Jacobi on S dp = g
+                dp = dp + omega_J * (g - self.S @ dp) / self.diagS
         du = self.Fu.apply(ru - alpha * (op.Bu.T @ dp))         # F dy = r_y - B^T dp
         dw = (rw - tau * (op.Bw.T @ dp)) / (tau * self.Dw)
         xn = x.copy()

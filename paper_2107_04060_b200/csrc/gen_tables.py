@@ -109,7 +109,20 @@ def element(shape, h=1.0):
         psi = np.array([sgn[k] * elen[k] / (2 * area) * (X - P[opp[k]]) for k in range(3)])
         Mw1 += w * psi @ psi.T
     Bw = np.array([-sgn[k] * elen[k] for k in range(3)])
-    return dict(Aeps=Aeps, Bu=Bu, Mw1=Mw1, Bw=Bw, Mp=area, sgn=np.array(sgn), elen=np.array(elen), g=g)
+    # exact-integration lambda term (div u, div v) of eq. block_form: div of a P1
+    # or bubble basis function is linear on the triangle, so it is integrated from its vertex values
+    # with int_T f g = |T|/12 (sum_i f_i g_i + sum_i f_i sum_j g_j) (exact for linear f, g)
+    dv = np.zeros((9, 3))                                # dv[q, v]: div phi_q at vertex v
+    for v in range(3):
+        lam = np.zeros(3); lam[v] = 1.0
+        for a in range(3):
+            dv[2 * a, v] = g[a][0]
+            dv[2 * a + 1, v] = g[a][1]
+        for k, e in enumerate(ed):
+            a, b = e[2], e[3]
+            dv[6 + k, v] = 4.0 * (lam[a] * g[b] + lam[b] * g[a]) @ nrm[k]
+    Ddiv = area / 12.0 * (dv @ dv.T + np.outer(dv.sum(1), dv.sum(1)))
+    return dict(Aeps=Aeps, Bu=Bu, Mw1=Mw1, Bw=Bw, Mp=area, sgn=np.array(sgn), elen=np.array(elen), g=g, Ddiv=Ddiv)
 
 
 # ----------------------------------------------------------------------------- merged stencil
@@ -313,6 +326,16 @@ def emit(path):
         "{" + ", ".join("{" + ", ".join(_f(v) for v in r) + "}" for r in E[s]["Mw1"]) + "}" for s in range(2)) + "};")
     w("static const double REF_BW[2][3] = {" + ", ".join("{" + ", ".join(_f(v) for v in E[s]["Bw"]) + "}" for s in range(2)) + "};")
     w("static const double REF_MP[2] = {" + ", ".join(_f(E[s]["Mp"]) for s in range(2)) + "};")
+    # exact minus reduced quadrature of the lambda term: (div u - P_Q div u, div v - P_Q div v) =
+    # Ddiv - Bu Bu^T / |T|; zero on the P1 rows (their divergence is constant), a 3 x 3 bubble block
+    ex = []
+    for s in range(2):
+        X = E[s]["Ddiv"] - np.outer(E[s]["Bu"], E[s]["Bu"]) / E[s]["Mp"]
+        assert np.abs(X[:6, :]).max() < 1e-13 and np.abs(X[:, :6]).max() < 1e-13
+        ex.append(X[6:, 6:])
+    w("// exact-integration lambda term minus its reduced quadrature on the bubbles (H, V, D), h-independent")
+    w("static const double REF_EXDIV[2][3][3] = {" + ", ".join(
+        "{" + ", ".join("{" + ", ".join(_f(v) for v in r) + "}" for r in ex[s]) + "}" for s in range(2)) + "};")
     w("// local DoF q (0..12) of shape s -> (dx, dy, plane) relative to the cell")
     w("static const int LOCAL_DOF[2][13][3] = {" + ", ".join(
         "{" + ", ".join("{%d,%d,%d}" % t for t in LOCAL[s]) + "}" for s in range(2)) + "};")

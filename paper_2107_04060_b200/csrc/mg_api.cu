@@ -51,6 +51,9 @@ struct Level {
     double* kinv = nullptr;  // 2 planes, heterogeneous K only
     double* jtab = nullptr;  // BSR Jacobi table: 5 planes (tau / D_w per RT0 edge, 1 / diag S per triangle)
     double* gbnd = nullptr;  // 9 x 400
+    double* cgz = nullptr;      // exact BSR (Jacobi-PCG on S): z, p, q, 2 planes each (allocated on first use)
+    double* cgp = nullptr;
+    double* cgq = nullptr;
     double* hv_cls = nullptr;   // heterogeneous Vanka: 9 x MG_HV_CLS class tables
     double* hv_sinv = nullptr;  // heterogeneous Vanka: MG_HV_NSINV planes of per-vertex S_v^{-1}
     double* ubnd = nullptr;  // 9 x 64
@@ -74,6 +77,10 @@ struct mg_ctx {
     int levels = 0;
     Material m{};
     bool het = false;
+    bool exact = false;           // exact-integration operator (mg_grid.quadrature = MG_EXACT)
+    double* cgst = nullptr;       // exact BSR: CG scalars (8 doubles) + partials + counter
+    double* cgpart = nullptr;
+    unsigned* cgcnt = nullptr;
     std::vector<Level> L;
     int Nc = 0;
     double* Ginv = nullptr;
@@ -154,9 +161,13 @@ int check_level(const mg_ctx* c, int level, int maxl) {
 
 NormSink no_norm() { return NormSink{nullptr, nullptr, nullptr, nullptr}; }
 
+// iteration cap of the exact-BSR CG on a level of n cells: Jacobi-PCG on the P0 graph operator S
+// needs O(n) iterations (cond ~ n^2); the device flag ends it earlier at the 1e-14 tolerance
+int cg_iters(int n) { return 24 * n + 64; }
+
 // does the first post-sweep on level l absorb the prolongation (relax_once with e_coarse)?
 bool fused_prolong(const mg_ctx* c, int l, const mg_cycle_opts& o) {
-    return c->fuse_prolong && o.relax == MG_VANKA && o.nu2 >= 1 && c->vanka_impl == 2 && !c->het &&
+    return c->fuse_prolong && o.relax == MG_VANKA && o.nu2 >= 1 && c->vanka_impl == 2 && !c->het && !c->exact &&
            c->L[l].n >= c->march_min_n;
 }
 
@@ -174,17 +185,23 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
             CK(launch_vanka_march2(P, xin, b, xout, false, S, s, &E));
             return MG_OK;
         }
-        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n && !c->het) CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
+        if (c->vanka_impl == 2 && Lv.n >= c->march_min_n && !c->het && !c->exact)
+            CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
         return MG_OK;
     }
-    const double omJ = o.jacobi_sweeps >= 1 ? o.omega_J : 0.0;
-    const bool march = c->bsr_impl == 1 && Lv.n >= c->march_min_n;
+    const bool exact_s = o.relax == MG_BSR_EXACT;
+    const double omJ = (!exact_s && o.jacobi_sweeps >= 1) ? o.omega_J : 0.0;
+    const bool march = c->bsr_impl == 1 && Lv.n >= c->march_min_n && !c->exact;
     if (march) CK(launch_bsr_a_march(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s, Lv.jtab));
     else CK(launch_bsr_a(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s));
     double* cur = Lv.dpa;
     double* nxt = Lv.dpb;
-    for (int k = 1; k < o.jacobi_sweeps;) {
+    if (exact_s) {   // exact BSR: S dp = g by Jacobi-PCG to fp64 accuracy
+        CK(launch_cg_exact(Lv.vp.L, Lv.jtab, Lv.g, Lv.dpa, Lv.cgz, Lv.cgp, Lv.cgq, c->cgpart, c->cgcnt, c->cgst,
+                           cg_iters(Lv.n), s));
+    }
+    for (int k = 1; !exact_s && k < o.jacobi_sweeps;) {
         if (c->jacobi_table) {
             CK(launch_bsr_jacobi_t(Lv.vp.L, o.omega_J, Lv.g, Lv.jtab, cur, nxt, s));
             k += 1;
@@ -196,6 +213,30 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     }
     if (march) CK(launch_bsr_b_march(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
     else CK(launch_bsr_b(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
+    return MG_OK;
+}
+
+// exact BSR work space: z, p, q (2 P0 planes each) per level and the CG scalars
+int ensure_cg(mg_ctx* c) {
+    if (c->cgst) return MG_OK;
+    for (auto& Lv : c->L) {
+        const size_t pb = sizeof(double) * 2 * Lv.plane;
+        Lv.cgz = (double*)dalloc(c, pb);
+        Lv.cgp = (double*)dalloc(c, pb);
+        Lv.cgq = (double*)dalloc(c, pb);
+        if (!Lv.cgz || !Lv.cgp || !Lv.cgq) return fail(MG_ENOMEM, "exact BSR work space");
+        CK(cudaMemset(Lv.cgz, 0, pb));
+        CK(cudaMemset(Lv.cgp, 0, pb));
+        CK(cudaMemset(Lv.cgq, 0, pb));
+    }
+    c->cgpart = (double*)dalloc(c, sizeof(double) * cg_partials_needed(c->L[0].n));
+    c->cgcnt = (unsigned*)dalloc(c, 64);
+    double* st = (double*)dalloc(c, sizeof(double) * 8);
+    if (!c->cgpart || !c->cgcnt || !st) return fail(MG_ENOMEM, "exact BSR work space");
+    CK(cudaMemset(c->cgcnt, 0, 64));
+    const double init[8] = {0, 0, 0, 0, 1e-28, 0, 0, 0};   // [4] = tol^2 (1e-14 in the D^{-1} norm)
+    CK(cudaMemcpy(st, init, sizeof(init), cudaMemcpyHostToDevice));
+    c->cgst = st;
     return MG_OK;
 }
 
@@ -253,7 +294,7 @@ int enqueue_cycle(mg_ctx* c, double* x0, const double* b0, const mg_cycle_opts& 
         if (int rc = lmark()) return rc;
         if (zero && o.nu1 == 0) CK(cudaMemsetAsync(xl, 0, sizeof(double) * Lv.len, s));
         const int mode = (zero && o.nu1 == 0) ? 2 : 1;
-        if (mode == 1 && c->restrict_impl == 1 && Lv.n >= c->march_min_n)
+        if (mode == 1 && c->restrict_impl == 1 && Lv.n >= c->march_min_n && !c->exact)
             CK(launch_restrict_march(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, a, bl, c->L[l + 1].b, s));
         else
             CK(launch_restrict(Lv.vp.L, c->L[l + 1].n, c->L[l + 1].pitch, mode, a, bl, c->L[l + 1].b, s));
@@ -372,12 +413,17 @@ int get_graph(mg_ctx* c, double* x, const double* b, const mg_cycle_opts& o, int
     return MG_OK;
 }
 
-int check_opts(const mg_cycle_opts* o) {
+int check_opts(mg_ctx* c, const mg_cycle_opts* o) {
     if (!o) return fail(MG_EINVAL, "null options");
     if (o->nu1 < 0 || o->nu2 < 0 || o->nu1 + o->nu2 < 0) return fail(MG_EINVAL, "nu1, nu2 must be >= 0");
-    if (o->relax != MG_VANKA && o->relax != MG_BSR) return fail(MG_EINVAL, "relax must be MG_VANKA or MG_BSR");
+    if (o->relax != MG_VANKA && o->relax != MG_BSR && o->relax != MG_BSR_EXACT)
+        return fail(MG_EINVAL, "relax must be MG_VANKA, MG_BSR or MG_BSR_EXACT");
     if (!std::isfinite(o->omega) || !std::isfinite(o->omega_J)) return fail(MG_EINVAL, "omega not finite");
     if (o->relax == MG_BSR && o->jacobi_sweeps < 0) return fail(MG_EINVAL, "jacobi_sweeps < 0");
+    if (o->relax == MG_BSR_EXACT && c->L[0].n > 1024)
+        return fail(MG_EINVAL, "exact BSR (a full S solve per relaxation) is limited to n <= 1024");
+    if (o->relax == MG_BSR_EXACT)
+        if (int rc = ensure_cg(c)) return rc;
     return MG_OK;
 }
 
@@ -417,6 +463,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (!(grid->inv_M > 0) || !std::isfinite(grid->inv_M))
         return fail(MG_EINVAL, "inv_M must be > 0 (the deflated solves need the -(1/M) M_p block)");
     if (!(grid->mu_f > 0)) return fail(MG_EINVAL, "mu_f must be > 0");
+    if (grid->quadrature != MG_RQ && grid->quadrature != MG_EXACT) return fail(MG_EINVAL, "quadrature must be MG_RQ or MG_EXACT");
     if (grid->K_field && !aligned(grid->K_field)) return fail(MG_EINVAL, "K_field not 16-byte aligned");
     const int nc = n >> (levels - 1);
     // the dense coarsest solve needs n_c <= 20; a context with a larger coarsest level offers the
@@ -430,6 +477,8 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     c->levels = levels;
     c->het = grid->K_field != nullptr;
     c->m = Material{lambda, mu, grid->K_field ? 1.0 : K, tau, alpha, grid->inv_M, grid->mu_f};
+    c->exact = grid->quadrature == MG_EXACT;
+    c->m.exact = c->exact ? 1 : 0;
     c->L.resize(levels);
     set_carveout(getenv("MG_CARVEOUT") ? atoi(getenv("MG_CARVEOUT")) : 100);
     kernels_init();
@@ -441,6 +490,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     // process-wide kernel knobs: every setup re-reads them (unset -> default), so they never stick
     set_small_tile_n(getenv("MG_SMALL_TILE_N") ? atoi(getenv("MG_SMALL_TILE_N")) : 128);
     set_pdl(getenv("MG_PDL") ? atoi(getenv("MG_PDL")) != 0 : 0);
+    set_prol_ws(getenv("MG_PROL_WS") ? atoi(getenv("MG_PROL_WS")) : 0);
     set_resid_march_n(getenv("MG_RESID_MARCH_N") ? atoi(getenv("MG_RESID_MARCH_N")) : 512);
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
@@ -665,6 +715,24 @@ int mg_relax_bsr(mg_ctx* c, int32_t level, double* x, const double* b, double om
     return MG_OK;
 }
 
+int mg_relax_bsr_exact(mg_ctx* c, int32_t level, double* x, const double* b, double omega, int32_t sweeps,
+                       cudaStream_t s) {
+    if (int rc = check_level(c, level, c ? c->levels - 1 : 0)) return rc;
+    if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    if (sweeps < 0) return fail(MG_EINVAL, "sweeps < 0");
+    mg_cycle_opts o{1, 1, MG_BSR_EXACT, omega, 0.0, 0};
+    if (int rc = check_opts(c, &o)) return rc;
+    Level& Lv = c->L[level];
+    double* a = x;
+    double* t = Lv.t;
+    for (int k = 0; k < sweeps; ++k) {
+        if (int rc = relax_once(c, level, a, b, t, false, o, no_norm(), s)) return rc;
+        std::swap(a, t);
+    }
+    if (a != x) CK(cudaMemcpyAsync(x, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+    return MG_OK;
+}
+
 int mg_restrict(mg_ctx* c, int32_t fl, const double* r, double* bc, cudaStream_t s) {
     if (int rc = check_level(c, fl, c ? c->levels - 2 : 0)) return rc;
     if (!aligned(r) || !aligned(bc)) return fail(MG_EINVAL, "null or misaligned pointer");
@@ -690,7 +758,7 @@ int mg_coarse_solve(mg_ctx* c, const double* b, double* x, cudaStream_t s) {
 
 int mg_cycle(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double* res_norm_host, cudaStream_t s) {
     if (!c) return fail(MG_EINVAL, "null context");
-    if (int rc = check_opts(o)) return rc;
+    if (int rc = check_opts(c, o)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (!c->Ginv) return fail(MG_EINVAL, "no dense coarsest solve on this context (n_c > 20)");
     if (c->levels == 1) {
@@ -713,7 +781,7 @@ int mg_cycle(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, doub
 int mg_cycle_async(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double* in_norm2_dev,
                    cudaStream_t s) {
     if (!c) return fail(MG_EINVAL, "null context");
-    if (int rc = check_opts(o)) return rc;
+    if (int rc = check_opts(c, o)) return rc;
     if (!aligned(x) || !aligned(b) || (in_norm2_dev && !aligned(in_norm2_dev)))
         return fail(MG_EINVAL, "null or misaligned pointer");
     if (!c->Ginv || c->levels < 2) return fail(MG_EINVAL, "mg_cycle_async needs levels >= 2 and a coarsest solve");
@@ -759,7 +827,7 @@ int mg_timing_levels(mg_ctx* c, float* ms, int32_t cap) {
 int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_iters,
               int32_t restart, double* history_host, int32_t* n_iters, cudaStream_t s) {
     if (!c) return fail(MG_EINVAL, "null context");
-    if (int rc = check_opts(o)) return rc;
+    if (int rc = check_opts(c, o)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (max_iters < 0 || restart < 1 || restart > 31)
         return fail(MG_EINVAL, "need max_iters >= 0, 1 <= restart <= 31");
@@ -928,7 +996,7 @@ int mg_time_step(mg_ctx* c, double* x, const double* b_load, const mg_cycle_opts
 int mg_solve(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, double rtol, int32_t max_cycles,
              double* history_host, int32_t* n_cycles, cudaStream_t s) {
     if (!c) return fail(MG_EINVAL, "null context");
-    if (int rc = check_opts(o)) return rc;
+    if (int rc = check_opts(c, o)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (max_cycles < 0) return fail(MG_EINVAL, "max_cycles < 0");
     if (c->levels == 1) return fail(MG_EINVAL, "mg_solve needs levels >= 2");

@@ -36,6 +36,8 @@ struct LevelParams {
     double bu[2][9];             // h (B_u1)_{shape,q}
     double mw1d[2][3];           // mu_f h^2 (M_w1)_{shape,e,e}   (diagonal, times K^{-1}_T)
     const int* stop;             // device flag of mg_solve: every kernel returns at entry if *stop != 0
+    double lamx;                 // exact-integration operator (eq. block_form): lambda, else 0;
+                                 // the residual adds lamx * REF_EXDIV on the bubbles of every triangle
 };
 
 // Device state of mg_solve, updated by the block that finishes a fused residual norm:
@@ -114,6 +116,7 @@ struct HostLevelTables {
 
 struct Material {
     double lambda, mu, K, tau, alpha, inv_M, mu_f;
+    int exact = 0;                // 1: exact-integration lambda term (eq. block_form), 0: A^RQ
 };
 
 // mg_setup.cpp

@@ -196,6 +196,20 @@ __device__ __forceinline__ void apply_rows_kr(const LevelParams& L, const double
     av[5] = a5; av[6] = a6; av[7] = a7; av[8] = a8; av[9] = a9;
 }
 
+// exact-integration operator (L.lamx = lambda != 0): the bubble rows add lambda * REF_EXDIV over the
+// two triangles of each edge -- H(i,j): LL(i,j), UR(i,j-1); V(i,j): LL(i,j), UR(i-1,j); D(i,j): LL(i,j),
+// UR(i,j) -- whose bubbles are LL(i,j): H(i,j), V(i,j), D(i,j) and UR(i,j): H(i,j+1), V(i+1,j), D(i,j)
+__device__ __forceinline__ void exact_bubble_add(double lx, const double* xm, const double* x0, const double* xp,
+                                                 int PS, double av[10]) {
+#define XB(dx, dy, pl) ((dy) < 0 ? xm : ((dy) > 0 ? xp : x0))[(pl) * PS + (dx)]
+    // REF_EXDIV is the same for both shapes in the local (H, V, D) order
+    constexpr double EHH = 4.0 / 9.0, EHV = -2.0 / 9.0, EHD = -0.15713484026367724, EDD = 2.0 / 9.0;
+    av[2] = fma(lx, 2.0 * EHH * XB(0, 0, 2) + EHV * (XB(0, 0, 3) + XB(1, -1, 3)) + EHD * (XB(0, 0, 4) + XB(0, -1, 4)), av[2]);
+    av[3] = fma(lx, 2.0 * EHH * XB(0, 0, 3) + EHV * (XB(0, 0, 2) + XB(-1, 1, 2)) + EHD * (XB(0, 0, 4) + XB(-1, 0, 4)), av[3]);
+    av[4] = fma(lx, 2.0 * EDD * XB(0, 0, 4) + EHD * (XB(0, 0, 2) + XB(0, 1, 2)) + EHD * (XB(0, 0, 3) + XB(1, 0, 3)), av[4]);
+#undef XB
+}
+
 // r = b - A x for the 10 DoFs of index (i, j); xs is a W x HT x 10 tile holding (i, j) at
 // (lx, ly) with a ring of at least 1.  Inactive rows give 0.
 template <int W, int HT, bool HET, bool NC = true>
@@ -204,6 +218,7 @@ __device__ __forceinline__ void residual_at(const LevelParams& L, const double* 
     const double* x0 = xs + ly * W + lx;
     double av[10];
     apply_rows<W * HT, HET>(L, x0 - W, x0, x0 + W, i, j, av);
+    if (L.lamx != 0.0) exact_bubble_add(L.lamx, x0 - W, x0, x0 + W, W * HT, av);
     const int n = L.n;
     const int64_t o = (int64_t)j * L.pitch + i;
     const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
@@ -236,6 +251,7 @@ __global__ void __launch_bounds__(RNT) residual_kernel(const LevelParams L, cons
             // out = A x (masked): the operator application of FGMRES (b unused)
             const double* x0 = xs + (ly + 1) * XW + (lx + 1);
             apply_rows<XW * XH, HET>(L, x0 - XW, x0, x0 + XW, i, j, rv);
+            if (L.lamx != 0.0) exact_bubble_add(L.lamx, x0 - XW, x0, x0 + XW, XW * XH, rv);
 #pragma unroll
             for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, j, L.n) ? rv[k] : 0.0;
         } else {
@@ -1438,8 +1454,21 @@ __host__ __device__ constexpr int pslot20(int dI, int dJ, int pl) { return pl >=
 // after its TMA box lands, with the same arithmetic as prolong_kernel (v = sum of w e_H in table
 // order, x + v), so the result is bitwise that of prolong_kernel followed by the sweep, and x + P e_H
 // never goes through HBM.
-template <bool XZERO, bool PROL>
-__global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march2_kernel(const __grid_constant__ CUtensorMap tmx,
+// PV (prolongation variant): 0 plain sweep; 1 fused prolongation by M2NP = 2 producer warps (each
+// thread all 10 planes of one column pair of two rows); 2 fused prolongation by 4 producer warps
+// (a warp-uniform half of the planes each) with warp-specialised register counts: the producer
+// warpgroup drops to M2WS_PREG registers (setmaxnreg.dec) and the compute warpgroup takes them
+// (setmaxnreg.inc to M2WS_CREG) -- the 6-warp variant runs every warp at the 96 registers 18 warps
+// per SM allow, against 166 in the plain sweep.
+#ifndef M2WS_PREG
+#define M2WS_PREG 40
+#endif
+#ifndef M2WS_CREG
+#define M2WS_CREG 120
+#endif
+__host__ __device__ constexpr int m2np(int pv) { return pv == 2 ? 4 : (pv == 1 ? M2NP : 0); }
+template <bool XZERO, int PV>
+__global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                const __grid_constant__ CUtensorMap tmb,
                                                                const VankaParams P, double* __restrict__ xo,
                                                                NormSink S, int MH, const ProlSrc E) {
@@ -1451,6 +1480,8 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
     double* cr = br + M2BR * M2ROW;         // [M2CR][20][M2C]   patch corrections
     uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M2CR * 20 * M2C);
     const LevelParams& L = P.L;
+    constexpr bool PROL = PV != 0;
+    constexpr int NPW = m2np(PV);            // producer warps
     if (*L.stop) return;
     // barrier of the four compute warps (the PROL producer warp never joins it)
     auto csync = [&]() {
@@ -1483,8 +1514,8 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
     if (t == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], M2NP);
-        mbar_init(&bars[3], M2NP);
+        mbar_init(&bars[2], NPW);
+        mbar_init(&bars[3], NPW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -1497,7 +1528,7 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
     // column pair (2I, 2I+1); pe[k][] holds the 20 coarse values of the task (pslot20)
     auto prol_task = [&](int y0, int count, int k, int& y, int& I, int& J) {
         const int lane = t & 31;
-        const int rsel = k + 2 * (lane >> 4);
+        const int rsel = (PV == 2 ? (k >> 1) : k) + 2 * (lane >> 4);
         y = y0 + rsel;
         I = (i0 >> 1) - 1 + (lane & 15);
         J = y >> 1;
@@ -1512,9 +1543,13 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
             if (!prol_task(y0, count, k, y, I, J)) return;
             const double* e0 = E.e + (int64_t)J * E.pitchc + I;
 #define PL(dI, dJ, pl) pe[pslot20(dI, dJ, pl)] = __ldg(e0 + (pl) * E.planec + (dJ) * E.pitchc + (dI));
-            PL(0, 0, 0) PL(0, 0, 1) PL(0, 0, 2) PL(0, 0, 3) PL(0, 0, 4) PL(0, 1, 0) PL(0, 1, 1)
-            PL(0, 1, 2) PL(1, 0, 0) PL(1, 0, 1) PL(1, 0, 3) PL(1, 1, 0) PL(1, 1, 1)
-            PL(0, 0, 5) PL(0, 0, 6) PL(0, 0, 7) PL(0, 0, 8) PL(0, 0, 9) PL(0, 1, 5) PL(1, 0, 6)
+            if (PV != 2 || (k & 1) == 0) {
+                PL(0, 0, 0) PL(0, 0, 1) PL(0, 0, 2) PL(0, 0, 3) PL(0, 0, 4) PL(0, 1, 0) PL(0, 1, 1)
+                PL(0, 1, 2) PL(1, 0, 0) PL(1, 0, 1) PL(1, 0, 3) PL(1, 1, 0) PL(1, 1, 1)
+            }
+            if (PV != 2 || (k & 1) == 1) {
+                PL(0, 0, 5) PL(0, 0, 6) PL(0, 0, 7) PL(0, 0, 8) PL(0, 0, 9) PL(0, 1, 5) PL(1, 0, 6)
+            }
 #undef PL
         }
     };
@@ -1541,8 +1576,18 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
         if (m1 & (1u << (kf))) xv.y += v;                                             \
         *x2 = xv;                                                                     \
     }
-            if (y & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
-            else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+            if (PV == 2) {   // warp-uniform plane half
+                if ((k & 1) == 0) {
+                    if (y & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) }
+                    else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) }
+                } else {
+                    if (y & 1) { PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
+                    else { PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+                }
+            } else {
+                if (y & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
+                else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+            }
 #undef PX
 #undef PQ
         }
@@ -1551,6 +1596,7 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
     if (PROL && t >= M2NT) {
         // ---- producer warp: the coarse values of a group are loaded before its TMA boxes are
         // awaited, so their latency overlaps the wait
+        if (PV == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(M2WS_PREG));
         double pe[20];
         auto publish = [&](int g) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // ring slots are refilled by TMA later
@@ -1571,9 +1617,10 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
             prol_apply(j0 + g * M2R + 2, M2R, pe);
             publish(g);
         }
-        if (S.out || S.state) norm_finish<M2NT + 32 * M2NP>(S, 0.0);
+        if (S.out || S.state) norm_finish<M2NT + 32 * NPW>(S, 0.0);
         return;
     }
+    if (PV == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(M2WS_CREG));
     if (t == 0) {
         issue(-1);
         issue(0);
@@ -1685,7 +1732,7 @@ __global__ void __launch_bounds__(PROL ? M2NT + 32 * M2NP : M2NT, 3) vanka_march
             }
         }
     }
-    if (S.out || S.state) norm_finish<PROL ? M2NT + 32 * M2NP : M2NT>(S, nrm);
+    if (S.out || S.state) norm_finish<M2NT + 32 * NPW>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2314,6 +2361,8 @@ static EncodeTiledFn g_encode = nullptr;
 
 static int g_resid_march_n = 512;   // residual / apply on levels with n >= this: marching kernel (MG_RESID_MARCH_N)
 void set_resid_march_n(int n) { g_resid_march_n = n; }
+static int g_prol_ws = 0;   // fused-prolongation sweep: 1 warp-specialised (4 producer warps, setmaxnreg; measured: ptxas keeps the 80-register launch cap), 0 the 6-warp kernel (default)
+void set_prol_ws(int on) { g_prol_ws = on; }
 static int g_pdl = 0;   // programmatic dependent launch (MG_PDL=1; measured no gain on the cycle graph)
 void set_pdl(int on) { g_pdl = on; }
 
@@ -2364,9 +2413,10 @@ void kernels_init() {
         cudaMemcpyToSymbol(c_local_dof, ld, sizeof(ld));
     }
     set_smem(bottom_kernel, BOT_SMEM);
-    set_smem(vanka_march2_kernel<false, false>, M2SMEM);
-    set_smem(vanka_march2_kernel<true, false>, M2SMEM);
-    set_smem(vanka_march2_kernel<false, true>, M2SMEM);
+    set_smem(vanka_march2_kernel<false, 0>, M2SMEM);
+    set_smem(vanka_march2_kernel<true, 0>, M2SMEM);
+    set_smem(vanka_march2_kernel<false, 1>, M2SMEM);
+    set_smem(vanka_march2_kernel<false, 2>, M2SMEM);
     set_smem(bsr_a_march_kernel<false, false>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<false, true>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<true, false>, BMA_SMEM);
@@ -2436,7 +2486,7 @@ int blocks_residual_march(int n) {
 
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
                             cudaStream_t s) {
-    if (!L.kinv_field && L.n >= g_resid_march_n) return launch_residual_march(r ? 0 : 2, L, x, b, r, S, s);
+    if (!L.kinv_field && L.lamx == 0.0 && L.n >= g_resid_march_n) return launch_residual_march(r ? 0 : 2, L, x, b, r, S, s);
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
     if (L.kinv_field) launch_k(residual_kernel<true, false>, grid, RNT, 0, s, L, x, b, r, S);
     else launch_k(residual_kernel<false, false>, grid, RNT, 0, s, L, x, b, r, S);
@@ -2444,7 +2494,7 @@ cudaError_t launch_residual(const LevelParams& L, const double* x, const double*
 }
 
 cudaError_t launch_apply(const LevelParams& L, const double* x, double* y, NormSink S, cudaStream_t s) {
-    if (!L.kinv_field && L.n >= g_resid_march_n) return launch_residual_march(1, L, x, nullptr, y, S, s);
+    if (!L.kinv_field && L.lamx == 0.0 && L.n >= g_resid_march_n) return launch_residual_march(1, L, x, nullptr, y, S, s);
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
     if (L.kinv_field) launch_k(residual_kernel<true, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
     else launch_k(residual_kernel<false, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
@@ -2710,6 +2760,149 @@ cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cud
     launch_k(vec_scale_kernel, 2 * DOT_BLOCKS, DOT_NT, 0, s, y, x, sc, len);
     return cudaGetLastError();
 }
+// ------------------------------------------------------------------------------------------
+// Exact BSR: S dp = g solved by Jacobi-preconditioned conjugate gradients on the
+// two P0 planes, S = s0 M_p + tau B_w D_w^{-1} B_w^T applied from the per-level Jacobi table (tau / D_w
+// per RT0 edge, 1 / diag S per triangle).  Two kernels per iteration with every scalar on the device
+// (graph-capturable; each kernel returns at entry once the iteration has converged):
+//   cg_a: p = z + beta p, q = S z + beta q (= S p), partial sums of p.q -> alpha = rz / pq
+//   cg_b: dp += alpha p, r -= alpha q, z = r / diag S, partial sums of r.z -> beta, convergence
+// CgState: [0] rz, [1] alpha, [2] beta, [3] rz0, [4] tol^2, [5] converged flag (as double), [6] its
+constexpr int CG_NT = 256;
+__device__ __forceinline__ double s_offdiag(const LevelParams& L, const double* __restrict__ tab,
+                                            const double* __restrict__ v, int sh, int i, int j) {
+    const int64_t plane = L.plane, pitch = L.pitch, o = (int64_t)j * pitch + i;
+    const double te[3] = {sh == 0 ? __ldg(tab + o) : __ldg(tab + o + pitch),
+                          sh == 0 ? __ldg(tab + plane + o) : __ldg(tab + plane + o + 1), __ldg(tab + 2 * plane + o)};
+    double off = 0.0;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        int ni, nj;
+        if (sh == 0) { ni = e == 1 ? i - 1 : i; nj = e == 0 ? j - 1 : j; }
+        else         { ni = e == 1 ? i + 1 : i; nj = e == 0 ? j + 1 : j; }
+        if (te[e] != 0.0) off = fma(te[e] * L.bw[sh][e] * L.bw[1 - sh][e], __ldg(v + (1 - sh) * plane + (int64_t)nj * pitch + ni), off);
+    }
+    return off;
+}
+
+// deterministic block sum + last-block finish (partials / counter private to the CG)
+template <int MODE>
+__device__ void cg_finish(double v, double* partials, unsigned* counter, double* st) {
+    const int nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+    const double t = block_sum<CG_NT>(v);
+    __shared__ unsigned last;
+    if (threadIdx.x == 0) {
+        partials[bid] = t;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == (unsigned)nb - 1u;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < nb; k += CG_NT) acc += __ldcg(partials + k);
+    const double tot = block_sum<CG_NT>(acc);
+    if (threadIdx.x == 0) {
+        if (MODE == 0) {          // tot = p.q
+            st[1] = tot > 0.0 ? st[0] / tot : 0.0;
+        } else if (MODE == 1) {   // tot = r.z (new)
+            st[2] = st[0] > 0.0 ? tot / st[0] : 0.0;
+            st[0] = tot;
+            st[6] += 1.0;
+            if (!(tot > st[4] * st[3])) st[5] = 1.0;
+        } else {                  // MODE 2: initial r.z
+            st[0] = tot;
+            st[3] = tot;
+            st[2] = 0.0;
+            st[6] = 0.0;
+            st[5] = tot > 0.0 ? 0.0 : 1.0;
+        }
+        *counter = 0u;
+    }
+}
+
+// init: r = g (in place), z = r / diag S, dp = 0, p = q = 0, rz = r.z
+__global__ void __launch_bounds__(CG_NT) cg_init_kernel(const LevelParams L, const double* __restrict__ tab, double* r,
+                                                        double* z, double* dp, double* p, double* q, double* partials,
+                                                        unsigned* counter, double* st) {
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    double v = 0.0;
+    if (i <= L.n && j <= L.n && !*L.stop) {
+        const int64_t o = (int64_t)j * L.pitch + i;
+#pragma unroll
+        for (int sh = 0; sh < 2; ++sh) {
+            const int64_t k = sh * L.plane + o;
+            const double zz = r[k] * __ldg(tab + (3 + sh) * L.plane + o);
+            z[k] = zz;
+            dp[k] = 0.0;
+            p[k] = 0.0;
+            q[k] = 0.0;
+            v = fma(r[k], zz, v);
+        }
+    }
+    cg_finish<2>(v, partials, counter, st);
+}
+
+__global__ void __launch_bounds__(CG_NT) cg_a_kernel(const LevelParams L, const double* __restrict__ tab,
+                                                     const double* __restrict__ z, double* p, double* q,
+                                                     double* partials, unsigned* counter, double* st) {
+    if (st[5] != 0.0 || *L.stop) return;
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const double beta = st[2];
+    double v = 0.0;
+    if (i < L.n && j < L.n) {
+        const int64_t o = (int64_t)j * L.pitch + i;
+#pragma unroll
+        for (int sh = 0; sh < 2; ++sh) {
+            const int64_t k = sh * L.plane + o;
+            const double zk = z[k];
+            const double sz = fma(zk, 1.0 / __ldg(tab + (3 + sh) * L.plane + o), s_offdiag(L, tab, z, sh, i, j));
+            const double pk = fma(beta, p[k], zk), qk = fma(beta, q[k], sz);
+            p[k] = pk;
+            q[k] = qk;
+            v = fma(pk, qk, v);
+        }
+    }
+    cg_finish<0>(v, partials, counter, st);
+}
+
+__global__ void __launch_bounds__(CG_NT) cg_b_kernel(const LevelParams L, const double* __restrict__ tab,
+                                                     const double* __restrict__ p, const double* __restrict__ q,
+                                                     double* r, double* z, double* dp, double* partials,
+                                                     unsigned* counter, double* st) {
+    if (st[5] != 0.0 || *L.stop) return;
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const double alpha = st[1];
+    double v = 0.0;
+    if (i < L.n && j < L.n) {
+        const int64_t o = (int64_t)j * L.pitch + i;
+#pragma unroll
+        for (int sh = 0; sh < 2; ++sh) {
+            const int64_t k = sh * L.plane + o;
+            dp[k] = fma(alpha, p[k], dp[k]);
+            const double rk = fma(-alpha, q[k], r[k]);
+            r[k] = rk;
+            const double zk = rk * __ldg(tab + (3 + sh) * L.plane + o);
+            z[k] = zk;
+            v = fma(rk, zk, v);
+        }
+    }
+    cg_finish<1>(v, partials, counter, st);
+}
+
+cudaError_t launch_cg_exact(const LevelParams& L, const double* tab, double* g, double* dp, double* z, double* p,
+                            double* q, double* partials, unsigned* counter, double* st, int max_iters,
+                            cudaStream_t s) {
+    dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
+    cg_init_kernel<<<grid, CG_NT, 0, s>>>(L, tab, g, z, dp, p, q, partials, counter, st);
+    for (int it = 0; it < max_iters; ++it) {
+        cg_a_kernel<<<grid, CG_NT, 0, s>>>(L, tab, z, p, q, partials, counter, st);
+        cg_b_kernel<<<grid, CG_NT, 0, s>>>(L, tab, p, q, g, z, dp, partials, counter, st);
+    }
+    return cudaGetLastError();
+}
+int cg_partials_needed(int n) { return ((n + 32) / 32) * ((n + 8) / 8); }
+
 // Backward-Euler history term (eq. discrete3 scaled by -1): the pressure rows of
 // b^m get -(1/M) M_p p^{m-1} + alpha B_u u^{m-1}, B_u u = -(div u, 1_T) of the 9 displacement DoFs
 // of triangle T (L.bu = h REF_BU in LOCAL_DOF order), M_p = h^2/2.  One thread per cell.
@@ -2797,9 +2990,11 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
-    if (x_zero) launch_k(vanka_march2_kernel<true, false>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
-    else if (E) launch_k(vanka_march2_kernel<false, true>, grid, M2NT + 32 * M2NP, M2SMEM, s, mx, mb, P, xo, S, MH, *E);
-    else launch_k(vanka_march2_kernel<false, false>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
+    if (x_zero) launch_k(vanka_march2_kernel<true, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
+    else if (E && g_prol_ws)
+        launch_k(vanka_march2_kernel<false, 2>, grid, M2NT + 32 * m2np(2), M2SMEM, s, mx, mb, P, xo, S, MH, *E);
+    else if (E) launch_k(vanka_march2_kernel<false, 1>, grid, M2NT + 32 * M2NP, M2SMEM, s, mx, mb, P, xo, S, MH, *E);
+    else launch_k(vanka_march2_kernel<false, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
     return cudaGetLastError();
 }
 int blocks_vanka_march2(int n) {

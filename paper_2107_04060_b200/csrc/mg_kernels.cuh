@@ -64,6 +64,13 @@ cudaError_t launch_scale(double* y, const double* x, double sc, int64_t len, cud
 // dst = src (len doubles), skipped when *stop != 0 (mg_solve's flag)
 cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* stop, cudaStream_t s);
 int dot_partials_needed();
+// exact BSR: S dp = g by Jacobi-PCG on the P0 planes (g is overwritten by the residual), up to
+// max_iters iterations, stopping (device-side flag) at r.z <= st[4] r0.z0; st: 8 device doubles
+// (st[4] = tol^2 set by the caller, st[6] = iterations done)
+cudaError_t launch_cg_exact(const LevelParams& L, const double* tab, double* g, double* dp, double* z, double* p,
+                            double* q, double* partials, unsigned* counter, double* st, int max_iters,
+                            cudaStream_t s);
+int cg_partials_needed(int n);
 // backward-Euler history term added to the pressure rows of b (x = the previous step's iterate)
 cudaError_t launch_step_rhs(const LevelParams& L, double inv_M, double alpha, const double* x, double* b,
                             cudaStream_t s);
@@ -83,6 +90,8 @@ int blocks_residual_march(int n);
 void set_small_tile_n(int N);
 // programmatic dependent launch of every kernel (1, default) or plain stream order (0)
 void set_pdl(int on);
+// fused-prolongation sweep variant: 1 warp-specialised with setmaxnreg (default), 0 the 6-warp kernel
+void set_prol_ws(int on);
 // residual / operator application on levels with n >= N through the marching kernel (scalar K)
 void set_resid_march_n(int N);
 // per-level Jacobi table (tau / D_w per RT0 edge, 1 / diag S per triangle; 5 planes) and the sweep using it

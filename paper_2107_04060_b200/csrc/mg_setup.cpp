@@ -25,7 +25,13 @@ int blk(int q) { return q < 9 ? 0 : (q < 12 ? 1 : 2); }   // 0 = u, 1 = w, 2 = p
 // Entry (q, q2) of the element matrix of A^RQ on a triangle of shape s at mesh size h.
 double elem_entry(int s, int q, int q2, const Material& m, double h, double kinv) {
     int a = blk(q), b = blk(q2);
-    if (a == 0 && b == 0) return 2.0 * m.mu * REF_AEPS[s][q][q2] + 2.0 * m.lambda * REF_BU[s][q] * REF_BU[s][q2];
+    if (a == 0 && b == 0) {
+        double v = 2.0 * m.mu * REF_AEPS[s][q][q2] + 2.0 * m.lambda * REF_BU[s][q] * REF_BU[s][q2];
+        // exact integration of lambda (div u, div v) (eq. block_form) = the reduced quadrature plus the
+        // bubble block REF_EXDIV (h-independent)
+        if (m.exact && q >= 6 && q2 >= 6) v += m.lambda * REF_EXDIV[s][q - 6][q2 - 6];
+        return v;
+    }
     if (a == 0 && b == 2) return m.alpha * h * REF_BU[s][q];
     if (a == 2 && b == 0) return m.alpha * h * REF_BU[s][q2];
     if (a == 1 && b == 1) return m.tau * m.mu_f * kinv * h * h * REF_MW1[s][q - 9][q2 - 9];
@@ -464,7 +470,12 @@ int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, i
     LevelParams& L = t->L;
     L.n = n;
     double kinv = 1.0 / m.K;
-#define Y(ci, s, q, q2) L.coef[ci] += elem_entry(s, q, q2, m, h, kinv);
+    // the merged / factored stencil is the reduced-quadrature one; an exact-integration level adds
+    // its bubble term separately in the residual (L.lamx)
+    Material m_rq = m;
+    m_rq.exact = 0;
+    L.lamx = m.exact ? m.lambda : 0.0;
+#define Y(ci, s, q, q2) L.coef[ci] += elem_entry(s, q, q2, m_rq, h, kinv);
     MG_STENCIL_CONTRIB(Y)
 #undef Y
     static_assert(MG_STENCIL_NGROUP == MG_NGROUP, "factored stencil size");

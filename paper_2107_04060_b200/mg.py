@@ -18,7 +18,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmg.so")
 
 MG_OK, MG_NOTCONV, MG_DIVERGED = 0, 1, 2
-MG_VANKA, MG_BSR = 0, 1
+MG_VANKA, MG_BSR, MG_BSR_EXACT = 0, 1, 2
+MG_RQ, MG_EXACT = 0, 1
+_RELAX = {"vanka": MG_VANKA, "bsr": MG_BSR, "bsr_exact": MG_BSR_EXACT}
 
 _lib = None
 _alloc_cbs = None
@@ -32,7 +34,8 @@ class MGError(RuntimeError):
 
 
 class Grid(ctypes.Structure):
-    _fields_ = [("n", ctypes.c_int32), ("K_field", _VP), ("inv_M", ctypes.c_double), ("mu_f", ctypes.c_double)]
+    _fields_ = [("n", ctypes.c_int32), ("K_field", _VP), ("inv_M", ctypes.c_double), ("mu_f", ctypes.c_double),
+                ("quadrature", ctypes.c_int32)]
 
 
 class CycleOpts(ctypes.Structure):
@@ -55,6 +58,7 @@ SIGNATURES = {
     "mg_relax_vanka": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_int32, _VP]),
     "mg_relax_bsr": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_int32, ctypes.c_int32, _VP]),
+    "mg_relax_bsr_exact": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_int32, _VP]),
     "mg_restrict": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP]),
     "mg_prolong": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP]),
     "mg_coarse_solve": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
@@ -156,13 +160,13 @@ class Opts:
     """V(nu1, nu2) cycle options (mg_cycle_opts)."""
     nu1: int = 1
     nu2: int = 1
-    relax: str = "vanka"        # "vanka" | "bsr"
+    relax: str = "vanka"        # "vanka" | "bsr" | "bsr_exact"
     omega: float = 0.74
     omega_J: float = 1.0
     jacobi_sweeps: int = 3
 
     def c(self) -> CycleOpts:
-        return CycleOpts(self.nu1, self.nu2, MG_VANKA if self.relax == "vanka" else MG_BSR,
+        return CycleOpts(self.nu1, self.nu2, _RELAX[self.relax],
                          float(self.omega), float(self.omega_J), int(self.jacobi_sweeps))
 
 
@@ -170,7 +174,7 @@ class Hierarchy:
     """An mg_ctx: the level hierarchy of one problem (mg_setup / mg_free)."""
 
     def __init__(self, n: int, levels: int, lam: float, mu: float, K: float = 1.0, tau: float = 1.0,
-                 alpha: float = 1.0, inv_M: float = 1.0, mu_f: float = 1.0, K_field=None):
+                 alpha: float = 1.0, inv_M: float = 1.0, mu_f: float = 1.0, K_field=None, quadrature: str = "rq"):
         import torch
         if not torch.cuda.is_available():
             raise MGError("no CUDA device: the multigrid path runs only on the GPU")
@@ -182,7 +186,7 @@ class Hierarchy:
             self._kf = torch.as_tensor(K_field, dtype=torch.float64, device="cuda").contiguous()
             assert self._kf.shape == (2, n, n)
             kf = self._kf.data_ptr()
-        grid = Grid(int(n), kf, float(inv_M), float(mu_f))
+        grid = Grid(int(n), kf, float(inv_M), float(mu_f), {"rq": MG_RQ, "exact": MG_EXACT}[quadrature])
         ctx = _VP()
         _check(self.lib.mg_setup(ctypes.byref(grid), float(lam), float(mu), float(K), float(tau), float(alpha),
                                  int(levels), ctypes.byref(ctx)), "mg_setup")
@@ -248,6 +252,10 @@ class Hierarchy:
     def relax_bsr(self, level, x, b, omega, omega_J, jacobi_sweeps, sweeps=1, stream=None):
         _check(self.lib.mg_relax_bsr(self.ctx, level, self._v(x, level), self._v(b, level), float(omega), float(omega_J),
                                      int(jacobi_sweeps), int(sweeps), _stream(stream)), "mg_relax_bsr")
+
+    def relax_bsr_exact(self, level, x, b, omega, sweeps=1, stream=None):
+        _check(self.lib.mg_relax_bsr_exact(self.ctx, level, self._v(x, level), self._v(b, level), float(omega),
+                                           int(sweeps), _stream(stream)), "mg_relax_bsr_exact")
 
     def restrict(self, fine_level, r, bc, stream=None):
         _check(self.lib.mg_restrict(self.ctx, fine_level, self._v(r, fine_level), self._v(bc, fine_level + 1), _stream(stream)), "mg_restrict")
