@@ -150,9 +150,10 @@ class Operator:
             rows["Aeps"].append(np.repeat(us, 9, axis=1).ravel())
             cols["Aeps"].append(np.tile(us, (1, 9)).ravel())
             vals["Aeps"].append(np.tile(E["Aeps"].ravel(), nt))
-            rows["Ddiv"].append(np.repeat(us, 9, axis=1).ravel())
-            cols["Ddiv"].append(np.tile(us, (1, 9)).ravel())
-            vals["Ddiv"].append(np.tile(E["Ddiv"].ravel(), nt))
+            if quadrature == "exact":   # assembled only for the exact-integration operator (memory)
+                rows["Ddiv"].append(np.repeat(us, 9, axis=1).ravel())
+                cols["Ddiv"].append(np.tile(us, (1, 9)).ravel())
+                vals["Ddiv"].append(np.tile(E["Ddiv"].ravel(), nt))
             rows["Bu"].append(np.repeat(ps, 9))
             cols["Bu"].append(us.ravel())
             vals["Bu"].append(np.tile(E["Bu"], nt))
@@ -166,7 +167,7 @@ class Operator:
             cols["Mp"].append(ps)
             vals["Mp"].append(np.full(nt, E["Mp"]))
         blk = {}
-        for k in rows:
+        for k in [k for k in rows if rows[k]]:
             blk[k] = sp.csr_matrix((np.concatenate(vals[k]), (np.concatenate(rows[k]), np.concatenate(cols[k]))),
                                    shape=(N, N))
         self.full = blk

@@ -56,6 +56,7 @@ struct Level {
     double* cgq = nullptr;
     double* hv_cls = nullptr;   // heterogeneous Vanka: 9 x MG_HV_CLS class tables
     double* hv_sinv = nullptr;  // heterogeneous Vanka: MG_HV_NSINV planes of per-vertex S_v^{-1}
+    HvInterior hv_int{};        // heterogeneous Vanka: the interior class table (kernel parameter)
     double* ubnd = nullptr;  // 9 x 64
     VankaParams vp;
     DispParams up;
@@ -187,7 +188,7 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         }
         if (c->vanka_impl == 2 && Lv.n >= c->march_min_n && !c->het && !c->exact)
             CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
-        else CK(launch_vanka(P, xin, b, xout, xzero, S, s));
+        else CK(launch_vanka(P, xin, b, xout, xzero, S, s, c->het ? &Lv.hv_int : nullptr));
         return MG_OK;
     }
     const bool exact_s = o.relax == MG_BSR_EXACT;
@@ -605,6 +606,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
             if (launch_hv_sinv(Lv.vp.L, dw, dw + hw.size(), Lv.hv_sinv, 0) != cudaSuccess)
                 return bail(fail(MG_ECUDA, "hv_sinv launch: %s", cudaGetErrorString(cudaGetLastError())));
             Lv.vp.hv = HetVankaTabs{Lv.hv_cls, Lv.hv_sinv};
+            memcpy(Lv.hv_int.t, hcls.data(), sizeof(Lv.hv_int.t));   // class 0 = interior
         }
     }
     // norms and solve state

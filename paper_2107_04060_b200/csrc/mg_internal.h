@@ -83,6 +83,10 @@ struct ProlSrc {                  // coarse iterate e_H for a sweep with fused p
 #define MG_HV_U 344               // [6][6] U (row = RT0 slot, column = basis vector)
 #define MG_HV_NSINV 21            // per-vertex planes: upper triangle of S~_v^{-1}, row by row
 #define MG_HV_W 288               // setup: per class 8 triangles x [6][6] U^T M_w,v U per unit K^{-1}
+// the interior vertex class's table by value (kernel parameter, read as constant-bank operands)
+struct HvInterior {
+    double t[MG_HV_CLS];
+};
 struct HetVankaTabs {
     const double* cls;            // device: MG_NCLASS x MG_HV_CLS
     const double* sinv;           // device: MG_HV_NSINV planes of (n+1) x pitch

@@ -123,14 +123,30 @@ __device__ __forceinline__ void load_tile(double* __restrict__ dst, const double
         t0 = threadIdx.x;
         nt = blockDim.x;
     }
-    for (int t = t0; t < NP * W * HT; t += nt) {
-        int p = t / (W * HT);
-        int rem = t - p * (W * HT);
-        int ly = rem / W;
-        int lx = rem - ly * W;
-        int i = i0 + lx, j = j0 + ly;
-        dst[t] = (i >= 0 && i <= n && j >= 0 && j <= n) ? gld<NC>(src + (p0 + p) * plane + (int64_t)j * pitch + i)
-                                                         : 0.0;
+    // U elements per thread in flight: all loads of a batch are issued before its shared-memory
+    // stores (one element per iteration would serialise ~NP W HT / nt global-load latencies, which
+    // is what bounds the latency-bound coarse levels)
+    constexpr int TOT = NP * W * HT, U = 8;
+    for (int base = t0; base < TOT; base += U * nt) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = base + u * nt;
+            v[u] = 0.0;
+            if (t < TOT) {
+                const int p = t / (W * HT);
+                const int rem = t - p * (W * HT);
+                const int ly = rem / W;
+                const int lx = rem - ly * W;
+                const int i = i0 + lx, j = j0 + ly;
+                if (i >= 0 && i <= n && j >= 0 && j <= n) v[u] = gld<NC>(src + (p0 + p) * plane + (int64_t)j * pitch + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = base + u * nt;
+            if (t < TOT) dst[t] = v[u];
+        }
     }
 }
 
@@ -383,9 +399,12 @@ __device__ __forceinline__ void patch_apply20(const VankaParams& P, int cls, con
 // Heterogeneous-K patch solve (mg_internal.h HetVankaTabs): the class-constant condensed tables
 // and the per-vertex inverse RT0 Schur complement S_v^{-1} (upper triangle, MG_HV_NSINV planes).
 // out[s * os] = (D K_v^{-1} r)_s for the vertex (a, b) of class cls.
-__device__ __forceinline__ void patch_apply_het(const VankaParams& P, int cls, int a, int b, const double rr[20],
-                                                double* out, int os) {
-    const double* T = P.hv.cls + cls * MG_HV_CLS;
+// T: the class table (the interior class's from the kernel parameter block -- constant-bank operands
+// -- the 8 boundary classes' from global memory); LD(k) reads entry k
+template <bool CONST_T>
+__device__ __forceinline__ void patch_apply_het_t(const VankaParams& P, const double* __restrict__ T, int a, int b,
+                                                  const double rr[20], double* out, int os) {
+#define LD(k) (CONST_T ? T[k] : __ldg(T + (k)))
     double ry[14];
 #pragma unroll
     for (int q = 0; q < 8; ++q) ry[q] = rr[q];
@@ -395,37 +414,29 @@ __device__ __forceinline__ void patch_apply_het(const VankaParams& P, int cls, i
     double ad[14];
 #pragma unroll
     for (int q = 0; q < 14; ++q) ad[q] = 0.0;
-    const double2* G2 = reinterpret_cast<const double2*>(T + MG_HV_G);
 #pragma unroll
-    for (int q = 0; q < 14; ++q) {
+    for (int c = 0; c < 14; ++c) {          // column-outer: the 14 output chains advance together
 #pragma unroll
-        for (int c2 = 0; c2 < 7; ++c2) {
-            const double2 g = __ldg(G2 + q * 7 + c2);
-            ad[q] = fma(g.x, ry[2 * c2], ad[q]);
-            ad[q] = fma(g.y, ry[2 * c2 + 1], ad[q]);
-        }
+        for (int q = 0; q < 14; ++q) ad[q] = fma(LD(MG_HV_G + q * 14 + c), ry[c], ad[q]);
     }
     // constant-pressure part of K_yy^{-1} r_y: -(1^T r_p) / (m gamma) on every active P0 slot
     double psum = 0.0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) psum += ry[8 + k];
-    const double cp = -psum * __ldg(T + MG_HV_PINV);
+    const double cp = -psum * LD(MG_HV_PINV);
     // s~ = U^T r_r - (U^T K_ry) a_def  (in the basis U; K_ry: P0 columns only)
     double sv[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         double v = 0.0;
 #pragma unroll
-        for (int e = 0; e < 6; ++e) v = fma(__ldg(T + MG_HV_U + e * 6 + j), rr[8 + e], v);
+        for (int e = 0; e < 6; ++e) v = fma(LD(MG_HV_U + e * 6 + j), rr[8 + e], v);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) v = fma(-__ldg(T + MG_HV_KRP + j * 6 + k), ad[8 + k], v);
+        for (int k = 0; k < 6; ++k) v = fma(-LD(MG_HV_KRP + j * 6 + k), ad[8 + k], v);
         sv[j] = v;
     }
     // z~ = S~_v^{-1} s~ (symmetric, upper triangle per vertex)
-    const int64_t o = (int64_t)b * P.L.pitch + a;
-    double si[21];
-#pragma unroll
-    for (int k = 0; k < 21; ++k) si[k] = __ldg(P.hv.sinv + k * P.L.plane + o);
+    const double* si = P.hv.sinv + (int64_t)b * P.L.pitch + a;
     double zr[6];
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
@@ -433,7 +444,7 @@ __device__ __forceinline__ void patch_apply_het(const VankaParams& P, int cls, i
 #pragma unroll
         for (int f = 0; f < 6; ++f) {
             const int lo = e < f ? e : f, hi = e < f ? f : e;
-            v = fma(si[lo * 6 - lo * (lo - 1) / 2 + (hi - lo)], sv[f], v);
+            v = fma(__ldg(si + (lo * 6 - lo * (lo - 1) / 2 + (hi - lo)) * P.L.plane), sv[f], v);
         }
         zr[e] = v;
     }
@@ -442,18 +453,25 @@ __device__ __forceinline__ void patch_apply_het(const VankaParams& P, int cls, i
     for (int q = 0; q < 14; ++q) {
         double v = ad[q] + (q >= 8 ? cp : 0.0);
 #pragma unroll
-        for (int e = 0; e < 6; ++e) v = fma(-__ldg(T + MG_HV_Q + q * 6 + e), zr[e], v);
+        for (int e = 0; e < 6; ++e) v = fma(-LD(MG_HV_Q + q * 6 + e), zr[e], v);
         const int sl = q < 8 ? q : q + 6;
-        out[sl * os] = __ldg(T + MG_HV_D + sl) * v;
+        out[sl * os] = LD(MG_HV_D + sl) * v;
     }
     // z_r = U z~
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
         double v = 0.0;
 #pragma unroll
-        for (int j = 0; j < 6; ++j) v = fma(__ldg(T + MG_HV_U + e * 6 + j), zr[j], v);
-        out[(8 + e) * os] = __ldg(T + MG_HV_D + 8 + e) * v;
+        for (int j = 0; j < 6; ++j) v = fma(LD(MG_HV_U + e * 6 + j), zr[j], v);
+        out[(8 + e) * os] = LD(MG_HV_D + 8 + e) * v;
     }
+#undef LD
+}
+
+__device__ __forceinline__ void patch_apply_het(const VankaParams& P, const HvInterior* Ti, int cls, int a, int b,
+                                                const double rr[20], double* out, int os) {
+    if (cls == 0 && Ti) patch_apply_het_t<true>(P, Ti->t, a, b, rr, out, os);
+    else patch_apply_het_t<false>(P, P.hv.cls + cls * MG_HV_CLS, a, b, rr, out, os);
 }
 
 // per-vertex S~_v^{-1} of the heterogeneous Vanka patches of one level (setup), in the basis U of
@@ -515,7 +533,7 @@ __global__ void __launch_bounds__(256) hv_sinv_kernel(const LevelParams L, const
 template <bool XZERO, int TX, int TY, bool NC, bool HET = false>
 __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double* __restrict__ x,
                                              const double* __restrict__ b, double* __restrict__ xo, int bx, int by,
-                                             int t, double* sm, bool active) {
+                                             int t, double* sm, bool active, const HvInterior* Ti = nullptr) {
     using T = VTile<TX, TY>;
     double* xs = sm;          // x tile (phase 1)
     double* cs = sm;          // patch corrections (phase 2-3), overlays xs
@@ -548,7 +566,7 @@ __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double*
         if (a <= n && bb <= n) {
             double rr[20];
             gather20<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
-            if (HET) patch_apply_het(P, vertex_class(a, bb, n), a, bb, rr, cs + t, T::PW * T::PH);
+            if (HET) patch_apply_het(P, Ti, vertex_class(a, bb, n), a, bb, rr, cs + t, T::PW * T::PH);
             else patch_apply20<(TX <= 8)>(P, vertex_class(a, bb, n), rr, cs + t, T::PW * T::PH);
         } else {
 #pragma unroll
@@ -600,6 +618,25 @@ __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const Vanka
     if (*P.L.stop) return;
     const double nrm =
         vanka_tile<XZERO, TX, TY, true, HET>(P, x, b, xo, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
+    if (S.out || S.state) norm_finish<VTile<TX, TY>::NT>(S, nrm);
+}
+
+// heterogeneous-K sweep: the interior class table travels in the parameter block
+#ifndef MG_HET_MINB
+#define MG_HET_MINB 2   // CTAs per SM the heterogeneous sweep is compiled for (measured at 2048^2: 2 CTAs with 80
+                        // registers and spills 1.33 ms per sweep, 1 CTA with 168 registers 1.51 ms)
+#endif
+template <bool XZERO, int TX = VTX, int TY = VTY>
+__global__ void __launch_bounds__(VTile<TX, TY>::NT, MG_HET_MINB) vanka_het_kernel(const VankaParams P,
+                                                           const __grid_constant__ HvInterior Ti,
+                                                           const double* __restrict__ x, const double* __restrict__ b,
+                                                           double* __restrict__ xo, NormSink S) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double sm[];
+    if (*P.L.stop) return;
+    const double nrm =
+        vanka_tile<XZERO, TX, TY, true, true>(P, x, b, xo, blockIdx.x, blockIdx.y, threadIdx.x, sm, true, &Ti);
     if (S.out || S.state) norm_finish<VTile<TX, TY>::NT>(S, nrm);
 }
 
@@ -701,18 +738,21 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
     const int fi = 2 * I, fj = 2 * J;
     double* x0 = x + (int64_t)fj * pitchf + fi;   // fi even, rows 256-B aligned: 16-B aligned pairs
     // the two fine columns 2I, 2I+1 of a fine row move as one 16-byte load / store (a warp covers
-    // 512 contiguous bytes per instruction)
+    // 512 contiguous bytes per instruction); all 20 pairs are loaded before the first store (a
+    // load after a store to the same array cannot be hoisted by the compiler: 20 serial round trips)
+    double2 xq[20];
+#pragma unroll
+    for (int q = 0; q < 20; ++q) xq[q] = *reinterpret_cast<const double2*>(x0 + (q >> 1) * planef + (q & 1) * pitchf);
 #define PROL2(dj, kf)                                                                   \
     {                                                                                   \
         double v = 0.0;                                                                 \
         MG_PROLONG_0_##dj##_##kf(MG_Q) const double v0 = v;                             \
         v = 0.0;                                                                        \
         MG_PROLONG_1_##dj##_##kf(MG_Q) const double v1 = v;                             \
-        double2* p2 = reinterpret_cast<double2*>(x0 + kf * planef + dj * pitchf);       \
-        double2 xv = *p2;                                                               \
+        double2 xv = xq[2 * kf + dj];                                                   \
         if (is_active(kf, fi, fj + dj, nf)) xv.x += v0;                                 \
         if (is_active(kf, fi + 1, fj + dj, nf)) xv.y += v1;                             \
-        *p2 = xv;                                                                       \
+        *reinterpret_cast<double2*>(x0 + kf * planef + dj * pitchf) = xv;               \
     }
 #define PROL4(kf) PROL2(0, kf) PROL2(1, kf)
     PROL4(0) PROL4(1) PROL4(2) PROL4(3) PROL4(4) PROL4(5) PROL4(6) PROL4(7) PROL4(8) PROL4(9)
@@ -2431,10 +2471,10 @@ void kernels_init() {
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
-    set_smem(vanka_kernel<false, VTX, VTY, true>, V_SMEM);
-    set_smem(vanka_kernel<true, VTX, VTY, true>, V_SMEM);
-    set_smem(vanka_kernel<false, VSX, VSY, true>, VTile<VSX, VSY>::SMEM);
-    set_smem(vanka_kernel<true, VSX, VSY, true>, VTile<VSX, VSY>::SMEM);
+    set_smem(vanka_het_kernel<false>, V_SMEM);
+    set_smem(vanka_het_kernel<true>, V_SMEM);
+    set_smem(vanka_het_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
+    set_smem(vanka_het_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(restrict_kernel<0, false>, C_SMEM_PLAIN);
     set_smem(restrict_kernel<2, false>, C_SMEM_PLAIN);
     set_smem(restrict_kernel<1, false>, C_SMEM_FUSED);
@@ -2944,18 +2984,19 @@ cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* 
 int dot_partials_needed() { return VK * DOT_BLOCKS; }
 
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
-                         NormSink S, cudaStream_t s) {
+                         NormSink S, cudaStream_t s, const HvInterior* Ti) {
     if (P.hv.cls) {   // heterogeneous K: condensed patch solves, K^{-1} field in the residual
+        if (!Ti) return cudaErrorInvalidValue;
         if (P.L.n <= g_small_tile_n) {
             using T = VTile<VSX, VSY>;
             dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
-            if (x_zero) launch_k(vanka_kernel<true, VSX, VSY, true>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
-            else launch_k(vanka_kernel<false, VSX, VSY, true>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+            if (x_zero) launch_k(vanka_het_kernel<true, VSX, VSY>, grid, T::NT, T::SMEM, s, P, *Ti, x, b, xo, S);
+            else launch_k(vanka_het_kernel<false, VSX, VSY>, grid, T::NT, T::SMEM, s, P, *Ti, x, b, xo, S);
             return cudaGetLastError();
         }
         dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
-        if (x_zero) launch_k(vanka_kernel<true, VTX, VTY, true>, grid, VNT, V_SMEM, s, P, x, b, xo, S);
-        else launch_k(vanka_kernel<false, VTX, VTY, true>, grid, VNT, V_SMEM, s, P, x, b, xo, S);
+        if (x_zero) launch_k(vanka_het_kernel<true>, grid, VNT, V_SMEM, s, P, *Ti, x, b, xo, S);
+        else launch_k(vanka_het_kernel<false>, grid, VNT, V_SMEM, s, P, *Ti, x, b, xo, S);
         return cudaGetLastError();
     }
     if (P.L.n <= g_small_tile_n) {

@@ -78,7 +78,7 @@ cudaError_t launch_step_rhs(const LevelParams& L, double inv_M, double alpha, co
 cudaError_t launch_hv_sinv(const LevelParams& L, const double* W, const double* C, double* sinv, cudaStream_t s);
 // P.hv.cls != nullptr: heterogeneous-K sweep (condensed patch solves, 2-D tiles on every level)
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
-                         bool x_zero, NormSink norm, cudaStream_t s);
+                         bool x_zero, NormSink norm, cudaStream_t s, const HvInterior* Ti = nullptr);
 // row-marching TMA variant of the same sweep (identical arithmetic); the production kernel
 // E != nullptr: relax x + P e_H (prolongation of the coarse iterate E->e fused into the sweep)
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,

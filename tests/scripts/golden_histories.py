@@ -110,7 +110,8 @@ def main():
                         maxrss_gb=round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6, 2)),
     )
     name = f"hist_cfg{a.config}_{a.relax}{'_alt' if a.alt else ''}.json"
-    with open(os.path.join(ROOT, "tests", "golden", name), "w") as f:
+    # GOLDEN_OUT: another directory (the 2048^2 oracle needs ~65 GB and runs on a larger host)
+    with open(os.path.join(os.environ.get("GOLDEN_OUT", os.path.join(ROOT, "tests", "golden")), name), "w") as f:
         json.dump(out, f)
     print("wrote", name, out["provenance"])
 
