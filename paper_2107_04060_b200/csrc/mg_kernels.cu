@@ -1506,7 +1506,10 @@ __host__ __device__ constexpr int pslot20(int dI, int dJ, int pl) { return pl >=
 #ifndef M2WS_CREG
 #define M2WS_CREG 120
 #endif
-__host__ __device__ constexpr int m2np(int pv) { return pv == 2 ? 4 : (pv == 1 ? M2NP : 0); }
+// PV 3: one producer warp doing both tasks of a group (rows y, y+2 and y+1, y+3) with their coarse
+// values double-buffered: 5 warps per CTA, 15 per SM, so the compute warps get 128 registers (4 warps
+// per SM sub-partition) instead of the 96 of the 6-warp kernel
+__host__ __device__ constexpr int m2np(int pv) { return pv == 2 ? 4 : (pv == 3 ? 1 : (pv == 1 ? M2NP : 0)); }
 template <bool XZERO, int PV>
 __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                const __grid_constant__ CUtensorMap tmb,
@@ -1576,9 +1579,8 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
     };
     // producer warp k (= M2NT / 32 + k) takes task k of every group part
     const int kp = (t >> 5) - M2NT / 32;
-    auto prol_load = [&](int y0, int count, double (&pe)[20]) {
+    auto prol_load = [&](int y0, int count, double (&pe)[20], int k) {
         {
-            const int k = kp;
             int y, I, J;
             if (!prol_task(y0, count, k, y, I, J)) return;
             const double* e0 = E.e + (int64_t)J * E.pitchc + I;
@@ -1593,12 +1595,11 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
 #undef PL
         }
     };
-    auto prol_apply = [&](int y0, int count, const double (&pe)[20]) {
+    auto prol_apply = [&](int y0, int count, const double (&pe)[20], int k) {
 #ifdef MG_PROL_NOOP
         return;   // diagnostic build: the pipeline without the arithmetic (wrong results)
 #endif
         {
-            const int k = kp;
             int y, I, J;
             if (!prol_task(y0, count, k, y, I, J)) return;
             double* xrow = xr + sx(y) * M2ROW + 2 * (t & 15);
@@ -1644,18 +1645,41 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
             if ((t & 31) == 0) mbar_arrive(&ready[(g + 1) & 1]);
         };
         mbar_wait_sleep(&bars[0], 0);
+        if (PV == 3) {
+            double pe1[20];
 #pragma unroll 1
-        for (int part = 0; part < 2; ++part) {   // group -1: rows j0 - R .. j0 + 1
-            prol_load(part ? j0 : j0 - M2R, part ? 2 : M2R, pe);
-            prol_apply(part ? j0 : j0 - M2R, part ? 2 : M2R, pe);
-        }
-        publish(-1);
+            for (int part = 0; part < 2; ++part) {   // group -1: rows j0 - R .. j0 + 1
+                const int y0 = part ? j0 : j0 - M2R, cnt = part ? 2 : M2R;
+                prol_load(y0, cnt, pe, 0);
+                prol_load(y0, cnt, pe1, 1);
+                prol_apply(y0, cnt, pe, 0);
+                prol_apply(y0, cnt, pe1, 1);
+            }
+            publish(-1);
 #pragma unroll 1
-        for (int g = 0; g < nsteps; ++g) {
-            prol_load(j0 + g * M2R + 2, M2R, pe);
-            mbar_wait_sleep(&bars[(g + 1) & 1], ((g + 1) >> 1) & 1);
-            prol_apply(j0 + g * M2R + 2, M2R, pe);
-            publish(g);
+            for (int g = 0; g < nsteps; ++g) {
+                const int y0 = j0 + g * M2R + 2;
+                prol_load(y0, M2R, pe, 0);
+                prol_load(y0, M2R, pe1, 1);
+                mbar_wait_sleep(&bars[(g + 1) & 1], ((g + 1) >> 1) & 1);
+                prol_apply(y0, M2R, pe, 0);
+                prol_apply(y0, M2R, pe1, 1);
+                publish(g);
+            }
+        } else {
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {   // group -1: rows j0 - R .. j0 + 1
+                prol_load(part ? j0 : j0 - M2R, part ? 2 : M2R, pe, kp);
+                prol_apply(part ? j0 : j0 - M2R, part ? 2 : M2R, pe, kp);
+            }
+            publish(-1);
+#pragma unroll 1
+            for (int g = 0; g < nsteps; ++g) {
+                prol_load(j0 + g * M2R + 2, M2R, pe, kp);
+                mbar_wait_sleep(&bars[(g + 1) & 1], ((g + 1) >> 1) & 1);
+                prol_apply(j0 + g * M2R + 2, M2R, pe, kp);
+                publish(g);
+            }
         }
         if (S.out || S.state) norm_finish<M2NT + 32 * NPW>(S, 0.0);
         return;
@@ -2457,6 +2481,7 @@ void kernels_init() {
     set_smem(vanka_march2_kernel<true, 0>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 1>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 2>, M2SMEM);
+    set_smem(vanka_march2_kernel<false, 3>, M2SMEM);
     set_smem(bsr_a_march_kernel<false, false>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<false, true>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<true, false>, BMA_SMEM);
@@ -3032,8 +3057,10 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
     if (x_zero) launch_k(vanka_march2_kernel<true, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
-    else if (E && g_prol_ws)
+    else if (E && g_prol_ws == 1)
         launch_k(vanka_march2_kernel<false, 2>, grid, M2NT + 32 * m2np(2), M2SMEM, s, mx, mb, P, xo, S, MH, *E);
+    else if (E && g_prol_ws == 3)
+        launch_k(vanka_march2_kernel<false, 3>, grid, M2NT + 32 * m2np(3), M2SMEM, s, mx, mb, P, xo, S, MH, *E);
     else if (E) launch_k(vanka_march2_kernel<false, 1>, grid, M2NT + 32 * M2NP, M2SMEM, s, mx, mb, P, xo, S, MH, *E);
     else launch_k(vanka_march2_kernel<false, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
     return cudaGetLastError();
