@@ -1471,9 +1471,18 @@ void set_smem(F* f, int bytes) {
 // rows), filled by one 3-D TMA box per row (32 columns x 1 row x 10 planes) and prefetched one
 // step ahead, which cuts shared memory to 72 KB per CTA.
 constexpr int M2T = 28, M2R = 4, M2W = M2T + 4, M2C = M2T + 1, M2NT = 128;
+// MG_PATCH_MMA: the interior patch solves of a row run as two small GEMMs on the fp64 tensor cores
+// (mma.sync m8n8k4: Y+ = G+ H+ (9 x 9 padded to 16 x 12) and Y- = G- H- (11 x 11 -> 16 x 12) over the
+// warp's 32 patch columns), staged through the row's patch-correction ring slot, whose stride is then
+// padded to 32 columns.  Replaces the 202 DFMA + ~101 constant loads per patch by 48 DMMA + fragment
+// traffic per warp and row ("what was tried" for the measurement).
+#ifndef MG_PATCH_MMA
+#define MG_PATCH_MMA 0
+#endif
+constexpr int M2CS = MG_PATCH_MMA ? 32 : M2C;   // patch-correction ring stride (patch columns)
 constexpr int M2XR = 10, M2BR = 9, M2CR = 5;
 constexpr int M2ROW = 10 * M2W;                                  // doubles per x / b ring row
-constexpr int M2SMEM = (M2XR * M2ROW + M2BR * M2ROW + M2CR * 20 * M2C) * 8 + 64;
+constexpr int M2SMEM = (M2XR * M2ROW + M2BR * M2ROW + M2CR * 20 * M2CS) * 8 + 64;
 static_assert(M2T + 2 <= 32 && M2R * 32 == M2NT, "one warp per row, one residual position per thread");
 static_assert(M2T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
 
@@ -1520,8 +1529,8 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                        // [M2XR][10][M2W]
     double* br = xr + M2XR * M2ROW;         // [M2BR][10][M2W]   b, overwritten by r
-    double* cr = br + M2BR * M2ROW;         // [M2CR][20][M2C]   patch corrections
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M2CR * 20 * M2C);
+    double* cr = br + M2BR * M2ROW;         // [M2CR][20][M2CS]  patch corrections
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cr + M2CR * 20 * M2CS);
     const LevelParams& L = P.L;
     constexpr bool PROL = PV != 0;
     constexpr int NPW = m2np(PV);            // producer warps
@@ -1685,6 +1694,22 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
         return;
     }
     if (PV == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(M2WS_CREG));
+#if MG_PATCH_MMA
+    // A fragments of the interior +/- blocks (m8n8k4 row-major A: lane holds row l/4, column l%4 of
+    // each 8 x 4 tile), zero padded; G+[r][c] = gpT[c][r]
+    double mmaA_p[2][3], mmaA_m[2][3];
+    {
+        const int gq = (t & 31) >> 2, tg = t & 3;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks) {
+                const int r = 8 * mt + gq, c = 4 * ks + tg;
+                mmaA_p[mt][ks] = (r < 9 && c < 9) ? P.gpT[c][r] : 0.0;
+                mmaA_m[mt][ks] = (r < 11 && c < 11) ? P.gmT[c][r] : 0.0;
+            }
+    }
+#endif
     if (t == 0) {
         issue(-1);
         issue(0);
@@ -1735,10 +1760,114 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
             issue(s + 1);
         }
         // ---- patch solves at vertex rows bb = j0 + s R + 1 + q (r rows bb - 1 and bb)
+#if MG_PATCH_MMA
+        {
+            const int q = t >> 5, px = t & 31;
+            const int a = i0 + px, bb = j0 + s * M2R + 1 + q;
+            double* col = cr + scs(1 + q) * (20 * M2CS);       // [20][32]: H, then Y, then the output
+            const bool valid = px < M2C && a <= n && bb >= 0 && bb <= n;
+            const int cls = valid ? vertex_class(a, bb, n) : 0;
+            double rr[20];
+            if (valid) {
+                const double* r0 = br + sbs(1 + q) * M2ROW + (px + 2);
+                const double* rm = br + sbs(q) * M2ROW + (px + 2);
+#define RR(dx, dy, pl) ((dy) < 0 ? rm : r0)[(pl) * M2W + (dx)]
+                rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+                rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+                rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+                rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+                rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+                rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+                rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+            } else {
+#pragma unroll
+                for (int k = 0; k < 20; ++k) rr[k] = 0.0;
+            }
+            // +/- inputs of the interior class (0 for boundary classes: their lanes take the dense path)
+            {
+                const bool mm = valid && cls == 0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    col[k * M2CS + px] = mm ? rr[2 + 2 * k] - rr[3 + 2 * k] : 0.0;            // hp[k]
+                    col[(11 + k) * M2CS + px] = mm ? rr[2 + 2 * k] + rr[3 + 2 * k] : 0.0;     // hm[2 + k]
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    col[(6 + k) * M2CS + px] = mm ? rr[14 + 2 * k] + rr[15 + 2 * k] : 0.0;    // hp[6 + k]
+                    col[(17 + k) * M2CS + px] = mm ? rr[14 + 2 * k] - rr[15 + 2 * k] : 0.0;   // hm[8 + k]
+                }
+                col[9 * M2CS + px] = mm ? rr[0] : 0.0;                                        // hm[0]
+                col[10 * M2CS + px] = mm ? rr[1] : 0.0;                                       // hm[1]
+            }
+            __syncwarp();
+            const int gq = px >> 2, tg = px & 3;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                double bp[3], bm[3];
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) {
+                    const int kp = 4 * ks + tg;
+                    bp[ks] = kp < 9 ? col[kp * M2CS + 8 * nt + gq] : 0.0;
+                    bm[ks] = kp < 11 ? col[(9 + kp) * M2CS + 8 * nt + gq] : 0.0;
+                }
+                double dp[2][2], dm[2][2];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    dp[mt][0] = dp[mt][1] = dm[mt][0] = dm[mt][1] = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < 3; ++ks) {
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                     : "+d"(dp[mt][0]), "+d"(dp[mt][1]) : "d"(mmaA_p[mt][ks]), "d"(bp[ks]));
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                     : "+d"(dm[mt][0]), "+d"(dm[mt][1]) : "d"(mmaA_m[mt][ks]), "d"(bm[ks]));
+                    }
+                }
+                __syncwarp();   // every lane has read its B fragments of these columns
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int r = 8 * mt + gq, c = 8 * nt + 2 * tg;
+                    if (r < 9) {
+                        col[r * M2CS + c] = dp[mt][0];
+                        col[r * M2CS + c + 1] = dp[mt][1];
+                    }
+                    if (r < 11) {
+                        col[(9 + r) * M2CS + c] = dm[mt][0];
+                        col[(9 + r) * M2CS + c + 1] = dm[mt][1];
+                    }
+                }
+            }
+            __syncwarp();
+            if (valid) {
+                if (cls == 0) {   // back to the spoke basis, in place in the lane's own column
+                    double yp[9], ym[11];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) yp[k] = col[k * M2CS + px];
+#pragma unroll
+                    for (int k = 0; k < 11; ++k) ym[k] = col[(9 + k) * M2CS + px];
+                    double* out = col + px;
+                    out[0] = ym[0];
+                    out[M2CS] = ym[1];
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) {
+                        out[(2 + 2 * k) * M2CS] = ym[2 + k] + yp[k];
+                        out[(3 + 2 * k) * M2CS] = ym[2 + k] - yp[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        out[(14 + 2 * k) * M2CS] = yp[6 + k] + ym[8 + k];
+                        out[(15 + 2 * k) * M2CS] = yp[6 + k] - ym[8 + k];
+                    }
+                } else {
+                    patch_apply20(P, cls, rr, col + px, M2CS);
+                }
+            }
+        }
+#else
         if ((t & 31) < M2C) {
             const int q = t >> 5, px = t & 31;
             const int a = i0 + px, bb = j0 + s * M2R + 1 + q;
-            double* out = cr + scs(1 + q) * (20 * M2C) + px;
+            double* out = cr + scs(1 + q) * (20 * M2CS) + px;
             if (a <= n && bb >= 0 && bb <= n) {
                 const double* r0 = br + sbs(1 + q) * M2ROW + (px + 2);
                 const double* rm = br + sbs(q) * M2ROW + (px + 2);
@@ -1752,21 +1881,22 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
                 rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
                 rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
 #undef RR
-                patch_apply20(P, vertex_class(a, bb, n), rr, out, M2C);
+                patch_apply20(P, vertex_class(a, bb, n), rr, out, M2CS);
             } else {
 #pragma unroll
-                for (int k = 0; k < 20; ++k) out[k * M2C] = 0.0;
+                for (int k = 0; k < 20; ++k) out[k * M2CS] = 0.0;
             }
         }
+#endif
         csync();
         // ---- owners y = j0 + s R + q: patch rows y and y + 1
         if (s >= 0 && (t & 31) < M2T) {
             const int q = t >> 5, lx = t & 31;
             const int y = j0 + s * M2R + q, i = i0 + lx;
             if (i <= n && y < j0 + rows) {
-                const double* c0 = cr + scs(q) * (20 * M2C) + lx;
-                const double* c1 = cr + scs(q + 1) * (20 * M2C) + lx;
-#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * M2C + (dx)]
+                const double* c0 = cr + scs(q) * (20 * M2CS) + lx;
+                const double* c1 = cr + scs(q + 1) * (20 * M2CS) + lx;
+#define CC(sl, dx, dy) ((dy) > 0 ? c1 : c0)[(sl) * M2CS + (dx)]
                 double d[10];
                 d[0] = CC(0, 0, 0);
                 d[1] = CC(1, 0, 0);
