@@ -169,9 +169,11 @@ int mg_relax_bsr(mg_ctx* ctx, int32_t level, double* x, const double* b, double 
  * the Jacobi sweeps replaced by the exact solution of S dp = g (eq. bsr_p), computed on the device
  * by Jacobi-preconditioned conjugate gradients to 1e-14 in the D_S^{-1} norm (at most 24 n + 64
  * iterations).  Level n <= 1024 (a full S solve per relaxation is the cost the paper avoids with
- * inexact BSR).  Work space allocated on first use.  In place on x. */
+ * inexact BSR).  Work space allocated on first use.  In place on x.  cg_iters_out: NULL or
+ * receives the CG iterations of the last S solve (the stream is then synchronised, and MG_NOTCONV is
+ * returned if that solve stopped at the iteration cap instead of the tolerance). */
 int mg_relax_bsr_exact(mg_ctx* ctx, int32_t level, double* x, const double* b, double omega, int32_t sweeps,
-                       cudaStream_t s);
+                       int32_t* cg_iters_out, cudaStream_t s);
 
 /* b_coarse = P^T r_fine between levels fine_level and fine_level+1 (R = P^T, PAPER.md:484;
  * P_u divergence preserving PAPER.md:510-566, P_w / P_p canonical).  Overwrites b_coarse. */

@@ -718,7 +718,7 @@ int mg_relax_bsr(mg_ctx* c, int32_t level, double* x, const double* b, double om
 }
 
 int mg_relax_bsr_exact(mg_ctx* c, int32_t level, double* x, const double* b, double omega, int32_t sweeps,
-                       cudaStream_t s) {
+                       int32_t* cg_iters_out, cudaStream_t s) {
     if (int rc = check_level(c, level, c ? c->levels - 1 : 0)) return rc;
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (sweeps < 0) return fail(MG_EINVAL, "sweeps < 0");
@@ -732,6 +732,13 @@ int mg_relax_bsr_exact(mg_ctx* c, int32_t level, double* x, const double* b, dou
         std::swap(a, t);
     }
     if (a != x) CK(cudaMemcpyAsync(x, a, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
+    if (cg_iters_out && sweeps > 0) {   // iterations of the last S solve; MG_NOTCONV if it hit the cap
+        double st[8];
+        CK(cudaMemcpyAsync(st, c->cgst, sizeof(st), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *cg_iters_out = (int32_t)st[6];
+        if (st[5] == 0.0) return MG_NOTCONV;
+    }
     return MG_OK;
 }
 

@@ -58,7 +58,8 @@ SIGNATURES = {
     "mg_relax_vanka": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_int32, _VP]),
     "mg_relax_bsr": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_int32, ctypes.c_int32, _VP]),
-    "mg_relax_bsr_exact": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_int32, _VP]),
+    "mg_relax_bsr_exact": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, ctypes.c_double, ctypes.c_int32,
+                                          ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_restrict": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP]),
     "mg_prolong": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP]),
     "mg_coarse_solve": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
@@ -254,8 +255,11 @@ class Hierarchy:
                                      int(jacobi_sweeps), int(sweeps), _stream(stream)), "mg_relax_bsr")
 
     def relax_bsr_exact(self, level, x, b, omega, sweeps=1, stream=None):
-        _check(self.lib.mg_relax_bsr_exact(self.ctx, level, self._v(x, level), self._v(b, level), float(omega),
-                                           int(sweeps), _stream(stream)), "mg_relax_bsr_exact")
+        """Exact BSR sweeps; returns (rc, CG iterations of the last S solve)."""
+        its = ctypes.c_int32(0)
+        rc = _check(self.lib.mg_relax_bsr_exact(self.ctx, level, self._v(x, level), self._v(b, level), float(omega),
+                                                int(sweeps), ctypes.byref(its), _stream(stream)), "mg_relax_bsr_exact")
+        return rc, its.value
 
     def restrict(self, fine_level, r, bc, stream=None):
         _check(self.lib.mg_restrict(self.ctx, fine_level, self._v(r, fine_level), self._v(bc, fine_level + 1), _stream(stream)), "mg_restrict")

@@ -94,8 +94,10 @@ def test_exact_bsr_sweep(n, pname, quad):
     x = mg_inputs.uniform_vector(n, 85)
     b = mg_inputs.uniform_rhs(n, 86)
     xd, bd = H.to_device(x), H.to_device(b)
-    H.relax_bsr_exact(0, xd, bd, 0.8, sweeps=1)
+    rc, its = H.relax_bsr_exact(0, xd, bd, 0.8, sweeps=1)
     torch.cuda.synchronize()
+    print(n, pname, quad, "CG iterations", its)
+    assert rc == 0 and 0 < its <= 24 * n + 64            # converged to the tolerance, not at the cap
     xO = m.from_active(S.sweep(m.to_active(x), m.to_active(b), 0.8, 0.0, 0))
     err = np.abs(H.to_host(xd) - xO).max() / np.abs(xO).max()
     assert err <= 1e-10, err
