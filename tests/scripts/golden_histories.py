@@ -40,12 +40,12 @@ import mg_inputs  # noqa: E402
 from oracle.cycle import Hierarchy  # noqa: E402
 
 U = 2.0 ** -53
-DEFAULT_CYCLES = {1: 10, 2: 20, 3: 5, 4: 4, 5: 3}
+DEFAULT_CYCLES = {1: 10, 2: 20, 3: 5, 4: 4, 5: 3}   # config 4 with Vanka: also 4 (the oracle needs ~110 GB)
 
 
 def opts_for(c, relax):
-    if relax == "vanka":
-        return dict(nu1=1, nu2=1, omega=c["omega"])
+    if relax == "vanka":   # config 4 with Vanka: the heterogeneous-K Vanka of reading A20 at omega = 0.74
+        return dict(nu1=1, nu2=1, omega=c.get("omega", 0.74))
     return dict(nu1=1, nu2=1, omega=c["bsr_omega"], omega_J=c["omega_J"], jacobi_sweeps=3)
 
 
