@@ -182,6 +182,17 @@ int mg_restrict(mg_ctx* ctx, int32_t fine_level, const double* r_fine, double* b
 /* x_fine += P e_coarse (same P).  In place on x_fine. */
 int mg_prolong(mg_ctx* ctx, int32_t fine_level, const double* e_coarse, double* x_fine,
                cudaStream_t s);
+/* The fused production variants the V-cycle launches, exposed for testing at full size:
+ * mg_residual_restrict: b_coarse = P^T (b - A_l x) on levels l -> l+1 in one pass (row-marching TMA
+ * kernel on levels with n >= 512, scalar K); mg_prolong_relax_vanka: x <- one Vanka sweep of
+ * x + P e_coarse (the first post-smoothing sweep with the coarse-grid correction fused in,
+ * PAPER.md:471-476; producer warps add P e to each TMA row of x) -- in place on x (level-l scratch
+ * used). Constant K; levels 0 .. levels-2. */
+int mg_residual_restrict(mg_ctx* ctx, int32_t fine_level, const double* x, const double* b, double* b_coarse,
+                         cudaStream_t s);
+int mg_prolong_relax_vanka(mg_ctx* ctx, int32_t level, double* x, const double* e_coarse, const double* b,
+                           double omega, cudaStream_t s);
+
 /* x = A_L^{-1} b on the coarsest level L = levels-1 (dense deflated inverse, reading A9). */
 int mg_coarse_solve(mg_ctx* ctx, const double* b, double* x, cudaStream_t s);
 

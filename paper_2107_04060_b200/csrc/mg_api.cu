@@ -592,7 +592,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         std::vector<double> hcls(MG_NCLASS * MG_HV_CLS), hw(MG_NCLASS * MG_HV_W), hc(MG_NCLASS * 36);
         for (int l = 0; l < levels; ++l) {
             Level& Lv = c->L[l];
-            if (host_hv_tables(Lv.n, c->m, hcls.data(), hw.data(), hc.data(), err, sizeof(err)))
+            if (host_hv_tables(Lv.n, c->m, hcls.data(), hw.data(), hc.data(), &Lv.hv_int.pm, err, sizeof(err)))
                 return bail(fail(MG_EINVAL, "level %d heterogeneous Vanka tables: %s", l, err));
             Lv.hv_cls = (double*)dalloc(c, sizeof(double) * hcls.size());
             Lv.hv_sinv = (double*)dalloc(c, sizeof(double) * MG_HV_NSINV * Lv.plane);
@@ -606,7 +606,6 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
             if (launch_hv_sinv(Lv.vp.L, dw, dw + hw.size(), Lv.hv_sinv, 0) != cudaSuccess)
                 return bail(fail(MG_ECUDA, "hv_sinv launch: %s", cudaGetErrorString(cudaGetLastError())));
             Lv.vp.hv = HetVankaTabs{Lv.hv_cls, Lv.hv_sinv};
-            memcpy(Lv.hv_int.t, hcls.data(), sizeof(Lv.hv_int.t));   // class 0 = interior
         }
     }
     // norms and solve state
@@ -746,6 +745,34 @@ int mg_restrict(mg_ctx* c, int32_t fl, const double* r, double* bc, cudaStream_t
     if (int rc = check_level(c, fl, c ? c->levels - 2 : 0)) return rc;
     if (!aligned(r) || !aligned(bc)) return fail(MG_EINVAL, "null or misaligned pointer");
     CK(launch_restrict(c->L[fl].vp.L, c->L[fl + 1].n, c->L[fl + 1].pitch, 0, nullptr, r, bc, s));
+    return MG_OK;
+}
+
+int mg_residual_restrict(mg_ctx* c, int32_t fl, const double* x, const double* b, double* bc, cudaStream_t s) {
+    if (int rc = check_level(c, fl, c ? c->levels - 2 : 0)) return rc;
+    if (!aligned(x) || !aligned(b) || !aligned(bc)) return fail(MG_EINVAL, "null or misaligned pointer");
+    const Level& Lv = c->L[fl];
+    // the cycle's own choice (enqueue_cycle): row-marching fused kernel on the big scalar-K RQ levels
+    if (c->restrict_impl == 1 && Lv.n >= c->march_min_n && !c->exact)
+        CK(launch_restrict_march(Lv.vp.L, c->L[fl + 1].n, c->L[fl + 1].pitch, x, b, bc, s));
+    else
+        CK(launch_restrict(Lv.vp.L, c->L[fl + 1].n, c->L[fl + 1].pitch, 1, x, b, bc, s));
+    return MG_OK;
+}
+
+int mg_prolong_relax_vanka(mg_ctx* c, int32_t level, double* x, const double* e, const double* b, double omega,
+                           cudaStream_t s) {
+    if (int rc = check_level(c, level, c ? c->levels - 2 : 0)) return rc;
+    if (!aligned(x) || !aligned(e) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
+    mg_cycle_opts o{1, 1, MG_VANKA, omega, 0.0, 0};
+    Level& Lv = c->L[level];
+    if (fused_prolong(c, level, o)) {   // the cycle's fused kernel: x + P e relaxed in one pass
+        if (int rc = relax_once(c, level, x, b, Lv.t, false, o, no_norm(), s, e)) return rc;
+    } else {
+        CK(launch_prolong(Lv.n, Lv.pitch, c->L[level + 1].n, c->L[level + 1].pitch, e, x, c->stop, s));
+        if (int rc = relax_once(c, level, x, b, Lv.t, false, o, no_norm(), s)) return rc;
+    }
+    CK(cudaMemcpyAsync(x, Lv.t, sizeof(double) * Lv.len, cudaMemcpyDeviceToDevice, s));
     return MG_OK;
 }
 

@@ -83,9 +83,23 @@ struct ProlSrc {                  // coarse iterate e_H for a sweep with fused p
 #define MG_HV_U 344               // [6][6] U (row = RT0 slot, column = basis vector)
 #define MG_HV_NSINV 21            // per-vertex planes: upper triangle of S~_v^{-1}, row by row
 #define MG_HV_W 288               // setup: per class 8 triangles x [6][6] U^T M_w,v U per unit K^{-1}
-// the interior vertex class's table by value (kernel parameter, read as constant-bank operands)
+// the interior vertex class's condensed patch solve in the +/- basis of the 180-degree rotation
+// (kernel parameter, constant-bank operands): y inputs h+ = (bubble differences, P0 sums), h- =
+// (u_x, u_y, bubble sums, P0 differences); RT0 differences (+) and sums (-); the RT0 basis U is
+// orthonormal per sector (kernel vector first), so every table is block diagonal:
+//   a+ = gp h+, a- = gm h-;  s~+ = up d - kp a+[3..5],  s~- = um s - km a-[5..7];
+//   z~ = S~_v^{-1} s~ (per vertex, mixes the sectors);  z+ = a+ + cp (P0 sums) - qp z~+,
+//   z- = a- - qm z~-;  RT0: y+ = up^T z~+, y- = um^T z~-;  slots a = (-) + (+), b = (-) - (+)
+//   (P0: a = (+) + (-), b = (+) - (-)), times the natural weights.
+struct HvInteriorPM {
+    double gp[6][6], gm[8][8];
+    double kp[3][3], km[3][3];
+    double up[3][3], um[3][3];     // [basis j][pair q]
+    double qp[6][3], qm[8][3];
+    double pinv;
+};
 struct HvInterior {
-    double t[MG_HV_CLS];
+    HvInteriorPM pm;
 };
 struct HetVankaTabs {
     const double* cls;            // device: MG_NCLASS x MG_HV_CLS
@@ -128,7 +142,8 @@ int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, i
 // condensed heterogeneous-Vanka tables of one level (see HetVankaTabs): cls[MG_NCLASS][MG_HV_CLS],
 // W[MG_NCLASS][MG_HV_W] (tau mu_f h^2 M_w1 of triangle (cell a-1+tx, b-1+ty, shape sh), tri = 4 sh + 2 ty + tx,
 // mapped onto the 6 RT0 patch slots), C[MG_NCLASS][36] (K_ry G_def K_yr)
-int host_hv_tables(int n, const Material& m, double* cls, double* W, double* C, char* err, int errlen);
+int host_hv_tables(int n, const Material& m, double* cls, double* W, double* C, HvInteriorPM* pm, char* err,
+                   int errlen);
 // dense coarsest operator: Ginv (N x N, column major: G[col*N + row]) of the deflated inverse and
 // the slot offsets (k*(n+1)*pitch + j*pitch + i) of the N active unknowns.  kinv: nullptr (scalar)
 // or 2 x n x n [shape][j][i].

@@ -468,9 +468,103 @@ __device__ __forceinline__ void patch_apply_het_t(const VankaParams& P, const do
 #undef LD
 }
 
+// interior vertex: the +/- form of the condensed solve (mg_internal.h HvInteriorPM), 232 FMA instead
+// of the slot form's 424; every table entry is a constant-bank operand
+__device__ __forceinline__ void patch_apply_het_pm(const VankaParams& P, const HvInteriorPM& T, int a, int b,
+                                                   const double rr[20], double* out, int os) {
+    double hp[6], hm[8], rd[3], rs[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        hp[q] = rr[2 + 2 * q] - rr[3 + 2 * q];
+        hp[3 + q] = rr[14 + 2 * q] + rr[15 + 2 * q];
+        hm[2 + q] = rr[2 + 2 * q] + rr[3 + 2 * q];
+        hm[5 + q] = rr[14 + 2 * q] - rr[15 + 2 * q];
+        rd[q] = rr[8 + 2 * q] - rr[9 + 2 * q];
+        rs[q] = rr[8 + 2 * q] + rr[9 + 2 * q];
+    }
+    hm[0] = rr[0];
+    hm[1] = rr[1];
+    double ap[6], am[8];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) ap[r] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) am[r] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {            // column-outer: independent output chains
+#pragma unroll
+        for (int r = 0; r < 8; ++r) am[r] = fma(T.gm[r][c], hm[c], am[r]);
+        if (c < 6) {
+#pragma unroll
+            for (int r = 0; r < 6; ++r) ap[r] = fma(T.gp[r][c], hp[c], ap[r]);
+        }
+    }
+    const double cp = -(hp[3] + hp[4] + hp[5]) * T.pinv;   // -(1^T r_p) / (m gamma)
+    double sv[6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        double vp = 0.0, vm = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            vp = fma(T.up[j][q], rd[q], vp);
+            vm = fma(T.um[j][q], rs[q], vm);
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            vp = fma(-T.kp[j][k], ap[3 + k], vp);
+            vm = fma(-T.km[j][k], am[5 + k], vm);
+        }
+        sv[j] = vp;
+        sv[3 + j] = vm;
+    }
+    const double* si = P.hv.sinv + (int64_t)b * P.L.pitch + a;
+    double zt[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+        double v = 0.0;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            const int lo = e < f ? e : f, hi = e < f ? f : e;
+            v = fma(__ldg(si + (lo * 6 - lo * (lo - 1) / 2 + (hi - lo)) * P.L.plane), sv[f], v);
+        }
+        zt[e] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        double v = ap[r] + (r >= 3 ? cp : 0.0);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) v = fma(-T.qp[r][j], zt[j], v);
+        ap[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        double v = am[r];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) v = fma(-T.qm[r][j], zt[3 + j], v);
+        am[r] = v;
+    }
+    // slots with the natural weights: u 1, bubble and RT0 1/2, P0 1/3
+    out[0] = am[0];
+    out[os] = am[1];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        out[(2 + 2 * q) * os] = 0.5 * (am[2 + q] + ap[q]);
+        out[(3 + 2 * q) * os] = 0.5 * (am[2 + q] - ap[q]);
+        double yp = 0.0, ym = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            yp = fma(T.up[j][q], zt[j], yp);
+            ym = fma(T.um[j][q], zt[3 + j], ym);
+        }
+        out[(8 + 2 * q) * os] = 0.5 * (ym + yp);
+        out[(9 + 2 * q) * os] = 0.5 * (ym - yp);
+        out[(14 + 2 * q) * os] = (1.0 / 3.0) * (ap[3 + q] + am[5 + q]);
+        out[(15 + 2 * q) * os] = (1.0 / 3.0) * (ap[3 + q] - am[5 + q]);
+    }
+}
+
 __device__ __forceinline__ void patch_apply_het(const VankaParams& P, const HvInterior* Ti, int cls, int a, int b,
                                                 const double rr[20], double* out, int os) {
-    if (cls == 0 && Ti) patch_apply_het_t<true>(P, Ti->t, a, b, rr, out, os);
+    if (cls == 0 && Ti) patch_apply_het_pm(P, Ti->pm, a, b, rr, out, os);
     else patch_apply_het_t<false>(P, P.hv.cls + cls * MG_HV_CLS, a, b, rr, out, os);
 }
 

@@ -245,7 +245,7 @@ void jacobi_eigen(long double A[6][6], long double V[6][6], int m) {
 // Condensed heterogeneous-Vanka tables of the vertex (a, b) (mg_internal.h HetVankaTabs): the patch
 // matrix without its M_w block (K0 with kinv = 0) split into y = slots 0..7, 14..19 and r = 8..13.
 bool hv_class_tables(int a, int b, int n, const Material& m, double h, double* cls, double* W, double* C,
-                     char* err, int errlen) {
+                     char* err, int errlen, HvInteriorPM* pm = nullptr) {
     Material m0 = m;
     m0.K = INFINITY;                                           // kinv = 0: K0 has no M_w block
     std::vector<double> K;
@@ -299,7 +299,49 @@ bool hv_class_tables(int a, int b, int n, const Material& m, double h, double* c
     long double U[6][6] = {};
     for (int e = 0; e < 6; ++e) U[e][e] = 1.0L;
     bool isnull[6] = {false, false, false, false, false, false};
-    if (na > 0) {
+    if (pm && na == 6) {
+        // interior class: one orthonormal basis per sector of the 180-degree rotation (RT0 pair
+        // differences = + sector, sums = - sector), kernel vectors first within each sector; the
+        // +/- split of the patch solve (HvInteriorPM) needs U block diagonal in that sense
+        const long double r2 = 1.0L / sqrtl(2.0L);
+        for (int sg = 0; sg < 2; ++sg) {
+            long double Tr[6][3] = {};
+            for (int q = 0; q < 3; ++q) {
+                Tr[2 * q][q] = r2;
+                Tr[2 * q + 1][q] = sg == 0 ? -r2 : r2;
+            }
+            long double M[6][6] = {}, E[6][6], mmax = 0.0L;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    long double s2 = 0.0L;
+                    for (int t = 0; t < 14; ++t) {
+                        long double bi = 0.0L, bj = 0.0L;
+                        for (int e = 0; e < 6; ++e) {
+                            bi += Kyr[t][e] * Tr[e][i];
+                            bj += Kyr[t][e] * Tr[e][j];
+                        }
+                        s2 += bi * bj;
+                    }
+                    M[i][j] = s2;
+                    mmax = fmaxl(mmax, fabsl(s2));
+                }
+            jacobi_eigen(M, E, 3);
+            int order[3], k = 0;
+            for (int i = 0; i < 3; ++i)
+                if (M[i][i] <= 1e-14L * mmax) order[k++] = i;
+            const int nnull = k;
+            for (int i = 0; i < 3; ++i)
+                if (!(M[i][i] <= 1e-14L * mmax)) order[k++] = i;
+            for (int j = 0; j < 3; ++j) {
+                for (int e = 0; e < 6; ++e) {
+                    long double v = 0.0L;
+                    for (int i = 0; i < 3; ++i) v += Tr[e][i] * E[i][order[j]];
+                    U[e][3 * sg + j] = v;
+                }
+                isnull[3 * sg + j] = j < nnull;
+            }
+        }
+    } else if (na > 0) {
         long double M[6][6] = {}, E[6][6];
         long double mmax = 0.0L;
         for (int i = 0; i < na; ++i)
@@ -386,6 +428,89 @@ bool hv_class_tables(int a, int b, int n, const Material& m, double h, double* c
                     }
             }
         }
+    if (pm && na == 6 && my == 14) {
+        // +/- tables of the interior class (mg_internal.h HvInteriorPM): hat input h = Tin y (pair
+        // differences / sums, P0 pairs the other way round), hat output Tout = Tin with 1/2 on the
+        // pair rows, so that slot a = hat- + hat+, slot b = hat- - hat+ (P0: a = + + -, b = + - -)
+        long double Tin[14][14] = {}, Tout[14][14] = {};
+        const int bub[3][2] = {{2, 3}, {4, 5}, {6, 7}}, p0[3][2] = {{8, 9}, {10, 11}, {12, 13}};
+        for (int q = 0; q < 3; ++q) {
+            Tin[q][bub[q][0]] = 1.0L; Tin[q][bub[q][1]] = -1.0L;              // + : bubble differences
+            Tin[3 + q][p0[q][0]] = 1.0L; Tin[3 + q][p0[q][1]] = 1.0L;         // + : P0 sums
+            Tin[8 + q][bub[q][0]] = 1.0L; Tin[8 + q][bub[q][1]] = 1.0L;       // - : bubble sums
+            Tin[11 + q][p0[q][0]] = 1.0L; Tin[11 + q][p0[q][1]] = -1.0L;      // - : P0 differences
+        }
+        Tin[6][0] = 1.0L;                                                       // - : u_x, u_y
+        Tin[7][1] = 1.0L;
+        for (int r = 0; r < 14; ++r)
+            for (int c = 0; c < 14; ++c) Tout[r][c] = (r == 6 || r == 7) ? Tin[r][c] : 0.5L * Tin[r][c];
+        std::vector<long double> TiI(14 * 14), ToI(14 * 14);
+        for (int r = 0; r < 14; ++r)
+            for (int c = 0; c < 14; ++c) {
+                TiI[r * 14 + c] = Tin[r][c];
+                ToI[r * 14 + c] = Tout[r][c];
+            }
+        if (!invert(TiI, 14) || !invert(ToI, 14)) { snprintf(err, errlen, "hat transform"); return false; }
+        // G^ = Tout G_def Tin^{-1}, Q^ = Tout Q U, K^ = U^T K_ry Tout^{-1}
+        long double Gh[14][14], Qh[14][6], Kh[6][14], gmax = 0.0L;
+        for (int r = 0; r < 14; ++r)
+            for (int c = 0; c < 14; ++c) {
+                long double s2 = 0.0L;
+                for (int t = 0; t < 14; ++t)
+                    for (int u = 0; u < 14; ++u) s2 += Tout[r][t] * Gd[t * 14 + u] * TiI[u * 14 + c];
+                Gh[r][c] = s2;
+                gmax = fmaxl(gmax, fabsl(s2));
+            }
+        for (int r = 0; r < 14; ++r)
+            for (int j2 = 0; j2 < 6; ++j2) {
+                long double s2 = 0.0L;
+                for (int t = 0; t < 14; ++t) s2 += Tout[r][t] * QU[t][j2];
+                Qh[r][j2] = s2;
+            }
+        for (int j2 = 0; j2 < 6; ++j2)
+            for (int c = 0; c < 14; ++c) {
+                long double s2 = 0.0L;
+                for (int t = 0; t < 14; ++t) s2 += KU[t][j2] * ToI[t * 14 + c];
+                Kh[j2][c] = s2;
+            }
+        auto blk = [](int r) { return r < 6 ? 0 : 1; };   // hat sector of a y component
+        long double off = 0.0L, qmax = 0.0L, kmax = 0.0L;
+        for (int r = 0; r < 14; ++r)
+            for (int c = 0; c < 14; ++c)
+                if (blk(r) != blk(c)) off = fmaxl(off, fabsl(Gh[r][c]) / gmax);
+        for (int r = 0; r < 14; ++r)
+            for (int j2 = 0; j2 < 6; ++j2) qmax = fmaxl(qmax, fabsl(Qh[r][j2]));
+        for (int j2 = 0; j2 < 6; ++j2)
+            for (int c = 0; c < 14; ++c) kmax = fmaxl(kmax, fabsl(Kh[j2][c]));
+        for (int r = 0; r < 14; ++r)
+            for (int j2 = 0; j2 < 6; ++j2)
+                if (blk(r) != j2 / 3) off = fmaxl(off, fabsl(Qh[r][j2]) / qmax);
+        for (int j2 = 0; j2 < 6; ++j2)
+            for (int c = 0; c < 14; ++c) {
+                const bool keep = (j2 < 3 && c >= 3 && c < 6) || (j2 >= 3 && c >= 11);
+                if (!keep) off = fmaxl(off, fabsl(Kh[j2][c]) / kmax);
+            }
+        if (off > 1e-11L) {
+            snprintf(err, errlen, "interior heterogeneous-Vanka tables are not +/- block diagonal (%.3Le)", off);
+            return false;
+        }
+        for (int r = 0; r < 6; ++r)
+            for (int c = 0; c < 6; ++c) pm->gp[r][c] = (double)Gh[r][c];
+        for (int r = 0; r < 8; ++r)
+            for (int c = 0; c < 8; ++c) pm->gm[r][c] = (double)Gh[6 + r][6 + c];
+        for (int j2 = 0; j2 < 3; ++j2)
+            for (int k = 0; k < 3; ++k) {
+                pm->kp[j2][k] = (double)Kh[j2][3 + k];
+                pm->km[j2][k] = (double)Kh[3 + j2][11 + k];
+                pm->up[j2][k] = (double)U[2 * k][j2];          // applied to RT0 differences / sums
+                pm->um[j2][k] = (double)U[2 * k][3 + j2];
+            }
+        for (int r = 0; r < 6; ++r)
+            for (int j2 = 0; j2 < 3; ++j2) pm->qp[r][j2] = (double)Qh[r][j2];
+        for (int r = 0; r < 8; ++r)
+            for (int j2 = 0; j2 < 3; ++j2) pm->qm[r][j2] = (double)Qh[6 + r][3 + j2];
+        pm->pinv = cls[MG_HV_PINV];
+    }
     return true;
 }
 
@@ -507,13 +632,14 @@ int host_level_tables(int n, const Material& m, HostLevelTables* t, char* err, i
     return 0;
 }
 
-int host_hv_tables(int n, const Material& m, double* cls, double* W, double* C, char* err, int errlen) {
+int host_hv_tables(int n, const Material& m, double* cls, double* W, double* C, HvInteriorPM* pm, char* err,
+                   int errlen) {
     const double h = 1.0 / n;
     for (int cy = 0; cy < 3; ++cy)
         for (int cx = 0; cx < 3; ++cx) {
             const int c = cx + 3 * cy;
             if (!hv_class_tables(class_coord(cx, n), class_coord(cy, n), n, m, h, cls + c * MG_HV_CLS,
-                                 W + c * MG_HV_W, C + c * 36, err, errlen))
+                                 W + c * MG_HV_W, C + c * 36, err, errlen, c == 0 ? pm : nullptr))
                 return -1;
         }
     return 0;

@@ -62,6 +62,8 @@ SIGNATURES = {
                                           ctypes.POINTER(ctypes.c_int32), _VP]),
     "mg_restrict": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP]),
     "mg_prolong": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP]),
+    "mg_residual_restrict": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP, _VP]),
+    "mg_prolong_relax_vanka": (ctypes.c_int, [_VP, ctypes.c_int32, _VP, _VP, _VP, ctypes.c_double, _VP]),
     "mg_coarse_solve": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
     "mg_cycle": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), _D, _VP]),
     "mg_solve": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(CycleOpts), ctypes.c_double, ctypes.c_int32,
@@ -266,6 +268,17 @@ class Hierarchy:
 
     def prolong(self, fine_level, e, xf, stream=None):
         _check(self.lib.mg_prolong(self.ctx, fine_level, self._v(e, fine_level + 1), self._v(xf, fine_level), _stream(stream)), "mg_prolong")
+
+    def residual_restrict(self, fine_level, x, b, bc, stream=None):
+        """b_coarse = P^T (b - A x), the cycle's fused production kernel."""
+        _check(self.lib.mg_residual_restrict(self.ctx, fine_level, self._v(x, fine_level), self._v(b, fine_level),
+                                             self._v(bc, fine_level + 1), _stream(stream)), "mg_residual_restrict")
+
+    def prolong_relax_vanka(self, level, x, e, b, omega, stream=None):
+        """x <- one Vanka sweep of x + P e (the cycle's fused post-sweep), in place."""
+        _check(self.lib.mg_prolong_relax_vanka(self.ctx, level, self._v(x, level), self._v(e, level + 1),
+                                               self._v(b, level), float(omega), _stream(stream)),
+               "mg_prolong_relax_vanka")
 
     def coarse_solve(self, b, x, stream=None):
         _check(self.lib.mg_coarse_solve(self.ctx, self._v(b, self.levels - 1), self._v(x, self.levels - 1), _stream(stream)), "mg_coarse_solve")

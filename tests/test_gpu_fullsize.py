@@ -186,3 +186,102 @@ def test_fullsize_solve(cfg):
     assert rn <= 2e-8 * hist[0], (rn, hist[0])
     H.close()
     torch.cuda.empty_cache()
+
+
+def _map_even(i, n):
+    """As _map, keeping the parity of i (fine index 2I <-> coarse index I stay aligned)."""
+    si = _map(i, n)
+    return si + ((i - si) & 1) if W + 1 < i < n - W - 1 else si
+
+
+def test_fullsize_fused_production_kernels(big):
+    """The two fused kernels the cycle runs on level 0 and that no other full-size test reaches:
+    the row-marching residual + restriction (mg_residual_restrict) and the post-sweep with the
+    prolongation fused in (mg_prolong_relax_vanka), at sampled DoFs against the oracle on windows
+    (fine mesh 2 NS / coarse NS for the restriction; fine NS / coarse NS / 2 for the post-sweep)."""
+    torch = _torch()
+    from oracle.fem import Operator
+    from oracle.mesh import Mesh
+    from oracle.relax import Vanka
+    from oracle.transfer import Transfer
+    H, n, pname = big["H"], big["n"], big["pname"]
+    nc = n // 2
+    lam, mu, K, tau, alpha, invM = C.PARAMS[pname]
+    x, b = big["x"], big["b"]
+    e = mg_inputs.uniform_vector(nc, 301)
+    xd, bd, ed = H.to_device(x), H.to_device(b), H.to_device(e, 1)
+    bc = H.zeros(1)
+    H.residual_restrict(0, xd, bd, bc)
+    H.prolong_relax_vanka(0, xd, ed, bd, 0.7)
+    torch.cuda.synchronize()
+    bcG, x1G = H.to_host(bc, 1), H.to_host(xd)
+    rng = np.random.default_rng(11)
+    # (1) residual + restriction at coarse samples
+    mf, mc = Mesh(2 * NS), Mesh(NS)
+    mf.h, mc.h = 1.0 / n, 1.0 / nc
+    opf = Operator(mf, lam, mu, tau, alpha, invM, 1.0, K=K)
+    T = Transfer(Mesh(2 * NS), Mesh(NS))
+    absA = opf.A.copy()
+    absA.data = np.abs(absA.data)
+    absR = abs(T.R)
+    worst = 0.0
+    for (I, J) in _samples(nc, rng, 24):
+        si, sj = _map(I, nc), _map(J, nc)
+        xs = np.zeros((10, 2 * NS + 1, 2 * NS + 1))
+        bs = np.zeros_like(xs)
+        for dj in range(-2 * W, 2 * W + 1):
+            for di in range(-2 * W, 2 * W + 1):
+                fi, fj, a, b2 = 2 * I + di, 2 * J + dj, 2 * si + di, 2 * sj + dj
+                if 0 <= fi <= n and 0 <= fj <= n and 0 <= a <= 2 * NS and 0 <= b2 <= 2 * NS:
+                    xs[:, b2, a] = x[:, fj, fi]
+                    bs[:, b2, a] = b[:, fj, fi]
+        xs[~mg_inputs.active_mask(2 * NS)] = 0.0
+        bs[~mg_inputs.active_mask(2 * NS)] = 0.0
+        xa, ba = mf.to_active(xs), mf.to_active(bs)
+        r = ba - opf.A @ xa
+        bO = mc.from_active(T.R @ r)
+        bnd = mc.from_active(64 * U * (absR @ (np.abs(ba) + absA @ np.abs(xa))))
+        act = mg_inputs.active_mask(nc)[:, J, I]
+        for k in range(10):
+            if act[k]:
+                d = abs(bcG[k, J, I] - bO[k, sj, si])
+                assert d <= bnd[k, sj, si], (I, J, k, d, bnd[k, sj, si])
+                worst = max(worst, d / bnd[k, sj, si])
+            else:
+                assert bcG[k, J, I] == 0.0
+    # (2) fused prolongation + Vanka sweep at fine samples
+    ms, mcs = Mesh(NS), Mesh(NS // 2)
+    ms.h, mcs.h = 1.0 / n, 1.0 / nc
+    ops = Operator(ms, lam, mu, tau, alpha, invM, 1.0, K=K)
+    V = Vanka(ops)
+    Ts = Transfer(Mesh(NS), Mesh(NS // 2))
+    worst_v = 0.0
+    for (i, j) in _samples(n, rng, 24):
+        si, sj = _map_even(i, n), _map_even(j, n)
+        xs, bs = np.zeros((10, NS + 1, NS + 1)), np.zeros((10, NS + 1, NS + 1))
+        for dj in range(-W, W + 1):
+            for di in range(-W, W + 1):
+                I2, J2, a, b2 = i + di, j + dj, si + di, sj + dj
+                if 0 <= I2 <= n and 0 <= J2 <= n and 0 <= a <= NS and 0 <= b2 <= NS:
+                    xs[:, b2, a] = x[:, J2, I2]
+                    bs[:, b2, a] = b[:, J2, I2]
+        es = np.zeros((10, NS // 2 + 1, NS // 2 + 1))
+        for dj in range(-W, W + 1):
+            for di in range(-W, W + 1):
+                I2, J2, a, b2 = i // 2 + di, j // 2 + dj, si // 2 + di, sj // 2 + dj
+                if 0 <= I2 <= nc and 0 <= J2 <= nc and 0 <= a <= NS // 2 and 0 <= b2 <= NS // 2:
+                    es[:, b2, a] = e[:, J2, I2]
+        for arr, mm in ((xs, NS), (bs, NS), (es, NS // 2)):
+            arr[~mg_inputs.active_mask(mm)] = 0.0
+        xa = ms.to_active(xs) + Ts.P @ mcs.to_active(es)
+        x1O = ms.from_active(V.sweep(xa, ms.to_active(bs), 0.7))
+        act = mg_inputs.active_mask(n)[:, j, i]
+        for k in range(10):
+            if not act[k]:
+                assert x1G[k, j, i] == 0.0
+                continue
+            ref = max(abs(x1O[k, sj, si]), np.abs(x1O).max() * 1e-3)
+            dv = abs(x1G[k, j, i] - x1O[k, sj, si])
+            assert dv <= 1e-9 * ref, (i, j, k, x1G[k, j, i], x1O[k, sj, si])
+            worst_v = max(worst_v, dv / ref)
+    print(f"n={n}: fused residual+restriction worst {worst:.2e} of its bound, fused post-sweep worst {worst_v:.2e}")
