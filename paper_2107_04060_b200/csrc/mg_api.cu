@@ -493,6 +493,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     set_pdl(getenv("MG_PDL") ? atoi(getenv("MG_PDL")) != 0 : 0);
     set_prol_ws(getenv("MG_PROL_WS") ? atoi(getenv("MG_PROL_WS")) : 0);
     set_resid_march_n(getenv("MG_RESID_MARCH_N") ? atoi(getenv("MG_RESID_MARCH_N")) : 512);
+    set_warp_min_n(getenv("MG_WARP_MIN_N") ? atoi(getenv("MG_WARP_MIN_N")) : 1024);
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = std::min(2, std::max(0, atoi(v)));
@@ -548,7 +549,8 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
         }
         if (c->het) Lv.kinv = (double*)dalloc(c, pb);
         Lv.jtab = (double*)dalloc(c, sizeof(double) * 5 * Lv.plane);
-        if (!Lv.t || !Lv.g || !Lv.dpa || !Lv.dpb || !Lv.gbnd || !Lv.ubnd || !Lv.jtab || (l > 0 && (!Lv.x || !Lv.b)) ||
+        Lv.vp.bcorr = (double*)dalloc(c, sizeof(double) * 20 * 4 * std::max(Lv.n, 1));
+        if (!Lv.vp.bcorr || !Lv.t || !Lv.g || !Lv.dpa || !Lv.dpb || !Lv.gbnd || !Lv.ubnd || !Lv.jtab || (l > 0 && (!Lv.x || !Lv.b)) ||
             (c->het && !Lv.kinv)) {
             delete t;
             return bail(fail(MG_ENOMEM, "device allocation failed at level %d", l));

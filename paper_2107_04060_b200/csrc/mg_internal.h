@@ -113,6 +113,8 @@ struct VankaParams {
     double gmT[11][11];
     const double* gbnd;          // device: MG_NCLASS x 20 x 20 (weighted, deflated), row major
     double omega;
+    double* bcorr;               // device scratch of the warp-marching sweep: the 20 patch outputs of the 4n
+                                 // boundary vertices ([20][4n], vanka_bnd_kernel), read instead of recomputed
 };
 
 struct DispParams {               // 8-DoF displacement Vanka (F_u^{-1} of BSR)

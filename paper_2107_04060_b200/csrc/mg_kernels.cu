@@ -2024,6 +2024,353 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
 }
 
 // ------------------------------------------------------------------------------------------
+// patch_apply20 with the 20 outputs in registers (the warp-marching sweep moves them between lanes
+// by shuffles instead of a shared-memory ring).  Same arithmetic and summation order as
+// patch_apply20 (interior: +/- blocks; boundary class: dense table, four output rows per pass).
+__device__ __forceinline__ void patch_apply20r(const VankaParams& P, int cls, const double rr[20], double o[20]) {
+    if (cls == 0) {
+        double hp[9], hm[11];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            hp[q] = rr[2 + 2 * q] - rr[3 + 2 * q];
+            hm[2 + q] = rr[2 + 2 * q] + rr[3 + 2 * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            hp[6 + q] = rr[14 + 2 * q] + rr[15 + 2 * q];
+            hm[8 + q] = rr[14 + 2 * q] - rr[15 + 2 * q];
+        }
+        hm[0] = rr[0];
+        hm[1] = rr[1];
+        double yp[9], ym[11];
+#pragma unroll
+        for (int a = 0; a < 9; ++a) yp[a] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 11; ++a) ym[a] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 11; ++c) {
+#pragma unroll
+            for (int a = 0; a < 11; ++a) ym[a] = fma(P.gmT[c][a], hm[c], ym[a]);
+            if (c < 9) {
+#pragma unroll
+                for (int a = 0; a < 9; ++a) yp[a] = fma(P.gpT[c][a], hp[c], yp[a]);
+            }
+        }
+        o[0] = ym[0];
+        o[1] = ym[1];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            o[2 + 2 * q] = ym[2 + q] + yp[q];
+            o[3 + 2 * q] = ym[2 + q] - yp[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            o[14 + 2 * q] = yp[6 + q] + ym[8 + q];
+            o[15 + 2 * q] = yp[6 + q] - ym[8 + q];
+        }
+    } else {
+        // boundary classes: vanka_bnd_kernel (the warp sweep never calls this with cls != 0)
+#pragma unroll
+        for (int k = 0; k < 20; ++k) o[k] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Boundary-vertex patch solves of the warp-marching sweep: one thread per boundary vertex (a or b in
+// {0, n}; index bnd_index), the four residual positions of its patch from a per-thread 4 x 4 x 10
+// x tile, the dense boundary-class inverse (patch_apply20, same order), the 20 outputs to
+// P.bcorr[k * 4n + index].  The warp kernel reads them instead of running the dense path, so its
+// interior path keeps its register budget.
+__host__ __device__ __forceinline__ int bnd_count(int n) { return 4 * n; }
+__device__ __forceinline__ int bnd_index(int a, int b, int n) {
+    return b == 0 ? a : (b == n ? (n + 1) + a : (a == 0 ? 2 * (n + 1) + (b - 1) : 2 * (n + 1) + (n - 1) + (b - 1)));
+}
+constexpr int WB_NT = 64, WB_SMEM = WB_NT * 160 * 8;
+template <bool XZERO>
+__global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, const double* __restrict__ x,
+                                                          const double* __restrict__ b) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(16) double smb[];
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n, nb = bnd_count(n);
+    const int t = blockIdx.x * WB_NT + threadIdx.x;
+    if (t >= nb) return;
+    int a, bb;
+    if (t <= n) { a = t; bb = 0; }
+    else if (t <= 2 * n + 1) { a = t - (n + 1); bb = n; }
+    else if (t < 2 * (n + 1) + (n - 1)) { a = 0; bb = t - 2 * (n + 1) + 1; }
+    else { a = n; bb = t - 2 * (n + 1) - (n - 1) + 1; }
+    // residuals at (a - 1 + px, bb - 1 + py), px, py in {0, 1}
+    double r[2][2][10];
+    if (XZERO) {
+#pragma unroll
+        for (int py = 0; py < 2; ++py)
+#pragma unroll
+            for (int px = 0; px < 2; ++px) {
+                const int i = a - 1 + px, j = bb - 1 + py;
+                const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) r[py][px][k] = in ? __ldg(b + k * L.plane + (int64_t)j * L.pitch + i) : 0.0;
+            }
+    } else {
+        double* tile = smb + threadIdx.x * 160;   // [10][4][4]: x at columns a-2 .. a+1, rows bb-2 .. bb+1
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+#pragma unroll
+            for (int ry = 0; ry < 4; ++ry)
+#pragma unroll
+                for (int rx = 0; rx < 4; ++rx) {
+                    const int i = a - 2 + rx, j = bb - 2 + ry;
+                    tile[k * 16 + ry * 4 + rx] =
+                        (i >= 0 && j >= 0 && i <= n && j <= n) ? __ldg(x + k * L.plane + (int64_t)j * L.pitch + i) : 0.0;
+                }
+#pragma unroll
+        for (int py = 0; py < 2; ++py)
+#pragma unroll
+            for (int px = 0; px < 2; ++px) {
+                const int i = a - 1 + px, j = bb - 1 + py;
+                const double* x0 = tile + (py + 1) * 4 + (px + 1);
+                double av[10];
+                apply_rows<16, false>(L, x0 - 4, x0, x0 + 4, i, j, av);
+                const unsigned m = active_mask(i, j, n);
+                const int64_t o = (i >= 0 && j >= 0 && i <= n && j <= n) ? (int64_t)j * L.pitch + i : 0;
+#pragma unroll
+                for (int k = 0; k < 10; ++k) r[py][px][k] = ((m >> k) & 1u) ? __ldg(b + k * L.plane + o) - av[k] : 0.0;
+            }
+    }
+    double rr[20];
+#define RR(dx, dy, pl) r[1 + (dy)][1 + (dx)][pl]
+    rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+    rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+    rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+    rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+    rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+    rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+    rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+    patch_apply20(P, vertex_class(a, bb, n), rr, P.bcorr + t, nb);
+}
+
+// ------------------------------------------------------------------------------------------
+// Warp-marching Vanka sweep (the level-0 hot kernel when MG_WARP_MIN_N <= n).  Same arithmetic as
+// vanka_march2_kernel / vanka_kernel (residual, 20-DoF patch solves, owner-computes update,
+// PAPER.md:575-588), organised so that no CTA-wide barrier is needed: every WARP marches down its
+// own strip of WT = 30 owned columns, one grid row per iteration --
+//   residual row y  (lane l: index i = i0 - 1 + l, all 32 lanes useful),
+//   patch row y     (lane l: vertex a = i0 - 1 + l; the residuals of the left neighbour arrive by
+//                    __shfl_up, those of row y - 1 are carried in registers from the previous iteration),
+//   owner row y - 1 (lane l: index i0 - 1 + l, 30 lanes own; the corrections of the right neighbour
+//                    arrive by __shfl_down, those of patch row y - 1 are carried as partial sums in
+//                    the owner's summation order).
+// Only x (a 4-row ring of 34-column, 10-plane TMA boxes) and b (2-row ring of 32-column boxes) pass
+// through shared memory, each row prefetched one iteration ahead on per-slot mbarriers: 16 KB per
+// warp, 14 warps per SM, and the r / patch-correction rings of the CTA kernel (and both of its
+// barriers per step) are gone.
+constexpr int WT = 30, WXW = WT + 4, WBW = WT + 4, WXR = 4, WBR = 1;   // TMA box origins: even columns (16 B)
+constexpr int WXROW = 10 * WXW, WBROW = 10 * WBW;
+constexpr int WXSLOT = (WXROW + 15) / 16 * 16;   // ring slot strides: 128-byte aligned TMA destinations
+constexpr int WBSLOT = (WBROW + 15) / 16 * 16;
+constexpr int W_WARP_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + 10 * 32) * 8 + 64 + 127) / 128 * 128;
+#ifndef MG_WPC
+#define MG_WPC 6   // warps per CTA (2 CTAs per SM)
+#endif
+constexpr int WPC = MG_WPC, W_NT = 32 * WPC, W_SMEM = WPC * W_WARP_BYTES;
+static_assert(2 * (W_SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
+static_assert((WXW * 8) % 16 == 0 && (WBW * 8) % 16 == 0 && (WXSLOT * 8) % 128 == 0 && (WBSLOT * 8) % 128 == 0,
+              "TMA box rows and ring slots 16 / 128-byte aligned");
+
+template <bool XZERO>
+__global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                             const __grid_constant__ CUtensorMap tmb,
+                                                             const VankaParams P, double* __restrict__ xo,
+                                                             NormSink S, int MH, int nstrips, int ntasks) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(128) double sm[];
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int task = blockIdx.x * WPC + w;
+    double nrm = 0.0;
+    if (task < ntasks) {
+        double* xr = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + w * W_WARP_BYTES);   // [WXR][10][WXW] (slot stride WXSLOT)
+        double* br = xr + WXR * WXSLOT;                                                              // [WBR][10][WBW]
+        double* cds = br + WBR * WBSLOT;                                                             // [10][32]
+        uint64_t* xbar = reinterpret_cast<uint64_t*>(cds + 10 * 32);                                 // [WXR]
+        uint64_t* bbar = xbar + WXR;                                                                 // [WBR]
+        // tasks of the two boundary strips first (their dense boundary patches make them the slowest;
+        // started in the first wave they do not trail the grid), then seg-major over the inner strips
+        int strip, seg;
+        const int nseg = ntasks / nstrips;
+        if (nstrips <= 2) {
+            strip = task % nstrips;
+            seg = task / nstrips;
+        } else if (task < 2 * nseg) {
+            strip = (task & 1) ? nstrips - 1 : 0;
+            seg = task >> 1;
+        } else {
+            strip = 1 + (task - 2 * nseg) % (nstrips - 2);
+            seg = (task - 2 * nseg) / (nstrips - 2);
+        }
+        const int i0 = strip * WT, j0 = seg * MH;
+        const int rows = min(MH, n + 1 - j0);
+        const int yend = j0 + rows;   // residual / patch rows j0 - 1 .. yend, owner rows j0 .. yend - 1
+        const int i = i0 - 1 + lane;  // residual position, patch vertex and owner index of this lane
+        // x row y: load number q = y - (j0 - 2), slot q % WXR; b row y: q = y - (j0 - 1), slot q % WBR
+        auto load_x = [&](int y) {
+            const int q = y - (j0 - 2);
+            uint64_t* bar = &xbar[q % WXR];
+            mbar_expect_tx(bar, WXROW * 8);
+            tma_load3(xr + (q % WXR) * WXSLOT, &tmx, i0 - 2, y, 0, bar);
+        };
+        auto load_b = [&](int y) {
+            const int q = y - (j0 - 1);
+            uint64_t* bar = &bbar[q % WBR];
+            mbar_expect_tx(bar, WBROW * 8);
+            tma_load3(br + (q % WBR) * WBSLOT, &tmb, i0 - 2, y, 0, bar);
+        };
+        auto wait_x = [&](int y) { const int q = y - (j0 - 2); mbar_wait(&xbar[q % WXR], (q / WXR) & 1); };
+        auto wait_b = [&](int y) { const int q = y - (j0 - 1); mbar_wait(&bbar[q % WBR], (q / WBR) & 1); };
+        auto xrow = [&](int y) { return xr + ((y - (j0 - 2)) % WXR) * WXSLOT; };
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < WXR; ++k) mbar_init(&xbar[k], 1);
+#pragma unroll
+            for (int k = 0; k < WBR; ++k) mbar_init(&bbar[k], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (!XZERO)
+#pragma unroll
+                for (int k = 0; k < WXR; ++k) load_x(j0 - 2 + k);
+#pragma unroll
+            for (int k = 0; k < WBR; ++k) load_b(j0 - 1 + k);
+        }
+        if (!XZERO) {
+            wait_x(j0 - 2);
+            wait_x(j0 - 1);
+        }
+        // carried from the previous iteration: r of row y - 1 (the planes the patch reads there), the
+        // left neighbour's plane-9 residual of row y - 1, the dy = 0 corrections of patch row y - 1
+        // (the corrections in shared memory, one column per lane: cds[k][lane], slot 9 = c18)
+        double rp3 = 0, rp4 = 0, rp6 = 0, rp7 = 0, rp8 = 0, rp9 = 0, rpl9 = 0;
+        double* cdl = cds + lane;
+#pragma unroll 1
+        for (int y = j0 - 1; y <= yend; ++y) {
+            // ---- residual row y
+            if (!XZERO) wait_x(y + 1);
+            wait_b(y);
+            double rv[10];
+            {
+                const double* bp = br + ((y - (j0 - 1)) % WBR) * WBSLOT + (lane + 1);
+                if (!XZERO) {
+                    const double* x0 = xrow(y) + (lane + 1);
+                    double av[10];
+                    apply_rows<WXW, false>(L, xrow(y - 1) + (lane + 1), x0, xrow(y + 1) + (lane + 1), i, y, av);
+                    const unsigned m = active_mask(i, y, n);
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) rv[k] = ((m >> k) & 1u) ? bp[k * WBW] - av[k] : 0.0;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) rv[k] = bp[k * WBW];
+                }
+            }
+            __syncwarp();
+            // b row y consumed: its slot takes row y + WBR (one iteration ahead)
+            if (lane == 0 && y + WBR <= yend) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                load_b(y + WBR);
+            }
+            if (lane >= 1 && lane <= WT && i <= n && y >= j0 && y < yend) {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+            }
+            // ---- patch row y (vertex (i, y)); left neighbour's residuals by shuffle
+            const double l2 = __shfl_up_sync(0xffffffffu, rv[2], 1), l4 = __shfl_up_sync(0xffffffffu, rv[4], 1);
+            const double l5 = __shfl_up_sync(0xffffffffu, rv[5], 1), l7 = __shfl_up_sync(0xffffffffu, rv[7], 1);
+            const double l8 = __shfl_up_sync(0xffffffffu, rv[8], 1), l9 = __shfl_up_sync(0xffffffffu, rv[9], 1);
+            double o[20];
+            if (y >= j0 && lane >= 1 && i <= n && y <= n) {
+                double rr[20];
+                rr[0] = rv[0]; rr[1] = rv[1];
+                rr[2] = rv[2]; rr[3] = l2;   rr[4] = rv[3]; rr[5] = rp3;
+                rr[6] = l4;    rr[7] = rp4;
+                rr[8] = rv[5]; rr[9] = l5;   rr[10] = rv[6]; rr[11] = rp6;
+                rr[12] = l7;   rr[13] = rp7;
+                rr[14] = rv[8]; rr[15] = rpl9; rr[16] = l8; rr[17] = rp9;
+                rr[18] = l9;   rr[19] = rp8;
+                if (i > 0 && i < n && y > 0 && y < n) {
+                    patch_apply20r(P, 0, rr, o);
+                } else {   // boundary vertex: its outputs were computed by vanka_bnd_kernel
+                    const int nb = bnd_count(n), bi = bnd_index(i, y, n);
+#pragma unroll
+                    for (int k = 0; k < 20; ++k) o[k] = __ldg(P.bcorr + k * nb + bi);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 20; ++k) o[k] = 0.0;
+            }
+            rp3 = rv[3]; rp4 = rv[4]; rp6 = rv[6]; rp7 = rv[7]; rp8 = rv[8]; rp9 = rv[9]; rpl9 = l9;
+            // ---- owner row y - 1: carried dy = 0 sums + the dy = 1 corrections of patch row y
+            const double r15 = __shfl_down_sync(0xffffffffu, o[15], 1);
+            if (y >= j0 + 1) {
+                const int yo = y - 1;
+                if (lane >= 1 && lane <= WT && i <= n) {
+                    double d[10];
+                    d[0] = cdl[0];
+                    d[1] = cdl[32];
+                    d[2] = cdl[64];
+                    d[3] = cdl[96] + o[5];
+                    d[4] = cdl[128] + o[7];
+                    d[5] = cdl[160];
+                    d[6] = cdl[192] + o[11];
+                    d[7] = cdl[224] + o[13];
+                    d[8] = cdl[256] + o[19];
+                    d[9] = (r15 + o[17]) + cdl[288];
+                    const double* xv = xrow(yo) + (lane + 1);
+                    const unsigned m = active_mask(i, yo, n);
+                    const int64_t off = (int64_t)yo * L.pitch + i;
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) {
+                        const double xk = XZERO ? 0.0 : xv[k * WXW];
+                        xo[k * L.plane + off] = ((m >> k) & 1u) ? fma(P.omega, d[k], xk) : 0.0;
+                    }
+                }
+            }
+            // dy = 0 corrections of patch row y, summed in the owner's order (right neighbour by shuffle)
+            {
+                const double s3 = __shfl_down_sync(0xffffffffu, o[3], 1), s6 = __shfl_down_sync(0xffffffffu, o[6], 1);
+                const double s9 = __shfl_down_sync(0xffffffffu, o[9], 1), s12 = __shfl_down_sync(0xffffffffu, o[12], 1);
+                const double s16 = __shfl_down_sync(0xffffffffu, o[16], 1), s18 = __shfl_down_sync(0xffffffffu, o[18], 1);
+                cdl[0] = o[0];
+                cdl[32] = o[1];
+                cdl[64] = o[2] + s3;
+                cdl[96] = o[4];
+                cdl[128] = s6;
+                cdl[160] = o[8] + s9;
+                cdl[192] = o[10];
+                cdl[224] = s12;
+                cdl[256] = o[14] + s16;
+                cdl[288] = s18;
+            }
+            // x row y - 1 is dead (last read: residual row y, owner row y - 1): its slot takes row y + 3
+            if (!XZERO) {
+                __syncwarp();
+                if (lane == 0 && y + 3 <= yend + 1) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    load_x(y + 3);
+                }
+            }
+        }
+    }
+    if (S.out || S.state) norm_finish<W_NT>(S, nrm);
+}
+
+// ------------------------------------------------------------------------------------------
 // accumulator slot of coarse plane kc within its restriction group (MG_RESTRICT_G0..G3)
 __host__ __device__ constexpr int rslot(int kc) {
     return kc >= 8 ? 1 : (kc <= 1 ? 0 : (kc <= 4 ? kc - 2 : kc - 5));
@@ -2706,6 +3053,10 @@ void kernels_init() {
     set_smem(vanka_march2_kernel<false, 1>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 2>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 3>, M2SMEM);
+    set_smem(vanka_warp_kernel<false>, W_SMEM);
+    set_smem(vanka_bnd_kernel<false>, WB_SMEM);
+    set_smem(vanka_bnd_kernel<true>, WB_SMEM);
+    set_smem(vanka_warp_kernel<true>, W_SMEM);
     set_smem(bsr_a_march_kernel<false, false>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<false, true>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<true, false>, BMA_SMEM);
@@ -3261,6 +3612,27 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
     return cudaGetLastError();
 }
 
+// warp-marching sweep (vanka_warp_kernel) on levels with n >= MG_WARP_MIN_N (0: off); its tasks are
+// (strip of WT columns, segment of MH rows), one per warp, sized to whole waves of the 2 x WPC warps
+// per SM with segments near MG_WARP_TARGET rows
+static int g_warp_min_n = 1024;
+static void warp_tasks(int n, int& MH, int& nstrips, int& ntasks) {
+    static int target = -1;
+    if (target < 0) {
+        const char* v = getenv("MG_WARP_TARGET");
+        target = v ? std::max(4, atoi(v)) : 128;
+    }
+    nstrips = (n + WT) / WT;   // ceil((n + 1) / WT)
+    const long slots = (long)sm_count() * 2 * WPC;
+    const long base = (n + target) / target;
+    const long waves = std::max(1L, (nstrips * base + slots / 2) / slots);
+    long nseg = std::max(1L, waves * slots / nstrips);
+    MH = std::max(8, (int)((n + nseg) / nseg));
+    nseg = (n + MH) / MH;
+    ntasks = (int)(nstrips * nseg);
+}
+void set_warp_min_n(int n) { g_warp_min_n = n; }
+
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
                                 NormSink S, cudaStream_t s, const ProlSrc* E) {
     const LevelParams& L = P.L;
@@ -3280,6 +3652,21 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
+    if (!E && g_warp_min_n > 0 && L.n >= g_warp_min_n) {
+        int wmh, nstrips, ntasks;
+        warp_tasks(L.n, wmh, nstrips, ntasks);
+        CUtensorMap wx, wb;
+        e = encode_vec_map(&wx, x_zero ? b : x, L.n, L.pitch, L.plane, WXW, 1);
+        if (e == cudaSuccess) e = encode_vec_map(&wb, b, L.n, L.pitch, L.plane, WBW, 1);
+        if (e != cudaSuccess) return e;
+        const dim3 wgrid((ntasks + WPC - 1) / WPC);
+        const dim3 bgrid((bnd_count(L.n) + WB_NT - 1) / WB_NT);
+        if (x_zero) launch_k(vanka_bnd_kernel<true>, bgrid, WB_NT, WB_SMEM, s, P, x, b);
+        else launch_k(vanka_bnd_kernel<false>, bgrid, WB_NT, WB_SMEM, s, P, x, b);
+        if (x_zero) launch_k(vanka_warp_kernel<true>, wgrid, W_NT, W_SMEM, s, wx, wb, P, xo, S, wmh, nstrips, ntasks);
+        else launch_k(vanka_warp_kernel<false>, wgrid, W_NT, W_SMEM, s, wx, wb, P, xo, S, wmh, nstrips, ntasks);
+        return cudaGetLastError();
+    }
     if (x_zero) launch_k(vanka_march2_kernel<true, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
     else if (E && g_prol_ws == 1)
         launch_k(vanka_march2_kernel<false, 2>, grid, M2NT + 32 * m2np(2), M2SMEM, s, mx, mb, P, xo, S, MH, *E);
@@ -3291,7 +3678,9 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
 }
 int blocks_vanka_march2(int n) {
     const int MH = march_height(n, M2T, M2R, 3, relax_target(n));
-    return ((n + M2T) / M2T) * ((n + MH) / MH);
+    int wmh, nstrips, ntasks;
+    warp_tasks(n, wmh, nstrips, ntasks);
+    return std::max(((n + M2T) / M2T) * ((n + MH) / MH), (ntasks + WPC - 1) / WPC);
 }
 
 

@@ -84,6 +84,8 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s, const ProlSrc* E = nullptr);
 int blocks_vanka_march2(int n);
+// levels with n >= N run the plain Vanka sweeps through the warp-marching kernel (0: never)
+void set_warp_min_n(int N);
 int blocks_residual_march(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)
