@@ -2086,9 +2086,35 @@ __device__ __forceinline__ int bnd_index(int a, int b, int n) {
     return b == 0 ? a : (b == n ? (n + 1) + a : (a == 0 ? 2 * (n + 1) + (b - 1) : 2 * (n + 1) + (n - 1) + (b - 1)));
 }
 constexpr int WB_NT = 64, WB_SMEM = WB_NT * 160 * 8;
-template <bool XZERO>
+// x(i, j) += P e_H (i, j) for one fine index, all ten planes (prolong_kernel's table chains, same order)
+__device__ __forceinline__ void prol_point(const ProlSrc& E, int i, int j, int n, double xk[10]) {
+    const int I = i >> 1, J = j >> 1;
+    if (i < 0 || j < 0 || I >= E.nc || J >= E.nc) return;
+    const double* e0 = E.e + (int64_t)J * E.pitchc + I;
+    const unsigned m = active_mask(i, j, n);
+#define EQ(dI, dJ, pl, wt) v = fma(wt, __ldg(e0 + (pl) * E.planec + (dJ) * E.pitchc + (dI)), v);
+#define P1(di, dj, kf)                                   \
+    {                                                    \
+        double v = 0.0;                                  \
+        MG_PROLONG_##di##_##dj##_##kf(EQ)                \
+        if (m & (1u << (kf))) xk[kf] += v;               \
+    }
+#define P10(di, dj) P1(di, dj, 0) P1(di, dj, 1) P1(di, dj, 2) P1(di, dj, 3) P1(di, dj, 4) \
+                    P1(di, dj, 5) P1(di, dj, 6) P1(di, dj, 7) P1(di, dj, 8) P1(di, dj, 9)
+    switch ((i & 1) + 2 * (j & 1)) {
+        case 0: P10(0, 0) break;
+        case 1: P10(1, 0) break;
+        case 2: P10(0, 1) break;
+        default: P10(1, 1) break;
+    }
+#undef P10
+#undef P1
+#undef EQ
+}
+
+template <bool XZERO, bool PROL>
 __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, const double* __restrict__ x,
-                                                          const double* __restrict__ b) {
+                                                          const double* __restrict__ b, const ProlSrc E) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(16) double smb[];
@@ -2117,15 +2143,18 @@ __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, c
     } else {
         double* tile = smb + threadIdx.x * 160;   // [10][4][4]: x at columns a-2 .. a+1, rows bb-2 .. bb+1
 #pragma unroll
-        for (int k = 0; k < 10; ++k)
+        for (int ry = 0; ry < 4; ++ry)
 #pragma unroll
-            for (int ry = 0; ry < 4; ++ry)
+            for (int rx = 0; rx < 4; ++rx) {
+                const int i = a - 2 + rx, j = bb - 2 + ry;
+                const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
+                double xk[10];
 #pragma unroll
-                for (int rx = 0; rx < 4; ++rx) {
-                    const int i = a - 2 + rx, j = bb - 2 + ry;
-                    tile[k * 16 + ry * 4 + rx] =
-                        (i >= 0 && j >= 0 && i <= n && j <= n) ? __ldg(x + k * L.plane + (int64_t)j * L.pitch + i) : 0.0;
-                }
+                for (int k = 0; k < 10; ++k) xk[k] = in ? __ldg(x + k * L.plane + (int64_t)j * L.pitch + i) : 0.0;
+                if (PROL && in) prol_point(E, i, j, n, xk);
+#pragma unroll
+                for (int k = 0; k < 10; ++k) tile[k * 16 + ry * 4 + rx] = xk[k];
+            }
 #pragma unroll
         for (int py = 0; py < 2; ++py)
 #pragma unroll
@@ -2173,19 +2202,39 @@ constexpr int WXROW = 10 * WXW, WBROW = 10 * WBW;
 constexpr int WXSLOT = (WXROW + 15) / 16 * 16;   // ring slot strides: 128-byte aligned TMA destinations
 constexpr int WBSLOT = (WBROW + 15) / 16 * 16;
 constexpr int W_WARP_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + 10 * 32) * 8 + 64 + 127) / 128 * 128;
+// PROL (first post-sweep with the coarse-grid correction x + P e_H fused in): + a 3-row ring of coarse
+// rows (20-column boxes from the even column at or below (i0 - 2) / 2, one TMA box per coarse row)
+constexpr int WCC = 20, WCROW = 10 * WCC, WCSLOT = (WCROW + 15) / 16 * 16, WCR = 3;
+// (the PROL kernel carries the patch-correction sums in registers instead of the [10][32] shared row,
+// which keeps it at 6 warps per CTA, 12 per SM; MG_WARP_CDREG=0: shared row, 5 warps per CTA)
+#ifndef MG_WARP_CDREG
+#define MG_WARP_CDREG 1
+#endif
+constexpr int W_WARP_BYTES_P =
+    ((WXR * WXSLOT + WBR * WBSLOT + (MG_WARP_CDREG ? 0 : 10 * 32) + WCR * WCSLOT) * 8 + 64 + 127) / 128 * 128;
 #ifndef MG_WPC
 #define MG_WPC 6   // warps per CTA (2 CTAs per SM)
 #endif
+#ifndef MG_WPC_P
+#define MG_WPC_P (MG_WARP_CDREG ? 6 : 5)
+#endif
+template <bool PROL> struct WGeom {
+    static constexpr int NW = PROL ? MG_WPC_P : MG_WPC, BYTES = PROL ? W_WARP_BYTES_P : W_WARP_BYTES;
+    static constexpr int NT = 32 * NW, SMEM = NW * BYTES;
+};
 constexpr int WPC = MG_WPC, W_NT = 32 * WPC, W_SMEM = WPC * W_WARP_BYTES;
-static_assert(2 * (W_SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
+static_assert(2 * (WGeom<false>::SMEM + 1024) <= 228 * 1024 && 2 * (WGeom<true>::SMEM + 1024) <= 228 * 1024,
+              "two CTAs per SM");
 static_assert((WXW * 8) % 16 == 0 && (WBW * 8) % 16 == 0 && (WXSLOT * 8) % 128 == 0 && (WBSLOT * 8) % 128 == 0,
               "TMA box rows and ring slots 16 / 128-byte aligned");
 
-template <bool XZERO>
-__global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_constant__ CUtensorMap tmx,
-                                                             const __grid_constant__ CUtensorMap tmb,
-                                                             const VankaParams P, double* __restrict__ xo,
-                                                             NormSink S, int MH, int nstrips, int ntasks) {
+template <bool XZERO, bool PROL>
+__global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                                        const __grid_constant__ CUtensorMap tmb,
+                                                                        const __grid_constant__ CUtensorMap tmc,
+                                                                        const VankaParams P, double* __restrict__ xo,
+                                                                        NormSink S, int MH, int nstrips, int ntasks,
+                                                                        const ProlSrc E) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) double sm[];
@@ -2193,14 +2242,17 @@ __global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_consta
     if (*L.stop) return;
     const int n = L.n;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int task = blockIdx.x * WPC + w;
+    const int task = blockIdx.x * WGeom<PROL>::NW + w;
     double nrm = 0.0;
     if (task < ntasks) {
-        double* xr = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + w * W_WARP_BYTES);   // [WXR][10][WXW] (slot stride WXSLOT)
+        double* xr = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + w * WGeom<PROL>::BYTES);   // [WXR][10][WXW] (slot stride WXSLOT)
         double* br = xr + WXR * WXSLOT;                                                              // [WBR][10][WBW]
-        double* cds = br + WBR * WBSLOT;                                                             // [10][32]
-        uint64_t* xbar = reinterpret_cast<uint64_t*>(cds + 10 * 32);                                 // [WXR]
+        constexpr bool CDREG = PROL && MG_WARP_CDREG;
+        double* cds = br + WBR * WBSLOT;                                                             // [10][32] (!CDREG)
+        double* cr = cds + (CDREG ? 0 : 10 * 32);                                                    // PROL: [WCR][10][WCC]
+        uint64_t* xbar = reinterpret_cast<uint64_t*>(cr + (PROL ? WCR * WCSLOT : 0));                // [WXR]
         uint64_t* bbar = xbar + WXR;                                                                 // [WBR]
+        uint64_t* cbar = bbar + WBR;                                                                 // PROL: [WCR]
         // tasks of the two boundary strips first (their dense boundary patches make them the slowest;
         // started in the first wave they do not trail the grid), then seg-major over the inner strips
         int strip, seg;
@@ -2235,34 +2287,103 @@ __global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_consta
         auto wait_x = [&](int y) { const int q = y - (j0 - 2); mbar_wait(&xbar[q % WXR], (q / WXR) & 1); };
         auto wait_b = [&](int y) { const int q = y - (j0 - 1); mbar_wait(&bbar[q % WBR], (q / WBR) & 1); };
         auto xrow = [&](int y) { return xr + ((y - (j0 - 2)) % WXR) * WXSLOT; };
+        // PROL: coarse row J (load number J - Jb, slot % WCR); fine row r needs coarse rows r >> 1, (r >> 1) + 1
+        const int I0 = (i0 - 2) >> 1, Iorg = I0 & ~1, Jb = (j0 - 2) >> 1, Jmax = ((yend + 1) >> 1) + 1;
+        auto load_c = [&](int J) {
+            const int q = J - Jb;
+            uint64_t* bar = &cbar[q % WCR];
+            mbar_expect_tx(bar, WCROW * 8);
+            tma_load3(cr + (q % WCR) * WCSLOT, &tmc, Iorg, J, 0, bar);
+        };
+        auto wait_c = [&](int J) { const int q = J - Jb; mbar_wait(&cbar[q % WCR], (q / WCR) & 1); };
+        auto crow = [&](int J) { return cr + ((J - Jb) % WCR) * WCSLOT; };
         if (lane == 0) {
 #pragma unroll
             for (int k = 0; k < WXR; ++k) mbar_init(&xbar[k], 1);
 #pragma unroll
             for (int k = 0; k < WBR; ++k) mbar_init(&bbar[k], 1);
+            if (PROL)
+#pragma unroll
+                for (int k = 0; k < WCR; ++k) mbar_init(&cbar[k], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
         if (lane == 0) {
+            if (PROL)
+#pragma unroll
+                for (int k = 0; k < WCR; ++k)
+                    if (Jb + k <= Jmax) load_c(Jb + k);
             if (!XZERO)
 #pragma unroll
                 for (int k = 0; k < WXR; ++k) load_x(j0 - 2 + k);
 #pragma unroll
             for (int k = 0; k < WBR; ++k) load_b(j0 - 1 + k);
         }
+        // PROL: x row r += P e_H in the ring (lanes 0-16: the column pair (2I, 2I+1), I = I0 + lane, of
+        // fine row r; the prolongation's table arithmetic in table order, bitwise prolong_kernel's)
+        auto prol_row = [&](int r) {
+            const int J = r >> 1;
+            wait_c(J);
+            wait_c(J + 1);
+            const int I = I0 + lane;
+            if (lane <= 16 && I >= 0 && I < E.nc && J >= 0 && J < E.nc) {
+                const double* c0 = crow(J) + (I - Iorg);
+                const double* c1 = crow(J + 1) + (I - Iorg);
+                double pe[20];
+#define PL(dI, dJ, pl) pe[pslot20(dI, dJ, pl)] = ((dJ) ? c1 : c0)[(pl) * WCC + (dI)];
+                PL(0, 0, 0) PL(0, 0, 1) PL(0, 0, 2) PL(0, 0, 3) PL(0, 0, 4) PL(0, 1, 0) PL(0, 1, 1)
+                PL(0, 1, 2) PL(1, 0, 0) PL(1, 0, 1) PL(1, 0, 3) PL(1, 1, 0) PL(1, 1, 1)
+                PL(0, 0, 5) PL(0, 0, 6) PL(0, 0, 7) PL(0, 0, 8) PL(0, 0, 9) PL(0, 1, 5) PL(1, 0, 6)
+#undef PL
+                double* xrw = xrow(r) + 2 * lane;
+                const int fi = 2 * I;
+                const unsigned m0 = active_mask(fi, r, n), m1 = active_mask(fi + 1, r, n);
+#define PQ(dI, dJ, pl, wt) v = fma(wt, pe[pslot20(dI, dJ, pl)], v);
+#define PX(dj, kf)                                                                    \
+    {                                                                                 \
+        double v = 0.0;                                                               \
+        MG_PROLONG_0_##dj##_##kf(PQ) const double v0 = v;                             \
+        v = 0.0;                                                                      \
+        MG_PROLONG_1_##dj##_##kf(PQ) double2* x2 = reinterpret_cast<double2*>(xrw + (kf) * WXW); \
+        double2 xv = *x2;                                                             \
+        if (m0 & (1u << (kf))) xv.x += v0;                                            \
+        if (m1 & (1u << (kf))) xv.y += v;                                             \
+        *x2 = xv;                                                                     \
+    }
+                if (r & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
+                else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+#undef PX
+#undef PQ
+            }
+            __syncwarp();
+            // after an odd fine row, coarse row J is dead: its slot takes J + WCR
+            if ((r & 1) && lane == 0 && J + WCR <= Jmax) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                load_c(J + WCR);
+            }
+        };
         if (!XZERO) {
             wait_x(j0 - 2);
             wait_x(j0 - 1);
+            if (PROL) {
+                prol_row(j0 - 2);
+                prol_row(j0 - 1);
+            }
         }
         // carried from the previous iteration: r of row y - 1 (the planes the patch reads there), the
         // left neighbour's plane-9 residual of row y - 1, the dy = 0 corrections of patch row y - 1
         // (the corrections in shared memory, one column per lane: cds[k][lane], slot 9 = c18)
         double rp3 = 0, rp4 = 0, rp6 = 0, rp7 = 0, rp8 = 0, rp9 = 0, rpl9 = 0;
         double* cdl = cds + lane;
+        double cdr[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) cdr[k] = 0.0;
+#define CD(k) (*(CDREG ? &cdr[k] : &cdl[32 * (k)]))
 #pragma unroll 1
         for (int y = j0 - 1; y <= yend; ++y) {
             // ---- residual row y
             if (!XZERO) wait_x(y + 1);
+            if (PROL) prol_row(y + 1);
             wait_b(y);
             double rv[10];
             {
@@ -2321,16 +2442,16 @@ __global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_consta
                 const int yo = y - 1;
                 if (lane >= 1 && lane <= WT && i <= n) {
                     double d[10];
-                    d[0] = cdl[0];
-                    d[1] = cdl[32];
-                    d[2] = cdl[64];
-                    d[3] = cdl[96] + o[5];
-                    d[4] = cdl[128] + o[7];
-                    d[5] = cdl[160];
-                    d[6] = cdl[192] + o[11];
-                    d[7] = cdl[224] + o[13];
-                    d[8] = cdl[256] + o[19];
-                    d[9] = (r15 + o[17]) + cdl[288];
+                    d[0] = CD(0);
+                    d[1] = CD(1);
+                    d[2] = CD(2);
+                    d[3] = CD(3) + o[5];
+                    d[4] = CD(4) + o[7];
+                    d[5] = CD(5);
+                    d[6] = CD(6) + o[11];
+                    d[7] = CD(7) + o[13];
+                    d[8] = CD(8) + o[19];
+                    d[9] = (r15 + o[17]) + CD(9);
                     const double* xv = xrow(yo) + (lane + 1);
                     const unsigned m = active_mask(i, yo, n);
                     const int64_t off = (int64_t)yo * L.pitch + i;
@@ -2346,16 +2467,16 @@ __global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_consta
                 const double s3 = __shfl_down_sync(0xffffffffu, o[3], 1), s6 = __shfl_down_sync(0xffffffffu, o[6], 1);
                 const double s9 = __shfl_down_sync(0xffffffffu, o[9], 1), s12 = __shfl_down_sync(0xffffffffu, o[12], 1);
                 const double s16 = __shfl_down_sync(0xffffffffu, o[16], 1), s18 = __shfl_down_sync(0xffffffffu, o[18], 1);
-                cdl[0] = o[0];
-                cdl[32] = o[1];
-                cdl[64] = o[2] + s3;
-                cdl[96] = o[4];
-                cdl[128] = s6;
-                cdl[160] = o[8] + s9;
-                cdl[192] = o[10];
-                cdl[224] = s12;
-                cdl[256] = o[14] + s16;
-                cdl[288] = s18;
+                CD(0) = o[0];
+                CD(1) = o[1];
+                CD(2) = o[2] + s3;
+                CD(3) = o[4];
+                CD(4) = s6;
+                CD(5) = o[8] + s9;
+                CD(6) = o[10];
+                CD(7) = s12;
+                CD(8) = o[14] + s16;
+                CD(9) = s18;
             }
             // x row y - 1 is dead (last read: residual row y, owner row y - 1): its slot takes row y + 3
             if (!XZERO) {
@@ -2367,7 +2488,8 @@ __global__ void __launch_bounds__(W_NT, 2) vanka_warp_kernel(const __grid_consta
             }
         }
     }
-    if (S.out || S.state) norm_finish<W_NT>(S, nrm);
+#undef CD
+    if (S.out || S.state) norm_finish<WGeom<PROL>::NT>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -3053,10 +3175,12 @@ void kernels_init() {
     set_smem(vanka_march2_kernel<false, 1>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 2>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 3>, M2SMEM);
-    set_smem(vanka_warp_kernel<false>, W_SMEM);
-    set_smem(vanka_bnd_kernel<false>, WB_SMEM);
-    set_smem(vanka_bnd_kernel<true>, WB_SMEM);
-    set_smem(vanka_warp_kernel<true>, W_SMEM);
+    set_smem(vanka_warp_kernel<false, false>, WGeom<false>::SMEM);
+    set_smem(vanka_warp_kernel<false, true>, WGeom<true>::SMEM);
+    set_smem(vanka_warp_kernel<true, false>, WGeom<false>::SMEM);
+    set_smem(vanka_bnd_kernel<false, false>, WB_SMEM);
+    set_smem(vanka_bnd_kernel<false, true>, WB_SMEM);
+    set_smem(vanka_bnd_kernel<true, false>, WB_SMEM);
     set_smem(bsr_a_march_kernel<false, false>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<false, true>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<true, false>, BMA_SMEM);
@@ -3616,14 +3740,16 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
 // (strip of WT columns, segment of MH rows), one per warp, sized to whole waves of the 2 x WPC warps
 // per SM with segments near MG_WARP_TARGET rows
 static int g_warp_min_n = 1024;
-static void warp_tasks(int n, int& MH, int& nstrips, int& ntasks) {
+static int g_warp_prol = 1;   // the fused-prolongation post-sweep through the warp kernel too (MG_WARP_PROL)
+void set_warp_prol(int on) { g_warp_prol = on; }
+static void warp_tasks(int n, int& MH, int& nstrips, int& ntasks, bool prol = false) {
     static int target = -1;
     if (target < 0) {
         const char* v = getenv("MG_WARP_TARGET");
         target = v ? std::max(4, atoi(v)) : 128;
     }
     nstrips = (n + WT) / WT;   // ceil((n + 1) / WT)
-    const long slots = (long)sm_count() * 2 * WPC;
+    const long slots = (long)sm_count() * 2 * (prol ? WGeom<true>::NW : WGeom<false>::NW);
     const long base = (n + target) / target;
     const long waves = std::max(1L, (nstrips * base + slots / 2) / slots);
     long nseg = std::max(1L, waves * slots / nstrips);
@@ -3652,19 +3778,31 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     dim3 grid((L.n + M2T) / M2T, (L.n + MH) / MH);
     const ProlSrc none{nullptr, 0, 0, 0};
     if (E && x_zero) return cudaErrorInvalidValue;
-    if (!E && g_warp_min_n > 0 && L.n >= g_warp_min_n) {
+    if (g_warp_min_n > 0 && L.n >= g_warp_min_n && (!E || g_warp_prol)) {
+        const bool prol = E != nullptr;
         int wmh, nstrips, ntasks;
-        warp_tasks(L.n, wmh, nstrips, ntasks);
-        CUtensorMap wx, wb;
+        warp_tasks(L.n, wmh, nstrips, ntasks, prol);
+        CUtensorMap wx, wb, wc;
         e = encode_vec_map(&wx, x_zero ? b : x, L.n, L.pitch, L.plane, WXW, 1);
         if (e == cudaSuccess) e = encode_vec_map(&wb, b, L.n, L.pitch, L.plane, WBW, 1);
+        if (e == cudaSuccess && prol) e = encode_vec_map(&wc, E->e, E->nc, E->pitchc, E->planec, WCC, 1);
         if (e != cudaSuccess) return e;
-        const dim3 wgrid((ntasks + WPC - 1) / WPC);
+        const ProlSrc Ev = prol ? *E : none;
+        const int nw = prol ? WGeom<true>::NW : WGeom<false>::NW;
+        const dim3 wgrid((ntasks + nw - 1) / nw);
         const dim3 bgrid((bnd_count(L.n) + WB_NT - 1) / WB_NT);
-        if (x_zero) launch_k(vanka_bnd_kernel<true>, bgrid, WB_NT, WB_SMEM, s, P, x, b);
-        else launch_k(vanka_bnd_kernel<false>, bgrid, WB_NT, WB_SMEM, s, P, x, b);
-        if (x_zero) launch_k(vanka_warp_kernel<true>, wgrid, W_NT, W_SMEM, s, wx, wb, P, xo, S, wmh, nstrips, ntasks);
-        else launch_k(vanka_warp_kernel<false>, wgrid, W_NT, W_SMEM, s, wx, wb, P, xo, S, wmh, nstrips, ntasks);
+        if (x_zero) launch_k(vanka_bnd_kernel<true, false>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
+        else if (prol) launch_k(vanka_bnd_kernel<false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
+        else launch_k(vanka_bnd_kernel<false, false>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
+        if (x_zero)
+            launch_k(vanka_warp_kernel<true, false>, wgrid, WGeom<false>::NT, WGeom<false>::SMEM, s, wx, wb, wx, P, xo, S,
+                     wmh, nstrips, ntasks, Ev);
+        else if (prol)
+            launch_k(vanka_warp_kernel<false, true>, wgrid, WGeom<true>::NT, WGeom<true>::SMEM, s, wx, wb, wc, P, xo, S,
+                     wmh, nstrips, ntasks, Ev);
+        else
+            launch_k(vanka_warp_kernel<false, false>, wgrid, WGeom<false>::NT, WGeom<false>::SMEM, s, wx, wb, wx, P, xo,
+                     S, wmh, nstrips, ntasks, Ev);
         return cudaGetLastError();
     }
     if (x_zero) launch_k(vanka_march2_kernel<true, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
@@ -3680,7 +3818,10 @@ int blocks_vanka_march2(int n) {
     const int MH = march_height(n, M2T, M2R, 3, relax_target(n));
     int wmh, nstrips, ntasks;
     warp_tasks(n, wmh, nstrips, ntasks);
-    return std::max(((n + M2T) / M2T) * ((n + MH) / MH), (ntasks + WPC - 1) / WPC);
+    int wmhp, nstripsp, ntasksp;
+    warp_tasks(n, wmhp, nstripsp, ntasksp, true);
+    return std::max(std::max(((n + M2T) / M2T) * ((n + MH) / MH), (ntasks + WPC - 1) / WPC),
+                    (ntasksp + WGeom<true>::NW - 1) / WGeom<true>::NW);
 }
 
 

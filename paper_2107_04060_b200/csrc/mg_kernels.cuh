@@ -86,6 +86,8 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
 int blocks_vanka_march2(int n);
 // levels with n >= N run the plain Vanka sweeps through the warp-marching kernel (0: never)
 void set_warp_min_n(int N);
+// the fused-prolongation post-sweep through the warp-marching kernel as well (1) or the CTA kernel (0)
+void set_warp_prol(int on);
 int blocks_residual_march(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)

@@ -266,21 +266,24 @@ def test_warp_sweep_bitwise(n, levels, pname, nu2):
     """The warp-marching Vanka sweep (vanka_warp_kernel: one warp per 30-column strip, residuals and
     patch corrections moved between lanes by shuffles) gives bitwise the iterates and fused norms
     of the CTA row-marching sweep on every level (same arithmetic, same summation order; PAPER.md:
-    575-588), for the zero-initial-guess pre-sweeps, the level-0 sweep with its fused norm, ragged
-    strips (49 columns = 30 + 19) and ragged row segments."""
+    575-588), for the zero-initial-guess pre-sweeps, the level-0 sweep with its fused norm, the first
+    post-sweep with the prolongation fused in, ragged strips (49 columns = 30 +
+    19) and ragged row segments."""
     torch = _torch()
     from paper_2107_04060_b200 import Opts
     b = mg_inputs.uniform_rhs(n, 5)
     out = []
-    for warp in ("1", "0"):
-        H = C.gpu_hierarchy(n, levels, pname, march=True,
-                            env={"MG_WARP_MIN_N": warp, "MG_FUSE_PROLONG": "0"})
+    # (warp kernel on every level, prolongation fused into the first post-sweep); the last is the
+    # reference: CTA marching kernels with a separate prolong_kernel
+    for warp, fuse in (("1", "1"), ("1", "0"), ("0", "1"), ("0", "0")):
+        H = C.gpu_hierarchy(n, levels, pname, march=True, env={"MG_WARP_MIN_N": warp, "MG_FUSE_PROLONG": fuse})
         xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
         hist = [H.cycle(xd, bd, Opts(1, nu2, "vanka", 0.7)) for _ in range(3)]
         out.append((H.to_host(xd), hist))
         H.close()
-    assert np.array_equal(out[0][0], out[1][0])
-    assert out[0][1] == out[1][1]
+    for k in range(3):
+        assert np.array_equal(out[k][0], out[3][0]), k
+        assert out[k][1] == out[3][1], k
 
 
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (128, 6, "stiff", 1)])
