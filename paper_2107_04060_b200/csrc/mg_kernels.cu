@@ -2024,6 +2024,30 @@ __global__ void __launch_bounds__(M2NT + 32 * m2np(PV), 3) vanka_march2_kernel(c
 }
 
 // ------------------------------------------------------------------------------------------
+// dense boundary-class patch solve out of line (the warp sweep's boundary lanes when no
+// vanka_bnd_kernel runs): patch_apply20's boundary branch, same order, through local memory so the
+// dense pass's coefficient loads never set the register budget of the interior path
+__device__ __noinline__ void patch_bnd20(const double* __restrict__ gb, const double* rr, double* o) {
+    const double2* G = reinterpret_cast<const double2*>(gb);
+#pragma unroll 1
+    for (int a = 0; a < 20; a += 4) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < 10; ++c2) {
+            const double2 g0 = __ldg(G + (a + 0) * 10 + c2), g1 = __ldg(G + (a + 1) * 10 + c2);
+            const double2 g2 = __ldg(G + (a + 2) * 10 + c2), g3 = __ldg(G + (a + 3) * 10 + c2);
+            s0 = fma(g0.x, rr[2 * c2], s0); s0 = fma(g0.y, rr[2 * c2 + 1], s0);
+            s1 = fma(g1.x, rr[2 * c2], s1); s1 = fma(g1.y, rr[2 * c2 + 1], s1);
+            s2 = fma(g2.x, rr[2 * c2], s2); s2 = fma(g2.y, rr[2 * c2 + 1], s2);
+            s3 = fma(g3.x, rr[2 * c2], s3); s3 = fma(g3.y, rr[2 * c2 + 1], s3);
+        }
+        o[a + 0] = s0;
+        o[a + 1] = s1;
+        o[a + 2] = s2;
+        o[a + 3] = s3;
+    }
+}
+
 // patch_apply20 with the 20 outputs in registers (the warp-marching sweep moves them between lanes
 // by shuffles instead of a shared-memory ring).  Same arithmetic and summation order as
 // patch_apply20 (interior: +/- blocks; boundary class: dense table, four output rows per pass).
@@ -2182,6 +2206,93 @@ __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, c
     patch_apply20(P, vertex_class(a, bb, n), rr, P.bcorr + t, nb);
 }
 
+// Cooperative version (the default): a CTA takes a run of 32 boundary vertices of one side, stages
+// the x tile (with P e_H added, PROL) in shared memory once, computes each residual position once
+// and splits the dense patch solves over 4 threads per vertex (5 outputs each, same order).
+constexpr int WB2_T = 32, WB2_NT = 128, WB2_XS = 10 * 4 * 35, WB2_RS = 10 * 2 * 33;
+template <bool XZERO, bool PROL>
+__global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P, const double* __restrict__ x,
+                                                            const double* __restrict__ b, const ProlSrc E) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double xt[WB2_XS];   // [10][PH + 2][PW + 2], plane stride 140
+    __shared__ double rt[WB2_RS];   // [10][PH][PW], plane stride 66
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n, nb = bnd_count(n), side = blockIdx.y, t = threadIdx.x;
+    const bool horiz = side < 2;
+    const int v0 = blockIdx.x * WB2_T;
+    // vertex run: horizontal sides a = v0 .. v0 + 31 at b = 0 / n; vertical b = v0 .. v0 + 31 at a = 0 / n
+    const int fixed = (side & 1) ? n : 0;
+    const int PW = horiz ? WB2_T + 1 : 2, PH = horiz ? 2 : WB2_T + 1;
+    const int pi0 = horiz ? v0 - 1 : fixed - 1, pj0 = horiz ? fixed - 1 : v0 - 1;   // residual origin
+    const int XW = PW + 2;
+    if (!XZERO) {
+        for (int p = t; p < (PW + 2) * (PH + 2); p += WB2_NT) {
+            const int ly = p / XW, lx = p - ly * XW;
+            const int i = pi0 - 1 + lx, j = pj0 - 1 + ly;
+            const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
+            double xk[10];
+#pragma unroll
+            for (int k = 0; k < 10; ++k) xk[k] = in ? __ldg(x + k * L.plane + (int64_t)j * L.pitch + i) : 0.0;
+            if (PROL && in) prol_point(E, i, j, n, xk);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) xt[k * 140 + p] = xk[k];
+        }
+        __syncthreads();
+    }
+    for (int p = t; p < PW * PH; p += WB2_NT) {
+        const int ly = p / PW, lx = p - ly * PW;
+        const int i = pi0 + lx, j = pj0 + ly;
+        const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
+        const int64_t o = in ? (int64_t)j * L.pitch + i : 0;
+        if (XZERO) {
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rt[k * 66 + p] = in ? __ldg(b + k * L.plane + o) : 0.0;
+        } else {
+            const double* x0 = xt + (ly + 1) * XW + (lx + 1);
+            double av[10];
+            apply_rows<140, false>(L, x0 - XW, x0, x0 + XW, i, j, av);
+            const unsigned m = active_mask(i, j, n);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rt[k * 66 + p] = ((m >> k) & 1u) ? __ldg(b + k * L.plane + o) - av[k] : 0.0;
+        }
+    }
+    __syncthreads();
+    // patches: vertex q = t / 4 of the run, outputs 5 (t % 4) .. 5 (t % 4) + 4
+    const int q = t >> 2, part = t & 3;
+    const int a = horiz ? v0 + q : fixed, bb = horiz ? fixed : v0 + q;
+    const bool valid = horiz ? (a <= n) : (bb >= 1 && bb <= n - 1);
+    if (!valid || (!horiz && n < 2)) return;
+    // residual of (a + dx, bb + dy), dx, dy in {-1, 0}: tile position (a + dx - pi0, bb + dy - pj0)
+    const double* r00 = rt + (bb - pj0) * PW + (a - pi0);
+#define RR(dx, dy, pl) r00[(pl) * 66 + (dy) * PW + (dx)]
+    double rr[20];
+    rr[0] = RR(0, 0, 0);   rr[1] = RR(0, 0, 1);
+    rr[2] = RR(0, 0, 2);   rr[3] = RR(-1, 0, 2);  rr[4] = RR(0, 0, 3);   rr[5] = RR(0, -1, 3);
+    rr[6] = RR(-1, 0, 4);  rr[7] = RR(0, -1, 4);
+    rr[8] = RR(0, 0, 5);   rr[9] = RR(-1, 0, 5);  rr[10] = RR(0, 0, 6);  rr[11] = RR(0, -1, 6);
+    rr[12] = RR(-1, 0, 7); rr[13] = RR(0, -1, 7);
+    rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
+    rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
+#undef RR
+    const double* G = P.gbnd + vertex_class(a, bb, n) * 400;
+    double* out = P.bcorr + bnd_index(a, bb, n);
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+        const int k = part * 5 + u;
+        const double2* g = reinterpret_cast<const double2*>(G + k * 20);
+        double sacc = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < 10; ++c2) {
+            const double2 gg = __ldg(g + c2);
+            sacc = fma(gg.x, rr[2 * c2], sacc);
+            sacc = fma(gg.y, rr[2 * c2 + 1], sacc);
+        }
+        out[k * nb] = sacc;
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Warp-marching Vanka sweep (the level-0 hot kernel when MG_WARP_MIN_N <= n).  Same arithmetic as
 // vanka_march2_kernel / vanka_kernel (residual, 20-DoF patch solves, owner-computes update,
@@ -2228,7 +2339,7 @@ static_assert(2 * (WGeom<false>::SMEM + 1024) <= 228 * 1024 && 2 * (WGeom<true>:
 static_assert((WXW * 8) % 16 == 0 && (WBW * 8) % 16 == 0 && (WXSLOT * 8) % 128 == 0 && (WBSLOT * 8) % 128 == 0,
               "TMA box rows and ring slots 16 / 128-byte aligned");
 
-template <bool XZERO, bool PROL>
+template <bool XZERO, bool PROL, bool BK>
 __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                         const __grid_constant__ CUtensorMap tmb,
                                                                         const __grid_constant__ CUtensorMap tmc,
@@ -2426,10 +2537,17 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
                 rr[18] = l9;   rr[19] = rp8;
                 if (i > 0 && i < n && y > 0 && y < n) {
                     patch_apply20r(P, 0, rr, o);
-                } else {   // boundary vertex: its outputs were computed by vanka_bnd_kernel
+                } else if (BK) {   // boundary vertex: its outputs were computed by vanka_bnd_kernel
                     const int nb = bnd_count(n), bi = bnd_index(i, y, n);
 #pragma unroll
                     for (int k = 0; k < 20; ++k) o[k] = __ldg(P.bcorr + k * nb + bi);
+                } else {           // boundary vertex: dense class inverse, out of line
+                    double rb[20], ob[20];
+#pragma unroll
+                    for (int k = 0; k < 20; ++k) rb[k] = rr[k];
+                    patch_bnd20(P.gbnd + vertex_class(i, y, n) * 400, rb, ob);
+#pragma unroll
+                    for (int k = 0; k < 20; ++k) o[k] = ob[k];
                 }
             } else {
 #pragma unroll
@@ -3175,10 +3293,16 @@ void kernels_init() {
     set_smem(vanka_march2_kernel<false, 1>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 2>, M2SMEM);
     set_smem(vanka_march2_kernel<false, 3>, M2SMEM);
-    set_smem(vanka_warp_kernel<false, false>, WGeom<false>::SMEM);
-    set_smem(vanka_warp_kernel<false, true>, WGeom<true>::SMEM);
-    set_smem(vanka_warp_kernel<true, false>, WGeom<false>::SMEM);
+    set_smem(vanka_warp_kernel<false, false, true>, WGeom<false>::SMEM);
+    set_smem(vanka_warp_kernel<false, true, true>, WGeom<true>::SMEM);
+    set_smem(vanka_warp_kernel<true, false, true>, WGeom<false>::SMEM);
+    set_smem(vanka_warp_kernel<false, false, false>, WGeom<false>::SMEM);
+    set_smem(vanka_warp_kernel<false, true, false>, WGeom<true>::SMEM);
+    set_smem(vanka_warp_kernel<true, false, false>, WGeom<false>::SMEM);
     set_smem(vanka_bnd_kernel<false, false>, WB_SMEM);
+    carve(vanka_bnd2_kernel<false, false>);
+    carve(vanka_bnd2_kernel<false, true>);
+    carve(vanka_bnd2_kernel<true, false>);
     set_smem(vanka_bnd_kernel<false, true>, WB_SMEM);
     set_smem(vanka_bnd_kernel<true, false>, WB_SMEM);
     set_smem(bsr_a_march_kernel<false, false>, BMA_SMEM);
@@ -3740,7 +3864,9 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
 // (strip of WT columns, segment of MH rows), one per warp, sized to whole waves of the 2 x WPC warps
 // per SM with segments near MG_WARP_TARGET rows
 static int g_warp_min_n = 1024;
-static int g_warp_prol = 1;   // the fused-prolongation post-sweep through the warp kernel too (MG_WARP_PROL)
+static int g_warp_prol = 1;
+static int g_warp_bk = 1;     // boundary-vertex patches precomputed by 1: vanka_bnd2_kernel, 2: vanka_bnd_kernel; 0: out of line in the sweep
+void set_warp_bk(int on) { g_warp_bk = on; }   // the fused-prolongation post-sweep through the warp kernel too (MG_WARP_PROL)
 void set_warp_prol(int on) { g_warp_prol = on; }
 static void warp_tasks(int n, int& MH, int& nstrips, int& ntasks, bool prol = false) {
     static int target = -1;
@@ -3791,18 +3917,29 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
         const int nw = prol ? WGeom<true>::NW : WGeom<false>::NW;
         const dim3 wgrid((ntasks + nw - 1) / nw);
         const dim3 bgrid((bnd_count(L.n) + WB_NT - 1) / WB_NT);
-        if (x_zero) launch_k(vanka_bnd_kernel<true, false>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
-        else if (prol) launch_k(vanka_bnd_kernel<false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
-        else launch_k(vanka_bnd_kernel<false, false>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
-        if (x_zero)
-            launch_k(vanka_warp_kernel<true, false>, wgrid, WGeom<false>::NT, WGeom<false>::SMEM, s, wx, wb, wx, P, xo, S,
-                     wmh, nstrips, ntasks, Ev);
-        else if (prol)
-            launch_k(vanka_warp_kernel<false, true>, wgrid, WGeom<true>::NT, WGeom<true>::SMEM, s, wx, wb, wc, P, xo, S,
-                     wmh, nstrips, ntasks, Ev);
-        else
-            launch_k(vanka_warp_kernel<false, false>, wgrid, WGeom<false>::NT, WGeom<false>::SMEM, s, wx, wb, wx, P, xo,
-                     S, wmh, nstrips, ntasks, Ev);
+        const dim3 bgrid2((L.n + WB2_T) / WB2_T, 4);
+        if (g_warp_bk == 1) {
+            if (x_zero) launch_k(vanka_bnd2_kernel<true, false>, bgrid2, WB2_NT, 0, s, P, x, b, Ev);
+            else if (prol) launch_k(vanka_bnd2_kernel<false, true>, bgrid2, WB2_NT, 0, s, P, x, b, Ev);
+            else launch_k(vanka_bnd2_kernel<false, false>, bgrid2, WB2_NT, 0, s, P, x, b, Ev);
+        } else if (g_warp_bk == 2) {
+            if (x_zero) launch_k(vanka_bnd_kernel<true, false>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
+            else if (prol) launch_k(vanka_bnd_kernel<false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
+            else launch_k(vanka_bnd_kernel<false, false>, bgrid, WB_NT, WB_SMEM, s, P, x, b, Ev);
+        }
+#define WLAUNCH(Z_, P_, B_)                                                                                     \
+    launch_k(vanka_warp_kernel<Z_, P_, B_>, wgrid, WGeom<P_>::NT, WGeom<P_>::SMEM, s, wx, wb, P_ ? wc : wx, P, xo, S, \
+             wmh, nstrips, ntasks, Ev)
+        if (g_warp_bk != 0) {
+            if (x_zero) WLAUNCH(true, false, true);
+            else if (prol) WLAUNCH(false, true, true);
+            else WLAUNCH(false, false, true);
+        } else {
+            if (x_zero) WLAUNCH(true, false, false);
+            else if (prol) WLAUNCH(false, true, false);
+            else WLAUNCH(false, false, false);
+        }
+#undef WLAUNCH
         return cudaGetLastError();
     }
     if (x_zero) launch_k(vanka_march2_kernel<true, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);

@@ -88,6 +88,8 @@ int blocks_vanka_march2(int n);
 void set_warp_min_n(int N);
 // the fused-prolongation post-sweep through the warp-marching kernel as well (1) or the CTA kernel (0)
 void set_warp_prol(int on);
+// boundary-vertex patches of the warp sweep: 1 precomputed by vanka_bnd_kernel, 0 inline (out-of-line call)
+void set_warp_bk(int on);
 int blocks_residual_march(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)
