@@ -12,7 +12,8 @@ lambda = 100, mu = 1, K = 1e-2, tau = alpha = 1, 1/M = 1, b ~ U(-1,1) from seed 
   of the K timed cycles (CUDA events on the launching stream, inputs resident in HBM).
 * e2e: the same metric through the public C-ABI call with HOST buffers (mg_solve_host: pinned host
   b and x copied in, K cycles, x copied back) timed by wall clock.
-* roofline: the dominant kernel (level-0 Vanka sweep, 2 launches per cycle) -- algorithmic bytes
+* roofline: the dominant kernel (level-0 Vanka sweep: warp-marching kernel + its boundary-vertex
+  kernel, 2 sweeps per cycle) -- algorithmic bytes
   (24 B per active DoF: read x, read b, write x) / its CUDA-event duration, against the measured
   HBM copy bandwidth of MEASURED_PEAKS.json.
 * cpu_baseline / --impl reference: the CPU oracle (oracle/, test infrastructure) timed as it
@@ -375,7 +376,9 @@ def main():
         # (which with the fused prolongation also reads e_H: + 8 B x N_1 ~ 2 B per fine DoF)
         alg_bytes = (24.0 * nact + (24.0 * nact + 8.0 * mg_inputs.n_active(n >> 1) if fused and n >= march_min
                                     else 24.0 * nact)) / 2.0
-        dom = ("vanka_march2_kernel (level 0: fused residual + 20-DoF patch solves + update; "
+        warp = n >= int(os.environ.get("MG_WARP_MIN_N", "1024")) > 0
+        dom = (("vanka_warp_kernel + vanka_bnd2_kernel" if warp else "vanka_march2_kernel") +
+               " (level 0: fused residual + 20-DoF patch solves + update; "
                "mean of the pre-sweep and the post-sweep" + (" with the prolongation fused in)" if fused else ")"))
     else:
         alg_bytes = 8.0 * nact * 4.8 + 8.0 * 0.2 * nact   # 3 + 1.8 passes (+0.2 K field)

@@ -2312,19 +2312,19 @@ constexpr int WT = 30, WXW = WT + 4, WBW = WT + 4, WXR = 4, WBR = 1;   // TMA bo
 constexpr int WXROW = 10 * WXW, WBROW = 10 * WBW;
 constexpr int WXSLOT = (WXROW + 15) / 16 * 16;   // ring slot strides: 128-byte aligned TMA destinations
 constexpr int WBSLOT = (WBROW + 15) / 16 * 16;
-constexpr int W_WARP_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + 10 * 32) * 8 + 64 + 127) / 128 * 128;
-// PROL (first post-sweep with the coarse-grid correction x + P e_H fused in): + a 3-row ring of coarse
-// rows (20-column boxes from the even column at or below (i0 - 2) / 2, one TMA box per coarse row)
-constexpr int WCC = 20, WCROW = 10 * WCC, WCSLOT = (WCROW + 15) / 16 * 16, WCR = 3;
-// (the PROL kernel carries the patch-correction sums in registers instead of the [10][32] shared row,
-// which keeps it at 6 warps per CTA, 12 per SM; MG_WARP_CDREG=0: shared row, 5 warps per CTA)
+// the patch-correction sums are carried in registers instead of a [10][32] shared row (MG_WARP_CDREG=1):
+// 14 KB per warp, 16 warps per SM for the plain sweep (126 registers), 12 with the fused prolongation
 #ifndef MG_WARP_CDREG
 #define MG_WARP_CDREG 1
 #endif
+constexpr int W_WARP_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + (MG_WARP_CDREG ? 0 : 10 * 32)) * 8 + 64 + 127) / 128 * 128;
+// PROL (first post-sweep with the coarse-grid correction x + P e_H fused in): + a 3-row ring of coarse
+// rows (20-column boxes from the even column at or below (i0 - 2) / 2, one TMA box per coarse row)
+constexpr int WCC = 20, WCROW = 10 * WCC, WCSLOT = (WCROW + 15) / 16 * 16, WCR = 3;
 constexpr int W_WARP_BYTES_P =
     ((WXR * WXSLOT + WBR * WBSLOT + (MG_WARP_CDREG ? 0 : 10 * 32) + WCR * WCSLOT) * 8 + 64 + 127) / 128 * 128;
 #ifndef MG_WPC
-#define MG_WPC 6   // warps per CTA (2 CTAs per SM)
+#define MG_WPC (MG_WARP_CDREG ? 8 : 6)   // warps per CTA (2 CTAs per SM)
 #endif
 #ifndef MG_WPC_P
 #define MG_WPC_P (MG_WARP_CDREG ? 6 : 5)
@@ -2358,7 +2358,7 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
     if (task < ntasks) {
         double* xr = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + w * WGeom<PROL>::BYTES);   // [WXR][10][WXW] (slot stride WXSLOT)
         double* br = xr + WXR * WXSLOT;                                                              // [WBR][10][WBW]
-        constexpr bool CDREG = PROL && MG_WARP_CDREG;
+        constexpr bool CDREG = MG_WARP_CDREG;
         double* cds = br + WBR * WBSLOT;                                                             // [10][32] (!CDREG)
         double* cr = cds + (CDREG ? 0 : 10 * 32);                                                    // PROL: [WCR][10][WCC]
         uint64_t* xbar = reinterpret_cast<uint64_t*>(cr + (PROL ? WCR * WCSLOT : 0));                // [WXR]
