@@ -47,6 +47,19 @@ __device__ __forceinline__ unsigned active_mask(int i, int j, int n) {
            (li && lj ? 0x390u : 0u);
 }
 
+// register slot of the coarse value e_H(I + dI, J + dJ, pl) in the fused prolongation: planes 0-4
+// use 13 slots, planes 5-9 use 7 (the union over both fine-row parities of MG_PROLONG's operands)
+__host__ __device__ constexpr int pslot(int dI, int dJ, int pl) {
+    return pl >= 5 ? (dI == 0 && dJ == 0 ? pl - 5 : (dJ == 1 ? 5 : 6))
+                   : (dI == 0 && dJ == 0 ? pl : dI == 0 ? 5 + pl : dJ == 0 ? (pl == 3 ? 10 : 8 + pl) : 11 + pl);
+}
+static_assert(pslot(0, 1, 2) == 7 && pslot(1, 0, 3) == 10 && pslot(1, 1, 1) == 12 && pslot(1, 0, 6) == 6, "pslot");
+__host__ __device__ constexpr int pslot20(int dI, int dJ, int pl) { return pl >= 5 ? 13 + pslot(dI, dJ, pl) : pslot(dI, dJ, pl); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // plane p of index (i, j) is an unknown (not Dirichlet, not outside the mesh; SURVEY 8 layout table).
 // Through the ten-plane mask: the unrolled per-plane tests of one index share one mask.
 __device__ __forceinline__ bool is_active(int p, int i, int j, int n) { return (active_mask(i, j, n) >> p) & 1u; }
@@ -115,7 +128,7 @@ __device__ __forceinline__ double gld(const double* p) {
     return __ldcg(p);   // L2: coherent with what other CTAs of this kernel wrote before a grid barrier
 }
 
-template <int W, int HT, int NP, bool NC = true>
+template <int W, int HT, int NP, bool NC = true, int U = 8>
 __device__ __forceinline__ void load_tile(double* __restrict__ dst, const double* __restrict__ src, int i0,
                                           int j0, int n, int pitch, int64_t plane, int p0 = 0, int t0 = -1,
                                           int nt = 0) {
@@ -126,7 +139,7 @@ __device__ __forceinline__ void load_tile(double* __restrict__ dst, const double
     // U elements per thread in flight: all loads of a batch are issued before its shared-memory
     // stores (one element per iteration would serialise ~NP W HT / nt global-load latencies, which
     // is what bounds the latency-bound coarse levels)
-    constexpr int TOT = NP * W * HT, U = 8;
+    constexpr int TOT = NP * W * HT;
     for (int base = t0; base < TOT; base += U * nt) {
         double v[U];
 #pragma unroll
@@ -702,6 +715,180 @@ __device__ __forceinline__ double vanka_tile(const VankaParams& P, const double*
     return nrm;
 }
 
+// Small-tile sweep of the latency-bound coarse levels (8 x 4 owners, 64 threads): the arithmetic of
+// vanka_tile, with every global read the kernel needs issued in its first round trip -- the stop flag,
+// the x tile, b at the residual positions and x at the owners (registers), and the dense inverses of
+// the boundary classes the tile touches (staged in shared memory) -- instead of one L2 round trip
+// per phase (stop flag, tile, b, boundary table, owner x).  Bitwise vanka_tile's results.
+struct VSmall {
+    using T = VTile<VSX, VSY>;
+    static constexpr int XS = T::XSZ, RS = 10 * T::RW * T::RH, CS = T::CSZ, GS = 8 * 400;
+    static constexpr int SMEM = (XS + RS + CS + GS) * 8 + 16 * 4;
+};
+// the boundary classes present among the vertices (a, b), a in [i0, i0 + TX], b in [j0, j0 + TY]
+__device__ __forceinline__ unsigned tile_classes(int i0, int j0, int tx, int ty, int n) {
+    const int a1 = min(i0 + tx, n), b1 = min(j0 + ty, n);
+    unsigned cxm = 0, cym = 0;
+    if (i0 <= a1) {
+        if (i0 == 0) cxm |= 2u;
+        if (a1 == n) cxm |= 4u;
+        if (max(i0, 1) <= min(a1, n - 1)) cxm |= 1u;
+    }
+    if (j0 <= b1) {
+        if (j0 == 0) cym |= 2u;
+        if (b1 == n) cym |= 4u;
+        if (max(j0, 1) <= min(b1, n - 1)) cym |= 1u;
+    }
+    unsigned m = 0;
+    for (int cy = 0; cy < 3; ++cy)
+        for (int cx = 0; cx < 3; ++cx)
+            if (((cxm >> cx) & 1u) && ((cym >> cy) & 1u)) m |= 1u << (cx + 3 * cy);
+    return m & ~1u;   // interior class 0: constant bank
+}
+
+template <bool XZERO>
+__global__ void __launch_bounds__(VTile<VSX, VSY>::NT, 4) vanka_small_kernel(const VankaParams P,
+                                                                             const double* __restrict__ x,
+                                                                             const double* __restrict__ b,
+                                                                             double* __restrict__ xo, NormSink S) {
+    pdl_wait();
+    pdl_trigger();
+    using T = VTile<VSX, VSY>;
+    extern __shared__ __align__(16) double sm[];
+    double* xs = sm;                      // x tile [10][XH][XW]
+    double* rs = xs + VSmall::XS;         // residual tile [10][RH][RW]
+    double* cs = rs + VSmall::RS;         // patch corrections [20][PH][PW]
+    double* gs = cs + VSmall::CS;         // dense inverses of the boundary classes present, in class order
+    const LevelParams& L = P.L;
+    const int stopv = *L.stop;            // checked after the loads are in flight
+    const int n = L.n, pitch = L.pitch, t = threadIdx.x;
+    const int64_t plane = L.plane;
+    const int i0 = blockIdx.x * VSX, j0 = blockIdx.y * VSY;
+    // b at this thread's residual position, x at its owner index (registers)
+    double bpre[10], xown[10];
+    const int ly = t / T::RW, lx = t - ly * T::RW;
+    {
+        const int i = i0 - 1 + lx, j = j0 - 1 + ly;
+        const bool in = t < T::RW * T::RH && i >= 0 && j >= 0 && i <= n && j <= n;
+        const int64_t o = in ? (int64_t)j * pitch + i : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) bpre[k] = in ? __ldg(b + k * plane + o) : 0.0;
+    }
+    const int ox = t % VSX, oy = t / VSX;
+    {
+        const int i = i0 + ox, j = j0 + oy;
+        const bool in = !XZERO && t < VSX * VSY && i <= n && j <= n;
+        const int64_t o = in ? (int64_t)j * pitch + i : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) xown[k] = in ? __ldg(x + k * plane + o) : 0.0;
+    }
+    const unsigned cm = tile_classes(i0, j0, VSX, VSY, n);
+    {
+        // cp.async: every 16-byte piece of the staged tables in flight at once, no registers
+        int slot = 0;
+        for (int c = 1; c < 9; ++c) {
+            if (!((cm >> c) & 1u)) continue;
+            const double* src = P.gbnd + c * 400;
+            double* dst = gs + slot * 400;
+            for (int q = t; q < 200; q += T::NT)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 2 * q)), "l"(src + 2 * q)
+                             : "memory");
+            ++slot;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    if (!XZERO) load_tile<T::XW, T::XH, 10, true, 16>(xs, x, i0 - 2, j0 - 2, n, pitch, plane, 0, t, T::NT);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (stopv) return;
+    // phase 1: r = b - A x on the tile + 1 ring
+    if (t < T::RW * T::RH) {
+        const int i = i0 - 1 + lx, j = j0 - 1 + ly;
+        double rv[10];
+        if (!XZERO) {
+            const double* x0 = xs + (ly + 1) * T::XW + (lx + 1);
+            double av[10];
+            apply_rows<T::XW * T::XH, false>(L, x0 - T::XW, x0, x0 + T::XW, i, j, av);
+            if (L.lamx != 0.0) exact_bubble_add(L.lamx, x0 - T::XW, x0, x0 + T::XW, T::XW * T::XH, av);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rv[k] = is_active(k, i, j, n) ? (bpre[k] - av[k]) : 0.0;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 10; ++k) rv[k] = bpre[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
+    }
+    __syncthreads();
+    // phase 2: patch solves at the vertices of the tile + high ring
+    if (t < T::PW * T::PH) {
+        const int py = t / T::PW, px = t - py * T::PW;
+        const int a = i0 + px, bb = j0 + py;
+        constexpr int OS = T::PW * T::PH;
+        if (a <= n && bb <= n) {
+            double rr[20];
+            gather20<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
+            const int cls = vertex_class(a, bb, n);
+            if (cls == 0) {
+                patch_apply20<true>(P, 0, rr, cs + t, OS);
+            } else {
+                const double2* G = reinterpret_cast<const double2*>(gs + __popc(cm & ((1u << cls) - 1u)) * 400);
+#pragma unroll
+                for (int a4 = 0; a4 < 20; a4 += 4) {
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+                    for (int c2 = 0; c2 < 10; ++c2) {
+                        const double2 g0 = G[(a4 + 0) * 10 + c2], g1 = G[(a4 + 1) * 10 + c2];
+                        const double2 g2 = G[(a4 + 2) * 10 + c2], g3 = G[(a4 + 3) * 10 + c2];
+                        s0 = fma(g0.x, rr[2 * c2], s0); s0 = fma(g0.y, rr[2 * c2 + 1], s0);
+                        s1 = fma(g1.x, rr[2 * c2], s1); s1 = fma(g1.y, rr[2 * c2 + 1], s1);
+                        s2 = fma(g2.x, rr[2 * c2], s2); s2 = fma(g2.y, rr[2 * c2 + 1], s2);
+                        s3 = fma(g3.x, rr[2 * c2], s3); s3 = fma(g3.y, rr[2 * c2 + 1], s3);
+                    }
+                    cs[(a4 + 0) * OS + t] = s0;
+                    cs[(a4 + 1) * OS + t] = s1;
+                    cs[(a4 + 2) * OS + t] = s2;
+                    cs[(a4 + 3) * OS + t] = s3;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 20; ++q) cs[q * OS + t] = 0.0;
+        }
+    }
+    __syncthreads();
+    // phase 3: owners
+    double nrm = 0.0;
+    if (t < VSX * VSY) {
+        const int i = i0 + ox, j = j0 + oy;
+        if (i <= n && j <= n) {
+            const double* c00 = cs + oy * T::PW + ox;
+#define CC(s_, dx, dy) c00[(s_) * (T::PW * T::PH) + (dy) * T::PW + (dx)]
+            double d[10];
+            d[0] = CC(0, 0, 0);
+            d[1] = CC(1, 0, 0);
+            d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+            d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+            d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+            d[5] = CC(8, 0, 0) + CC(9, 1, 0);
+            d[6] = CC(10, 0, 0) + CC(11, 0, 1);
+            d[7] = CC(12, 1, 0) + CC(13, 0, 1);
+            d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
+            d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
+#undef CC
+            const int64_t o = (int64_t)j * pitch + i;
+            const double* r00 = rs + (oy + 1) * T::RW + (ox + 1);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                xo[k * plane + o] = is_active(k, i, j, n) ? fma(P.omega, d[k], xown[k]) : 0.0;
+                const double rv = r00[k * T::RW * T::RH];
+                nrm = fma(rv, rv, nrm);
+            }
+        }
+    }
+    if (S.out || S.state) norm_finish<T::NT>(S, nrm);
+}
+
 template <bool XZERO, int TX = VTX, int TY = VTY, bool HET = false>
 __global__ void __launch_bounds__(VTile<TX, TY>::NT, 2) vanka_kernel(const VankaParams P, const double* __restrict__ x,
                                                        const double* __restrict__ b, double* __restrict__ xo,
@@ -803,6 +990,71 @@ __device__ __forceinline__ void restrict_tile(const LevelParams& L, int nc, int 
 #undef RF
 }
 
+// Small-tile fused residual + restriction (4 x 2 coarse indices, 64 threads) with the stop flag, the x
+// tile and b at the residual positions all read in the first round trip; bitwise restrict_tile<1>.
+template <bool HET>
+__global__ void __launch_bounds__(CTile<CSX, CSY>::NT, 4) restrict_small_kernel(const LevelParams L, int nc, int pitchc,
+                                                                              const double* __restrict__ x,
+                                                                              const double* __restrict__ br,
+                                                                              double* __restrict__ bc) {
+    pdl_wait();
+    pdl_trigger();
+    using T = CTile<CSX, CSY>;
+    extern __shared__ double sm[];
+    double* rs = sm;
+    double* xs = sm + 10 * T::RW * T::RH;
+    const int stopv = *L.stop;
+    const int t = threadIdx.x;
+    const int I0 = blockIdx.x * CSX, J0 = blockIdx.y * CSY;
+    const int fi0 = 2 * I0 - 2, fj0 = 2 * J0 - 2;
+    const int ly = t / T::RW, lx = t - ly * T::RW;
+    const int i = fi0 + lx, j = fj0 + ly;
+    double bpre[10];
+    {
+        const bool in = t < T::RW * T::RH && i >= 0 && j >= 0 && i <= L.n && j <= L.n;
+        const int64_t o = in ? (int64_t)j * L.pitch + i : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) bpre[k] = in ? __ldg(br + k * L.plane + o) : 0.0;
+    }
+    load_tile<T::XW, T::XH, 10, true, 16>(xs, x, fi0 - 1, fj0 - 1, L.n, L.pitch, L.plane, 0, t, T::NT);
+    __syncthreads();
+    if (stopv) return;
+    if (t < T::RW * T::RH) {
+        const double* x0 = xs + (ly + 1) * T::XW + (lx + 1);
+        double av[10];
+        apply_rows<T::XW * T::XH, HET>(L, x0 - T::XW, x0, x0 + T::XW, i, j, av);
+        if (L.lamx != 0.0) exact_bubble_add(L.lamx, x0 - T::XW, x0, x0 + T::XW, T::XW * T::XH, av);
+#pragma unroll
+        for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = is_active(k, i, j, L.n) ? (bpre[k] - av[k]) : 0.0;
+    }
+    __syncthreads();
+    if (t >= 5 * CSX * CSY) return;
+    const int c = t % (CSX * CSY), grp = t / (CSX * CSY);
+    const int cy = c / CSX, cx = c - cy * CSX;
+    const int I = I0 + cx, J = J0 + cy;
+    if (I > nc || J > nc) return;
+    const double* r00 = rs + (2 * cy + 2) * T::RW + (2 * cx + 2);
+    const int64_t planec = (int64_t)(nc + 1) * pitchc;
+    const int64_t o = (int64_t)J * pitchc + I;
+#define RF(cdI, cdJ, di, dj, kf) r00[(kf) * (T::RW * T::RH) + (-2 * (cdJ) + (dj)) * T::RW + (-2 * (cdI) + (di))]
+#define MG_T(cdI, cdJ, di, dj, kf, w) acc = fma(w, RF(cdI, cdJ, di, dj, kf), acc);
+#define OUT(k)                                                       \
+    {                                                                \
+        double acc = 0.0;                                            \
+        MG_RESTRICT_##k(MG_T) bc[k * planec + o] = is_active(k, I, J, nc) ? acc : 0.0; \
+    }
+    switch (grp) {
+        case 0: OUT(0) OUT(1) break;
+        case 1: OUT(2) OUT(3) break;
+        case 2: OUT(4) OUT(5) break;
+        case 3: OUT(6) OUT(7) break;
+        default: OUT(8) OUT(9) break;
+    }
+#undef OUT
+#undef MG_T
+#undef RF
+}
+
 template <int MODE, bool HET, int TX = CX, int TY = CY>
 __global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const LevelParams L, int nc, int pitchc,
                                                           const double* __restrict__ x,
@@ -817,18 +1069,21 @@ __global__ void __launch_bounds__(CTile<TX, TY>::NT, 2) restrict_kernel(const Le
 
 // ------------------------------------------------------------------------------------------
 // prolongation x_f += P e_c: one thread per coarse cell writes its 4 fine indices
+// EARLY (the latency-bound coarse levels): the stop flag, the 20 fine pairs and the 20 coarse values are
+// all read before the flag is tested -- one round trip instead of three; the bandwidth-bound large
+// levels keep the stop test first (fewer registers in flight, more CTAs per SM).  Same arithmetic.
+template <bool EARLY>
 __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc, int pitchc,
                                                       const double* __restrict__ e, double* __restrict__ x,
                                                       const int* __restrict__ stop) {
     pdl_wait();
     pdl_trigger();
-    if (*stop) return;
+    if (!EARLY && *stop) return;
+    const int stopv = EARLY ? *stop : 0;
     const int I = blockIdx.x * 32 + (threadIdx.x & 31), J = blockIdx.y * 8 + (threadIdx.x >> 5);
     if (I >= nc || J >= nc) return;
     const int64_t planec = (int64_t)(nc + 1) * pitchc, planef = (int64_t)(nf + 1) * pitchf;
     const double* e0 = e + (int64_t)J * pitchc + I;
-#define EC(dI, dJ, pl) __ldg(e0 + (pl) * planec + (dJ) * pitchc + (dI))
-#define MG_Q(dI, dJ, pl, w) v = fma(w, EC(dI, dJ, pl), v);
     const int fi = 2 * I, fj = 2 * J;
     double* x0 = x + (int64_t)fj * pitchf + fi;   // fi even, rows 256-B aligned: 16-B aligned pairs
     // the two fine columns 2I, 2I+1 of a fine row move as one 16-byte load / store (a warp covers
@@ -837,6 +1092,16 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
     double2 xq[20];
 #pragma unroll
     for (int q = 0; q < 20; ++q) xq[q] = *reinterpret_cast<const double2*>(x0 + (q >> 1) * planef + (q & 1) * pitchf);
+    double pe[20];
+    if (EARLY) {
+#define PL(dI, dJ, pl) pe[pslot20(dI, dJ, pl)] = __ldg(e0 + (pl) * planec + (dJ) * pitchc + (dI));
+        PL(0, 0, 0) PL(0, 0, 1) PL(0, 0, 2) PL(0, 0, 3) PL(0, 0, 4) PL(0, 1, 0) PL(0, 1, 1)
+        PL(0, 1, 2) PL(1, 0, 0) PL(1, 0, 1) PL(1, 0, 3) PL(1, 1, 0) PL(1, 1, 1)
+        PL(0, 0, 5) PL(0, 0, 6) PL(0, 0, 7) PL(0, 0, 8) PL(0, 0, 9) PL(0, 1, 5) PL(1, 0, 6)
+#undef PL
+        if (stopv) return;
+    }
+#define MG_Q(dI, dJ, pl, w) v = fma(w, EARLY ? pe[pslot20(dI, dJ, pl)] : __ldg(e0 + (pl) * planec + (dJ) * pitchc + (dI)), v);
 #define PROL2(dj, kf)                                                                   \
     {                                                                                   \
         double v = 0.0;                                                                 \
@@ -853,7 +1118,6 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
 #undef PROL4
 #undef PROL2
 #undef MG_Q
-#undef EC
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1496,9 +1760,6 @@ int g_carveout = cudaSharedmemCarveoutMaxShared;   // MG_CARVEOUT (-1: driver de
 
 // ------------------------------------------------------------------------------------------
 // mbarrier / TMA helpers of the row-marching kernels
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -1580,17 +1841,9 @@ constexpr int M2SMEM = (M2XR * M2ROW + M2BR * M2ROW + M2CR * 20 * M2CS) * 8 + 64
 static_assert(M2T + 2 <= 32 && M2R * 32 == M2NT, "one warp per row, one residual position per thread");
 static_assert(M2T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
 
-// register slot of the coarse value e_H(I + dI, J + dJ, pl) in the fused prolongation: planes 0-4
-// use 13 slots, planes 5-9 use 7 (the union over both fine-row parities of MG_PROLONG's operands)
-__host__ __device__ constexpr int pslot(int dI, int dJ, int pl) {
-    return pl >= 5 ? (dI == 0 && dJ == 0 ? pl - 5 : (dJ == 1 ? 5 : 6))
-                   : (dI == 0 && dJ == 0 ? pl : dI == 0 ? 5 + pl : dJ == 0 ? (pl == 3 ? 10 : 8 + pl) : 11 + pl);
-}
-static_assert(pslot(0, 1, 2) == 7 && pslot(1, 0, 3) == 10 && pslot(1, 1, 1) == 12 && pslot(1, 0, 6) == 6, "pslot");
 
 constexpr int M2NP = 2;   // producer warps of the fused-prolongation sweep (one per row parity of a group;
                           // measured: one warp for both 1.39 ms, two 1.36 ms at 4096^2)
-__host__ __device__ constexpr int pslot20(int dI, int dJ, int pl) { return pl >= 5 ? 13 + pslot(dI, dJ, pl) : pslot(dI, dJ, pl); }
 
 // PROL: the sweep relaxes x + P e_H instead of x (the coarse-grid correction of the V-cycle fused
 // into the first post-smoothing sweep): every x row is corrected in the ring right
@@ -3318,6 +3571,8 @@ void kernels_init() {
     set_smem(vanka_kernel<false>, V_SMEM);
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
+    set_smem(vanka_small_kernel<false>, VSmall::SMEM);
+    set_smem(vanka_small_kernel<true>, VSmall::SMEM);
     set_smem(vanka_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_het_kernel<false>, V_SMEM);
     set_smem(vanka_het_kernel<true>, V_SMEM);
@@ -3329,6 +3584,8 @@ void kernels_init() {
     set_smem(restrict_kernel<1, true>, C_SMEM_FUSED);
     set_smem(restrict_kernel<1, false, CSX, CSY>, CTile<CSX, CSY>::SMEM_FUSED);
     set_smem(restrict_kernel<1, true, CSX, CSY>, CTile<CSX, CSY>::SMEM_FUSED);
+    set_smem(restrict_small_kernel<false>, CTile<CSX, CSY>::SMEM_FUSED);
+    set_smem(restrict_small_kernel<true>, CTile<CSX, CSY>::SMEM_FUSED);
     set_smem(coarse_kernel, 4096 * 8);
     set_smem(bsr_a_kernel<false, false>, BA_SMEM);
     set_smem(bsr_a_kernel<false, true>, BA_SMEM);
@@ -3346,7 +3603,9 @@ static_assert(BANT >= BA_RW * BA_RH && BANT % 32 == 0, "bsr_a thread mapping");
 static_assert(BBNT >= BB_RW * BB_RH && BBNT % 32 == 0, "bsr_b thread mapping");
 
 int blocks_residual(int n) { return ((n + RTX) / RTX) * ((n + RTY) / RTY); }
-int g_small_tile_n = 128;   // levels with n <= this use the small 2-D tiles (mg_setup: MG_SMALL_TILE_N)
+int g_small_tile_n = 128;
+int g_small_diet = 1;   // small-tile sweeps through vanka_small_kernel (all global reads in one round trip; MG_SMALL_DIET)
+void set_small_diet(int on) { g_small_diet = on; }   // levels with n <= this use the small 2-D tiles (mg_setup: MG_SMALL_TILE_N)
 void set_small_tile_n(int n) { g_small_tile_n = n; }
 int blocks_vanka(int n) {
     return n <= g_small_tile_n ? ((n + VSX) / VSX) * ((n + VSY) / VSY) : ((n + VTX) / VTX) * ((n + VTY) / VTY);
@@ -3850,8 +4109,13 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
     if (P.L.n <= g_small_tile_n) {
         using T = VTile<VSX, VSY>;
         dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
-        if (x_zero) launch_k(vanka_kernel<true, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
-        else launch_k(vanka_kernel<false, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+        if (g_small_diet) {
+            if (x_zero) launch_k(vanka_small_kernel<true>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S);
+            else launch_k(vanka_small_kernel<false>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S);
+        } else {
+            if (x_zero) launch_k(vanka_kernel<true, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+            else launch_k(vanka_kernel<false, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
+        }
         return cudaGetLastError();
     }
     dim3 grid((P.L.n + VTX) / VTX, (P.L.n + VTY) / VTY);
@@ -4022,8 +4286,14 @@ cudaError_t launch_restrict(const LevelParams& Lf, int nc, int pitchc, int mode,
         using T = CTile<CSX, CSY>;
         dim3 grid((nc + CSX) / CSX, (nc + CSY) / CSY);
         if (mode == 1) {
-            if (Lf.kinv_field) launch_k(restrict_kernel<1, true, CSX, CSY>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
-            else launch_k(restrict_kernel<1, false, CSX, CSY>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+            if (g_small_diet) {
+                if (Lf.kinv_field) launch_k(restrict_small_kernel<true>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+                else launch_k(restrict_small_kernel<false>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+            } else if (Lf.kinv_field) {
+                launch_k(restrict_kernel<1, true, CSX, CSY>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+            } else {
+                launch_k(restrict_kernel<1, false, CSX, CSY>, grid, T::NT, T::SMEM_FUSED, s, Lf, nc, pitchc, x, br, bc);
+            }
         } else if (mode == 0) {
             launch_k(restrict_kernel<0, false, CSX, CSY>, grid, T::NT, T::SMEM_PLAIN, s, Lf, nc, pitchc, x, br, bc);
         } else {
@@ -4068,7 +4338,8 @@ cudaError_t launch_bottom(const BottomArgs& A, cudaStream_t s) {
 cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double* e, double* x, const int* stop,
                            cudaStream_t s) {
     dim3 grid((nc + 31) / 32, (nc + 7) / 8);
-    launch_k(prolong_kernel, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
+    if (nf <= 256 && g_small_diet) launch_k(prolong_kernel<true>, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
+    else launch_k(prolong_kernel<false>, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
     return cudaGetLastError();
 }
 
@@ -4160,7 +4431,8 @@ cudaError_t launch_kinv_coarsen(int nf, int pitchf, const double* kf, int pitchc
 
 // the kernels launched without a dynamic shared-memory attribute (set_smem carves the others)
 static void carve_all() {
-    carve(prolong_kernel);
+    carve(prolong_kernel<true>);
+    carve(prolong_kernel<false>);
     carve(residual_kernel<false, false>);
     carve(residual_kernel<true, false>);
     carve(residual_kernel<false, true>);

@@ -94,6 +94,8 @@ int blocks_residual_march(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)
 void set_small_tile_n(int N);
+// small-tile sweeps with every global read in the first round trip (vanka_small_kernel) or vanka_kernel
+void set_small_diet(int on);
 // programmatic dependent launch of every kernel (1, default) or plain stream order (0)
 void set_pdl(int on);
 // fused-prolongation sweep variant: 1 warp-specialised with setmaxnreg (default), 0 the 6-warp kernel

@@ -286,6 +286,25 @@ def test_warp_sweep_bitwise(n, levels, pname, nu2):
         assert out[k][1] == out[3][1], k
 
 
+@pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (48, 3, "mixed", 2), (128, 6, "stiff", 1)])
+def test_small_tile_sweep_bitwise(n, levels, pname, nu):
+    """The small-tile sweep with all of its global reads in the first round trip (vanka_small_kernel:
+    b and owner x in registers, the boundary classes' inverses staged in shared memory) gives bitwise
+    vanka_kernel's iterates and norms on the levels with n <= 128 (same arithmetic, same order)."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    b = mg_inputs.uniform_rhs(n, 6)
+    out = []
+    for diet in ("1", "0"):
+        H = C.gpu_hierarchy(n, levels, pname, env={"MG_SMALL_DIET": diet})
+        xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+        hist = [H.cycle(xd, bd, Opts(nu, nu, "vanka", 0.7)) for _ in range(3)]
+        out.append((H.to_host(xd), hist))
+        H.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (128, 6, "stiff", 1)])
 def test_bottom_kernel_bitwise(n, levels, pname, nu):
     """The grid-wide bottom of the V-cycle (levels with n <= 128 and the coarsest solve in one
