@@ -2635,6 +2635,8 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
         const int rows = min(MH, n + 1 - j0);
         const int yend = j0 + rows;   // residual / patch rows j0 - 1 .. yend, owner rows j0 .. yend - 1
         const int i = i0 - 1 + lane;  // residual position, patch vertex and owner index of this lane
+        // every residual position / owner of the strip strictly inside the domain (warp uniform)
+        const bool inner = i0 - 1 >= 1 && i0 + WT <= n - 1;
         // x row y: load number q = y - (j0 - 2), slot q % WXR; b row y: q = y - (j0 - 1), slot q % WBR
         auto load_x = [&](int y) {
             const int q = y - (j0 - 2);
@@ -2714,8 +2716,26 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
         if (m1 & (1u << (kf))) xv.y += v;                                             \
         *x2 = xv;                                                                     \
     }
-                if (r & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
-                else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+#define PXF(dj, kf)                                                                   \
+    {                                                                                 \
+        double v = 0.0;                                                               \
+        MG_PROLONG_0_##dj##_##kf(PQ) const double v0 = v;                             \
+        v = 0.0;                                                                      \
+        MG_PROLONG_1_##dj##_##kf(PQ) double2* x2 = reinterpret_cast<double2*>(xrw + (kf) * WXW); \
+        double2 xv = *x2;                                                             \
+        xv.x += v0;                                                                   \
+        xv.y += v;                                                                    \
+        *x2 = xv;                                                                     \
+    }
+                // warp-uniform: every fine index of the row active (inner strip, inner row) -> no masks
+                if (I0 >= 1 && r >= 1 && r <= n - 1) {
+                    if (r & 1) { PXF(1, 0) PXF(1, 1) PXF(1, 2) PXF(1, 3) PXF(1, 4) PXF(1, 5) PXF(1, 6) PXF(1, 7) PXF(1, 8) PXF(1, 9) }
+                    else { PXF(0, 0) PXF(0, 1) PXF(0, 2) PXF(0, 3) PXF(0, 4) PXF(0, 5) PXF(0, 6) PXF(0, 7) PXF(0, 8) PXF(0, 9) }
+                } else {
+                    if (r & 1) { PX(1, 0) PX(1, 1) PX(1, 2) PX(1, 3) PX(1, 4) PX(1, 5) PX(1, 6) PX(1, 7) PX(1, 8) PX(1, 9) }
+                    else { PX(0, 0) PX(0, 1) PX(0, 2) PX(0, 3) PX(0, 4) PX(0, 5) PX(0, 6) PX(0, 7) PX(0, 8) PX(0, 9) }
+                }
+#undef PXF
 #undef PX
 #undef PQ
             }
@@ -2756,9 +2776,14 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
                     const double* x0 = xrow(y) + (lane + 1);
                     double av[10];
                     apply_rows<WXW, false>(L, xrow(y - 1) + (lane + 1), x0, xrow(y + 1) + (lane + 1), i, y, av);
-                    const unsigned m = active_mask(i, y, n);
+                    if (inner && y >= 1 && y <= n - 1) {   // warp-uniform: every position fully active
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) rv[k] = ((m >> k) & 1u) ? bp[k * WBW] - av[k] : 0.0;
+                        for (int k = 0; k < 10; ++k) rv[k] = bp[k * WBW] - av[k];
+                    } else {
+                        const unsigned m = active_mask(i, y, n);
+#pragma unroll
+                        for (int k = 0; k < 10; ++k) rv[k] = ((m >> k) & 1u) ? bp[k * WBW] - av[k] : 0.0;
+                    }
                 } else {
 #pragma unroll
                     for (int k = 0; k < 10; ++k) rv[k] = bp[k * WBW];
@@ -2824,12 +2849,17 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
                     d[8] = CD(8) + o[19];
                     d[9] = (r15 + o[17]) + CD(9);
                     const double* xv = xrow(yo) + (lane + 1);
-                    const unsigned m = active_mask(i, yo, n);
                     const int64_t off = (int64_t)yo * L.pitch + i;
+                    if (inner && yo >= 1 && yo <= n - 1) {   // warp-uniform: every owner fully active
 #pragma unroll
-                    for (int k = 0; k < 10; ++k) {
-                        const double xk = XZERO ? 0.0 : xv[k * WXW];
-                        xo[k * L.plane + off] = ((m >> k) & 1u) ? fma(P.omega, d[k], xk) : 0.0;
+                        for (int k = 0; k < 10; ++k) xo[k * L.plane + off] = fma(P.omega, d[k], XZERO ? 0.0 : xv[k * WXW]);
+                    } else {
+                        const unsigned m = active_mask(i, yo, n);
+#pragma unroll
+                        for (int k = 0; k < 10; ++k) {
+                            const double xk = XZERO ? 0.0 : xv[k * WXW];
+                            xo[k * L.plane + off] = ((m >> k) & 1u) ? fma(P.omega, d[k], xk) : 0.0;
+                        }
                     }
                 }
             }
