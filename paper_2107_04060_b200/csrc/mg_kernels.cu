@@ -3808,6 +3808,33 @@ __global__ void __launch_bounds__(GS_NT) vec_gs_kernel(const double* __restrict_
     const int64_t n2 = len / 2;
     const int64_t stride = (int64_t)gridDim.x * GS_NT;
     const double2* w2 = reinterpret_cast<const double2*>(w);
+    if (MODE == 1 && KB <= 16) {
+        // one element pair per thread and step with the k basis pairs held in registers: the update
+        // and the dots of the updated pair read the basis once (re-reading it through L2 halved the
+        // pass's bandwidth at k = 9-16)
+        for (int64_t e0 = (int64_t)blockIdx.x * GS_NT + threadIdx.x; e0 < n2; e0 += stride) {
+            double2 a0 = w2[e0];
+            double2 vv[KB];
+#pragma unroll
+            for (int q = 0; q < KB; ++q)
+                vv[q] = q < k ? __ldg(reinterpret_cast<const double2*>(V.p[q]) + e0) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < KB; ++q)
+                if (q < k) {
+                    a0.x = fma(-cq[q], vv[q].x, a0.x);
+                    a0.y = fma(-cq[q], vv[q].y, a0.y);
+                }
+            reinterpret_cast<double2*>(wo)[e0] = a0;
+#pragma unroll
+            for (int q = 0; q < KB; ++q)
+                if (q < k) {
+                    acc[q] = fma(a0.x, vv[q].x, acc[q]);
+                    acc[q] = fma(a0.y, vv[q].y, acc[q]);
+                }
+            acc[NA - 1] = fma(a0.x, a0.x, acc[NA - 1]);
+            acc[NA - 1] = fma(a0.y, a0.y, acc[NA - 1]);
+        }
+    } else
     for (int64_t e0 = (int64_t)blockIdx.x * GS_NT + threadIdx.x; e0 < n2; e0 += 2 * stride) {
         const int64_t e1 = e0 + stride;
         const bool has1 = e1 < n2;
@@ -3889,27 +3916,37 @@ __global__ void __launch_bounds__(GS_NT) vec_gs_kernel(const double* __restrict_
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == GS_BLOCKS - 1);
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
     __syncthreads();
     if (last) {
         __threadfence();
         for (int r = threadIdx.x; r < nres; r += GS_NT) {
             double t = 0.0;
-            for (int u = 0; u < GS_BLOCKS; ++u) t += __ldcg(partials + r * GS_BLOCKS + u);
+            for (int u = 0; u < (int)gridDim.x; ++u) t += __ldcg(partials + r * GS_BLOCKS + u);
             out[r] = t;
         }
         if (threadIdx.x == 0) *counter = 0u;
     }
 }
 
+// grid of a Gram-Schmidt pass: one wave of resident CTAs (the register-heavy buckets fit 2-3 CTAs per
+// SM: a fixed 4 x 148 grid ran them in two partial waves at 3.6 TB/s), at most GS_BLOCKS
+template <typename F>
+static int gs_blocks(F* f) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, GS_NT, 0) != cudaSuccess || per <= 0) per = 1;
+    return std::min(GS_BLOCKS, per * sm_count());
+}
 template <int KB>
 static void launch_gs_kb(int mode, const double* w, double* wo, const GsPtrs& V, int k, const double* c,
                          const double* sc, int64_t len, double* partials, unsigned* counter, double* out, cudaStream_t s) {
+    static const int nb[4] = {gs_blocks(vec_gs_kernel<0, KB>), gs_blocks(vec_gs_kernel<1, KB>),
+                              gs_blocks(vec_gs_kernel<2, KB>), gs_blocks(vec_gs_kernel<3, KB>)};
     switch (mode) {
-        case 0: launch_k(vec_gs_kernel<0, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
-        case 1: launch_k(vec_gs_kernel<1, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
-        case 2: launch_k(vec_gs_kernel<2, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
-        default: launch_k(vec_gs_kernel<3, KB>, GS_BLOCKS, GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        case 0: launch_k(vec_gs_kernel<0, KB>, nb[0], GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        case 1: launch_k(vec_gs_kernel<1, KB>, nb[1], GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        case 2: launch_k(vec_gs_kernel<2, KB>, nb[2], GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
+        default: launch_k(vec_gs_kernel<3, KB>, nb[3], GS_NT, 0, s, w, wo, V, k, c, sc, len, partials, counter, out); break;
     }
 }
 
