@@ -497,6 +497,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     set_small_diet(getenv("MG_SMALL_DIET") ? atoi(getenv("MG_SMALL_DIET")) : 1);
     set_warp_prol(getenv("MG_WARP_PROL") ? atoi(getenv("MG_WARP_PROL")) : 1);
     set_warp_bk(getenv("MG_WARP_BK") ? atoi(getenv("MG_WARP_BK")) : 1);
+    set_warp_bsr(getenv("MG_WARP_BSR") ? atoi(getenv("MG_WARP_BSR")) : 0);
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = std::min(2, std::max(0, atoi(v)));

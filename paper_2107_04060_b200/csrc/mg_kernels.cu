@@ -3402,6 +3402,254 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
         }
     }
 }
+// ------------------------------------------------------------------------------------------
+// patch_apply8 with the 8 outputs in registers (same arithmetic and order)
+__device__ __forceinline__ void patch_apply8r(const DispParams& U, int cls, const double rr[8], double o[8]) {
+    if (cls == 0) {
+        double hp[3], hm[5];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            hp[q] = rr[2 + 2 * q] - rr[3 + 2 * q];
+            hm[2 + q] = rr[2 + 2 * q] + rr[3 + 2 * q];
+        }
+        hm[0] = rr[0];
+        hm[1] = rr[1];
+        double yp[3] = {0, 0, 0}, ym[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+#pragma unroll
+            for (int a = 0; a < 5; ++a) ym[a] = fma(U.umT[c][a], hm[c], ym[a]);
+            if (c < 3) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) yp[a] = fma(U.upT[c][a], hp[c], yp[a]);
+            }
+        }
+        o[0] = ym[0];
+        o[1] = ym[1];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            o[2 + 2 * q] = ym[2 + q] + yp[q];
+            o[3 + 2 * q] = ym[2 + q] - yp[q];
+        }
+    } else {
+        // boundary classes: one output row of coefficient loads in flight -- the next row's address
+        // depends on this row's sum through an opaque (never taken) NaN test, so ptxas cannot hoist all
+        // 64 loads and spill the interior path (a NaN sum only ever meets NaN sums)
+        const double* G = U.ubnd + cls * 64;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) sacc = fma(__ldg(G + a * 8 + c), rr[c], sacc);
+            o[a] = sacc;
+            int dep;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.nan.f64 p, %1, %1;\n\tselp.s32 %0, 1, 0, p;\n\t}" : "=r"(dep) : "d"(sacc));
+            G += dep;
+        }
+    }
+}
+
+// Warp-marching BSR stage B (round 2; levels with n >= MG_WARP_MIN_N): the arithmetic of
+// bsr_b_march_kernel (r, y_u = r_u - alpha B_u^T dp, F_u^{-1} by 8-DoF displacement patches,
+// dw = D_w^{-1}(r_w - tau B_w^T dp), x + omega (du, dw, dp)) organised like
+// vanka_warp_kernel: one warp per 30-column strip, one row per iteration -- residual and y_u row y,
+// patch row y (left neighbour's y_u by shuffle, row y - 1's carried), owner row y - 1 (right
+// neighbour's corrections by shuffle, patch row y - 1's dy = 0 sums carried, r_w of row y - 1
+// carried).  x (4 rows), b (1), dp and K^{-1} (4 rows, 2 planes) arrive by TMA one iteration ahead.
+constexpr int WQ_DROW = 2 * WXW, WQ_DSLOT = (WQ_DROW + 15) / 16 * 16, WQ_DR = 4;
+template <bool HET> struct WQGeom {
+    static constexpr int BYTES = ((WXR * WXSLOT + WBSLOT + (HET ? 2 : 1) * WQ_DR * WQ_DSLOT) * 8 + 128 + 127) / 128 * 128;
+    static constexpr int NW = 232448 / BYTES > 12 ? 12 : 232448 / BYTES;   // one CTA per SM, <= 168 registers
+    static constexpr int NT = 32 * NW, SMEM = NW * BYTES;
+};
+template <bool HET, bool XZERO>
+__global__ void __launch_bounds__(WQGeom<HET>::NT, 1) bsr_b_warp_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                                       const __grid_constant__ CUtensorMap tmb,
+                                                                       const __grid_constant__ CUtensorMap tmd,
+                                                                       const __grid_constant__ CUtensorMap tmk,
+                                                                       const LevelParams L, const DispParams U,
+                                                                       double omega, double* __restrict__ xo, int MH,
+                                                                       int nstrips, int ntasks) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(128) double sm[];
+    if (*L.stop) return;
+    const int n = L.n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int task = blockIdx.x * WQGeom<HET>::NW + w;
+    if (task >= ntasks) return;
+    double* xr = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + w * WQGeom<HET>::BYTES);
+    double* br = xr + WXR * WXSLOT;
+    double* dr = br + WBSLOT;                          // [WQ_DR][2][WXW] dp
+    double* kr = dr + WQ_DR * WQ_DSLOT;                // [WQ_DR][2][WXW] K^{-1} (HET)
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(kr + (HET ? WQ_DR * WQ_DSLOT : 0));
+    uint64_t* bbar = xbar + WXR;
+    uint64_t* dbar = bbar + 1;
+    const int i0 = (task % nstrips) * WT, j0 = (task / nstrips) * MH;
+    const int rows = min(MH, n + 1 - j0);
+    const int yend = j0 + rows;
+    const int i = i0 - 1 + lane;
+    // x rows j0 - 2 .. yend + 1 (q = y - j0 + 2), b rows j0 - 1 .. yend (q = y - j0 + 1), dp / K rows
+    // j0 - 2 .. yend (q = y - j0 + 2)
+    auto load_x = [&](int y) {
+        const int q = y - (j0 - 2);
+        mbar_expect_tx(&xbar[q % WXR], WXROW * 8);
+        tma_load3(xr + (q % WXR) * WXSLOT, &tmx, i0 - 2, y, 0, &xbar[q % WXR]);
+    };
+    auto load_b = [&](int y) {
+        mbar_expect_tx(bbar, WBROW * 8);
+        tma_load3(br, &tmb, i0 - 2, y, 0, bbar);
+    };
+    auto load_d = [&](int y) {
+        const int q = y - (j0 - 2);
+        mbar_expect_tx(&dbar[q % WQ_DR], (HET ? 2 : 1) * WQ_DROW * 8);
+        tma_load3(dr + (q % WQ_DR) * WQ_DSLOT, &tmd, i0 - 2, y, 0, &dbar[q % WQ_DR]);
+        if (HET) tma_load3(kr + (q % WQ_DR) * WQ_DSLOT, &tmk, i0 - 2, y, 0, &dbar[q % WQ_DR]);
+    };
+    auto wait_x = [&](int y) { const int q = y - (j0 - 2); mbar_wait(&xbar[q % WXR], (q / WXR) & 1); };
+    auto wait_b = [&](int y) { const int q = y - (j0 - 1); mbar_wait(bbar, q & 1); };
+    auto wait_d = [&](int y) { const int q = y - (j0 - 2); mbar_wait(&dbar[q % WQ_DR], (q / WQ_DR) & 1); };
+    auto xrow = [&](int y) { return xr + ((y - (j0 - 2)) % WXR) * WXSLOT; };
+    auto drow = [&](int y) { return dr + ((y - (j0 - 2)) % WQ_DR) * WQ_DSLOT; };
+    auto krow = [&](int y) { return kr + ((y - (j0 - 2)) % WQ_DR) * WQ_DSLOT; };
+    // dp / K^{-1} of triangle sh of cell (ci, cj) (cj one of the rows in the ring)
+    auto dpc = [&](int ci, int cj, int sh) { return drow(cj)[sh * WXW + (ci - (i0 - 2))]; };
+    auto kinv = [&](int ci, int cj, int sh) -> double {
+        if (!HET) return L.kinv;
+        return krow(cj)[sh * WXW + (ci - (i0 - 2))];
+    };
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < WXR; ++k) mbar_init(&xbar[k], 1);
+        mbar_init(bbar, 1);
+#pragma unroll
+        for (int k = 0; k < WQ_DR; ++k) mbar_init(&dbar[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0) {
+        if (!XZERO)
+#pragma unroll
+            for (int k = 0; k < WXR; ++k) load_x(j0 - 2 + k);
+        load_b(j0 - 1);
+        // dp / K rows j0 - 2 .. j0 (the end of iteration y loads row y + 2 into the slot of row y - 2)
+#pragma unroll
+        for (int k = 0; k < WQ_DR - 1; ++k)
+            if (j0 - 2 + k <= yend) load_d(j0 - 2 + k);
+    }
+    if (!XZERO) {
+        wait_x(j0 - 2);
+        wait_x(j0 - 1);
+    }
+    wait_d(j0 - 2);
+    // carried: y_u of row y - 1 (planes 3, 4), the left neighbour's plane-4 y_u of row y - 1 is not
+    // needed (gather8 reads (a-1, b) only in the current row), r_w of row y - 1, the dy = 0 sums
+    double yp3 = 0, yp4 = 0, rw5 = 0, rw6 = 0, rw7 = 0;
+    double cd0 = 0, cd1 = 0, cd2 = 0, cd3 = 0, cd4 = 0;
+#pragma unroll 1
+    for (int y = j0 - 1; y <= yend; ++y) {
+        if (!XZERO) wait_x(y + 1);
+        wait_b(y);
+        wait_d(y);
+        // ---- r and y_u, row y
+        double rv[8];
+        {
+            const double* bp = br + (lane + 1);
+            if (!XZERO) {
+                const double* x0 = xrow(y) + (lane + 1);
+                double av[10];
+                if (HET) apply_rows_kr<WXW, WXW>(L, xrow(y - 1) + (lane + 1), x0, xrow(y + 1) + (lane + 1),
+                                                 krow(y - 1) + (lane + 1), krow(y) + (lane + 1), av);
+                else apply_rows<WXW, false>(L, xrow(y - 1) + (lane + 1), x0, xrow(y + 1) + (lane + 1), i, y, av);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) rv[k] = is_active(k, i, y, n) ? bp[k * WBW] - av[k] : 0.0;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) rv[k] = bp[k * WBW];
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && y + 1 <= yend) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            load_b(y + 1);
+        }
+        double yu[5];
+        {
+            double bt[5] = {0, 0, 0, 0, 0};
+#define MG_I(k, cdx, cdy, sh, qq) bt[k] = fma(L.bu[sh][qq], dpc(i + (cdx), y + (cdy), sh), bt[k]);
+            MG_INCIDENT_0(MG_I) MG_INCIDENT_1(MG_I) MG_INCIDENT_2(MG_I) MG_INCIDENT_3(MG_I) MG_INCIDENT_4(MG_I)
+#undef MG_I
+#pragma unroll
+            for (int k = 0; k < 5; ++k) yu[k] = is_active(k, i, y, n) ? rv[k] - L.alpha * bt[k] : rv[k];
+        }
+        // ---- patch row y (vertex (i, y)); gather8: (a, b) own, (a - 1, b) by shuffle, (a, b - 1) carried
+        const double l2 = __shfl_up_sync(0xffffffffu, yu[2], 1), l4 = __shfl_up_sync(0xffffffffu, yu[4], 1);
+        double o[8];
+        if (y >= j0 && lane >= 1 && i <= n && y <= n) {
+            double rr[8];
+            rr[0] = yu[0]; rr[1] = yu[1]; rr[2] = yu[2]; rr[3] = l2; rr[4] = yu[3]; rr[5] = yp3; rr[6] = l4; rr[7] = yp4;
+            patch_apply8r(U, vertex_class(i, y, n), rr, o);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = 0.0;
+        }
+        yp3 = yu[3];
+        yp4 = yu[4];
+        // ---- owner row y - 1
+        if (y >= j0 + 1 && lane >= 1 && lane <= WT && i <= n) {
+            const int yo = y - 1;
+            double d[10];
+            d[0] = cd0;
+            d[1] = cd1;
+            d[2] = cd2;
+            d[3] = cd3 + o[5];
+            d[4] = cd4 + o[7];
+            double bw[3] = {0, 0, 0};
+#define MG_I(k, cdx, cdy, sh, qq) bw[(k) - 5] = fma(L.bw[sh][(qq) - 9], dpc(i + (cdx), yo + (cdy), sh), bw[(k) - 5]);
+            MG_INCIDENT_5(MG_I) MG_INCIDENT_6(MG_I) MG_INCIDENT_7(MG_I)
+#undef MG_I
+            const double rwv[3] = {rw5, rw6, rw7};
+#pragma unroll
+            for (int k = 5; k < 8; ++k) {
+                double dwk = 0.0;
+#define MG_I(kk, cdx, cdy, sh, qq) dwk = fma(L.mw1d[sh][(qq) - 9], kinv(i + (cdx), yo + (cdy), sh), dwk);
+                if (k == 5) { MG_INCIDENT_5(MG_I) }
+                else if (k == 6) { MG_INCIDENT_6(MG_I) }
+                else { MG_INCIDENT_7(MG_I) }
+#undef MG_I
+                d[k] = is_active(k, i, yo, n) ? (rwv[k - 5] - L.tau * bw[k - 5]) / (L.tau * dwk) : 0.0;
+            }
+            d[8] = dpc(i, yo, 0);
+            d[9] = dpc(i, yo, 1);
+            const double* xv = xrow(yo) + (lane + 1);
+            const int64_t off = (int64_t)yo * L.pitch + i;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                const double xk = XZERO ? 0.0 : xv[k * WXW];
+                xo[k * L.plane + off] = is_active(k, i, yo, n) ? fma(omega, d[k], xk) : 0.0;
+            }
+        }
+        rw5 = rv[5];
+        rw6 = rv[6];
+        rw7 = rv[7];
+        {
+            const double s3 = __shfl_down_sync(0xffffffffu, o[3], 1), s6 = __shfl_down_sync(0xffffffffu, o[6], 1);
+            cd0 = o[0];
+            cd1 = o[1];
+            cd2 = o[2] + s3;
+            cd3 = o[4];
+            cd4 = s6;
+        }
+        // x row y - 1 and dp / K row y - 2 are dead: their slots take rows y + 3 and y + 2
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (!XZERO && y + 3 <= yend + 1) load_x(y + 3);
+            if (y + 2 <= yend) load_d(y + 2);
+        }
+    }
+}
+
 #undef MG_GATHER8
 
 // ------------------------------------------------------------------------------------------
@@ -3582,6 +3830,10 @@ void kernels_init() {
     set_smem(vanka_warp_kernel<false, false, false>, WGeom<false>::SMEM);
     set_smem(vanka_warp_kernel<false, true, false>, WGeom<true>::SMEM);
     set_smem(vanka_warp_kernel<true, false, false>, WGeom<false>::SMEM);
+    set_smem(bsr_b_warp_kernel<false, false>, WQGeom<false>::SMEM);
+    set_smem(bsr_b_warp_kernel<false, true>, WQGeom<false>::SMEM);
+    set_smem(bsr_b_warp_kernel<true, false>, WQGeom<true>::SMEM);
+    set_smem(bsr_b_warp_kernel<true, true>, WQGeom<true>::SMEM);
     set_smem(vanka_bnd_kernel<false, false>, WB_SMEM);
     carve(vanka_bnd2_kernel<false, false>);
     carve(vanka_bnd2_kernel<false, true>);
@@ -4199,14 +4451,20 @@ static int g_warp_prol = 1;
 static int g_warp_bk = 1;     // boundary-vertex patches precomputed by 1: vanka_bnd2_kernel, 2: vanka_bnd_kernel; 0: out of line in the sweep
 void set_warp_bk(int on) { g_warp_bk = on; }   // the fused-prolongation post-sweep through the warp kernel too (MG_WARP_PROL)
 void set_warp_prol(int on) { g_warp_prol = on; }
+static void warp_tasks_nw(int n, int slots_per_sm, int& MH, int& nstrips, int& ntasks);
 static void warp_tasks(int n, int& MH, int& nstrips, int& ntasks, bool prol = false) {
+    warp_tasks_nw(n, 2 * (prol ? WGeom<true>::NW : WGeom<false>::NW), MH, nstrips, ntasks);
+}
+static int g_warp_bsr = 0;   // BSR stage B through bsr_b_warp_kernel on the warp levels (MG_WARP_BSR; measured: no gain, off)
+void set_warp_bsr(int on) { g_warp_bsr = on; }
+static void warp_tasks_nw(int n, int slots_per_sm, int& MH, int& nstrips, int& ntasks) {
     static int target = -1;
     if (target < 0) {
         const char* v = getenv("MG_WARP_TARGET");
         target = v ? std::max(4, atoi(v)) : 128;
     }
     nstrips = (n + WT) / WT;   // ceil((n + 1) / WT)
-    const long slots = (long)sm_count() * 2 * (prol ? WGeom<true>::NW : WGeom<false>::NW);
+    const long slots = (long)sm_count() * slots_per_sm;
     const long base = (n + target) / target;
     const long waves = std::max(1L, (nstrips * base + slots / 2) / slots);
     long nseg = std::max(1L, waves * slots / nstrips);
@@ -4322,6 +4580,26 @@ cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double
     const bool het = L.kinv_field != nullptr;
     if (e == cudaSuccess) e = encode_vec_map(&mk, het ? L.kinv_field : dp, L.n, L.pitch, L.plane, BQ_W, 1, 2);
     if (e != cudaSuccess) return e;
+    if (g_warp_min_n > 0 && L.n >= g_warp_min_n && g_warp_bsr) {
+        CUtensorMap wx, wb, wd, wk;
+        e = encode_vec_map(&wx, x_zero ? b : x, L.n, L.pitch, L.plane, WXW, 1);
+        if (e == cudaSuccess) e = encode_vec_map(&wb, b, L.n, L.pitch, L.plane, WBW, 1);
+        if (e == cudaSuccess) e = encode_vec_map(&wd, dp, L.n, L.pitch, L.plane, WXW, 1, 2);
+        if (e == cudaSuccess) e = encode_vec_map(&wk, het ? L.kinv_field : dp, L.n, L.pitch, L.plane, WXW, 1, 2);
+        if (e != cudaSuccess) return e;
+        int wmh, nstrips, ntasks;
+        const int nw = het ? WQGeom<true>::NW : WQGeom<false>::NW;
+        warp_tasks_nw(L.n, nw, wmh, nstrips, ntasks);
+        const dim3 wgrid((ntasks + nw - 1) / nw);
+#define WB_LAUNCH(H_, Z_) launch_k(bsr_b_warp_kernel<H_, Z_>, wgrid, WQGeom<H_>::NT, WQGeom<H_>::SMEM, s, wx, wb, wd, wk, L, U, \
+                                   omega, xo, wmh, nstrips, ntasks)
+        if (het && x_zero) WB_LAUNCH(true, true);
+        else if (het) WB_LAUNCH(true, false);
+        else if (x_zero) WB_LAUNCH(false, true);
+        else WB_LAUNCH(false, false);
+#undef WB_LAUNCH
+        return cudaGetLastError();
+    }
     const int MH = march_height(L.n, BB_T, BQ_R, 3, relax_target(L.n));
     dim3 grid((L.n + BB_T) / BB_T, (L.n + MH) / MH);
 #define BB_LAUNCH(H_, Z_) launch_k(bsr_b_march_kernel<H_, Z_>, grid, BQ_NT, BB2_SMEM, s, mx, mb, md, mk, L, U, omega, xo, MH)

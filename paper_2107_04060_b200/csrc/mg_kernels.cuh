@@ -90,6 +90,8 @@ void set_warp_min_n(int N);
 void set_warp_prol(int on);
 // boundary-vertex patches of the warp sweep: 1 precomputed by vanka_bnd_kernel, 0 inline (out-of-line call)
 void set_warp_bk(int on);
+// BSR stage B through the warp-marching kernel on the levels with n >= MG_WARP_MIN_N (1) or the CTA kernel (0)
+void set_warp_bsr(int on);
 int blocks_residual_march(int n);
 // levels with n <= N use small 2-D tiles (8 x 4 owners / 4 x 2 coarse indices) in the single-pass
 // kernels: more, shorter CTAs for the latency-bound coarse levels (process-wide knob)

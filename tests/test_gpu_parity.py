@@ -286,6 +286,27 @@ def test_warp_sweep_bitwise(n, levels, pname, nu2):
         assert out[k][1] == out[3][1], k
 
 
+@pytest.mark.parametrize("n,levels,pname,het,nJ", [(64, 5, "unit", 3, 3), (48, 3, "mixed", None, 1),
+                                                    (96, 4, "stiff", 7, 2), (64, 5, "cfg5", None, 3)])
+def test_warp_bsr_bitwise(n, levels, pname, het, nJ):
+    """The warp-marching BSR stage B (bsr_b_warp_kernel: y_u and the displacement-patch corrections
+    moved by shuffles, dp and K^{-1} in TMA rings) gives bitwise the iterates and norms of the CTA
+    marching stage (same arithmetic, same order), with and without a K field,
+    zero-initial-guess levels, ragged strips and segments."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    b = mg_inputs.uniform_rhs(n, 8)
+    out = []
+    for warp in ("1", "0"):
+        H = C.gpu_hierarchy(n, levels, pname, het, march=True, env={"MG_WARP_MIN_N": warp, "MG_WARP_BSR": warp})
+        xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+        hist = [H.cycle(xd, bd, Opts(1, 1, "bsr", 0.7, 0.9, nJ)) for _ in range(3)]
+        out.append((H.to_host(xd), hist))
+        H.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (48, 3, "mixed", 2), (128, 6, "stiff", 1)])
 def test_small_tile_sweep_bitwise(n, levels, pname, nu):
     """The small-tile sweep with all of its global reads in the first round trip (vanka_small_kernel:
