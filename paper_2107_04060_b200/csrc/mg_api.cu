@@ -168,8 +168,9 @@ int cg_iters(int n) { return 24 * n + 64; }
 
 // does the first post-sweep on level l absorb the prolongation (relax_once with e_coarse)?
 bool fused_prolong(const mg_ctx* c, int l, const mg_cycle_opts& o) {
-    return c->fuse_prolong && o.relax == MG_VANKA && o.nu2 >= 1 && c->vanka_impl == 2 && !c->het && !c->exact &&
-           c->L[l].n >= c->march_min_n;
+    if (!c->fuse_prolong || o.relax != MG_VANKA || o.nu2 < 1 || c->het || c->exact) return false;
+    if (c->vanka_impl == 2 && c->L[l].n >= c->march_min_n) return true;   // marching / warp sweeps
+    return c->L[l].n <= small_tile_n() && small_diet();                   // small-tile sweep (vanka_small_kernel)
 }
 
 // one relaxation sweep on level l: xin -> xout (out of place).  e_coarse != nullptr (only where
@@ -183,7 +184,8 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         if (e_coarse) {
             const Level& Lc = c->L[l + 1];
             const ProlSrc E{e_coarse, Lc.n, Lc.pitch, (int64_t)(Lc.n + 1) * Lc.pitch};
-            CK(launch_vanka_march2(P, xin, b, xout, false, S, s, &E));
+            if (Lv.n <= small_tile_n()) CK(launch_vanka(P, xin, b, xout, false, S, s, nullptr, &E));
+            else CK(launch_vanka_march2(P, xin, b, xout, false, S, s, &E));
             return MG_OK;
         }
         if (c->vanka_impl == 2 && Lv.n >= c->march_min_n && !c->het && !c->exact)

@@ -724,6 +724,7 @@ struct VSmall {
     using T = VTile<VSX, VSY>;
     static constexpr int XS = T::XSZ, RS = 10 * T::RW * T::RH, CS = T::CSZ, GS = 8 * 400;
     static constexpr int SMEM = (XS + RS + CS + GS) * 8 + 16 * 4;
+    static constexpr int SMEM_P = SMEM + 10 * ((VSX + 4) / 2 + 1) * ((VSY + 4) / 2 + 1) * 8;
 };
 // the boundary classes present among the vertices (a, b), a in [i0, i0 + TX], b in [j0, j0 + TY]
 __device__ __forceinline__ unsigned tile_classes(int i0, int j0, int tx, int ty, int n) {
@@ -746,11 +747,17 @@ __device__ __forceinline__ unsigned tile_classes(int i0, int j0, int tx, int ty,
     return m & ~1u;   // interior class 0: constant bank
 }
 
-template <bool XZERO>
+// PROL: the first post-sweep relaxes x + P e_H (the coarse-grid correction fused in):
+// the coarse tile under the x tile arrives with the first round trip, one thread per coarse cell adds
+// P e_H to its 2 x 2 fine indices of the x tile (prolong_kernel's table chains), bitwise prolong_kernel
+// followed by the sweep; the launch of prolong_kernel on the level disappears.
+constexpr int VS_CW = (VSX + 4) / 2 + 1, VS_CH = (VSY + 4) / 2 + 1, VS_CS = 10 * VS_CW * VS_CH;
+template <bool XZERO, bool PROL = false>
 __global__ void __launch_bounds__(VTile<VSX, VSY>::NT, 4) vanka_small_kernel(const VankaParams P,
                                                                              const double* __restrict__ x,
                                                                              const double* __restrict__ b,
-                                                                             double* __restrict__ xo, NormSink S) {
+                                                                             double* __restrict__ xo, NormSink S,
+                                                                             const ProlSrc E) {
     pdl_wait();
     pdl_trigger();
     using T = VTile<VSX, VSY>;
@@ -759,6 +766,7 @@ __global__ void __launch_bounds__(VTile<VSX, VSY>::NT, 4) vanka_small_kernel(con
     double* rs = xs + VSmall::XS;         // residual tile [10][RH][RW]
     double* cs = rs + VSmall::RS;         // patch corrections [20][PH][PW]
     double* gs = cs + VSmall::CS;         // dense inverses of the boundary classes present, in class order
+    double* es = gs + VSmall::GS;         // PROL: coarse tile [10][VS_CH][VS_CW] from coarse (i0/2 - 1, j0/2 - 1)
     const LevelParams& L = P.L;
     const int stopv = *L.stop;            // checked after the loads are in flight
     const int n = L.n, pitch = L.pitch, t = threadIdx.x;
@@ -775,7 +783,7 @@ __global__ void __launch_bounds__(VTile<VSX, VSY>::NT, 4) vanka_small_kernel(con
         for (int k = 0; k < 10; ++k) bpre[k] = in ? __ldg(b + k * plane + o) : 0.0;
     }
     const int ox = t % VSX, oy = t / VSX;
-    {
+    if (!PROL) {
         const int i = i0 + ox, j = j0 + oy;
         const bool in = !XZERO && t < VSX * VSY && i <= n && j <= n;
         const int64_t o = in ? (int64_t)j * pitch + i : 0;
@@ -798,9 +806,44 @@ __global__ void __launch_bounds__(VTile<VSX, VSY>::NT, 4) vanka_small_kernel(con
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     if (!XZERO) load_tile<T::XW, T::XH, 10, true, 16>(xs, x, i0 - 2, j0 - 2, n, pitch, plane, 0, t, T::NT);
+    if (PROL) load_tile<VS_CW, VS_CH, 10, true, 16>(es, E.e, i0 / 2 - 1, j0 / 2 - 1, E.nc, E.pitchc, E.planec, 0, t, T::NT);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (stopv) return;
+    if (PROL) {
+        // x tile + P e_H: thread c < 24 takes coarse cell (I, J) = (i0/2 - 1 + cx, j0/2 - 1 + cy) and its fine
+        // indices (2I + di, 2J + dj) at tile position (2cx + di, 2cy + dj)
+        constexpr int NCX = T::XW / 2, NCY = T::XH / 2;
+        if (t < NCX * NCY) {
+            const int cy = t / NCX, cx = t - cy * NCX;
+            const int I = i0 / 2 - 1 + cx, J = j0 / 2 - 1 + cy;
+            if (I >= 0 && J >= 0 && I < E.nc && J < E.nc) {
+                const double* e0 = es + cy * VS_CW + cx;
+#define EQ(dI, dJ, pl, wt) v = fma(wt, e0[(pl) * (VS_CW * VS_CH) + (dJ) * VS_CW + (dI)], v);
+#define P2(dj, kf)                                                                       \
+    {                                                                                    \
+        double v = 0.0;                                                                  \
+        MG_PROLONG_0_##dj##_##kf(EQ) const double v0 = v;                                \
+        v = 0.0;                                                                         \
+        MG_PROLONG_1_##dj##_##kf(EQ) const double v1 = v;                                \
+        double* xp2 = xs + (kf) * (T::XW * T::XH) + (2 * cy + (dj)) * T::XW + 2 * cx;    \
+        if (is_active(kf, 2 * I, 2 * J + (dj), n)) xp2[0] += v0;                         \
+        if (is_active(kf, 2 * I + 1, 2 * J + (dj), n)) xp2[1] += v1;                     \
+    }
+#define P4(kf) P2(0, kf) P2(1, kf)
+                P4(0) P4(1) P4(2) P4(3) P4(4) P4(5) P4(6) P4(7) P4(8) P4(9)
+#undef P4
+#undef P2
+#undef EQ
+            }
+        }
+        __syncthreads();
+        // the owners' x: the prolongated tile value
+        if (t < VSX * VSY) {
+#pragma unroll
+            for (int k = 0; k < 10; ++k) xown[k] = xs[k * (T::XW * T::XH) + (oy + 2) * T::XW + (ox + 2)];
+        }
+    }
     // phase 1: r = b - A x on the tile + 1 ring
     if (t < T::RW * T::RH) {
         const int i = i0 - 1 + lx, j = j0 - 1 + ly;
@@ -3854,6 +3897,7 @@ void kernels_init() {
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_small_kernel<false>, VSmall::SMEM);
+    set_smem(vanka_small_kernel<false, true>, VSmall::SMEM_P);
     set_smem(vanka_small_kernel<true>, VSmall::SMEM);
     set_smem(vanka_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_het_kernel<false>, V_SMEM);
@@ -3887,7 +3931,9 @@ static_assert(BBNT >= BB_RW * BB_RH && BBNT % 32 == 0, "bsr_b thread mapping");
 int blocks_residual(int n) { return ((n + RTX) / RTX) * ((n + RTY) / RTY); }
 int g_small_tile_n = 128;
 int g_small_diet = 1;   // small-tile sweeps through vanka_small_kernel (all global reads in one round trip; MG_SMALL_DIET)
-void set_small_diet(int on) { g_small_diet = on; }   // levels with n <= this use the small 2-D tiles (mg_setup: MG_SMALL_TILE_N)
+void set_small_diet(int on) { g_small_diet = on; }
+int small_tile_n() { return g_small_tile_n; }
+int small_diet() { return g_small_diet; }   // levels with n <= this use the small 2-D tiles (mg_setup: MG_SMALL_TILE_N)
 void set_small_tile_n(int n) { g_small_tile_n = n; }
 int blocks_vanka(int n) {
     return n <= g_small_tile_n ? ((n + VSX) / VSX) * ((n + VSY) / VSY) : ((n + VTX) / VTX) * ((n + VTY) / VTY);
@@ -4410,7 +4456,8 @@ cudaError_t launch_copy(double* dst, const double* src, int64_t len, const int* 
 int dot_partials_needed() { return VK * DOT_BLOCKS; }
 
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xo, bool x_zero,
-                         NormSink S, cudaStream_t s, const HvInterior* Ti) {
+                         NormSink S, cudaStream_t s, const HvInterior* Ti, const ProlSrc* E) {
+    if (E && (P.hv.cls || P.L.n > g_small_tile_n || !g_small_diet || x_zero)) return cudaErrorInvalidValue;
     if (P.hv.cls) {   // heterogeneous K: condensed patch solves, K^{-1} field in the residual
         if (!Ti) return cudaErrorInvalidValue;
         if (P.L.n <= g_small_tile_n) {
@@ -4428,9 +4475,11 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
     if (P.L.n <= g_small_tile_n) {
         using T = VTile<VSX, VSY>;
         dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
+        const ProlSrc none{nullptr, 0, 0, 0};
         if (g_small_diet) {
-            if (x_zero) launch_k(vanka_small_kernel<true>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S);
-            else launch_k(vanka_small_kernel<false>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S);
+            if (x_zero) launch_k(vanka_small_kernel<true>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S, none);
+            else if (E) launch_k(vanka_small_kernel<false, true>, grid, T::NT, VSmall::SMEM_P, s, P, x, b, xo, S, *E);
+            else launch_k(vanka_small_kernel<false>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S, none);
         } else {
             if (x_zero) launch_k(vanka_kernel<true, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);
             else launch_k(vanka_kernel<false, VSX, VSY>, grid, T::NT, T::SMEM, s, P, x, b, xo, S);

@@ -77,8 +77,12 @@ cudaError_t launch_step_rhs(const LevelParams& L, double inv_M, double alpha, co
 // per-vertex S_v^{-1} planes of the heterogeneous Vanka patches (setup; L.kinv_field set)
 cudaError_t launch_hv_sinv(const LevelParams& L, const double* W, const double* C, double* sinv, cudaStream_t s);
 // P.hv.cls != nullptr: heterogeneous-K sweep (condensed patch solves, 2-D tiles on every level)
+// E != nullptr (levels with n <= small_tile_n, MG_SMALL_DIET): relax x + P e_H (prolongation fused in)
 cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b, double* xout,
-                         bool x_zero, NormSink norm, cudaStream_t s, const HvInterior* Ti = nullptr);
+                         bool x_zero, NormSink norm, cudaStream_t s, const HvInterior* Ti = nullptr,
+                         const ProlSrc* E = nullptr);
+int small_tile_n();
+int small_diet();
 // row-marching TMA variant of the same sweep (identical arithmetic); the production kernel
 // E != nullptr: relax x + P e_H (prolongation of the coarse iterate E->e fused into the sweep)
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
