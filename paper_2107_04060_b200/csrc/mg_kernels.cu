@@ -4517,7 +4517,12 @@ static void warp_tasks_nw(int n, int slots_per_sm, int& MH, int& nstrips, int& n
     const long base = (n + target) / target;
     const long waves = std::max(1L, (nstrips * base + slots / 2) / slots);
     long nseg = std::max(1L, waves * slots / nstrips);
-    MH = std::max(8, (int)((n + nseg) / nseg));
+    static int minrows = -1;   // shortest segment (MG_WARP_MINROWS): the per-task prologue and pipeline fill
+    if (minrows < 0) {
+        const char* v = getenv("MG_WARP_MINROWS");
+        minrows = v ? std::max(4, atoi(v)) : 8;
+    }
+    MH = std::max(minrows, (int)((n + nseg) / nseg));
     nseg = (n + MH) / MH;
     ntasks = (int)(nstrips * nseg);
 }
