@@ -181,7 +181,9 @@ __device__ __forceinline__ double kinv_ww(const LevelParams& L, int ci, int cj, 
 // A x for the 10 DoFs of index (i, j) (eq. block_form_rq): xm, x0, xp point at (i, j-1), (i, j),
 // (i, j+1) in plane 0 of a shared-memory tile whose planes are PS doubles apart and whose rows
 // hold the column neighbours contiguously (all offsets compile-time constants).
-template <int PS, bool HET>
+// ROWS: bit k set -> row k is evaluated (a row subset for the small-tile kernels that split a
+// position's rows over several threads; each row's accumulation is the same sequence either way)
+template <int PS, bool HET, unsigned ROWS = 0x3FFu>
 __device__ __forceinline__ void apply_rows(const LevelParams& L, const double* xm, const double* x0, const double* xp,
                                            int i, int j, double av[10]) {
 #define XS(dx, dy, pl) ((dy) < 0 ? xm : ((dy) > 0 ? xp : x0))[(pl) * PS + (dx)]
@@ -189,11 +191,11 @@ __device__ __forceinline__ void apply_rows(const LevelParams& L, const double* x
     // factored stencil (mg_tables.h MG_STENCIL_FACT): entries sharing a coefficient up to sign are
     // summed first, then one FMA per coefficient group; rows interleaved round-robin (10
     // independent accumulator chains)
-#define MG_A(row, g, sg, e) a##row = fma(sg L.cg[g], e, a##row);
+#define MG_A(row, g, sg, e) if ((ROWS >> (row)) & 1u) a##row = fma(sg L.cg[g], e, a##row);
     MG_STENCIL_FACT(MG_A)
 #undef MG_A
 #define MG_W(row, cdx, cdy, sh, dx, dy, pl, e, e2) \
-    a##row = fma(L.ww[sh][e][e2] * kinv_ww<HET>(L, i + (cdx), j + (cdy), sh), XS(dx, dy, pl), a##row);
+    if ((ROWS >> (row)) & 1u) a##row = fma(L.ww[sh][e][e2] * kinv_ww<HET>(L, i + (cdx), j + (cdy), sh), XS(dx, dy, pl), a##row);
     MG_STENCIL_WW_5(MG_W)
     MG_STENCIL_WW_6(MG_W)
     MG_STENCIL_WW_7(MG_W)
@@ -930,6 +932,230 @@ __global__ void __launch_bounds__(VTile<VSX, VSY>::NT, 4) vanka_small_kernel(con
         }
     }
     if (S.out || S.state) norm_finish<T::NT>(S, nrm);
+}
+
+// Four threads per position (vanka_small4_kernel, MG_SMALL_DIET=2): the small-tile sweep above with each
+// residual position's ten rows split over four threads (rows {0,2}, {1,3}, {4,5,6}, {7,8,9}: ~48 FMA +
+// loads each), each patch solve's twenty outputs split over four threads (the +/- blocks by output
+// pairs, the dense boundary inverses 5 rows each) and the prolongation's planes split likewise -- on the
+// latency-bound coarse levels a kernel is one warp's serial instruction stream, which this cuts ~4x.
+// Same arithmetic and order per value: bitwise vanka_small_kernel.
+constexpr int VS4_NT = 256;
+template <int G> struct RowGroup;
+template <> struct RowGroup<0> { static constexpr unsigned M = 0x005u; };
+template <> struct RowGroup<1> { static constexpr unsigned M = 0x00Au; };
+template <> struct RowGroup<2> { static constexpr unsigned M = 0x070u; };
+template <> struct RowGroup<3> { static constexpr unsigned M = 0x380u; };
+template <bool XZERO, bool PROL = false>
+__global__ void __launch_bounds__(VS4_NT, 2) vanka_small4_kernel(const VankaParams P, const double* __restrict__ x,
+                                                                 const double* __restrict__ b, double* __restrict__ xo,
+                                                                 NormSink S, const ProlSrc E) {
+    pdl_wait();
+    pdl_trigger();
+    using T = VTile<VSX, VSY>;
+    extern __shared__ __align__(16) double sm[];
+    double* xs = sm;
+    double* rs = xs + VSmall::XS;
+    double* cs = rs + VSmall::RS;
+    double* gs = cs + VSmall::CS;
+    double* es = gs + VSmall::GS;
+    const LevelParams& L = P.L;
+    const int stopv = *L.stop;
+    const int n = L.n, pitch = L.pitch, t = threadIdx.x;
+    const int64_t plane = L.plane;
+    const int i0 = blockIdx.x * VSX, j0 = blockIdx.y * VSY;
+    const int pos = t & 63, grp = t >> 6;   // grp warp-uniform (two warps per group)
+    const unsigned gm = grp == 0 ? RowGroup<0>::M : grp == 1 ? RowGroup<1>::M : grp == 2 ? RowGroup<2>::M : RowGroup<3>::M;
+    const int ly = pos / T::RW, lx = pos - ly * T::RW;
+    double bpre[10];
+    {
+        const int i = i0 - 1 + lx, j = j0 - 1 + ly;
+        const bool in = pos < T::RW * T::RH && i >= 0 && j >= 0 && i <= n && j <= n;
+        const int64_t o = in ? (int64_t)j * pitch + i : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) bpre[k] = (in && ((gm >> k) & 1u)) ? __ldg(b + k * plane + o) : 0.0;
+    }
+    const int ox = t % VSX, oy = t / VSX;
+    double xown[10];
+    if (!PROL) {
+        const int i = i0 + ox, j = j0 + oy;
+        const bool in = !XZERO && t < VSX * VSY && i <= n && j <= n;
+        const int64_t o = in ? (int64_t)j * pitch + i : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) xown[k] = in ? __ldg(x + k * plane + o) : 0.0;
+    }
+    const unsigned cm = tile_classes(i0, j0, VSX, VSY, n);
+    {
+        int slot = 0;
+        for (int c = 1; c < 9; ++c) {
+            if (!((cm >> c) & 1u)) continue;
+            const double* src = P.gbnd + c * 400;
+            double* dst = gs + slot * 400;
+            for (int q = t; q < 200; q += VS4_NT)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 2 * q)), "l"(src + 2 * q)
+                             : "memory");
+            ++slot;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    if (!XZERO) load_tile<T::XW, T::XH, 10, true, 4>(xs, x, i0 - 2, j0 - 2, n, pitch, plane, 0, t, VS4_NT);
+    if (PROL) load_tile<VS_CW, VS_CH, 10, true, 4>(es, E.e, i0 / 2 - 1, j0 / 2 - 1, E.nc, E.pitchc, E.planec, 0, t, VS4_NT);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (stopv) return;
+    if (PROL) {
+        // coarse cell c = t % 32 (24 used), plane group grp: {0,1,2}, {3,4}, {5,6,7}, {8,9}
+        constexpr int NCX = T::XW / 2, NCY = T::XH / 2;
+        const int c = t & 31, pg = t >> 5;
+        if (c < NCX * NCY && pg < 4) {
+            const int cy = c / NCX, cx = c - cy * NCX;
+            const int I = i0 / 2 - 1 + cx, J = j0 / 2 - 1 + cy;
+            if (I >= 0 && J >= 0 && I < E.nc && J < E.nc) {
+                const double* e0 = es + cy * VS_CW + cx;
+#define EQ(dI, dJ, pl, wt) v = fma(wt, e0[(pl) * (VS_CW * VS_CH) + (dJ) * VS_CW + (dI)], v);
+#define P2(dj, kf)                                                                       \
+    {                                                                                    \
+        double v = 0.0;                                                                  \
+        MG_PROLONG_0_##dj##_##kf(EQ) const double v0 = v;                                \
+        v = 0.0;                                                                         \
+        MG_PROLONG_1_##dj##_##kf(EQ) const double v1 = v;                                \
+        double* xp2 = xs + (kf) * (T::XW * T::XH) + (2 * cy + (dj)) * T::XW + 2 * cx;    \
+        if (is_active(kf, 2 * I, 2 * J + (dj), n)) xp2[0] += v0;                         \
+        if (is_active(kf, 2 * I + 1, 2 * J + (dj), n)) xp2[1] += v1;                     \
+    }
+#define P4(kf) P2(0, kf) P2(1, kf)
+                if (pg == 0) { P4(0) P4(1) P4(2) }
+                else if (pg == 1) { P4(3) P4(4) }
+                else if (pg == 2) { P4(5) P4(6) P4(7) }
+                else { P4(8) P4(9) }
+#undef P4
+#undef P2
+#undef EQ
+            }
+        }
+        __syncthreads();
+        if (t < VSX * VSY) {
+#pragma unroll
+            for (int k = 0; k < 10; ++k) xown[k] = xs[k * (T::XW * T::XH) + (oy + 2) * T::XW + (ox + 2)];
+        }
+    }
+    // phase 1: rows of group grp at residual position pos
+    if (pos < T::RW * T::RH) {
+        const int i = i0 - 1 + lx, j = j0 - 1 + ly;
+        double av[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) av[k] = 0.0;
+        if (!XZERO) {
+            const double* x0 = xs + (ly + 1) * T::XW + (lx + 1);
+            if (grp == 0) apply_rows<T::XW * T::XH, false, RowGroup<0>::M>(L, x0 - T::XW, x0, x0 + T::XW, i, j, av);
+            else if (grp == 1) apply_rows<T::XW * T::XH, false, RowGroup<1>::M>(L, x0 - T::XW, x0, x0 + T::XW, i, j, av);
+            else if (grp == 2) apply_rows<T::XW * T::XH, false, RowGroup<2>::M>(L, x0 - T::XW, x0, x0 + T::XW, i, j, av);
+            else apply_rows<T::XW * T::XH, false, RowGroup<3>::M>(L, x0 - T::XW, x0, x0 + T::XW, i, j, av);
+            if (L.lamx != 0.0) exact_bubble_add(L.lamx, x0 - T::XW, x0, x0 + T::XW, T::XW * T::XH, av);
+        }
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+            if ((gm >> k) & 1u)
+                rs[k * T::RW * T::RH + pos] = XZERO ? bpre[k] : (is_active(k, i, j, n) ? (bpre[k] - av[k]) : 0.0);
+    }
+    __syncthreads();
+    // phase 2: patch part grp of vertex pos
+    constexpr int OS = T::PW * T::PH;
+    if (pos < OS) {
+        const int py = pos / T::PW, px = pos - py * T::PW;
+        const int a = i0 + px, bb = j0 + py;
+        if (a <= n && bb <= n) {
+            double rr[20];
+            gather20<T::RW, T::RH>(rs + (py + 1) * T::RW + (px + 1), rr);
+            const int cls = vertex_class(a, bb, n);
+            double* out = cs + pos;
+            if (cls == 0) {
+                double hp[9], hm[11];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    hp[q] = rr[2 + 2 * q] - rr[3 + 2 * q];
+                    hm[2 + q] = rr[2 + 2 * q] + rr[3 + 2 * q];
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    hp[6 + q] = rr[14 + 2 * q] + rr[15 + 2 * q];
+                    hm[8 + q] = rr[14 + 2 * q] - rr[15 + 2 * q];
+                }
+                hm[0] = rr[0];
+                hm[1] = rr[1];
+                auto ymr = [&](int r) { double v = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 11; ++c) v = fma(P.gmT[c][r], hm[c], v);
+                    return v; };
+                auto ypr = [&](int r) { double v = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) v = fma(P.gpT[c][r], hp[c], v);
+                    return v; };
+                // output pair of unit q (0..5: (yp[q], ym[2+q]) -> 2+2q, 3+2q; 6..8: (yp[q], ym[2+q]) -> 14+2(q-6), +1)
+                auto unit = [&](int q) {
+                    const double p = ypr(q), m = ymr(2 + q);
+                    if (q < 6) {
+                        out[(2 + 2 * q) * OS] = m + p;
+                        out[(3 + 2 * q) * OS] = m - p;
+                    } else {
+                        out[(14 + 2 * (q - 6)) * OS] = p + m;
+                        out[(15 + 2 * (q - 6)) * OS] = p - m;
+                    }
+                };
+                if (grp == 0) { out[0] = ymr(0); out[OS] = ymr(1); unit(0); unit(1); }
+                else if (grp == 1) { unit(2); unit(3); unit(4); }
+                else if (grp == 2) { unit(5); unit(6); }
+                else { unit(7); unit(8); }
+            } else {
+                const double2* G = reinterpret_cast<const double2*>(gs + __popc(cm & ((1u << cls) - 1u)) * 400);
+#pragma unroll
+                for (int u = 0; u < 5; ++u) {
+                    const int k = 5 * grp + u;
+                    double sacc = 0.0;
+#pragma unroll
+                    for (int c2 = 0; c2 < 10; ++c2) {
+                        const double2 g = G[k * 10 + c2];
+                        sacc = fma(g.x, rr[2 * c2], sacc);
+                        sacc = fma(g.y, rr[2 * c2 + 1], sacc);
+                    }
+                    out[k * OS] = sacc;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 5; ++u) cs[(5 * grp + u) * OS + pos] = 0.0;
+        }
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    if (t < VSX * VSY) {
+        const int i = i0 + ox, j = j0 + oy;
+        if (i <= n && j <= n) {
+            const double* c00 = cs + oy * T::PW + ox;
+#define CC(s_, dx, dy) c00[(s_) * (T::PW * T::PH) + (dy) * T::PW + (dx)]
+            double d[10];
+            d[0] = CC(0, 0, 0);
+            d[1] = CC(1, 0, 0);
+            d[2] = CC(2, 0, 0) + CC(3, 1, 0);
+            d[3] = CC(4, 0, 0) + CC(5, 0, 1);
+            d[4] = CC(6, 1, 0) + CC(7, 0, 1);
+            d[5] = CC(8, 0, 0) + CC(9, 1, 0);
+            d[6] = CC(10, 0, 0) + CC(11, 0, 1);
+            d[7] = CC(12, 1, 0) + CC(13, 0, 1);
+            d[8] = CC(14, 0, 0) + CC(16, 1, 0) + CC(19, 0, 1);
+            d[9] = CC(15, 1, 1) + CC(17, 0, 1) + CC(18, 1, 0);
+#undef CC
+            const int64_t o = (int64_t)j * pitch + i;
+            const double* r00 = rs + (oy + 1) * T::RW + (ox + 1);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                xo[k * plane + o] = is_active(k, i, j, n) ? fma(P.omega, d[k], xown[k]) : 0.0;
+                const double rv = r00[k * T::RW * T::RH];
+                nrm = fma(rv, rv, nrm);
+            }
+        }
+    }
+    if (S.out || S.state) norm_finish<VS4_NT>(S, nrm);
 }
 
 template <bool XZERO, int TX = VTX, int TY = VTY, bool HET = false>
@@ -3898,6 +4124,9 @@ void kernels_init() {
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_small_kernel<false>, VSmall::SMEM);
     set_smem(vanka_small_kernel<false, true>, VSmall::SMEM_P);
+    set_smem(vanka_small4_kernel<false>, VSmall::SMEM);
+    set_smem(vanka_small4_kernel<true>, VSmall::SMEM);
+    set_smem(vanka_small4_kernel<false, true>, VSmall::SMEM_P);
     set_smem(vanka_small_kernel<true>, VSmall::SMEM);
     set_smem(vanka_kernel<true, VSX, VSY>, VTile<VSX, VSY>::SMEM);
     set_smem(vanka_het_kernel<false>, V_SMEM);
@@ -3930,7 +4159,8 @@ static_assert(BBNT >= BB_RW * BB_RH && BBNT % 32 == 0, "bsr_b thread mapping");
 
 int blocks_residual(int n) { return ((n + RTX) / RTX) * ((n + RTY) / RTY); }
 int g_small_tile_n = 128;
-int g_small_diet = 1;   // small-tile sweeps through vanka_small_kernel (all global reads in one round trip; MG_SMALL_DIET)
+int g_small_diet = 2;   // small-tile sweeps: 2 vanka_small4_kernel (4 threads per position), 1 vanka_small_kernel (all global
+                        // reads in one round trip), 0 vanka_kernel + prolong_kernel (MG_SMALL_DIET)
 void set_small_diet(int on) { g_small_diet = on; }
 int small_tile_n() { return g_small_tile_n; }
 int small_diet() { return g_small_diet; }   // levels with n <= this use the small 2-D tiles (mg_setup: MG_SMALL_TILE_N)
@@ -4476,7 +4706,11 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
         using T = VTile<VSX, VSY>;
         dim3 grid((P.L.n + VSX) / VSX, (P.L.n + VSY) / VSY);
         const ProlSrc none{nullptr, 0, 0, 0};
-        if (g_small_diet) {
+        if (g_small_diet == 2) {
+            if (x_zero) launch_k(vanka_small4_kernel<true>, grid, VS4_NT, VSmall::SMEM, s, P, x, b, xo, S, none);
+            else if (E) launch_k(vanka_small4_kernel<false, true>, grid, VS4_NT, VSmall::SMEM_P, s, P, x, b, xo, S, *E);
+            else launch_k(vanka_small4_kernel<false>, grid, VS4_NT, VSmall::SMEM, s, P, x, b, xo, S, none);
+        } else if (g_small_diet) {
             if (x_zero) launch_k(vanka_small_kernel<true>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S, none);
             else if (E) launch_k(vanka_small_kernel<false, true>, grid, T::NT, VSmall::SMEM_P, s, P, x, b, xo, S, *E);
             else launch_k(vanka_small_kernel<false>, grid, T::NT, VSmall::SMEM, s, P, x, b, xo, S, none);

@@ -316,14 +316,16 @@ def test_small_tile_sweep_bitwise(n, levels, pname, nu):
     from paper_2107_04060_b200 import Opts
     b = mg_inputs.uniform_rhs(n, 6)
     out = []
-    for diet in ("1", "0"):
+    # 2: four threads per position (vanka_small4_kernel), 1: vanka_small_kernel, 0: vanka_kernel + prolong_kernel
+    for diet in ("2", "1", "0"):
         H = C.gpu_hierarchy(n, levels, pname, env={"MG_SMALL_DIET": diet})
         xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
         hist = [H.cycle(xd, bd, Opts(nu, nu, "vanka", 0.7)) for _ in range(3)]
         out.append((H.to_host(xd), hist))
         H.close()
-    assert np.array_equal(out[0][0], out[1][0])
-    assert out[0][1] == out[1][1]
+    for k in range(2):
+        assert np.array_equal(out[k][0], out[2][0]), k
+        assert out[k][1] == out[2][1], k
 
 
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (32, 4, "mixed", 2), (128, 6, "stiff", 1)])
