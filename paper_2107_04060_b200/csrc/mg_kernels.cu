@@ -1538,6 +1538,36 @@ __global__ void __launch_bounds__(256) coarse_kernel(int N, const double* __rest
     }
 }
 
+// small coarsest systems (N <= CS_MAXN): G staged in shared memory by cp.async while the right-hand side
+// is gathered, then the same per-row FMA chains in k order (bitwise coarse_kernel) read from shared memory
+constexpr int CS_MAXN = 160;
+__global__ void __launch_bounds__(256) coarse_smem_kernel(int N, const double* __restrict__ G,
+                                                          const int64_t* __restrict__ slots,
+                                                          const double* __restrict__ b, double* __restrict__ x,
+                                                          const int* __restrict__ stop) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(16) double csm[];
+    double* gs = csm;                       // [N][N] column major (as G)
+    double* rb = csm + ((N * N + 1) & ~1);  // [N]
+    const int stopv = *stop;
+    const int NN = N * N;
+    for (int q = threadIdx.x; 2 * q + 1 < NN; q += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(gs + 2 * q)), "l"(G + 2 * q) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if ((NN & 1) && threadIdx.x == 0) gs[NN - 1] = __ldg(G + NN - 1);
+    for (int k = threadIdx.x; k < N; k += blockDim.x) rb[k] = __ldg(b + slots[k]);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (stopv) return;
+    for (int row = threadIdx.x; row < N; row += blockDim.x) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < N; ++k) acc = fma(gs[k * N + row], rb[k], acc);
+        x[slots[row]] = acc;
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // inexact Braess-Sarazin
 constexpr int BTX = 32, BTY = 8, BANT = 416, BBNT = 352;   // one position per thread in every phase
@@ -4142,6 +4172,7 @@ void kernels_init() {
     set_smem(restrict_small_kernel<false>, CTile<CSX, CSY>::SMEM_FUSED);
     set_smem(restrict_small_kernel<true>, CTile<CSX, CSY>::SMEM_FUSED);
     set_smem(coarse_kernel, 4096 * 8);
+    set_smem(coarse_smem_kernel, (((CS_MAXN * CS_MAXN + 1) & ~1) + CS_MAXN) * 8);
     set_smem(bsr_a_kernel<false, false>, BA_SMEM);
     set_smem(bsr_a_kernel<false, true>, BA_SMEM);
     set_smem(bsr_a_kernel<true, false>, BA_SMEM);
@@ -4978,6 +5009,10 @@ cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double*
 
 cudaError_t launch_coarse(int N, const double* G, const int64_t* slots, const double* b, double* x,
                           const int* stop, cudaStream_t s) {
+    if (N <= CS_MAXN && (reinterpret_cast<uintptr_t>(G) & 15) == 0) {
+        launch_k(coarse_smem_kernel, 1, 256, (size_t)(((N * N + 1) & ~1) + N) * 8, s, N, G, slots, b, x, stop);
+        return cudaGetLastError();
+    }
     int blocks = N <= 1024 ? 1 : (N + 255) / 256;
     launch_k(coarse_kernel, blocks, 256, N * 8, s, N, G, slots, b, x, stop);
     return cudaGetLastError();
