@@ -2769,8 +2769,10 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
     pdl_trigger();
     __shared__ double xt[WB2_XS];   // [10][PH + 2][PW + 2], plane stride 140
     __shared__ double rt[WB2_RS];   // [10][PH][PW], plane stride 66
+    __shared__ __align__(16) double gt[3 * 400];   // the dense inverses of this side's (at most 3) vertex classes
     const LevelParams& L = P.L;
-    if (*L.stop) return;
+    // every global read of the kernel is issued before the stop flag is tested (one L2 round trip)
+    const int stopv = *L.stop;
     const int n = L.n, nb = bnd_count(n), side = blockIdx.y, t = threadIdx.x;
     const bool horiz = side < 2;
     const int v0 = blockIdx.x * WB2_T;
@@ -2779,6 +2781,21 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
     const int PW = horiz ? WB2_T + 1 : 2, PH = horiz ? 2 : WB2_T + 1;
     const int pi0 = horiz ? v0 - 1 : fixed - 1, pj0 = horiz ? fixed - 1 : v0 - 1;   // residual origin
     const int XW = PW + 2;
+    // classes: bottom 3, 4, 5; top 6, 7, 8; left 1; right 2 (vertex_class)
+    const int c0 = side == 0 ? 3 : side == 1 ? 6 : side == 2 ? 1 : 2, ncls = horiz ? 3 : 1;
+    for (int q = t; q < ncls * 200; q += WB2_NT)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(gt + 2 * q)), "l"(P.gbnd + c0 * 400 + 2 * q)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    double bpre[10];
+    {
+        const int ly = t / PW, lx = t - ly * PW;
+        const int i = pi0 + lx, j = pj0 + ly;
+        const bool in = t < PW * PH && i >= 0 && j >= 0 && i <= n && j <= n;
+        const int64_t o = in ? (int64_t)j * L.pitch + i : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) bpre[k] = in ? __ldg(b + k * L.plane + o) : 0.0;
+    }
     if (!XZERO) {
         for (int p = t; p < (PW + 2) * (PH + 2); p += WB2_NT) {
             const int ly = p / XW, lx = p - ly * XW;
@@ -2791,23 +2808,24 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
 #pragma unroll
             for (int k = 0; k < 10; ++k) xt[k * 140 + p] = xk[k];
         }
-        __syncthreads();
     }
-    for (int p = t; p < PW * PH; p += WB2_NT) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (stopv) return;
+    if (t < PW * PH) {
+        const int p = t;
         const int ly = p / PW, lx = p - ly * PW;
         const int i = pi0 + lx, j = pj0 + ly;
-        const bool in = i >= 0 && j >= 0 && i <= n && j <= n;
-        const int64_t o = in ? (int64_t)j * L.pitch + i : 0;
         if (XZERO) {
 #pragma unroll
-            for (int k = 0; k < 10; ++k) rt[k * 66 + p] = in ? __ldg(b + k * L.plane + o) : 0.0;
+            for (int k = 0; k < 10; ++k) rt[k * 66 + p] = bpre[k];
         } else {
             const double* x0 = xt + (ly + 1) * XW + (lx + 1);
             double av[10];
             apply_rows<140, false>(L, x0 - XW, x0, x0 + XW, i, j, av);
             const unsigned m = active_mask(i, j, n);
 #pragma unroll
-            for (int k = 0; k < 10; ++k) rt[k * 66 + p] = ((m >> k) & 1u) ? __ldg(b + k * L.plane + o) - av[k] : 0.0;
+            for (int k = 0; k < 10; ++k) rt[k * 66 + p] = ((m >> k) & 1u) ? bpre[k] - av[k] : 0.0;
         }
     }
     __syncthreads();
@@ -2828,7 +2846,7 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
     rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
     rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
 #undef RR
-    const double* G = P.gbnd + vertex_class(a, bb, n) * 400;
+    const double* G = gt + (vertex_class(a, bb, n) - c0) * 400;
     double* out = P.bcorr + bnd_index(a, bb, n);
 #pragma unroll
     for (int u = 0; u < 5; ++u) {
@@ -2837,7 +2855,7 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
         double sacc = 0.0;
 #pragma unroll
         for (int c2 = 0; c2 < 10; ++c2) {
-            const double2 gg = __ldg(g + c2);
+            const double2 gg = g[c2];
             sacc = fma(gg.x, rr[2 * c2], sacc);
             sacc = fma(gg.y, rr[2 * c2 + 1], sacc);
         }
