@@ -367,10 +367,12 @@ def main():
     fused = o.relax == "vanka" and os.environ.get("MG_FUSE_PROLONG", "1") != "0" and \
         os.environ.get("MG_VANKA_IMPL", "2") == "2" and not het and args.quadrature == "rq"
     if o.relax == "vanka" and het:
-        # heterogeneous Vanka (2-D tile kernel): read x, b, write x + the per-vertex S~^{-1} table
-        # (21 doubles per vertex = 16.8 B per active DoF at 10 DoFs per vertex) + K^{-1} (2 per cell)
+        # heterogeneous Vanka: read x, b, write x + the per-vertex S~^{-1} table (21 doubles per vertex
+        # = 16.8 B per active DoF at 10 DoFs per vertex) + K^{-1} (2 per cell)
         alg_bytes = (24.0 + 16.8 + 1.6) * nact
-        dom = "vanka_kernel<HET> (level 0: residual with the K^{-1} field + condensed patch solves + update)"
+        hwarp = n >= int(os.environ.get("MG_HET_WARP_N", "1024")) > 0
+        dom = (("vanka_hwarp_kernel + vanka_bnd_kernel<HET>" if hwarp else "vanka_het_kernel") +
+               " (level 0: residual with the K^{-1} field + condensed patch solves + update)")
     elif o.relax == "vanka":
         # read x, read b, write x over the active DoFs; averaged over the pre-sweep and the post-sweep
         # (which with the fused prolongation also reads e_H: + 8 B x N_1 ~ 2 B per fine DoF)

@@ -118,6 +118,7 @@ struct mg_ctx {
     int launches = 0;             // kernel launches enqueued by the last captured cycle
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 0: 2-D tiles everywhere
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
+    int het_warp_n = 1024;        // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one kernel
                                   // (measured slower: one CTA 442 us, grid-wide cooperative 323 us vs 247 us
@@ -190,6 +191,8 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         }
         if (c->vanka_impl == 2 && Lv.n >= c->march_min_n && !c->het && !c->exact)
             CK(launch_vanka_march2(P, xin, b, xout, xzero, S, s));
+        else if (c->het && !c->exact && c->het_warp_n > 0 && Lv.n >= c->het_warp_n)
+            CK(launch_vanka_hwarp(P, Lv.hv_int, xin, b, xout, xzero, S, s));
         else CK(launch_vanka(P, xin, b, xout, xzero, S, s, c->het ? &Lv.hv_int : nullptr));
         return MG_OK;
     }
@@ -488,6 +491,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_VANKA_IMPL")) c->vanka_impl = atoi(v);
     if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
     if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
+    if (const char* v = getenv("MG_HET_WARP_N")) c->het_warp_n = atoi(v);
     if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_BSR_IMPL")) c->bsr_impl = atoi(v);
     // process-wide kernel knobs: every setup re-reads them (unset -> default), so they never stick

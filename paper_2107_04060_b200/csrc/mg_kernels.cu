@@ -1389,6 +1389,51 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int pitchf, int nc
 #undef MG_Q
 }
 
+// Bandwidth-bound levels (nf > 256): the same chains with the ten fine planes split over blockIdx.z
+// (two planes per thread: 4 fine pairs in flight, ~40 registers, full occupancy; prolong_kernel<false>
+// holds all 20 pairs in 136 registers -> one 256-thread CTA per SM, 2.4 TB/s at 2048^2).  Bitwise
+// prolong_kernel: every output is the same FMA chain in table order.
+__global__ void __launch_bounds__(256) prolong_planes_kernel(int nf, int pitchf, int nc, int pitchc,
+                                                             const double* __restrict__ e, double* __restrict__ x,
+                                                             const int* __restrict__ stop) {
+    pdl_wait();
+    pdl_trigger();
+    if (*stop) return;
+    const int I = blockIdx.x * 32 + (threadIdx.x & 31), J = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (I >= nc || J >= nc) return;
+    const int64_t planec = (int64_t)(nc + 1) * pitchc, planef = (int64_t)(nf + 1) * pitchf;
+    const double* e0 = e + (int64_t)J * pitchc + I;
+    const int fi = 2 * I, fj = 2 * J;
+    double* x0 = x + (int64_t)fj * pitchf + fi;
+    const int ka = 2 * blockIdx.z;   // planes ka, ka + 1
+    double2 xq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xq[q] = *reinterpret_cast<const double2*>(x0 + (ka + (q >> 1)) * planef + (q & 1) * pitchf);
+#define MG_Q(dI, dJ, pl, w) v = fma(w, __ldg(e0 + (pl) * planec + (dJ) * pitchc + (dI)), v);
+#define PROL2(dj, kf, slot)                                                             \
+    {                                                                                   \
+        double v = 0.0;                                                                 \
+        MG_PROLONG_0_##dj##_##kf(MG_Q) const double v0 = v;                             \
+        v = 0.0;                                                                        \
+        MG_PROLONG_1_##dj##_##kf(MG_Q) const double v1 = v;                             \
+        double2 xv = xq[slot];                                                          \
+        if (is_active(kf, fi, fj + dj, nf)) xv.x += v0;                                 \
+        if (is_active(kf, fi + 1, fj + dj, nf)) xv.y += v1;                             \
+        *reinterpret_cast<double2*>(x0 + kf * planef + dj * pitchf) = xv;               \
+    }
+#define PROL8(ka_, kb_) PROL2(0, ka_, 0) PROL2(1, ka_, 1) PROL2(0, kb_, 2) PROL2(1, kb_, 3)
+    switch (blockIdx.z) {
+        case 0: PROL8(0, 1) break;
+        case 1: PROL8(2, 3) break;
+        case 2: PROL8(4, 5) break;
+        case 3: PROL8(6, 7) break;
+        default: PROL8(8, 9) break;
+    }
+#undef PROL8
+#undef PROL2
+#undef MG_Q
+}
+
 // ------------------------------------------------------------------------------------------
 // Bottom of the V-cycle in ONE CTA (Vanka, levels with n <= 32 down to the coarsest): the same tile
 // functions as the per-level kernels, run by 16 virtual blocks of 64 threads over the tiles of a
@@ -2688,7 +2733,7 @@ __device__ __forceinline__ void prol_point(const ProlSrc& E, int i, int j, int n
 #undef EQ
 }
 
-template <bool XZERO, bool PROL>
+template <bool XZERO, bool PROL, bool HET = false>
 __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, const double* __restrict__ x,
                                                           const double* __restrict__ b, const ProlSrc E) {
     pdl_wait();
@@ -2738,7 +2783,7 @@ __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, c
                 const int i = a - 1 + px, j = bb - 1 + py;
                 const double* x0 = tile + (py + 1) * 4 + (px + 1);
                 double av[10];
-                apply_rows<16, false>(L, x0 - 4, x0, x0 + 4, i, j, av);
+                apply_rows<16, HET>(L, x0 - 4, x0, x0 + 4, i, j, av);
                 const unsigned m = active_mask(i, j, n);
                 const int64_t o = (i >= 0 && j >= 0 && i <= n && j <= n) ? (int64_t)j * L.pitch + i : 0;
 #pragma unroll
@@ -2755,7 +2800,8 @@ __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, c
     rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
     rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
 #undef RR
-    patch_apply20(P, vertex_class(a, bb, n), rr, P.bcorr + t, nb);
+    if (HET) patch_apply_het_t<false>(P, P.hv.cls + vertex_class(a, bb, n) * MG_HV_CLS, a, bb, rr, P.bcorr + t, nb);
+    else patch_apply20(P, vertex_class(a, bb, n), rr, P.bcorr + t, nb);
 }
 
 // Cooperative version (the default): a CTA takes a run of 32 boundary vertices of one side, stages
@@ -3208,6 +3254,241 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
     }
 #undef CD
     if (S.out || S.state) norm_finish<WGeom<PROL>::NT>(S, nrm);
+}
+
+// ------------------------------------------------------------------------------------------
+// Warp-marching heterogeneous-K Vanka sweep (round 2; K-field levels with n >= MG_HET_WARP_N): the
+// organisation of vanka_warp_kernel (one warp per 30-column strip, one row per iteration, residuals and
+// corrections moved by shuffles, no CTA barrier) with the arithmetic of vanka_het_kernel -- the residual
+// reads K^{-1} from a 4-row TMA ring of the two K^{-1} planes (apply_rows_kr), interior patches run the
+// condensed +/- solve with the per-vertex S~^{-1} (patch_apply_het_pm, 21 coalesced loads per row), the
+// boundary vertices' outputs come from vanka_bnd_kernel<.., HET>.  Same summation order in the owner phase:
+// bitwise vanka_het_kernel.
+constexpr int HW_KR = 4, HW_KROW = 2 * WXW, HW_KSLOT = (HW_KROW + 15) / 16 * 16;
+constexpr int HW_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + HW_KR * HW_KSLOT) * 8 + 128 + 127) / 128 * 128;
+#ifndef MG_HW_NW
+#define MG_HW_NW 6
+#endif
+constexpr int HW_NW = MG_HW_NW, HW_NT = 32 * HW_NW, HW_SMEM = HW_NW * HW_BYTES;
+static_assert(2 * (HW_SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
+
+template <bool XZERO>
+__global__ void __launch_bounds__(HW_NT, 2) vanka_hwarp_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const __grid_constant__ CUtensorMap tmb,
+                                                               const __grid_constant__ CUtensorMap tmk,
+                                                               const VankaParams P, const __grid_constant__ HvInterior Ti,
+                                                               double* __restrict__ xo, NormSink S, int MH, int nstrips,
+                                                               int ntasks) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ __align__(128) double sm[];
+    const LevelParams& L = P.L;
+    if (*L.stop) return;
+    const int n = L.n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int task = blockIdx.x * HW_NW + w;
+    double nrm = 0.0;
+    if (task < ntasks) {
+        double* xr = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + w * HW_BYTES);   // [WXR][10][WXW]
+        double* br = xr + WXR * WXSLOT;                                                      // [WBR][10][WBW]
+        double* kr = br + WBR * WBSLOT;                                                      // [HW_KR][2][WXW]
+        uint64_t* xbar = reinterpret_cast<uint64_t*>(kr + HW_KR * HW_KSLOT);                 // [WXR]
+        uint64_t* bbar = xbar + WXR;                                                         // [WBR]
+        uint64_t* kbar = bbar + WBR;                                                         // [HW_KR]
+        int strip, seg;
+        const int nseg = ntasks / nstrips;
+        if (nstrips <= 2) {
+            strip = task % nstrips;
+            seg = task / nstrips;
+        } else if (task < 2 * nseg) {
+            strip = (task & 1) ? nstrips - 1 : 0;
+            seg = task >> 1;
+        } else {
+            strip = 1 + (task - 2 * nseg) % (nstrips - 2);
+            seg = (task - 2 * nseg) / (nstrips - 2);
+        }
+        const int i0 = strip * WT, j0 = seg * MH;
+        const int rows = min(MH, n + 1 - j0);
+        const int yend = j0 + rows;
+        const int i = i0 - 1 + lane;
+        const bool inner = i0 - 1 >= 1 && i0 + WT <= n - 1;
+        auto load_x = [&](int y) {
+            const int q = y - (j0 - 2);
+            uint64_t* bar = &xbar[q % WXR];
+            mbar_expect_tx(bar, WXROW * 8);
+            tma_load3(xr + (q % WXR) * WXSLOT, &tmx, i0 - 2, y, 0, bar);
+        };
+        auto load_b = [&](int y) {
+            const int q = y - (j0 - 1);
+            uint64_t* bar = &bbar[q % WBR];
+            mbar_expect_tx(bar, WBROW * 8);
+            tma_load3(br + (q % WBR) * WBSLOT, &tmb, i0 - 2, y, 0, bar);
+        };
+        // K^{-1} cell row y (cells (., y)): load number q = y - (j0 - 2), slot q % HW_KR
+        auto load_k = [&](int y) {
+            const int q = y - (j0 - 2);
+            uint64_t* bar = &kbar[q % HW_KR];
+            mbar_expect_tx(bar, HW_KROW * 8);
+            tma_load3(kr + (q % HW_KR) * HW_KSLOT, &tmk, i0 - 2, y, 0, bar);
+        };
+        auto wait_x = [&](int y) { const int q = y - (j0 - 2); mbar_wait(&xbar[q % WXR], (q / WXR) & 1); };
+        auto wait_b = [&](int y) { const int q = y - (j0 - 1); mbar_wait(&bbar[q % WBR], (q / WBR) & 1); };
+        auto wait_k = [&](int y) { const int q = y - (j0 - 2); mbar_wait(&kbar[q % HW_KR], (q / HW_KR) & 1); };
+        auto xrow = [&](int y) { return xr + ((y - (j0 - 2)) % WXR) * WXSLOT; };
+        auto krow = [&](int y) { return kr + ((y - (j0 - 2)) % HW_KR) * HW_KSLOT; };
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < WXR; ++k) mbar_init(&xbar[k], 1);
+#pragma unroll
+            for (int k = 0; k < WBR; ++k) mbar_init(&bbar[k], 1);
+#pragma unroll
+            for (int k = 0; k < HW_KR; ++k) mbar_init(&kbar[k], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (!XZERO) {
+#pragma unroll
+                for (int k = 0; k < WXR; ++k) load_x(j0 - 2 + k);
+                // K rows j0 - 2 .. j0 (the end of iteration y loads row y + 2 into the slot of row y - 2)
+#pragma unroll
+                for (int k = 0; k < HW_KR - 1; ++k)
+                    if (j0 - 2 + k <= yend) load_k(j0 - 2 + k);
+            }
+#pragma unroll
+            for (int k = 0; k < WBR; ++k) load_b(j0 - 1 + k);
+        }
+        if (!XZERO) {
+            wait_x(j0 - 2);
+            wait_x(j0 - 1);
+            wait_k(j0 - 2);
+        }
+        double rp3 = 0, rp4 = 0, rp6 = 0, rp7 = 0, rp8 = 0, rp9 = 0, rpl9 = 0;
+        double cdr[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) cdr[k] = 0.0;
+#pragma unroll 1
+        for (int y = j0 - 1; y <= yend; ++y) {
+            // ---- residual row y
+            if (!XZERO) {
+                wait_x(y + 1);
+                wait_k(y);
+            }
+            wait_b(y);
+            double rv[10];
+            {
+                const double* bp = br + ((y - (j0 - 1)) % WBR) * WBSLOT + (lane + 1);
+                if (!XZERO) {
+                    const double* x0 = xrow(y) + (lane + 1);
+                    double av[10];
+                    apply_rows_kr<WXW, WXW>(L, xrow(y - 1) + (lane + 1), x0, xrow(y + 1) + (lane + 1),
+                                            krow(y - 1) + (lane + 1), krow(y) + (lane + 1), av);
+                    if (inner && y >= 1 && y <= n - 1) {
+#pragma unroll
+                        for (int k = 0; k < 10; ++k) rv[k] = bp[k * WBW] - av[k];
+                    } else {
+                        const unsigned m = active_mask(i, y, n);
+#pragma unroll
+                        for (int k = 0; k < 10; ++k) rv[k] = ((m >> k) & 1u) ? bp[k * WBW] - av[k] : 0.0;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) rv[k] = bp[k * WBW];
+                }
+            }
+            __syncwarp();
+            if (lane == 0 && y + WBR <= yend) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                load_b(y + WBR);
+            }
+            if (lane >= 1 && lane <= WT && i <= n && y >= j0 && y < yend) {
+#pragma unroll
+                for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+            }
+            // ---- patch row y (vertex (i, y)); left neighbour's residuals by shuffle
+            const double l2 = __shfl_up_sync(0xffffffffu, rv[2], 1), l4 = __shfl_up_sync(0xffffffffu, rv[4], 1);
+            const double l5 = __shfl_up_sync(0xffffffffu, rv[5], 1), l7 = __shfl_up_sync(0xffffffffu, rv[7], 1);
+            const double l8 = __shfl_up_sync(0xffffffffu, rv[8], 1), l9 = __shfl_up_sync(0xffffffffu, rv[9], 1);
+            double o[20];
+            if (y >= j0 && lane >= 1 && i <= n && y <= n) {
+                double rr[20];
+                rr[0] = rv[0]; rr[1] = rv[1];
+                rr[2] = rv[2]; rr[3] = l2;   rr[4] = rv[3]; rr[5] = rp3;
+                rr[6] = l4;    rr[7] = rp4;
+                rr[8] = rv[5]; rr[9] = l5;   rr[10] = rv[6]; rr[11] = rp6;
+                rr[12] = l7;   rr[13] = rp7;
+                rr[14] = rv[8]; rr[15] = rpl9; rr[16] = l8; rr[17] = rp9;
+                rr[18] = l9;   rr[19] = rp8;
+                if (i > 0 && i < n && y > 0 && y < n) {
+                    patch_apply_het_pm(P, Ti.pm, i, y, rr, o, 1);
+                } else {   // boundary vertex: its outputs were computed by vanka_bnd_kernel<.., HET>
+                    const int nb = bnd_count(n), bi = bnd_index(i, y, n);
+#pragma unroll
+                    for (int k = 0; k < 20; ++k) o[k] = __ldg(P.bcorr + k * nb + bi);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 20; ++k) o[k] = 0.0;
+            }
+            rp3 = rv[3]; rp4 = rv[4]; rp6 = rv[6]; rp7 = rv[7]; rp8 = rv[8]; rp9 = rv[9]; rpl9 = l9;
+            // ---- owner row y - 1
+            const double r15 = __shfl_down_sync(0xffffffffu, o[15], 1);
+            if (y >= j0 + 1) {
+                const int yo = y - 1;
+                if (lane >= 1 && lane <= WT && i <= n) {
+                    double d[10];
+                    d[0] = cdr[0];
+                    d[1] = cdr[1];
+                    d[2] = cdr[2];
+                    d[3] = cdr[3] + o[5];
+                    d[4] = cdr[4] + o[7];
+                    d[5] = cdr[5];
+                    d[6] = cdr[6] + o[11];
+                    d[7] = cdr[7] + o[13];
+                    d[8] = cdr[8] + o[19];
+                    d[9] = (r15 + o[17]) + cdr[9];
+                    const double* xv = xrow(yo) + (lane + 1);
+                    const int64_t off = (int64_t)yo * L.pitch + i;
+                    if (inner && yo >= 1 && yo <= n - 1) {
+#pragma unroll
+                        for (int k = 0; k < 10; ++k) xo[k * L.plane + off] = fma(P.omega, d[k], XZERO ? 0.0 : xv[k * WXW]);
+                    } else {
+                        const unsigned m = active_mask(i, yo, n);
+#pragma unroll
+                        for (int k = 0; k < 10; ++k) {
+                            const double xk = XZERO ? 0.0 : xv[k * WXW];
+                            xo[k * L.plane + off] = ((m >> k) & 1u) ? fma(P.omega, d[k], xk) : 0.0;
+                        }
+                    }
+                }
+            }
+            {
+                const double s3 = __shfl_down_sync(0xffffffffu, o[3], 1), s6 = __shfl_down_sync(0xffffffffu, o[6], 1);
+                const double s9 = __shfl_down_sync(0xffffffffu, o[9], 1), s12 = __shfl_down_sync(0xffffffffu, o[12], 1);
+                const double s16 = __shfl_down_sync(0xffffffffu, o[16], 1), s18 = __shfl_down_sync(0xffffffffu, o[18], 1);
+                cdr[0] = o[0];
+                cdr[1] = o[1];
+                cdr[2] = o[2] + s3;
+                cdr[3] = o[4];
+                cdr[4] = s6;
+                cdr[5] = o[8] + s9;
+                cdr[6] = o[10];
+                cdr[7] = s12;
+                cdr[8] = o[14] + s16;
+                cdr[9] = s18;
+            }
+            // x row y - 1 and K row y - 2 are dead: their slots take rows y + 3 and y + 2
+            if (!XZERO) {
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (y + 3 <= yend + 1) load_x(y + 3);
+                    if (y + 2 <= yend) load_k(y + 2);
+                }
+            }
+        }
+    }
+    if (S.out || S.state) norm_finish<HW_NT>(S, nrm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -4147,6 +4428,10 @@ void kernels_init() {
     set_smem(vanka_warp_kernel<false, false, false>, WGeom<false>::SMEM);
     set_smem(vanka_warp_kernel<false, true, false>, WGeom<true>::SMEM);
     set_smem(vanka_warp_kernel<true, false, false>, WGeom<false>::SMEM);
+    set_smem(vanka_hwarp_kernel<false>, HW_SMEM);
+    set_smem(vanka_hwarp_kernel<true>, HW_SMEM);
+    set_smem(vanka_bnd_kernel<false, false, true>, WB_SMEM);
+    set_smem(vanka_bnd_kernel<true, false, true>, WB_SMEM);
     set_smem(bsr_b_warp_kernel<false, false>, WQGeom<false>::SMEM);
     set_smem(bsr_b_warp_kernel<false, true>, WQGeom<false>::SMEM);
     set_smem(bsr_b_warp_kernel<true, false>, WQGeom<true>::SMEM);
@@ -4877,6 +5162,27 @@ cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const dou
     else launch_k(vanka_march2_kernel<false, 0>, grid, M2NT, M2SMEM, s, mx, mb, P, xo, S, MH, none);
     return cudaGetLastError();
 }
+// heterogeneous-K warp-marching sweep (vanka_hwarp_kernel) + its boundary kernel
+cudaError_t launch_vanka_hwarp(const VankaParams& P, const HvInterior& Ti, const double* x, const double* b, double* xo,
+                               bool x_zero, NormSink S, cudaStream_t s) {
+    const LevelParams& L = P.L;
+    if (!P.hv.cls || !L.kinv_field) return cudaErrorInvalidValue;
+    int wmh, nstrips, ntasks;
+    warp_tasks_nw(L.n, 2 * HW_NW, wmh, nstrips, ntasks);
+    CUtensorMap wx, wb, wk;
+    cudaError_t e = encode_vec_map(&wx, x_zero ? b : x, L.n, L.pitch, L.plane, WXW, 1);
+    if (e == cudaSuccess) e = encode_vec_map(&wb, b, L.n, L.pitch, L.plane, WBW, 1);
+    if (e == cudaSuccess) e = encode_vec_map(&wk, L.kinv_field, L.n, L.pitch, L.plane, WXW, 1, 2);
+    if (e != cudaSuccess) return e;
+    const ProlSrc none{nullptr, 0, 0, 0};
+    const dim3 bgrid((bnd_count(L.n) + WB_NT - 1) / WB_NT);
+    if (x_zero) launch_k(vanka_bnd_kernel<true, false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, none);
+    else launch_k(vanka_bnd_kernel<false, false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, none);
+    const dim3 wgrid((ntasks + HW_NW - 1) / HW_NW);
+    if (x_zero) launch_k(vanka_hwarp_kernel<true>, wgrid, HW_NT, HW_SMEM, s, wx, wb, wk, P, Ti, xo, S, wmh, nstrips, ntasks);
+    else launch_k(vanka_hwarp_kernel<false>, wgrid, HW_NT, HW_SMEM, s, wx, wb, wk, P, Ti, xo, S, wmh, nstrips, ntasks);
+    return cudaGetLastError();
+}
 int blocks_vanka_march2(int n) {
     const int MH = march_height(n, M2T, M2R, 3, relax_target(n));
     int wmh, nstrips, ntasks;
@@ -5020,7 +5326,15 @@ cudaError_t launch_bottom(const BottomArgs& A, cudaStream_t s) {
 cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double* e, double* x, const int* stop,
                            cudaStream_t s) {
     dim3 grid((nc + 31) / 32, (nc + 7) / 8);
-    if (nf <= 256 && g_small_diet) launch_k(prolong_kernel<true>, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
+    static int planes_n = -1;   // levels with nf >= this: the plane-split kernel (MG_PROL_PLANES_N; 0 = off)
+    if (planes_n < 0) {
+        const char* v = getenv("MG_PROL_PLANES_N");
+        planes_n = v ? atoi(v) : 512;
+    }
+    if (planes_n > 0 && nf >= planes_n) {
+        grid.z = 5;
+        launch_k(prolong_planes_kernel, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
+    } else if (nf <= 256 && g_small_diet) launch_k(prolong_kernel<true>, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
     else launch_k(prolong_kernel<false>, grid, 256, 0, s, nf, pitchf, nc, pitchc, e, x, stop);
     return cudaGetLastError();
 }

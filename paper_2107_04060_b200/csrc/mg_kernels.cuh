@@ -88,6 +88,9 @@ int small_diet();
 cudaError_t launch_vanka_march2(const VankaParams& P, const double* x, const double* b, double* xout,
                                 bool x_zero, NormSink norm, cudaStream_t s, const ProlSrc* E = nullptr);
 int blocks_vanka_march2(int n);
+// heterogeneous-K warp-marching sweep (vanka_hwarp_kernel; bitwise vanka_het_kernel) and its boundary kernel
+cudaError_t launch_vanka_hwarp(const VankaParams& P, const HvInterior& Ti, const double* x, const double* b,
+                               double* xout, bool x_zero, NormSink norm, cudaStream_t s);
 // levels with n >= N run the plain Vanka sweeps through the warp-marching kernel (0: never)
 void set_warp_min_n(int N);
 // the fused-prolongation post-sweep through the warp-marching kernel as well (1) or the CTA kernel (0)

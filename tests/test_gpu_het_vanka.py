@@ -77,3 +77,25 @@ def test_het_vanka_cycle_history(n, levels, pname, het, cycles):
     e_oo = C.block_rel_err(m, m.from_active(xsA[-1]), m.from_active(xsO[-1]))
     for k in e_go:
         assert e_go[k] <= 1e-9 + 4 * e_oo[k], (e_go, e_oo)
+
+
+@pytest.mark.parametrize("n,levels,pname,het,nu", [(64, 5, "unit", 3, 1), (96, 4, "stiff", 7, 2), (132, 3, "mixed", 5, 1),
+                                                   (31, 2, "unit", 3, 1)])
+def test_het_warp_sweep_bitwise(n, levels, pname, het, nu):
+    """The warp-marching heterogeneous-K Vanka sweep (vanka_hwarp_kernel: K^{-1} rows in a TMA ring,
+    residuals and patch corrections moved by shuffles, boundary-vertex patches from vanka_bnd_kernel)
+    gives bitwise the iterates and norms of the 2-D tile kernel vanka_het_kernel (same arithmetic, same
+    summation order, reading A20) on every level -- ragged strips and
+    segments, zero-initial-guess levels, odd n."""
+    _torch()
+    from paper_2107_04060_b200 import Opts
+    b = mg_inputs.uniform_rhs(n, 11)
+    out = []
+    for warp in ("1", "0"):
+        H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_HET_WARP_N": warp})
+        xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+        hist = [H.cycle(xd, bd, Opts(nu, nu, "vanka", 0.74)) for _ in range(3)]
+        out.append((H.to_host(xd), hist))
+        H.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
