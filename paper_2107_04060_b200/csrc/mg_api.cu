@@ -118,7 +118,7 @@ struct mg_ctx {
     int launches = 0;             // kernel launches enqueued by the last captured cycle
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 0: 2-D tiles everywhere
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
-    int het_warp_n = 1024;        // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
+    int het_warp_n = 512;         // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one kernel
                                   // (measured slower: one CTA 442 us, grid-wide cooperative 323 us vs 247 us

@@ -2808,7 +2808,7 @@ __global__ void __launch_bounds__(WB_NT) vanka_bnd_kernel(const VankaParams P, c
 // the x tile (with P e_H added, PROL) in shared memory once, computes each residual position once
 // and splits the dense patch solves over 4 threads per vertex (5 outputs each, same order).
 constexpr int WB2_T = 32, WB2_NT = 128, WB2_XS = 10 * 4 * 35, WB2_RS = 10 * 2 * 33;
-template <bool XZERO, bool PROL>
+template <bool XZERO, bool PROL, bool HET = false>
 __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P, const double* __restrict__ x,
                                                             const double* __restrict__ b, const ProlSrc E) {
     pdl_wait();
@@ -2829,8 +2829,10 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
     const int XW = PW + 2;
     // classes: bottom 3, 4, 5; top 6, 7, 8; left 1; right 2 (vertex_class)
     const int c0 = side == 0 ? 3 : side == 1 ? 6 : side == 2 ? 1 : 2, ncls = horiz ? 3 : 1;
-    for (int q = t; q < ncls * 200; q += WB2_NT)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(gt + 2 * q)), "l"(P.gbnd + c0 * 400 + 2 * q)
+    // HET: the side's condensed class tables (MG_HV_CLS doubles each) instead of the dense inverses
+    const double* gsrc = HET ? P.hv.cls + c0 * MG_HV_CLS : P.gbnd + c0 * 400;
+    for (int q = t; q < ncls * (HET ? MG_HV_CLS / 2 : 200); q += WB2_NT)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(gt + 2 * q)), "l"(gsrc + 2 * q)
                      : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
     double bpre[10];
@@ -2868,7 +2870,7 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
         } else {
             const double* x0 = xt + (ly + 1) * XW + (lx + 1);
             double av[10];
-            apply_rows<140, false>(L, x0 - XW, x0, x0 + XW, i, j, av);
+            apply_rows<140, HET>(L, x0 - XW, x0, x0 + XW, i, j, av);
             const unsigned m = active_mask(i, j, n);
 #pragma unroll
             for (int k = 0; k < 10; ++k) rt[k * 66 + p] = ((m >> k) & 1u) ? bpre[k] - av[k] : 0.0;
@@ -2876,9 +2878,10 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
     }
     __syncthreads();
     // patches: vertex q = t / 4 of the run, outputs 5 (t % 4) .. 5 (t % 4) + 4
-    const int q = t >> 2, part = t & 3;
+    // HET: one thread per vertex runs the condensed solve (class table in shared memory, S~^{-1} per vertex)
+    const int q = HET ? t : t >> 2, part = t & 3;
     const int a = horiz ? v0 + q : fixed, bb = horiz ? fixed : v0 + q;
-    const bool valid = horiz ? (a <= n) : (bb >= 1 && bb <= n - 1);
+    const bool valid = (horiz ? (a <= n) : (bb >= 1 && bb <= n - 1)) && (!HET || t < WB2_T);
     if (!valid || (!horiz && n < 2)) return;
     // residual of (a + dx, bb + dy), dx, dy in {-1, 0}: tile position (a + dx - pi0, bb + dy - pj0)
     const double* r00 = rt + (bb - pj0) * PW + (a - pi0);
@@ -2892,8 +2895,12 @@ __global__ void __launch_bounds__(WB2_NT) vanka_bnd2_kernel(const VankaParams P,
     rr[14] = RR(0, 0, 8);  rr[15] = RR(-1, -1, 9); rr[16] = RR(-1, 0, 8); rr[17] = RR(0, -1, 9);
     rr[18] = RR(-1, 0, 9); rr[19] = RR(0, -1, 8);
 #undef RR
-    const double* G = gt + (vertex_class(a, bb, n) - c0) * 400;
     double* out = P.bcorr + bnd_index(a, bb, n);
+    if (HET) {
+        patch_apply_het_t<true>(P, gt + (vertex_class(a, bb, n) - c0) * MG_HV_CLS, a, bb, rr, out, nb);
+        return;
+    }
+    const double* G = gt + (vertex_class(a, bb, n) - c0) * 400;
 #pragma unroll
     for (int u = 0; u < 5; ++u) {
         const int k = part * 5 + u;
@@ -3278,7 +3285,7 @@ __global__ void __launch_bounds__(HW_NT, 2) vanka_hwarp_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmk,
                                                                const VankaParams P, const __grid_constant__ HvInterior Ti,
                                                                double* __restrict__ xo, NormSink S, int MH, int nstrips,
-                                                               int ntasks) {
+                                                               int ntasks, int pf) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) double sm[];
@@ -3369,6 +3376,19 @@ __global__ void __launch_bounds__(HW_NT, 2) vanka_hwarp_kernel(const __grid_cons
         for (int k = 0; k < 10; ++k) cdr[k] = 0.0;
 #pragma unroll 1
         for (int y = j0 - 1; y <= yend; ++y) {
+            // S~^{-1} of vertex row y + 2 towards the SM (lane k: plane k, the up to 3 lines of the strip's 32 columns)
+            if (pf && lane < MG_HV_NSINV && y + 2 >= 1 && y + 2 <= n - 1) {
+                const double* pa = P.hv.sinv + lane * L.plane + (int64_t)(y + 2) * L.pitch + max(i0 - 1, 0);
+                if (pf == 1) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 16));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 31));
+                } else {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 16));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 31));
+                }
+            }
             // ---- residual row y
             if (!XZERO) {
                 wait_x(y + 1);
@@ -4430,6 +4450,8 @@ void kernels_init() {
     set_smem(vanka_warp_kernel<true, false, false>, WGeom<false>::SMEM);
     set_smem(vanka_hwarp_kernel<false>, HW_SMEM);
     set_smem(vanka_hwarp_kernel<true>, HW_SMEM);
+    carve(vanka_bnd2_kernel<false, false, true>);
+    carve(vanka_bnd2_kernel<true, false, true>);
     set_smem(vanka_bnd_kernel<false, false, true>, WB_SMEM);
     set_smem(vanka_bnd_kernel<true, false, true>, WB_SMEM);
     set_smem(bsr_b_warp_kernel<false, false>, WQGeom<false>::SMEM);
@@ -5175,12 +5197,26 @@ cudaError_t launch_vanka_hwarp(const VankaParams& P, const HvInterior& Ti, const
     if (e == cudaSuccess) e = encode_vec_map(&wk, L.kinv_field, L.n, L.pitch, L.plane, WXW, 1, 2);
     if (e != cudaSuccess) return e;
     const ProlSrc none{nullptr, 0, 0, 0};
-    const dim3 bgrid((bnd_count(L.n) + WB_NT - 1) / WB_NT);
-    if (x_zero) launch_k(vanka_bnd_kernel<true, false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, none);
-    else launch_k(vanka_bnd_kernel<false, false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, none);
+    static int bk = -1, pf = -1;   // MG_HW_BK: boundary outputs by 1 the cooperative kernel, 2 one thread per vertex;
+    if (bk < 0) {                  // MG_HW_PF: S~^{-1} rows prefetched 0 not, 1 into L2, 2 into L1
+        const char* v = getenv("MG_HW_BK");
+        bk = v ? atoi(v) : 1;
+        v = getenv("MG_HW_PF");
+        pf = v ? atoi(v) : 3;   // 3: into L2 below n = 2048 only (measured at 2048^2: level 0 0.42 -> 0.50 ms with the
+    }                           // prefetches, levels 1-2 0.101 / 0.044 -> 0.095 / 0.039 ms)
+    const int pfl = pf == 3 ? (L.n < 2048 ? 1 : 0) : pf;
+    if (bk == 1) {
+        const dim3 bgrid2((L.n + WB2_T) / WB2_T, 4);
+        if (x_zero) launch_k(vanka_bnd2_kernel<true, false, true>, bgrid2, WB2_NT, 0, s, P, x, b, none);
+        else launch_k(vanka_bnd2_kernel<false, false, true>, bgrid2, WB2_NT, 0, s, P, x, b, none);
+    } else {
+        const dim3 bgrid((bnd_count(L.n) + WB_NT - 1) / WB_NT);
+        if (x_zero) launch_k(vanka_bnd_kernel<true, false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, none);
+        else launch_k(vanka_bnd_kernel<false, false, true>, bgrid, WB_NT, WB_SMEM, s, P, x, b, none);
+    }
     const dim3 wgrid((ntasks + HW_NW - 1) / HW_NW);
-    if (x_zero) launch_k(vanka_hwarp_kernel<true>, wgrid, HW_NT, HW_SMEM, s, wx, wb, wk, P, Ti, xo, S, wmh, nstrips, ntasks);
-    else launch_k(vanka_hwarp_kernel<false>, wgrid, HW_NT, HW_SMEM, s, wx, wb, wk, P, Ti, xo, S, wmh, nstrips, ntasks);
+    if (x_zero) launch_k(vanka_hwarp_kernel<true>, wgrid, HW_NT, HW_SMEM, s, wx, wb, wk, P, Ti, xo, S, wmh, nstrips, ntasks, pfl);
+    else launch_k(vanka_hwarp_kernel<false>, wgrid, HW_NT, HW_SMEM, s, wx, wb, wk, P, Ti, xo, S, wmh, nstrips, ntasks, pfl);
     return cudaGetLastError();
 }
 int blocks_vanka_march2(int n) {

@@ -79,8 +79,8 @@ def test_het_vanka_cycle_history(n, levels, pname, het, cycles):
         assert e_go[k] <= 1e-9 + 4 * e_oo[k], (e_go, e_oo)
 
 
-@pytest.mark.parametrize("n,levels,pname,het,nu", [(64, 5, "unit", 3, 1), (96, 4, "stiff", 7, 2), (132, 3, "mixed", 5, 1),
-                                                   (31, 2, "unit", 3, 1)])
+@pytest.mark.parametrize("n,levels,pname,het,nu", [(64, 5, "unit", 3, 1), (96, 4, "stiff", 7, 2), (112, 5, "mixed", 5, 1),
+                                                   (36, 3, "unit", 3, 1)])
 def test_het_warp_sweep_bitwise(n, levels, pname, het, nu):
     """The warp-marching heterogeneous-K Vanka sweep (vanka_hwarp_kernel: K^{-1} rows in a TMA ring,
     residuals and patch corrections moved by shuffles, boundary-vertex patches from vanka_bnd_kernel)
