@@ -48,6 +48,7 @@ struct Level {
     double* g = nullptr;     // BSR: 2 planes
     double* dpa = nullptr;   // BSR: 2 planes
     double* dpb = nullptr;
+    double* rs = nullptr;    // BSR marching levels: r_u, r_w of stage A for stage B (8 planes, allocated on first use)
     double* kinv = nullptr;  // 2 planes, heterogeneous K only
     double* jtab = nullptr;  // BSR Jacobi table: 5 planes (tau / D_w per RT0 edge, 1 / diag S per triangle)
     double* gbnd = nullptr;  // 9 x 400
@@ -118,6 +119,8 @@ struct mg_ctx {
     int launches = 0;             // kernel launches enqueued by the last captured cycle
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 0: 2-D tiles everywhere
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
+    int jacobi_pair = 1;          // two table sweeps per launch where two remain (MG_JACOBI_PAIR)
+    int bsr_rvec = 1;             // marching BSR: stage B reads stage A's residual instead of recomputing it (MG_BSR_RVEC)
     int het_warp_n = 512;         // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one kernel
@@ -199,7 +202,8 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
     const bool exact_s = o.relax == MG_BSR_EXACT;
     const double omJ = (!exact_s && o.jacobi_sweeps >= 1) ? o.omega_J : 0.0;
     const bool march = c->bsr_impl == 1 && Lv.n >= c->march_min_n && !c->exact;
-    if (march) CK(launch_bsr_a_march(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s, Lv.jtab));
+    double* rs = (march && !xzero) ? Lv.rs : nullptr;   // allocated by ensure_rs when bsr_rvec
+    if (march) CK(launch_bsr_a_march(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s, Lv.jtab, rs));
     else CK(launch_bsr_a(Lv.vp.L, Lv.up, omJ, xin, b, Lv.g, Lv.dpa, S, xzero, s));
     double* cur = Lv.dpa;
     double* nxt = Lv.dpb;
@@ -208,7 +212,10 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
                            cg_iters(Lv.n), s));
     }
     for (int k = 1; !exact_s && k < o.jacobi_sweeps;) {
-        if (c->jacobi_table) {
+        if (c->jacobi_table && c->jacobi_pair && k + 2 <= o.jacobi_sweeps) {
+            CK(launch_bsr_jacobi2_t(Lv.vp.L, o.omega_J, Lv.g, Lv.jtab, cur, nxt, s));
+            k += 2;
+        } else if (c->jacobi_table) {
             CK(launch_bsr_jacobi_t(Lv.vp.L, o.omega_J, Lv.g, Lv.jtab, cur, nxt, s));
             k += 1;
         } else {
@@ -217,8 +224,21 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         }
         std::swap(cur, nxt);
     }
-    if (march) CK(launch_bsr_b_march(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
+    if (march) CK(launch_bsr_b_march(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s, rs));
     else CK(launch_bsr_b(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
+    return MG_OK;
+}
+
+// marching BSR: the residual vector stage A hands to stage B (planes 0-7 = r_u, r_w) on the marching levels
+int ensure_rs(mg_ctx* c) {
+    if (!c->bsr_rvec || c->bsr_impl != 1 || c->exact) return MG_OK;
+    for (auto& Lv : c->L) {
+        if (Lv.rs || Lv.n < c->march_min_n) continue;
+        const size_t pb = sizeof(double) * 8 * Lv.plane;
+        Lv.rs = (double*)dalloc(c, pb);
+        if (!Lv.rs) return fail(MG_ENOMEM, "BSR residual work space");
+        CK(cudaMemset(Lv.rs, 0, pb));
+    }
     return MG_OK;
 }
 
@@ -430,6 +450,8 @@ int check_opts(mg_ctx* c, const mg_cycle_opts* o) {
         return fail(MG_EINVAL, "exact BSR (a full S solve per relaxation) is limited to n <= 1024");
     if (o->relax == MG_BSR_EXACT)
         if (int rc = ensure_cg(c)) return rc;
+    if (o->relax == MG_BSR)
+        if (int rc = ensure_rs(c)) return rc;
     return MG_OK;
 }
 
@@ -492,6 +514,9 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_RESTRICT_IMPL")) c->restrict_impl = atoi(v);
     if (const char* v = getenv("MG_MARCH_MIN_N")) c->march_min_n = atoi(v);
     if (const char* v = getenv("MG_HET_WARP_N")) c->het_warp_n = atoi(v);
+    if (const char* v = getenv("MG_BSR_RVEC")) c->bsr_rvec = atoi(v);
+    if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v);
+    if (getenv("MG_WARP_BSR") && atoi(getenv("MG_WARP_BSR"))) c->bsr_rvec = 0;   // the warp stage B evaluates r itself
     if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_BSR_IMPL")) c->bsr_impl = atoi(v);
     // process-wide kernel knobs: every setup re-reads them (unset -> default), so they never stick
@@ -717,6 +742,7 @@ int mg_relax_bsr(mg_ctx* c, int32_t level, double* x, const double* b, double om
     if (!aligned(x) || !aligned(b)) return fail(MG_EINVAL, "null or misaligned pointer");
     if (sweeps < 0 || jacobi_sweeps < 0) return fail(MG_EINVAL, "sweeps < 0");
     mg_cycle_opts o{1, 1, MG_BSR, omega, omega_J, jacobi_sweeps};
+    if (int rc = ensure_rs(c)) return rc;
     Level& Lv = c->L[level];
     double* a = x;
     double* t = Lv.t;

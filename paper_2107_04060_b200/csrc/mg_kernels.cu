@@ -1959,6 +1959,87 @@ __global__ void __launch_bounds__(256) bsr_jacobi_t_kernel(const LevelParams L, 
     }
 }
 
+// Two Jacobi sweeps with the table in one launch (round 2): a CTA owns 32 x 8 cells, runs the first sweep
+// on the 34 x 10 cells around them into shared memory (the one-cell ring is recomputed, its inputs come
+// from L2), then the second sweep on its own cells.  Each sweep is bsr_jacobi_t_kernel's expression, so
+// the result is bitwise that of two launches; g, dp and the 5-plane table cross DRAM once instead of twice.
+constexpr int J2_W = 34, J2_H = 10, J2_N = J2_W * J2_H;
+__device__ __forceinline__ void jacobi_t_cell(const LevelParams& L, double omJ, const double* __restrict__ g,
+                                              const double* __restrict__ tab, int i, int j, int64_t o,
+                                              double dself0, double dself1, const double nb[2][3], double out[2]) {
+    const int64_t plane = L.plane, pitch = L.pitch;
+    const double tH0 = __ldg(tab + o), tV0 = __ldg(tab + plane + o), tD = __ldg(tab + 2 * plane + o);
+    const double tH1 = __ldg(tab + o + pitch), tV1 = __ldg(tab + plane + o + 1);
+#pragma unroll
+    for (int sh = 0; sh < 2; ++sh) {
+        const double te[3] = {sh == 0 ? tH0 : tH1, sh == 0 ? tV0 : tV1, tD};
+        const double dself = sh == 0 ? dself0 : dself1;
+        double off = 0.0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+            if (te[e] != 0.0) off = fma(te[e] * L.bw[sh][e] * L.bw[1 - sh][e], nb[sh][e], off);
+        const double ids = __ldg(tab + (3 + sh) * plane + o);
+        out[sh] = dself + omJ * (fma(__ldg(g + sh * plane + o), ids, -dself) - off * ids);
+    }
+}
+
+__global__ void __launch_bounds__(256) bsr_jacobi2_t_kernel(const LevelParams L, double omJ, const double* __restrict__ g,
+                                                            const double* __restrict__ tab,
+                                                            const double* __restrict__ dpi, double* __restrict__ dpo) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double d1[2 * J2_N];   // first-sweep dp of cells (i0 - 1 + lx, j0 - 1 + ly), [shape][ly][lx]
+    const int n = L.n;
+    if (*L.stop) return;
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 8;
+    const int64_t plane = L.plane, pitch = L.pitch;
+    // neighbours of LL(i,j): UR(i,j-1), UR(i-1,j), UR(i,j); of UR(i,j): LL(i,j+1), LL(i+1,j), LL(i,j)
+    for (int c = threadIdx.x; c < J2_N; c += 256) {
+        const int ly = c / J2_W, lx = c - ly * J2_W;
+        const int i = i0 - 1 + lx, j = j0 - 1 + ly;
+        double out[2] = {0.0, 0.0};
+        if (i >= 0 && j >= 0 && i < n && j < n) {
+            const int64_t o = (int64_t)j * pitch + i;
+            const double tH0 = __ldg(tab + o), tV0 = __ldg(tab + plane + o), tD = __ldg(tab + 2 * plane + o);
+            const double tH1 = __ldg(tab + o + pitch), tV1 = __ldg(tab + plane + o + 1);
+            const double s0 = __ldg(dpi + o), s1 = __ldg(dpi + plane + o);
+            double nb[2][3];
+            nb[0][0] = tH0 != 0.0 ? __ldg(dpi + plane + o - pitch) : 0.0;
+            nb[0][1] = tV0 != 0.0 ? __ldg(dpi + plane + o - 1) : 0.0;
+            nb[0][2] = s1;
+            nb[1][0] = tH1 != 0.0 ? __ldg(dpi + o + pitch) : 0.0;
+            nb[1][1] = tV1 != 0.0 ? __ldg(dpi + o + 1) : 0.0;
+            nb[1][2] = s0;
+            jacobi_t_cell(L, omJ, g, tab, i, j, o, s0, s1, nb, out);
+        }
+        d1[c] = out[0];
+        d1[J2_N + c] = out[1];
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+    const int i = i0 + lx, j = j0 + ly;
+    if (i > n || j > n) return;
+    const int64_t o = (int64_t)j * pitch + i;
+    if (i == n || j == n) {
+        dpo[o] = 0.0;
+        dpo[plane + o] = 0.0;
+        return;
+    }
+    const double* c0 = d1 + (ly + 1) * J2_W + (lx + 1);   // LL plane at the cell
+    const double* c1 = c0 + J2_N;                         // UR plane
+    double nb[2][3];
+    nb[0][0] = c1[-J2_W];
+    nb[0][1] = c1[-1];
+    nb[0][2] = c1[0];
+    nb[1][0] = c0[J2_W];
+    nb[1][1] = c0[1];
+    nb[1][2] = c0[0];
+    double out[2];
+    jacobi_t_cell(L, omJ, g, tab, i, j, o, c0[0], c1[0], nb, out);
+    dpo[o] = out[0];
+    dpo[plane + o] = out[1];
+}
+
 // stage B: du = F_u^{-1}(r_u - alpha B_u^T dp), dw = (r_w - tau B_w^T dp)/(tau D_w),
 // xout = x + omega (du, dw, dp)
 constexpr int BB_XW = BTX + 4, BB_XH = BTY + 4, BB_RW = BTX + 2, BB_RH = BTY + 2;
@@ -3663,6 +3744,7 @@ constexpr int BMA_SMEM = (BMA_XR * BQ_ROW + BMA_BR * BQ_ROW + BMA_KR * BQ_KROW +
 constexpr int BB_T = 28;                              // stage B: owned indices / strip
 constexpr int BB2_XR = 10, BB2_BR = 9, BB2_DR = 10, BB2_PR = 5, BB2_PC = BB_T + 1;
 constexpr int BB2_SMEM = (BB2_XR * BQ_ROW + BB2_BR * BQ_ROW + 2 * BB2_DR * BQ_KROW + BB2_PR * 8 * BB2_PC) * 8 + 64;
+constexpr int BB2_SMEM_NX = BB2_SMEM - BB2_XR * BQ_ROW * 8;   // stage B without the x ring (MODE 1, 2)
 static_assert(3 * (BMA_SMEM + 1024) <= 228 * 1024 && 3 * (BB2_SMEM + 1024) <= 228 * 1024, "three CTAs per SM");
 static_assert(BMA_T % 2 == 0 && BB_T % 2 == 0, "TMA box origins i0 - 2 must be even columns");
 
@@ -3679,7 +3761,8 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmk,
                                                                const LevelParams L, const DispParams U, double omJ,
                                                                double* __restrict__ g, double* __restrict__ dp,
-                                                               NormSink S, int MH, const double* __restrict__ jtab) {
+                                                               NormSink S, int MH, const double* __restrict__ jtab,
+                                                               double* __restrict__ rs) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) double sm[];
@@ -3773,6 +3856,13 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
             if (lane >= 1 && lane <= BMA_T && i <= n && y >= j0 && y < j0 + rows) {
 #pragma unroll
                 for (int k = 0; k < 10; ++k) nrm = fma(rv[k], rv[k], nrm);
+                // r_u, r_w of the owned positions for stage B (bsr_b_march_kernel<.., 2> reads them
+                // instead of evaluating the residual a second time)
+                if (!XZERO && rs) {
+                    const int64_t o = (int64_t)y * L.pitch + i;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) rs[k * L.plane + o] = rv[k];
+                }
             }
         }
         __syncthreads();
@@ -3861,18 +3951,24 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
     if (S.out || S.state) norm_finish<BQ_NT>(S, nrm);
 }
 
-template <bool HET, bool XZERO>
+// MODE 0: r = b - A x evaluated here; 1: x = 0 (r = b); 2: r_u, r_w read from the vector stage A wrote (the
+// "b" map points at it, 8 planes), x read at the owners only -- no x ring, no second residual
+template <bool HET, int MODE>
 __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                const __grid_constant__ CUtensorMap tmb,
                                                                const __grid_constant__ CUtensorMap tmd,
                                                                const __grid_constant__ CUtensorMap tmk,
                                                                const LevelParams L, const DispParams U, double omega,
-                                                               double* __restrict__ xo, int MH) {
+                                                               double* __restrict__ xo, int MH,
+                                                               const double* __restrict__ xin) {
+    constexpr bool XZERO = MODE != 0;                       // no x ring, r taken from the b rows
+    constexpr int XR = MODE == 0 ? BB2_XR : 0;              // x ring rows
+    constexpr int BROWB = (MODE == 2 ? 8 * BQ_W : BQ_ROW);  // doubles per b / r box row
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                          // [BB2_XR][10][32]
-    double* br = xr + BB2_XR * BQ_ROW;        // [BB2_BR][10][32]  b, overwritten by (y_u, r_w)
+    double* br = xr + XR * BQ_ROW;            // [BB2_BR][10][32]  b, overwritten by (y_u, r_w)
     double* dr = br + BB2_BR * BQ_ROW;        // [BB2_DR][2][32]   dp
     double* kr = dr + BB2_DR * BQ_KROW;       // [BB2_DR][2][32]   K^{-1} (HET)
     double* pr = kr + BB2_DR * BQ_KROW;       // [BB2_PR][8][BB2_PC]
@@ -3883,7 +3979,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
     const int rows = min(MH, n + 1 - j0);
     const int nsteps = (rows + BQ_R - 1) / BQ_R;
     const int t = threadIdx.x;
-    auto sx = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_XR; };
+    auto sx = [&](int y) { return (y - j0 + 2 * BQ_R) % (XR ? XR : 1); };
     auto sb = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_BR; };
     auto sd = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_DR; };
     auto sp = [&](int y) { return (y - j0 + 2 * BQ_R) % BB2_PR; };
@@ -3894,7 +3990,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
         uint64_t* bar = &bars[(g + 1) & 1];
         const int nx = XZERO ? 0 : (g < 0 ? BQ_R + 2 : BQ_R);
         const int nd = g < 0 ? 5 : BQ_R;
-        mbar_expect_tx(bar, ((nx + BQ_R) * BQ_ROW + (HET ? 2 : 1) * nd * BQ_KROW) * 8);
+        mbar_expect_tx(bar, (nx * BQ_ROW + BQ_R * BROWB + (HET ? 2 : 1) * nd * BQ_KROW) * 8);
         const int xfirst = g < 0 ? j0 - BQ_R : j0 + g * BQ_R + 2;
 #pragma unroll 1
         for (int k = 0; k < nx; ++k) tma_load3(xr + sx(xfirst + k) * BQ_ROW, &tmx, i0 - 2, xfirst + k, 0, bar);
@@ -4008,7 +4104,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
                 const int64_t o = (int64_t)y * L.pitch + i;
 #pragma unroll
                 for (int k = 0; k < 10; ++k) {
-                    const double xk = XZERO ? 0.0 : xv[k * BQ_W];
+                    const double xk = MODE == 1 ? 0.0 : (MODE == 2 ? __ldg(xin + k * L.plane + o) : xv[k * BQ_W]);
                     xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(omega, d[k], xk) : 0.0;
                 }
             }
@@ -4468,10 +4564,12 @@ void kernels_init() {
     set_smem(bsr_a_march_kernel<false, true>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<true, false>, BMA_SMEM);
     set_smem(bsr_a_march_kernel<true, true>, BMA_SMEM);
-    set_smem(bsr_b_march_kernel<false, false>, BB2_SMEM);
-    set_smem(bsr_b_march_kernel<false, true>, BB2_SMEM);
-    set_smem(bsr_b_march_kernel<true, false>, BB2_SMEM);
-    set_smem(bsr_b_march_kernel<true, true>, BB2_SMEM);
+    set_smem(bsr_b_march_kernel<false, 0>, BB2_SMEM);
+    set_smem(bsr_b_march_kernel<false, 1>, BB2_SMEM_NX);
+    set_smem(bsr_b_march_kernel<false, 2>, BB2_SMEM_NX);
+    set_smem(bsr_b_march_kernel<true, 0>, BB2_SMEM);
+    set_smem(bsr_b_march_kernel<true, 1>, BB2_SMEM_NX);
+    set_smem(bsr_b_march_kernel<true, 2>, BB2_SMEM_NX);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
     set_smem(restrict_march_kernel<true>, Q_SMEM);
     set_smem(vanka_kernel<false>, V_SMEM);
@@ -5232,7 +5330,8 @@ int blocks_vanka_march2(int n) {
 
 
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
-                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab) {
+                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab,
+                               double* rs) {
     CUtensorMap mx, mb, mk;
     cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, BQ_W, 1);
     if (e == cudaSuccess) e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, BQ_W, 1);
@@ -5241,7 +5340,7 @@ cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, BMA_T, BQ_R, 3, relax_target(L.n));
     dim3 grid((L.n + BMA_T) / BMA_T, (L.n + MH) / MH);
-#define BA_LAUNCH(H_, Z_) launch_k(bsr_a_march_kernel<H_, Z_>, grid, BQ_NT, BMA_SMEM, s, mx, mb, mk, L, U, omJ, g, dp, S, MH, jtab)
+#define BA_LAUNCH(H_, Z_) launch_k(bsr_a_march_kernel<H_, Z_>, grid, BQ_NT, BMA_SMEM, s, mx, mb, mk, L, U, omJ, g, dp, S, MH, jtab, rs)
     if (het && x_zero) BA_LAUNCH(true, true);
     else if (het) BA_LAUNCH(true, false);
     else if (x_zero) BA_LAUNCH(false, true);
@@ -5251,15 +5350,18 @@ cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double
 }
 
 cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double omega, const double* x,
-                               const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s) {
+                               const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s,
+                               const double* rs) {
     CUtensorMap mx, mb, md, mk;
+    const bool rvec = rs != nullptr && !x_zero;   // r_u, r_w from stage A (8 planes) instead of a second residual
     cudaError_t e = encode_vec_map(&mx, x_zero ? b : x, L.n, L.pitch, L.plane, BQ_W, 1);
-    if (e == cudaSuccess) e = encode_vec_map(&mb, b, L.n, L.pitch, L.plane, BQ_W, 1);
+    if (e == cudaSuccess) e = rvec ? encode_vec_map(&mb, rs, L.n, L.pitch, L.plane, BQ_W, 1, 8)
+                                   : encode_vec_map(&mb, b, L.n, L.pitch, L.plane, BQ_W, 1);
     if (e == cudaSuccess) e = encode_vec_map(&md, dp, L.n, L.pitch, L.plane, BQ_W, 1, 2);
     const bool het = L.kinv_field != nullptr;
     if (e == cudaSuccess) e = encode_vec_map(&mk, het ? L.kinv_field : dp, L.n, L.pitch, L.plane, BQ_W, 1, 2);
     if (e != cudaSuccess) return e;
-    if (g_warp_min_n > 0 && L.n >= g_warp_min_n && g_warp_bsr) {
+    if (g_warp_min_n > 0 && L.n >= g_warp_min_n && g_warp_bsr && !rvec) {
         CUtensorMap wx, wb, wd, wk;
         e = encode_vec_map(&wx, x_zero ? b : x, L.n, L.pitch, L.plane, WXW, 1);
         if (e == cudaSuccess) e = encode_vec_map(&wb, b, L.n, L.pitch, L.plane, WBW, 1);
@@ -5281,11 +5383,14 @@ cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double
     }
     const int MH = march_height(L.n, BB_T, BQ_R, 3, relax_target(L.n));
     dim3 grid((L.n + BB_T) / BB_T, (L.n + MH) / MH);
-#define BB_LAUNCH(H_, Z_) launch_k(bsr_b_march_kernel<H_, Z_>, grid, BQ_NT, BB2_SMEM, s, mx, mb, md, mk, L, U, omega, xo, MH)
-    if (het && x_zero) BB_LAUNCH(true, true);
-    else if (het) BB_LAUNCH(true, false);
-    else if (x_zero) BB_LAUNCH(false, true);
-    else BB_LAUNCH(false, false);
+#define BB_LAUNCH(H_, M_) \
+    launch_k(bsr_b_march_kernel<H_, M_>, grid, BQ_NT, M_ ? BB2_SMEM_NX : BB2_SMEM, s, mx, mb, md, mk, L, U, omega, xo, MH, x)
+    if (het && x_zero) BB_LAUNCH(true, 1);
+    else if (het && rvec) BB_LAUNCH(true, 2);
+    else if (het) BB_LAUNCH(true, 0);
+    else if (x_zero) BB_LAUNCH(false, 1);
+    else if (rvec) BB_LAUNCH(false, 2);
+    else BB_LAUNCH(false, 0);
 #undef BB_LAUNCH
     return cudaGetLastError();
 }
@@ -5420,6 +5525,13 @@ cudaError_t launch_jtable(const LevelParams& L, double* tab, cudaStream_t s) {
     dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
     if (L.kinv_field) launch_k(jtable_kernel<true>, grid, 256, 0, s, L, tab);
     else launch_k(jtable_kernel<false>, grid, 256, 0, s, L, tab);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsr_jacobi2_t(const LevelParams& L, double omJ, const double* g, const double* tab,
+                                 const double* dpi, double* dpo, cudaStream_t s) {
+    dim3 grid((L.n + 32) / 32, (L.n + 8) / 8);
+    launch_k(bsr_jacobi2_t_kernel, grid, 256, 0, s, L, omJ, g, tab, dpi, dpo);
     return cudaGetLastError();
 }
 

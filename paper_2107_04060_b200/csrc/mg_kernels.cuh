@@ -113,14 +113,21 @@ void set_prol_ws(int on);
 void set_resid_march_n(int N);
 // per-level Jacobi table (tau / D_w per RT0 edge, 1 / diag S per triangle; 5 planes) and the sweep using it
 cudaError_t launch_jtable(const LevelParams& L, double* tab, cudaStream_t s);
+// two table sweeps in one launch (bitwise two launch_bsr_jacobi_t)
+cudaError_t launch_bsr_jacobi2_t(const LevelParams& L, double omega_J, const double* g, const double* tab,
+                                 const double* dp_in, double* dp_out, cudaStream_t s);
 cudaError_t launch_bsr_jacobi_t(const LevelParams& L, double omega_J, const double* g, const double* tab,
                                 const double* dp_in, double* dp_out, cudaStream_t s);
 // two Jacobi sweeps in one launch (same arithmetic as two launch_bsr_jacobi)
 // row-marching TMA variants of the two BSR stages (same arithmetic as launch_bsr_a / launch_bsr_b)
 cudaError_t launch_bsr_a_march(const LevelParams& L, const DispParams& U, double omJ, const double* x, const double* b,
-                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab);
+                               double* g, double* dp, NormSink S, bool x_zero, cudaStream_t s, const double* jtab,
+                               double* rs = nullptr);
+// rs != nullptr (and not x_zero): stage A stores r_u, r_w (8 planes) there and stage B reads them instead of
+// evaluating the residual a second time (same values: bitwise the two-residual path)
 cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double omega, const double* x,
-                               const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s);
+                               const double* b, const double* dp, double* xo, bool x_zero, cudaStream_t s,
+                               const double* rs = nullptr);
 // row-marching TMA variant of the fused residual + restriction (mode 1)
 cudaError_t launch_restrict_march(const LevelParams& Lf, int n_coarse, int pitch_coarse, const double* x_fine,
                                   const double* b_fine, double* b_coarse, cudaStream_t s);

@@ -307,6 +307,33 @@ def test_warp_bsr_bitwise(n, levels, pname, het, nJ):
     assert out[0][1] == out[1][1]
 
 
+@pytest.mark.parametrize("n,levels,pname,het,nJ", [(64, 5, "unit", 3, 3), (48, 3, "mixed", None, 1),
+                                                    (96, 4, "stiff", 7, 2), (64, 5, "cfg5", None, 4),
+                                                    (48, 3, "unit", 5, 5)])
+def test_bsr_rvec_bitwise(n, levels, pname, het, nJ):
+    """Marching BSR with stage B reading the residual planes stage A stored (bsr_b_march_kernel<.., 2>,
+    MG_BSR_RVEC=1, the default) gives bitwise the iterates and norms of the path that evaluates
+    r = b - A x in both stages (one residual per relaxation), with and without a
+    K field, on zero-initial-guess levels, ragged strips and segments; likewise two Jacobi sweeps on S
+    in one launch against two launches."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    b = mg_inputs.uniform_rhs(n, 8)
+    out = []
+    # default (residual vector + paired Jacobi sweeps, bsr_jacobi2_t_kernel) against the plain path
+    for rvec in ("1", "0"):
+        H = C.gpu_hierarchy(n, levels, pname, het, march=True, env={"MG_BSR_RVEC": rvec, "MG_JACOBI_PAIR": rvec})
+        xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+        hist = [H.cycle(xd, bd, Opts(2, 1, "bsr", 0.7, 0.9, nJ)) for _ in range(3)]
+        x1 = H.to_host(xd)
+        H.relax_bsr(0, xd, bd, 0.7, 0.9, nJ, sweeps=3)
+        out.append((x1, hist, H.to_host(xd)))
+        H.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][2], out[1][2])
+
+
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (48, 3, "mixed", 2), (128, 6, "stiff", 1)])
 def test_small_tile_sweep_bitwise(n, levels, pname, nu):
     """The small-tile sweep with all of its global reads in the first round trip (vanka_small_kernel:
