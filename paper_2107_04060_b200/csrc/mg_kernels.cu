@@ -3830,6 +3830,20 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
     const int64_t plane = L.plane;
     double nrm = 0.0;
     for (int s = -1; s < nsteps; ++s) {
+        // the Jacobi table entries of this thread's cell (g phase), issued a whole step ahead of their use
+        double tpre[7];
+        {
+            const int yc = j0 + s * BQ_R + (t >> 5), ic = i0 + (t & 31);
+            const bool ok = s >= 0 && (t & 31) < BMA_T && ic < n && yc < n && yc < j0 + rows;
+            const double* tb = jtab + (ok ? (int64_t)yc * L.pitch + ic : 0);
+            tpre[0] = ok ? __ldg(tb) : 0.0;
+            tpre[1] = ok ? __ldg(tb + plane) : 0.0;
+            tpre[2] = ok ? __ldg(tb + 2 * plane) : 0.0;
+            tpre[3] = ok ? __ldg(tb + L.pitch) : 0.0;
+            tpre[4] = ok ? __ldg(tb + plane + 1) : 0.0;
+            tpre[5] = ok ? __ldg(tb + 3 * plane) : 0.0;
+            tpre[6] = ok ? __ldg(tb + 4 * plane) : 0.0;
+        }
         mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
         const int q = t >> 5, lane = t & 31;
         // ---- residual rows y = j0 + sR + 2 + q at columns i0-1 .. i0+27
@@ -3909,9 +3923,8 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                     const double* r1 = br + sb(y + 1) * BQ_ROW + (lane + 2);
                     // tau / D_w of the five edges of the cell (H(i,y), V(i,y), D(i,y), H(i,y+1),
                     // V(i+1,y); 0 if inactive) and 1 / diag S of its triangles: the Jacobi table
-                    const double* tb = jtab + o;
-                    const double tH0 = __ldg(tb), tV0 = __ldg(tb + plane), tD = __ldg(tb + 2 * plane);
-                    const double tH1 = __ldg(tb + L.pitch), tV1 = __ldg(tb + plane + 1);
+                    const double tH0 = tpre[0], tV0 = tpre[1], tD = tpre[2];
+                    const double tH1 = tpre[3], tV1 = tpre[4];
                     const double itau2 = 1.0 / (L.tau * L.tau);
 #pragma unroll
                     for (int sh = 0; sh < 2; ++sh) {
@@ -3932,7 +3945,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_a_march_kernel(const __grid_cons
                         const double rp = r0[(8 + sh) * BQ_W];
                         const double gv = L.alpha * gu + L.tau * gw - rp;
                         g[sh * plane + o] = gv;
-                        dp[sh * plane + o] = omJ * gv * __ldg(tb + (3 + sh) * plane);
+                        dp[sh * plane + o] = omJ * gv * tpre[5 + sh];
                     }
                 } else {
                     g[o] = 0.0;
@@ -4022,6 +4035,15 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
         issue(0);
     }
     for (int s = -1; s < nsteps; ++s) {
+        // MODE 2: x of this thread's owner position, issued a whole step ahead of its use
+        double xpre[10];
+        if (MODE == 2) {
+            const int yo = j0 + s * BQ_R + (t >> 5), io = i0 + (t & 31);
+            const bool ok = s >= 0 && (t & 31) < BB_T && io <= n && yo < j0 + rows;
+            const int64_t oo = ok ? (int64_t)yo * L.pitch + io : 0;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) xpre[k] = ok ? __ldg(xin + k * L.plane + oo) : 0.0;
+        }
         mbar_wait(&bars[(s + 1) & 1], ((s + 1) >> 1) & 1);
         const int q = t >> 5, lane = t & 31;
         // ---- rows y = j0 + sR + 1 + q at columns i0-1 .. i0+28: r, then y_u = r_u - alpha B_u^T dp
@@ -4104,7 +4126,7 @@ __global__ void __launch_bounds__(BQ_NT, 3) bsr_b_march_kernel(const __grid_cons
                 const int64_t o = (int64_t)y * L.pitch + i;
 #pragma unroll
                 for (int k = 0; k < 10; ++k) {
-                    const double xk = MODE == 1 ? 0.0 : (MODE == 2 ? __ldg(xin + k * L.plane + o) : xv[k * BQ_W]);
+                    const double xk = MODE == 1 ? 0.0 : (MODE == 2 ? xpre[k] : xv[k * BQ_W]);
                     xo[k * L.plane + o] = is_active(k, i, y, n) ? fma(omega, d[k], xk) : 0.0;
                 }
             }
