@@ -1,5 +1,2 @@
 set -x
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "bsr" > gpurun_out/s3_bsr.log 2>&1; echo "rc=$?" >> gpurun_out/s3_bsr.log
-B="python bench.py --config 4 --no-cpu-baseline --no-e2e --no-solve"
-timeout 200 $B > gpurun_out/s3_c4_pre.json 2> gpurun_out/s3_c4_pre.err
-timeout 200 $B > gpurun_out/s3_c4_pre2.json 2> gpurun_out/s3_c4_pre2.err
+CFG=4 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"bsr_" -c 5 -o gpurun_out/s3_bsr2 python tools/two_cycles.py > gpurun_out/s3_ncu_bsr2.log 2>&1
