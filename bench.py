@@ -378,7 +378,7 @@ def main():
         # (which with the fused prolongation also reads e_H: + 8 B x N_1 ~ 2 B per fine DoF)
         alg_bytes = (24.0 * nact + (24.0 * nact + 8.0 * mg_inputs.n_active(n >> 1) if fused and n >= march_min
                                     else 24.0 * nact)) / 2.0
-        warp = n >= int(os.environ.get("MG_WARP_MIN_N", "1024")) > 0
+        warp = n >= int(os.environ.get("MG_WARP_MIN_N", "512")) > 0
         dom = (("vanka_warp_kernel + vanka_bnd2_kernel" if warp else "vanka_march2_kernel") +
                " (level 0: fused residual + 20-DoF patch solves + update; "
                "mean of the pre-sweep and the post-sweep" + (" with the prolongation fused in)" if fused else ")"))

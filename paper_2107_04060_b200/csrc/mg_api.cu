@@ -524,7 +524,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     set_pdl(getenv("MG_PDL") ? atoi(getenv("MG_PDL")) != 0 : 0);
     set_prol_ws(getenv("MG_PROL_WS") ? atoi(getenv("MG_PROL_WS")) : 0);
     set_resid_march_n(getenv("MG_RESID_MARCH_N") ? atoi(getenv("MG_RESID_MARCH_N")) : 512);
-    set_warp_min_n(getenv("MG_WARP_MIN_N") ? atoi(getenv("MG_WARP_MIN_N")) : 1024);
+    set_warp_min_n(getenv("MG_WARP_MIN_N") ? atoi(getenv("MG_WARP_MIN_N")) : 512);
     set_small_diet(getenv("MG_SMALL_DIET") ? atoi(getenv("MG_SMALL_DIET")) : 2);
     set_warp_prol(getenv("MG_WARP_PROL") ? atoi(getenv("MG_WARP_PROL")) : 1);
     set_warp_bk(getenv("MG_WARP_BK") ? atoi(getenv("MG_WARP_BK")) : 1);

@@ -5205,7 +5205,7 @@ cudaError_t launch_vanka(const VankaParams& P, const double* x, const double* b,
 // warp-marching sweep (vanka_warp_kernel) on levels with n >= MG_WARP_MIN_N (0: off); its tasks are
 // (strip of WT columns, segment of MH rows), one per warp, sized to whole waves of the 2 x WPC warps
 // per SM with segments near MG_WARP_TARGET rows
-static int g_warp_min_n = 1024;
+static int g_warp_min_n = 512;
 static int g_warp_prol = 1;
 static int g_warp_bk = 1;     // boundary-vertex patches precomputed by 1: vanka_bnd2_kernel, 2: vanka_bnd_kernel; 0: out of line in the sweep
 void set_warp_bk(int on) { g_warp_bk = on; }   // the fused-prolongation post-sweep through the warp kernel too (MG_WARP_PROL)
