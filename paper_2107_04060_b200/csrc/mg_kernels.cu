@@ -485,8 +485,11 @@ __device__ __forceinline__ void patch_apply_het_t(const VankaParams& P, const do
 
 // interior vertex: the +/- form of the condensed solve (mg_internal.h HvInteriorPM), 232 FMA instead
 // of the slot form's 424; every table entry is a constant-bank operand
+// PRE: the vertex's 21 S~^{-1} entries come preloaded in sq (registers) instead of being read here
+template <bool PRE = false>
 __device__ __forceinline__ void patch_apply_het_pm(const VankaParams& P, const HvInteriorPM& T, int a, int b,
-                                                   const double rr[20], double* out, int os) {
+                                                   const double rr[20], double* out, int os,
+                                                   const double* sq = nullptr) {
     double hp[6], hm[8], rd[3], rs[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -539,7 +542,8 @@ __device__ __forceinline__ void patch_apply_het_pm(const VankaParams& P, const H
 #pragma unroll
         for (int f = 0; f < 6; ++f) {
             const int lo = e < f ? e : f, hi = e < f ? f : e;
-            v = fma(__ldg(si + (lo * 6 - lo * (lo - 1) / 2 + (hi - lo)) * P.L.plane), sv[f], v);
+            const int q = lo * 6 - lo * (lo - 1) / 2 + (hi - lo);
+            v = fma(PRE ? sq[q] : __ldg(si + q * P.L.plane), sv[f], v);
         }
         zt[e] = v;
     }
@@ -3357,6 +3361,9 @@ constexpr int HW_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + HW_KR * HW_KSLOT) * 8 +
 #ifndef MG_HW_NW
 #define MG_HW_NW 6
 #endif
+#ifndef MG_HW_EARLY
+#define MG_HW_EARLY 0   // 1: S~^{-1} of the row's vertices loaded into registers before the residual phase
+#endif
 constexpr int HW_NW = MG_HW_NW, HW_NT = 32 * HW_NW, HW_SMEM = HW_NW * HW_BYTES;
 static_assert(2 * (HW_SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
 
@@ -3470,6 +3477,16 @@ __global__ void __launch_bounds__(HW_NT, 2) vanka_hwarp_kernel(const __grid_cons
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 31));
                 }
             }
+#if MG_HW_EARLY
+            // the S~^{-1} entries of this lane's vertex (i, y), issued before the residual phase
+            double sq[MG_HV_NSINV];
+            {
+                const bool vin = y >= j0 && lane >= 1 && i > 0 && i < n && y > 0 && y < n;
+                const double* si = P.hv.sinv + (vin ? (int64_t)y * L.pitch + i : 0);
+#pragma unroll
+                for (int q = 0; q < MG_HV_NSINV; ++q) sq[q] = vin ? __ldg(si + q * L.plane) : 0.0;
+            }
+#endif
             // ---- residual row y
             if (!XZERO) {
                 wait_x(y + 1);
@@ -3521,7 +3538,11 @@ __global__ void __launch_bounds__(HW_NT, 2) vanka_hwarp_kernel(const __grid_cons
                 rr[14] = rv[8]; rr[15] = rpl9; rr[16] = l8; rr[17] = rp9;
                 rr[18] = l9;   rr[19] = rp8;
                 if (i > 0 && i < n && y > 0 && y < n) {
+#if MG_HW_EARLY
+                    patch_apply_het_pm<true>(P, Ti.pm, i, y, rr, o, 1, sq);
+#else
                     patch_apply_het_pm(P, Ti.pm, i, y, rr, o, 1);
+#endif
                 } else {   // boundary vertex: its outputs were computed by vanka_bnd_kernel<.., HET>
                     const int nb = bnd_count(n), bi = bnd_index(i, y, n);
 #pragma unroll
