@@ -119,6 +119,7 @@ struct mg_ctx {
     int launches = 0;             // kernel launches enqueued by the last captured cycle
     int vanka_impl = 2;           // 2: row-granular marching TMA kernel (default), 0: 2-D tiles everywhere
     int restrict_impl = 1;        // 1: row-marching TMA fused residual + restriction, 0: 2-D tile kernel
+    int jacobi_fuse_b = 1;        // 2-D tile levels: the last two table sweeps inside stage B (MG_JACOBI_FUSE_B)
     int jacobi_pair = 1;          // two table sweeps per launch where two remain (MG_JACOBI_PAIR)
     int bsr_rvec = 1;             // marching BSR: stage B reads stage A's residual instead of recomputing it (MG_BSR_RVEC)
     int het_warp_n = 512;         // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
@@ -211,8 +212,11 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         CK(launch_cg_exact(Lv.vp.L, Lv.jtab, Lv.g, Lv.dpa, Lv.cgz, Lv.cgp, Lv.cgq, c->cgpart, c->cgcnt, c->cgst,
                            cg_iters(Lv.n), s));
     }
-    for (int k = 1; !exact_s && k < o.jacobi_sweeps;) {
-        if (c->jacobi_table && c->jacobi_pair && k + 2 <= o.jacobi_sweeps) {
+    // 2-D tile levels: the last two table sweeps run inside stage B (one launch less per relaxation)
+    const bool fuse_b = !march && !exact_s && c->jacobi_table && c->jacobi_fuse_b && o.jacobi_sweeps >= 3;
+    const int jend = fuse_b ? o.jacobi_sweeps - 2 : o.jacobi_sweeps;
+    for (int k = 1; !exact_s && k < jend;) {
+        if (c->jacobi_table && c->jacobi_pair && k + 2 <= jend) {
             CK(launch_bsr_jacobi2_t(Lv.vp.L, o.omega_J, Lv.g, Lv.jtab, cur, nxt, s));
             k += 2;
         } else if (c->jacobi_table) {
@@ -225,6 +229,7 @@ int relax_once(mg_ctx* c, int l, const double* xin, const double* b, double* xou
         std::swap(cur, nxt);
     }
     if (march) CK(launch_bsr_b_march(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s, rs));
+    else if (fuse_b) CK(launch_bsr_b(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s, Lv.g, Lv.jtab, o.omega_J));
     else CK(launch_bsr_b(Lv.vp.L, Lv.up, o.omega, xin, b, cur, xout, xzero, s));
     return MG_OK;
 }
@@ -516,6 +521,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_HET_WARP_N")) c->het_warp_n = atoi(v);
     if (const char* v = getenv("MG_BSR_RVEC")) c->bsr_rvec = atoi(v);
     if (const char* v = getenv("MG_JACOBI_PAIR")) c->jacobi_pair = atoi(v);
+    if (const char* v = getenv("MG_JACOBI_FUSE_B")) c->jacobi_fuse_b = atoi(v);
     if (getenv("MG_WARP_BSR") && atoi(getenv("MG_WARP_BSR"))) c->bsr_rvec = 0;   // the warp stage B evaluates r itself
     if (const char* v = getenv("MG_FUSE_PROLONG")) c->fuse_prolong = atoi(v) != 0;
     if (const char* v = getenv("MG_BSR_IMPL")) c->bsr_impl = atoi(v);

@@ -2063,7 +2063,9 @@ struct BBTile {
 template <bool HET, bool XZERO, int TX = BTX, int TY = BTY>
 __global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const LevelParams L, const DispParams U, double omega,
                                                        const double* __restrict__ x, const double* __restrict__ b,
-                                                       const double* __restrict__ dp, double* __restrict__ xo) {
+                                                       const double* __restrict__ dp, double* __restrict__ xo,
+                                                       const double* __restrict__ jg, const double* __restrict__ jtab,
+                                                       double omJ) {
     pdl_wait();
     pdl_trigger();
     using T = BBTile<TX, TY>;
@@ -2076,11 +2078,54 @@ __global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const Leve
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-    for (int t = threadIdx.x; t < 2 * T::DW * T::DH; t += T::NT) {
-        const int sh = t / (T::DW * T::DH), rem = t - sh * (T::DW * T::DH);
-        const int ly = rem / T::DW, lx = rem - ly * T::DW;
-        const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
-        ps[t] = (ci >= 0 && cj >= 0 && ci < n && cj < n) ? __ldg(dp + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+    if (jg) {
+        // the last two table Jacobi sweeps fused in (latency-bound levels: one launch less per relaxation):
+        // dp on the cells two rings further out, one sweep into q2, the second into ps -- each cell the
+        // expression of bsr_jacobi_t_kernel, so ps is bitwise what two launches would have left in dp
+        constexpr int W1 = T::DW + 4, H1 = T::DH + 4, W2 = T::DW + 2, H2 = T::DH + 2;
+        static_assert(2 * W1 * H1 + 2 * W2 * H2 <= T::USZ, "Jacobi scratch aliases the x tile");
+        double* q1 = sm;
+        double* q2 = q1 + 2 * W1 * H1;
+        for (int t = threadIdx.x; t < 2 * W1 * H1; t += T::NT) {
+            const int sh = t / (W1 * H1), rem = t - sh * (W1 * H1);
+            const int ly = rem / W1, lx = rem - ly * W1;
+            const int ci = i0 - 4 + lx, cj = j0 - 4 + ly;
+            q1[t] = (ci >= 0 && cj >= 0 && ci < n && cj < n) ? __ldg(dp + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+        }
+        __syncthreads();
+        auto sweep = [&](const double* src, int WS, int HS, double* dst, int WD, int HD, int org) {
+            // dst cell (lx, ly) = mesh cell (i0 - org + lx, j0 - org + ly) = src cell (lx + 1, ly + 1)
+            for (int t = threadIdx.x; t < WD * HD; t += T::NT) {
+                const int ly = t / WD, lx = t - ly * WD;
+                const int ci = i0 - org + lx, cj = j0 - org + ly;
+                double out[2] = {0.0, 0.0};
+                if (ci >= 0 && cj >= 0 && ci < n && cj < n) {
+                    const double* p0 = src + (ly + 1) * WS + (lx + 1);
+                    const double* p1 = p0 + WS * HS;
+                    double nb[2][3];
+                    nb[0][0] = p1[-WS];
+                    nb[0][1] = p1[-1];
+                    nb[0][2] = p1[0];
+                    nb[1][0] = p0[WS];
+                    nb[1][1] = p0[1];
+                    nb[1][2] = p0[0];
+                    jacobi_t_cell(L, omJ, jg, jtab, ci, cj, (int64_t)cj * pitch + ci, p0[0], p1[0], nb, out);
+                }
+                dst[t] = out[0];
+                dst[WD * HD + t] = out[1];
+            }
+        };
+        sweep(q1, W1, H1, q2, W2, H2, 3);
+        __syncthreads();
+        sweep(q2, W2, H2, ps, T::DW, T::DH, 2);
+        __syncthreads();   // q1 / q2 alias the x tile loaded next
+    } else {
+        for (int t = threadIdx.x; t < 2 * T::DW * T::DH; t += T::NT) {
+            const int sh = t / (T::DW * T::DH), rem = t - sh * (T::DW * T::DH);
+            const int ly = rem / T::DW, lx = rem - ly * T::DW;
+            const int ci = i0 - 2 + lx, cj = j0 - 2 + ly;
+            ps[t] = (ci >= 0 && cj >= 0 && ci < n && cj < n) ? __ldg(dp + sh * plane + (int64_t)cj * pitch + ci) : 0.0;
+        }
     }
     if (!XZERO) {
         load_tile<T::XW, T::XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
@@ -5587,12 +5632,13 @@ cudaError_t launch_bsr_jacobi_t(const LevelParams& L, double omJ, const double* 
 
 
 cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega, const double* x, const double* b,
-                         const double* dp, double* xo, bool x_zero, cudaStream_t s) {
+                         const double* dp, double* xo, bool x_zero, cudaStream_t s, const double* jg,
+                         const double* jtab, double omJ) {
     const bool het = L.kinv_field != nullptr;
     if (L.n <= g_small_tile_n) {
         using T = BBTile<VSX, VSY>;
         dim3 grid((L.n + VSX) / VSX, (L.n + VSY) / VSY);
-#define BBS(H_, Z_) launch_k(bsr_b_kernel<H_, Z_, VSX, VSY>, grid, T::NT, T::SMEM, s, L, U, omega, x, b, dp, xo)
+#define BBS(H_, Z_) launch_k(bsr_b_kernel<H_, Z_, VSX, VSY>, grid, T::NT, T::SMEM, s, L, U, omega, x, b, dp, xo, jg, jtab, omJ)
         if (het && x_zero) BBS(true, true);
         else if (het) BBS(true, false);
         else if (x_zero) BBS(false, true);
@@ -5601,10 +5647,10 @@ cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega
         return cudaGetLastError();
     }
     dim3 grid((L.n + BTX) / BTX, (L.n + BTY) / BTY);
-    if (het && x_zero) launch_k(bsr_b_kernel<true, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
-    else if (het) launch_k(bsr_b_kernel<true, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
-    else if (x_zero) launch_k(bsr_b_kernel<false, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
-    else launch_k(bsr_b_kernel<false, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo);
+    if (het && x_zero) launch_k(bsr_b_kernel<true, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo, jg, jtab, omJ);
+    else if (het) launch_k(bsr_b_kernel<true, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo, jg, jtab, omJ);
+    else if (x_zero) launch_k(bsr_b_kernel<false, true>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo, jg, jtab, omJ);
+    else launch_k(bsr_b_kernel<false, false>, grid, BBNT, BB_SMEM, s, L, U, omega, x, b, dp, xo, jg, jtab, omJ);
     return cudaGetLastError();
 }
 

@@ -145,8 +145,11 @@ cudaError_t launch_bsr_a(const LevelParams& L, const DispParams& U, double omega
                          cudaStream_t s);
 cudaError_t launch_bsr_jacobi(const LevelParams& L, double omega_J, const double* g, const double* dp_in,
                               double* dp_out, cudaStream_t s);
+// jg != nullptr: the last two table Jacobi sweeps run inside the kernel (dp holds the sweep before them; g = jg,
+// table = jtab, weight omJ): bitwise two launch_bsr_jacobi_t + the plain stage B
 cudaError_t launch_bsr_b(const LevelParams& L, const DispParams& U, double omega, const double* x,
-                         const double* b, const double* dp, double* xout, bool x_zero, cudaStream_t s);
+                         const double* b, const double* dp, double* xout, bool x_zero, cudaStream_t s,
+                         const double* jg = nullptr, const double* jtab = nullptr, double omJ = 0.0);
 cudaError_t launch_kinv_coarsen(int n_fine, int pitch_fine, const double* kf, int pitch_coarse, double* kc,
                                 cudaStream_t s);
 cudaError_t launch_kinv_from_K(int n, int pitch, const double* K, double* kinv, cudaStream_t s);

@@ -334,6 +334,27 @@ def test_bsr_rvec_bitwise(n, levels, pname, het, nJ):
     assert np.array_equal(out[0][2], out[1][2])
 
 
+@pytest.mark.parametrize("n,levels,pname,het,nJ", [(64, 5, "unit", 3, 3), (48, 3, "mixed", None, 4),
+                                                    (256, 7, "unit", None, 3), (160, 5, "stiff", 7, 5)])
+def test_bsr_jacobi_fused_b_bitwise(n, levels, pname, het, nJ):
+    """The 2-D tile stage B with the last two table Jacobi sweeps run inside it (MG_JACOBI_FUSE_B=1, the
+    default on the levels below the marching threshold) gives bitwise the iterates and
+    norms of separate Jacobi launches followed by the plain stage B: small 8 x 4 and 32 x 8 tiles, with and
+    without a K field, n_J = 3, 4, 5."""
+    torch = _torch()
+    from paper_2107_04060_b200 import Opts
+    b = mg_inputs.uniform_rhs(n, 9)
+    out = []
+    for fuse in ("1", "0"):
+        H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_JACOBI_FUSE_B": fuse, "MG_JACOBI_PAIR": fuse})
+        xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
+        hist = [H.cycle(xd, bd, Opts(2, 1, "bsr", 0.7, 0.9, nJ)) for _ in range(3)]
+        out.append((H.to_host(xd), hist))
+        H.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("n,levels,pname,nu", [(64, 5, "cfg5", 1), (48, 3, "mixed", 2), (128, 6, "stiff", 1)])
 def test_small_tile_sweep_bitwise(n, levels, pname, nu):
     """The small-tile sweep with all of its global reads in the first round trip (vanka_small_kernel:
