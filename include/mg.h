@@ -235,7 +235,8 @@ int mg_solve(mg_ctx* ctx, double* x, const double* b, const mg_cycle_opts* opts,
 /* Flexible GMRES(restart) on level 0, right-preconditioned by one V(nu1, nu2) cycle from a zero
  * initial guess per iteration -- the paper's solver for every timed experiment (PAPER.md:922,
  * SURVEY 8(f) rank 1).  Arnoldi by classical Gram-Schmidt with a second pass when the first one
- * cancelled more than half of the vector (DGKS criterion), fused into passes over memory (dots;
+ * cancelled the vector by more than 10x (the DGKS test with eta = 0.1; one pass then leaves the new
+ * vector orthogonal to ~10 u, enough for a basis of at most 31 vectors), fused into passes over memory (dots;
  * first update + second dots; second update + norm) on an unscaled basis whose scales are kept on
  * the host; deterministic device dot products; Givens rotations on the host.  Starts from the given x, stops at estimated
  * ||r_k|| <= rtol ||r_0|| or max_iters.  history_host: NULL or max_iters+1 doubles: history[0] =

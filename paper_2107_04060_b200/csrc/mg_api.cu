@@ -130,6 +130,9 @@ struct mg_ctx {
     int jacobi_table = 1;         // 1: Jacobi sweeps from the per-level table (bsr_jacobi_t_kernel)
     int bsr_impl = 1;             // 1: row-marching BSR stages on levels with n >= march_min_n, 0: 2-D tiles
     int fuse_prolong = 1;         // 1: prolongation fused into the first post-sweep of marching Vanka levels
+    double dgks_eta2 = 0.01;      // selective reorthogonalisation (DGKS form): second Gram-Schmidt pass when the first
+                                  // cancelled more than 10x, |U'|^2 < eta^2 |U|^2 (MG_DGKS_ETA2; 0.5 = the classical 1/sqrt2:
+                                  // a pass in every iteration here; one pass leaves orthogonality ~ u / eta per vector)
     int cgs_passes = 0;           // FGMRES Gram-Schmidt: 0 adaptive (second pass when |U'| < |U|/sqrt2,
                                   // the DGKS criterion), 1 single, 2 always twice (MG_CGS_PASSES)
     cudaEvent_t ev[6] = {};
@@ -538,6 +541,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     if (const char* v = getenv("MG_JACOBI_TABLE")) c->jacobi_table = atoi(v) != 0;
     if (const char* v = getenv("MG_BOTTOM_N")) c->bottom_n = atoi(v);
     if (const char* v = getenv("MG_CGS_PASSES")) c->cgs_passes = std::min(2, std::max(0, atoi(v)));
+    if (const char* v = getenv("MG_DGKS_ETA2")) c->dgks_eta2 = atof(v);
     auto bail = [&](int rc) {
         mg_free(c);
         return rc;
@@ -992,11 +996,11 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
             CK(launch_gs(1, c->kw, c->kv[j + 1], V, kk, d1, s2d, len, c->kpart, c->kcnt, d2, s));
             bool two = c->cgs_passes == 2;
             if (c->cgs_passes == 0) {
-                // DGKS: reorthogonalise only when the first pass cancelled more than half of U
-                // (|U'|^2 < |U|^2 / 2); |U|^2 and |U'|^2 come with the two passes' dot products
+                // DGKS-type test: reorthogonalise only when the first pass cancelled U by more than 1 / eta
+                // (|U'|^2 < eta^2 |U|^2); |U|^2 and |U'|^2 come with the two passes' dot products
                 CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
-                two = hh[40 + kk] < 0.5 * hh[kk];
+                two = hh[40 + kk] < c->dgks_eta2 * hh[kk];
             }
             if (two) CK(launch_gs(2, c->kv[j + 1], c->kv[j + 1], V, kk, d2, s2d, len, c->kpart, c->kcnt, d3, s));
             CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));

@@ -80,19 +80,21 @@ def test_het_vanka_cycle_history(n, levels, pname, het, cycles):
 
 
 @pytest.mark.parametrize("n,levels,pname,het,nu", [(64, 5, "unit", 3, 1), (96, 4, "stiff", 7, 2), (112, 5, "mixed", 5, 1),
-                                                   (36, 3, "unit", 3, 1)])
+                                                   (36, 3, "unit", 3, 1), (576, 7, "unit", 3, 1)])
 def test_het_warp_sweep_bitwise(n, levels, pname, het, nu):
     """The warp-marching heterogeneous-K Vanka sweep (vanka_hwarp_kernel: K^{-1} rows in a TMA ring,
     residuals and patch corrections moved by shuffles, boundary-vertex patches from vanka_bnd_kernel)
     gives bitwise the iterates and norms of the 2-D tile kernel vanka_het_kernel (same arithmetic, same
     summation order, reading A20) on every level -- ragged strips and
-    segments, zero-initial-guess levels, odd n."""
+    segments, zero-initial-guess levels; the 576^2 case runs the production dispatch (warp sweep on the
+    576 level with the S~^{-1} prefetch, 2-D tiles below) against the 2-D tiles everywhere."""
     _torch()
     from paper_2107_04060_b200 import Opts
     b = mg_inputs.uniform_rhs(n, 11)
     out = []
     for warp in ("1", "0"):
-        H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_HET_WARP_N": warp})
+        knob = ("512" if n >= 512 else "1") if warp == "1" else "0"
+        H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_HET_WARP_N": knob})
         xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
         hist = [H.cycle(xd, bd, Opts(nu, nu, "vanka", 0.74)) for _ in range(3)]
         out.append((H.to_host(xd), hist))

@@ -335,7 +335,8 @@ def test_bsr_rvec_bitwise(n, levels, pname, het, nJ):
 
 
 @pytest.mark.parametrize("n,levels,pname,het,nJ", [(64, 5, "unit", 3, 3), (48, 3, "mixed", None, 4),
-                                                    (256, 7, "unit", None, 3), (160, 5, "stiff", 7, 5)])
+                                                    (256, 7, "unit", None, 3), (160, 5, "stiff", 7, 5),
+                                                    (576, 7, "unit", 3, 3)])
 def test_bsr_jacobi_fused_b_bitwise(n, levels, pname, het, nJ):
     """The 2-D tile stage B with the last two table Jacobi sweeps run inside it (MG_JACOBI_FUSE_B=1, the
     default on the levels below the marching threshold) gives bitwise the iterates and
@@ -346,7 +347,9 @@ def test_bsr_jacobi_fused_b_bitwise(n, levels, pname, het, nJ):
     b = mg_inputs.uniform_rhs(n, 9)
     out = []
     for fuse in ("1", "0"):
-        H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_JACOBI_FUSE_B": fuse, "MG_JACOBI_PAIR": fuse})
+        # the 576^2 case: production dispatch (marching stages with the residual vector on the 576 level)
+        H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_JACOBI_FUSE_B": fuse, "MG_JACOBI_PAIR": fuse,
+                                                        "MG_BSR_RVEC": fuse})
         xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
         hist = [H.cycle(xd, bd, Opts(2, 1, "bsr", 0.7, 0.9, nJ)) for _ in range(3)]
         out.append((H.to_host(xd), hist))
