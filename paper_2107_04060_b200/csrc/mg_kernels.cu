@@ -257,6 +257,28 @@ __device__ __forceinline__ void residual_at(const LevelParams& L, const double* 
     for (int k = 0; k < 10; ++k) r[k] = is_active(k, i, j, n) ? (gld<NC>(b + k * L.plane + (in ? o : 0)) - av[k]) : 0.0;
 }
 
+// residual_at with b already in registers (bp[k] = b of plane k at (i, j), anything where inactive): the
+// latency-bound tile kernels issue these loads together with the x tile instead of after it
+template <int W, int HT, bool HET>
+__device__ __forceinline__ void residual_at_b(const LevelParams& L, const double* __restrict__ xs, int lx, int ly,
+                                              int i, int j, const double bp[10], double r[10]) {
+    const double* x0 = xs + ly * W + lx;
+    double av[10];
+    apply_rows<W * HT, HET>(L, x0 - W, x0, x0 + W, i, j, av);
+    if (L.lamx != 0.0) exact_bubble_add(L.lamx, x0 - W, x0, x0 + W, W * HT, av);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) r[k] = is_active(k, i, j, L.n) ? (bp[k] - av[k]) : 0.0;
+}
+// the b values residual_at would read for position (i, j) (0 outside the mesh)
+__device__ __forceinline__ void load_b10(const LevelParams& L, const double* __restrict__ b, int i, int j, bool on,
+                                         double bp[10]) {
+    const int n = L.n;
+    const bool in = on && i >= 0 && j >= 0 && i <= n && j <= n;
+    const int64_t o = in ? (int64_t)j * L.pitch + i : 0;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) bp[k] = in ? __ldg(b + k * L.plane + o) : 0.0;
+}
+
 // ------------------------------------------------------------------------------------------
 // residual
 constexpr int RTX = 32, RTY = 8, RNT = 256;
@@ -1755,12 +1777,20 @@ __global__ void __launch_bounds__(BATile<TX, TY>::NT, 2) bsr_a_kernel(const Leve
     const int64_t plane = L.plane;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
     if (!XZERO) {
+        // b of this thread's residual position travels with the x tile (one round trip instead of two)
+        constexpr bool PRE = TX <= 8;   // small (latency-bound) tiles only
+        double bp[10];
+        if (PRE) {
+            const int t = threadIdx.x, ly = t / T::RW, lx = t - ly * T::RW;
+            load_b10(L, b, i0 - 1 + lx, j0 - 1 + ly, t < T::RW * T::RH, bp);
+        }
         load_tile<T::XW, T::XH, 10>(xs, x, i0 - 2, j0 - 2, n, pitch, plane);
         __syncthreads();
         if (const int t = threadIdx.x; t < T::RW * T::RH) {
             const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            if (PRE) residual_at_b<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, bp, rv);
+            else residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
             for (int k = 0; k < 10; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
@@ -2078,6 +2108,22 @@ __global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const Leve
     const int n = L.n, pitch = L.pitch;
     const int64_t plane = L.plane;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    // this thread's owner x, the D_w of its RT0 DoFs and b of its residual position: issued with the first
+    // round trip of the kernel instead of at their uses (latency-bound levels)
+    // (small tiles only: the 32 x 8 tile runs at its 80-register cap and is bandwidth- rather than latency-bound)
+    constexpr bool PRE = TX <= 8;
+    double xown[10], dwown[3], bp[10];
+    if (PRE) {
+        const int olx = threadIdx.x % TX, oly = threadIdx.x / TX, oi = i0 + olx, oj = j0 + oly;
+        const bool own = threadIdx.x < TX * TY && oi <= n && oj <= n;
+        const int64_t oo = own ? (int64_t)oj * pitch + oi : 0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) xown[k] = (!XZERO && own) ? __ldg(x + k * plane + oo) : 0.0;
+#pragma unroll
+        for (int k = 5; k < 8; ++k) dwown[k - 5] = own ? Dw_at<HET>(L, k, oi, oj) : 1.0;
+        const int t = threadIdx.x, ly = t / T::RW, lx = t - ly * T::RW;
+        if (!XZERO) load_b10(L, b, i0 - 1 + lx, j0 - 1 + ly, t < T::RW * T::RH, bp);
+    }
     if (jg) {
         // the last two table Jacobi sweeps fused in (latency-bound levels: one launch less per relaxation):
         // dp on the cells two rings further out, one sweep into q2, the second into ps -- each cell the
@@ -2133,7 +2179,8 @@ __global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const Leve
         if (const int t = threadIdx.x; t < T::RW * T::RH) {
             const int ly = t / T::RW, lx = t - ly * T::RW;
             double rv[10];
-            residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
+            if (PRE) residual_at_b<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, bp, rv);
+            else residual_at<T::XW, T::XH, HET>(L, xs, lx + 1, ly + 1, i0 - 1 + lx, j0 - 1 + ly, b, rv);
 #pragma unroll
             for (int k = 0; k < 8; ++k) rs[k * T::RW * T::RH + t] = rv[k];
         }
@@ -2188,7 +2235,7 @@ __global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const Leve
 #undef MG_I
 #pragma unroll
     for (int k = 5; k < 8; ++k) {
-        const double dwk = Dw_at<HET>(L, k, i, j);
+        const double dwk = PRE ? dwown[k - 5] : Dw_at<HET>(L, k, i, j);
         d[k] = is_active(k, i, j, n) ? (r00[k * T::RW * T::RH] - L.tau * bw[k - 5]) / (L.tau * dwk) : 0.0;
     }
     d[8] = p00[0];
@@ -2196,7 +2243,7 @@ __global__ void __launch_bounds__(BBTile<TX, TY>::NT, 2) bsr_b_kernel(const Leve
     const int64_t o = (int64_t)j * pitch + i;
 #pragma unroll
     for (int k = 0; k < 10; ++k) {
-        const double xv = XZERO ? 0.0 : __ldg(x + k * plane + o);
+        const double xv = XZERO ? 0.0 : (PRE ? xown[k] : __ldg(x + k * plane + o));
         xo[k * plane + o] = is_active(k, i, j, n) ? fma(omega, d[k], xv) : 0.0;
     }
 }
