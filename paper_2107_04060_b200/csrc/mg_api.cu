@@ -95,7 +95,7 @@ struct mg_ctx {
     SolveState* state = nullptr;  // device struct
     double* hist = nullptr;
     int hist_cap = 0;
-    double* pinned = nullptr;     // host: 4 doubles
+    double* pinned = nullptr;     // host: 4 doubles + 256 of FGMRES scratch (device dots in, scales out)
     // e2e buffers
     double* hx = nullptr;
     double* hb = nullptr;
@@ -666,7 +666,7 @@ int mg_setup(const mg_grid* grid, double lambda, double mu, double K, double tau
     cudaMemset(c->counter, 0, 64);
     cudaMemset(c->stop, 0, 64);
     for (int l = 0; l < levels; ++l) c->L[l].vp.L.stop = c->stop;
-    if (cudaMallocHost(&c->pinned, 4 * sizeof(double)) != cudaSuccess) return bail(fail(MG_ENOMEM, "pinned alloc failed"));
+    if (cudaMallocHost(&c->pinned, (4 + 256) * sizeof(double)) != cudaSuccess) return bail(fail(MG_ENOMEM, "pinned alloc failed"));
     // coarsest dense deflated inverse (reading A9)
     if (dense_ok) {
         Level& Lc = c->L[levels - 1];
@@ -995,25 +995,29 @@ int mg_fgmres(mg_ctx* c, double* x, const double* b, const mg_cycle_opts* o, dou
             CK(launch_gs(0, c->kw, nullptr, V, kk, nullptr, nullptr, len, c->kpart, c->kcnt, d1, s));
             CK(launch_gs(1, c->kw, c->kv[j + 1], V, kk, d1, s2d, len, c->kpart, c->kcnt, d2, s));
             bool two = c->cgs_passes == 2;
+            bool have = false;   // hh already holds the dots of this iteration (no second pass followed)
             if (c->cgs_passes == 0) {
                 // DGKS-type test: reorthogonalise only when the first pass cancelled U by more than 1 / eta
                 // (|U'|^2 < eta^2 |U|^2); |U|^2 and |U'|^2 come with the two passes' dot products
                 CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 two = hh[40 + kk] < c->dgks_eta2 * hh[kk];
+                have = !two;
             }
             if (two) CK(launch_gs(2, c->kv[j + 1], c->kv[j + 1], V, kk, d2, s2d, len, c->kpart, c->kcnt, d3, s));
-            CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            if (!have) {
+                CK(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * 81, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+            }
             const double rho = std::sqrt(two ? hh[80] : hh[40 + kk]);
             // h_ij = (A z_j) . v_i = s_j s_i <U, W_i> = s_j (c1_i + c2_i) / s_i
             for (int i = 0; i <= j; ++i)
                 H[i * m + j] = sv[j] * sv[i] * (hh[i] + (two ? hh[40 + i] : 0.0));
             H[(j + 1) * m + j] = sv[j] * rho;
             sv[j + 1] = rho > 0.0 ? 1.0 / rho : 0.0;
-            hh[90] = sv[j + 1] * sv[j + 1];
-            CK(cudaMemcpyAsync(s2d + j + 1, hh.data() + 90, sizeof(double), cudaMemcpyHostToDevice, s));
-            CK(cudaStreamSynchronize(s));   // hh[90] is host scratch reused next iteration
+            // one pinned slot per basis index: no synchronisation needed before the next iteration reuses hh
+            c->pinned[4 + 128 + j + 1] = sv[j + 1] * sv[j + 1];
+            CK(cudaMemcpyAsync(s2d + j + 1, c->pinned + 4 + 128 + j + 1, sizeof(double), cudaMemcpyHostToDevice, s));
             for (int i = 0; i < j; ++i) {   // previous Givens rotations
                 const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
                 H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
