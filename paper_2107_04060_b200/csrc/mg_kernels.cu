@@ -3720,10 +3720,17 @@ constexpr int Q_RW = 2 * QT + 2, Q_XW = 2 * QT + 6;          // fine r columns, 
 constexpr int QNT = Q_RW * QF;                               // 128 threads
 constexpr int Q_XCH = 10 * QF * Q_XW, Q_BCH = 10 * QF * Q_RW;
 constexpr int Q_SMEM = (3 * Q_XCH + 3 * Q_BCH) * 8 + 64;
+// K field (third session): the K^{-1} planes of the x chunks' rows as a third chunk ring (same rows and columns as
+// the x chunk, 2 planes) instead of gathers from global memory inside the residual
+constexpr int Q_KCH = 2 * QF * Q_XW;
+constexpr int Q_SMEM_K = (3 * Q_XCH + 3 * Q_BCH + 3 * Q_KCH) * 8 + 64;
+static_assert(3 * (Q_SMEM_K + 1024) <= 228 * 1024, "three CTAs per SM");
+static_assert((Q_KCH * 8) % 128 == 0, "K chunk slots 128-byte aligned");
 
 template <bool HET>
 __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_constant__ CUtensorMap tmx,
                                                                 const __grid_constant__ CUtensorMap tmb,
+                                                                const __grid_constant__ CUtensorMap tmk,
                                                                 const LevelParams L, int nc, int pitchc,
                                                                 double* __restrict__ bc, int MH) {
     pdl_wait();
@@ -3731,7 +3738,8 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;                    // [3][10][QF][Q_XW]
     double* br = xr + 3 * Q_XCH;        // [3][10][QF][Q_RW]  (b, overwritten by r)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(br + 3 * Q_BCH);
+    double* kq = br + 3 * Q_BCH;        // HET: [3][2][QF][Q_XW]  K^{-1} of the x chunks' rows
+    uint64_t* bars = reinterpret_cast<uint64_t*>(kq + (HET ? 3 * Q_KCH : 0));
     if (*L.stop) return;
     constexpr bool DI = !HET;   // de-interleaved r columns (see the residual phase)
     const int n = L.n;
@@ -3744,8 +3752,9 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
     // x chunk c: fine rows [F0 + (c-1) QF - 1, F0 + c QF - 1); b chunk d: fine rows [F0 + (d-1) QF, F0 + d QF)
     auto issue_x = [&](int c) {
         if (c < nxc) {
-            mbar_expect_tx(&bars[c % 3], Q_XCH * 8);
+            mbar_expect_tx(&bars[c % 3], (Q_XCH + (HET ? Q_KCH : 0)) * 8);
             tma_load3(xr + (c % 3) * Q_XCH, &tmx, 2 * I0 - 4, F0 + (c - 1) * QF - 1, 0, &bars[c % 3]);
+            if (HET) tma_load3(kq + (c % 3) * Q_KCH, &tmk, 2 * I0 - 4, F0 + (c - 1) * QF - 1, 0, &bars[c % 3]);
         }
     };
     auto issue_b = [&](int d) {
@@ -3783,7 +3792,16 @@ __global__ void __launch_bounds__(QNT, 3) restrict_march_kernel(const __grid_con
             const double* x0 = (y0 < QF ? base1 + y0 * Q_XW : base2 + (y0 - QF) * Q_XW);
             const double* xp = (yp < QF ? base1 + yp * Q_XW : base2 + (yp - QF) * Q_XW);
             double av[10];
-            apply_rows<QF * Q_XW, HET>(L, xm, x0, xp, i, y, av);
+            if (HET) {
+                // K^{-1} of the cell rows y - 1 and y: rows ym, y0 of the K chunks (cells outside the mesh: 0)
+                const double* kb1 = kq + ((s + 1) % 3) * Q_KCH + (lx + 2);
+                const double* kb2 = kq + ((s + 2) % 3) * Q_KCH + (lx + 2);
+                const double* km = (ym < QF ? kb1 + ym * Q_XW : kb2 + (ym - QF) * Q_XW);
+                const double* k0 = (y0 < QF ? kb1 + y0 * Q_XW : kb2 + (y0 - QF) * Q_XW);
+                apply_rows_kr<QF * Q_XW, QF * Q_XW>(L, xm, x0, xp, km, k0, av);
+            } else {
+                apply_rows<QF * Q_XW, false>(L, xm, x0, xp, i, y, av);
+            }
             const double* bp = br + bslot * Q_BCH + q * Q_RW + lx;
             double rv[10];
 #pragma unroll
@@ -4706,7 +4724,7 @@ void kernels_init() {
     set_smem(bsr_b_march_kernel<true, 1>, BB2_SMEM_NX);
     set_smem(bsr_b_march_kernel<true, 2>, BB2_SMEM_NX);
     set_smem(restrict_march_kernel<false>, Q_SMEM);
-    set_smem(restrict_march_kernel<true>, Q_SMEM);
+    set_smem(restrict_march_kernel<true>, Q_SMEM_K);
     set_smem(vanka_kernel<false>, V_SMEM);
     set_smem(vanka_kernel<true>, V_SMEM);
     set_smem(vanka_kernel<false, VSX, VSY>, VTile<VSX, VSY>::SMEM);
@@ -5532,15 +5550,17 @@ cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double
 
 cudaError_t launch_restrict_march(const LevelParams& Lf, int nc, int pitchc, const double* x, const double* b,
                                   double* bc, cudaStream_t s) {
-    CUtensorMap mx, mb;
+    CUtensorMap mx, mb, mk;
     cudaError_t e = encode_vec_map(&mx, x, Lf.n, Lf.pitch, Lf.plane, Q_XW, QF);
     if (e != cudaSuccess) return e;
     e = encode_vec_map(&mb, b, Lf.n, Lf.pitch, Lf.plane, Q_RW, QF);
     if (e != cudaSuccess) return e;
+    e = encode_vec_map(&mk, Lf.kinv_field ? Lf.kinv_field : b, Lf.n, Lf.pitch, Lf.plane, Q_XW, QF, 2);
+    if (e != cudaSuccess) return e;
     const int MH = march_height(nc, QT, QR, 3, 128);
     dim3 grid((nc + QT) / QT, (nc + MH) / MH);
-    if (Lf.kinv_field) launch_k(restrict_march_kernel<true>, grid, QNT, Q_SMEM, s, mx, mb, Lf, nc, pitchc, bc, MH);
-    else launch_k(restrict_march_kernel<false>, grid, QNT, Q_SMEM, s, mx, mb, Lf, nc, pitchc, bc, MH);
+    if (Lf.kinv_field) launch_k(restrict_march_kernel<true>, grid, QNT, Q_SMEM_K, s, mx, mb, mk, Lf, nc, pitchc, bc, MH);
+    else launch_k(restrict_march_kernel<false>, grid, QNT, Q_SMEM, s, mx, mb, mk, Lf, nc, pitchc, bc, MH);
     return cudaGetLastError();
 }
 
