@@ -4526,16 +4526,21 @@ __global__ void __launch_bounds__(WQGeom<HET>::NT, 1) bsr_b_warp_kernel(const __
 // MODE 0: r = b - A x (+||r||^2), MODE 1: y = A x on the active slots (FGMRES), MODE 2: ||b - A x||^2.
 constexpr int RM_T = 28, RM_R = 4, RM_NT = 128, RM_XR = 10, RM_W = 32, RM_ROW = 10 * RM_W;
 constexpr int RM_SMEM = RM_XR * RM_ROW * 8 + 64;
+// K field (third session): the two K^{-1} planes of the cell rows in a ring of their own (rows y - 1, y of residual
+// row y; group g: rows j0+gR .. j0+gR+3, g = 0 also j0-1), read by apply_rows_kr
+constexpr int RM_KROW = 2 * RM_W, RM_SMEM_K = (RM_XR * RM_ROW + RM_XR * RM_KROW) * 8 + 64;
 
-template <int MODE>
+template <int MODE, bool HET = false>
 __global__ void __launch_bounds__(RM_NT) residual_march_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                               const __grid_constant__ CUtensorMap tmk,
                                                                const LevelParams L, const double* __restrict__ b,
                                                                double* __restrict__ r, NormSink S, int MH) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) double sm[];
     double* xr = sm;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xr + RM_XR * RM_ROW);
+    double* kr = xr + RM_XR * RM_ROW;   // HET: [RM_XR][2][RM_W]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(kr + (HET ? RM_XR * RM_KROW : 0));
     if (*L.stop) return;
     const int n = L.n;
     const int i0 = blockIdx.x * RM_T, j0 = blockIdx.y * MH;
@@ -4549,9 +4554,13 @@ __global__ void __launch_bounds__(RM_NT) residual_march_kernel(const __grid_cons
         uint64_t* bar = &bars[g & 1];
         const int nx = g == 0 ? RM_R + 2 : RM_R;
         const int first = g == 0 ? j0 - 1 : j0 + g * RM_R + 1;
-        mbar_expect_tx(bar, nx * RM_ROW * 8);
+        const int nk = HET ? (g == 0 ? RM_R + 1 : RM_R) : 0;
+        const int kfirst = g == 0 ? j0 - 1 : j0 + g * RM_R;
+        mbar_expect_tx(bar, (nx * RM_ROW + nk * RM_KROW) * 8);
 #pragma unroll 1
         for (int k = 0; k < nx; ++k) tma_load3(xr + sx(first + k) * RM_ROW, &tmx, i0 - 2, first + k, 0, bar);
+#pragma unroll 1
+        for (int k = 0; k < nk; ++k) tma_load3(kr + sx(kfirst + k) * RM_KROW, &tmk, i0 - 2, kfirst + k, 0, bar);
     };
     if (t == 0) {
         mbar_init(&bars[0], 1);
@@ -4571,7 +4580,9 @@ __global__ void __launch_bounds__(RM_NT) residual_march_kernel(const __grid_cons
         if (lane >= 2 && lane < RM_T + 2 && i <= n && y < j0 + rows) {
             const double* x0 = xr + sx(y) * RM_ROW + lane;
             double av[10];
-            apply_rows<RM_W, false>(L, xr + sx(y - 1) * RM_ROW + lane, x0, xr + sx(y + 1) * RM_ROW + lane, i, y, av);
+            if (HET) apply_rows_kr<RM_W, RM_W>(L, xr + sx(y - 1) * RM_ROW + lane, x0, xr + sx(y + 1) * RM_ROW + lane,
+                                               kr + sx(y - 1) * RM_KROW + lane, kr + sx(y) * RM_KROW + lane, av);
+            else apply_rows<RM_W, false>(L, xr + sx(y - 1) * RM_ROW + lane, x0, xr + sx(y + 1) * RM_ROW + lane, i, y, av);
             const unsigned am = active_mask(i, y, n);
             const int64_t o = (int64_t)y * L.pitch + i;
 #pragma unroll
@@ -4781,14 +4792,21 @@ int blocks_bsr(int n) {
 
 static cudaError_t launch_residual_march(int mode, const LevelParams& L, const double* x, const double* b, double* r,
                                          NormSink S, cudaStream_t s) {
-    CUtensorMap mx;
+    CUtensorMap mx, mk;
     cudaError_t e = encode_vec_map(&mx, x, L.n, L.pitch, L.plane, RM_W, 1);
+    if (e != cudaSuccess) return e;
+    const bool het = L.kinv_field != nullptr;
+    e = encode_vec_map(&mk, het ? L.kinv_field : x, L.n, L.pitch, L.plane, RM_W, 1, 2);
     if (e != cudaSuccess) return e;
     const int MH = march_height(L.n, RM_T, RM_R, 6, 64);
     dim3 grid((L.n + RM_T) / RM_T, (L.n + MH) / MH);
-    if (mode == 0) launch_k(residual_march_kernel<0>, grid, RM_NT, RM_SMEM, s, mx, L, b, r, S, MH);
-    else if (mode == 1) launch_k(residual_march_kernel<1>, grid, RM_NT, RM_SMEM, s, mx, L, b, r, S, MH);
-    else launch_k(residual_march_kernel<2>, grid, RM_NT, RM_SMEM, s, mx, L, b, r, S, MH);
+    if (het) {
+        if (mode == 0) launch_k(residual_march_kernel<0, true>, grid, RM_NT, RM_SMEM_K, s, mx, mk, L, b, r, S, MH);
+        else if (mode == 1) launch_k(residual_march_kernel<1, true>, grid, RM_NT, RM_SMEM_K, s, mx, mk, L, b, r, S, MH);
+        else launch_k(residual_march_kernel<2, true>, grid, RM_NT, RM_SMEM_K, s, mx, mk, L, b, r, S, MH);
+    } else if (mode == 0) launch_k(residual_march_kernel<0>, grid, RM_NT, RM_SMEM, s, mx, mk, L, b, r, S, MH);
+    else if (mode == 1) launch_k(residual_march_kernel<1>, grid, RM_NT, RM_SMEM, s, mx, mk, L, b, r, S, MH);
+    else launch_k(residual_march_kernel<2>, grid, RM_NT, RM_SMEM, s, mx, mk, L, b, r, S, MH);
     return cudaGetLastError();
 }
 int blocks_residual_march(int n) {
@@ -4798,7 +4816,7 @@ int blocks_residual_march(int n) {
 
 cudaError_t launch_residual(const LevelParams& L, const double* x, const double* b, double* r, NormSink S,
                             cudaStream_t s) {
-    if (!L.kinv_field && L.lamx == 0.0 && L.n >= g_resid_march_n) return launch_residual_march(r ? 0 : 2, L, x, b, r, S, s);
+    if (L.lamx == 0.0 && L.n >= g_resid_march_n) return launch_residual_march(r ? 0 : 2, L, x, b, r, S, s);
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
     if (L.kinv_field) launch_k(residual_kernel<true, false>, grid, RNT, 0, s, L, x, b, r, S);
     else launch_k(residual_kernel<false, false>, grid, RNT, 0, s, L, x, b, r, S);
@@ -4806,7 +4824,7 @@ cudaError_t launch_residual(const LevelParams& L, const double* x, const double*
 }
 
 cudaError_t launch_apply(const LevelParams& L, const double* x, double* y, NormSink S, cudaStream_t s) {
-    if (!L.kinv_field && L.lamx == 0.0 && L.n >= g_resid_march_n) return launch_residual_march(1, L, x, nullptr, y, S, s);
+    if (L.lamx == 0.0 && L.n >= g_resid_march_n) return launch_residual_march(1, L, x, nullptr, y, S, s);
     dim3 grid((L.n + RTX) / RTX, (L.n + RTY) / RTY);
     if (L.kinv_field) launch_k(residual_kernel<true, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
     else launch_k(residual_kernel<false, true>, grid, RNT, 0, s, L, x, nullptr, y, S);
@@ -5744,6 +5762,9 @@ static void carve_all() {
     carve(residual_march_kernel<0>);
     carve(residual_march_kernel<1>);
     carve(residual_march_kernel<2>);
+    carve(residual_march_kernel<0, true>);
+    carve(residual_march_kernel<1, true>);
+    carve(residual_march_kernel<2, true>);
     carve(bsr_jacobi_kernel<false>);
     carve(bsr_jacobi_kernel<true>);
     carve(bsr_jacobi_t_kernel<0>);

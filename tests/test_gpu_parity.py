@@ -40,10 +40,11 @@ def _inactive_zero(H, v, level=0):
                                                (16, "stiff", None, False), (40, "cfg5", None, False),
                                                (66, "mixed", None, False), (24, "unit", 3, False),
                                                (34, "mixed", 7, False), (40, "cfg5", None, True),
-                                               (66, "mixed", None, True), (130, "stiff", None, True)])
+                                               (66, "mixed", None, True), (130, "stiff", None, True),
+                                               (34, "mixed", 7, True), (66, "unit", 3, True)])
 def test_residual(n, pname, het, march):
     """r = b - A x and its norm; march=True runs the row-marching residual kernel (production for
-    n >= 512, scalar K) on small grids."""
+    n >= 512; with a K field its K^{-1} rows arrive in a TMA ring) on small grids."""
     torch = _torch()
     H = C.gpu_hierarchy(n, C.small_coarse_levels(n), pname, het, env={"MG_RESID_MARCH_N": "0"} if march else None)
     op = C.operator(n, pname, het)
