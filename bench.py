@@ -370,7 +370,7 @@ def main():
         # heterogeneous Vanka: read x, b, write x + the per-vertex S~^{-1} table (21 doubles per vertex
         # = 16.8 B per active DoF at 10 DoFs per vertex) + K^{-1} (2 per cell)
         alg_bytes = (24.0 + 16.8 + 1.6) * nact
-        hwarp = n >= int(os.environ.get("MG_HET_WARP_N", "512")) > 0
+        hwarp = n >= int(os.environ.get("MG_HET_WARP_N", "256")) > 0
         dom = (("vanka_hwarp_kernel + vanka_bnd_kernel<HET>" if hwarp else "vanka_het_kernel") +
                " (level 0: residual with the K^{-1} field + condensed patch solves + update)")
     elif o.relax == "vanka":

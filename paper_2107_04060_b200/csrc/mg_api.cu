@@ -122,7 +122,7 @@ struct mg_ctx {
     int jacobi_fuse_b = 1;        // 2-D tile levels: the last two table sweeps inside stage B (MG_JACOBI_FUSE_B)
     int jacobi_pair = 1;          // two table sweeps per launch where two remain (MG_JACOBI_PAIR)
     int bsr_rvec = 1;             // marching BSR: stage B reads stage A's residual instead of recomputing it (MG_BSR_RVEC)
-    int het_warp_n = 512;         // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
+    int het_warp_n = 256;         // K-field levels with n >= this: warp-marching het Vanka sweep (MG_HET_WARP_N; 0 = 2-D tiles)
     int march_min_n = 512;        // levels with fewer cells per side use the single-pass 2-D tile kernels
     int bottom_n = 0;             // > 0: Vanka levels with n <= bottom_n (down to the coarsest) in one kernel
                                   // (measured slower: one CTA 442 us, grid-wide cooperative 323 us vs 247 us

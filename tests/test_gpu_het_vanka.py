@@ -93,7 +93,7 @@ def test_het_warp_sweep_bitwise(n, levels, pname, het, nu):
     b = mg_inputs.uniform_rhs(n, 11)
     out = []
     for warp in ("1", "0"):
-        knob = ("512" if n >= 512 else "1") if warp == "1" else "0"
+        knob = ("256" if n >= 512 else "1") if warp == "1" else "0"
         H = C.gpu_hierarchy(n, levels, pname, het, env={"MG_HET_WARP_N": knob})
         xd, bd = H.to_device(np.zeros_like(b)), H.to_device(b)
         hist = [H.cycle(xd, bd, Opts(nu, nu, "vanka", 0.74)) for _ in range(3)]
