@@ -9,6 +9,11 @@
 //   prolong_kernel      x += P e_H
 //   coarse_kernel       dense deflated coarsest solve       (reading A9)
 //   bsr_a/jacobi/b      inexact Braess-Sarazin stages
+// and their production forms on the big levels (same arithmetic, bitwise-tested against the tile kernels):
+//   vanka_warp_kernel / vanka_hwarp_kernel (+ vanka_bnd2_kernel)   warp-marching sweeps, scalar K / K field
+//   restrict_march_kernel, residual_march_kernel                   row-marching TMA rings (K^{-1} ring with a K field)
+//   bsr_a_march_kernel, bsr_jacobi2_t_kernel, bsr_b_march_kernel   marching BSR stages; stage B reads stage A's residual
+//   prolong_planes_kernel                                          plane-split prolongation
 //
 // Tiles: a CTA owns TX x TY grid indices (each index owns 10 DoFs) and recomputes the residual
 // on a halo ring instead of exchanging it, so every sweep reads x and b once and writes x once
@@ -3446,7 +3451,8 @@ __global__ void __launch_bounds__(WGeom<PROL>::NT, 2) vanka_warp_kernel(const __
 // corrections moved by shuffles, no CTA barrier) with the arithmetic of vanka_het_kernel -- the residual
 // reads K^{-1} from a 4-row TMA ring of the two K^{-1} planes (apply_rows_kr), interior patches run the
 // condensed +/- solve with the per-vertex S~^{-1} (patch_apply_het_pm, 21 coalesced loads per row), the
-// boundary vertices' outputs come from vanka_bnd_kernel<.., HET>.  Same summation order in the owner phase:
+// boundary vertices' outputs come from vanka_bnd2_kernel<.., HET> (MG_HW_BK=2: vanka_bnd_kernel<.., HET>).  Same
+// summation order in the owner phase:
 // bitwise vanka_het_kernel.
 constexpr int HW_KR = 4, HW_KROW = 2 * WXW, HW_KSLOT = (HW_KROW + 15) / 16 * 16;
 constexpr int HW_BYTES = ((WXR * WXSLOT + WBR * WBSLOT + HW_KR * HW_KSLOT) * 8 + 128 + 127) / 128 * 128;
@@ -3635,7 +3641,7 @@ __global__ void __launch_bounds__(HW_NT, 2) vanka_hwarp_kernel(const __grid_cons
 #else
                     patch_apply_het_pm(P, Ti.pm, i, y, rr, o, 1);
 #endif
-                } else {   // boundary vertex: its outputs were computed by vanka_bnd_kernel<.., HET>
+                } else {   // boundary vertex: its outputs were computed by the boundary kernel (launch_vanka_hwarp)
                     const int nb = bnd_count(n), bi = bnd_index(i, y, n);
 #pragma unroll
                     for (int k = 0; k < 20; ++k) o[k] = __ldg(P.bcorr + k * nb + bi);
