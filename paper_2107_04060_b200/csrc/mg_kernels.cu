@@ -5649,7 +5649,7 @@ cudaError_t launch_prolong(int nf, int pitchf, int nc, int pitchc, const double*
     static int planes_n = -1;   // levels with nf >= this: the plane-split kernel (MG_PROL_PLANES_N; 0 = off)
     if (planes_n < 0) {
         const char* v = getenv("MG_PROL_PLANES_N");
-        planes_n = v ? atoi(v) : 512;
+        planes_n = v ? atoi(v) : 256;
     }
     if (planes_n > 0 && nf >= planes_n) {
         grid.z = 5;
