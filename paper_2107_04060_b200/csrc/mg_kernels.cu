@@ -5385,7 +5385,7 @@ static void warp_tasks_nw(int n, int slots_per_sm, int& MH, int& nstrips, int& n
     static int minrows = -1;   // shortest segment (MG_WARP_MINROWS): the per-task prologue and pipeline fill
     if (minrows < 0) {
         const char* v = getenv("MG_WARP_MINROWS");
-        minrows = v ? std::max(4, atoi(v)) : 8;
+        minrows = v ? std::max(4, atoi(v)) : 4;   // 8 until the warp sweeps took over the 512^2 level: config 3 0.428 -> 0.418 ms
     }
     MH = std::max(minrows, (int)((n + nseg) / nseg));
     nseg = (n + MH) / MH;
