@@ -5558,7 +5558,13 @@ cudaError_t launch_bsr_b_march(const LevelParams& L, const DispParams& U, double
 #undef WB_LAUNCH
         return cudaGetLastError();
     }
-    const int MH = march_height(L.n, BB_T, BQ_R, 3, relax_target(L.n));
+    // resident CTAs per SM: 3 with the x ring (68 KB), 5 without it (43 KB; MODE 1 and 2) -- MG_BSR_B_SLOTS overrides
+    static int bslots = -1;
+    if (bslots < 0) {
+        const char* v = getenv("MG_BSR_B_SLOTS");
+        bslots = v ? atoi(v) : 0;
+    }
+    const int MH = march_height(L.n, BB_T, BQ_R, bslots > 0 ? bslots : ((rvec || x_zero) ? 5 : 3), relax_target(L.n));
     dim3 grid((L.n + BB_T) / BB_T, (L.n + MH) / MH);
 #define BB_LAUNCH(H_, M_) \
     launch_k(bsr_b_march_kernel<H_, M_>, grid, BQ_NT, M_ ? BB2_SMEM_NX : BB2_SMEM, s, mx, mb, md, mk, L, U, omega, xo, MH, x)
